@@ -1,0 +1,262 @@
+"""Drop-in HODLR matvec on B200 (the north-star path).
+
+``matvec(H, x, working)`` has the signature and error behaviour of the
+reference's spec'd operator ``linops.matvec`` (/root/reference/SPEC.md:334-342,
+Algorithm 3 HODLR_MATVEC):
+
+* ``H``: a HODLR matrix -- the reference's ``hodlrmp.hodlr.HodlrMatrix`` or this
+  package's ``model.HodlrMatrix`` (anything with ``n``, ``depth``,
+  ``working_format``, ``offdiag_blocks()`` and ``leaves()``, hodlr.py:95-135);
+* ``x``: length-n real vector (or n x s block of right-hand sides);
+* ``working``: the working precision (default ``H.working_format``); fp64 and
+  fp32 run on the GPU, other formats raise ``NotImplementedError``;
+* length mismatch -> ``ValueError``; overflow propagates as inf.
+
+The matrix is packed once per ``H`` into the device layout (cached weakly by
+identity; ``HodlrMatrix`` is ``eq=False`` so it hashes by identity) and every
+call runs the hand-written sm_100a kernels through the C ABI.  ``x`` is rounded
+to the working format on entry (RNE, as ``round_matrix`` would).  There is no
+CPU path: without the CUDA extension or a GPU the call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import weakref
+
+import numpy as np
+
+from . import _lib
+from .formats import FP32, FP64, format_code
+
+__all__ = ["matvec", "HodlrOperator", "descriptor", "operator_for"]
+
+_WORKING_DTYPE = {4: np.float64, 3: np.float32}
+
+
+def _f64(a) -> np.ndarray:
+    a = np.asarray(a)
+    if a.dtype != np.float64:
+        a = a.astype(np.float64)
+    if any(s % 8 for s in a.strides):
+        a = np.ascontiguousarray(a)
+    return a
+
+
+class _Descriptor:
+    """ctypes ``hodlr_desc`` for H plus the numpy arrays it points into."""
+
+    def __init__(self, H):
+        n, depth = int(H.n), int(H.depth)
+        self.keep = []
+        leaves = list(H.leaves())
+        if len(leaves) != 2 ** depth:
+            raise ValueError(f"expected {2 ** depth} leaves, got {len(leaves)}")
+        bounds = np.array([rng[0] for _, rng, _ in leaves] + [n], dtype=np.int64)
+        lptrs = (_lib.c_dp * len(leaves))()
+        lds = np.empty(len(leaves), dtype=np.int64)
+        for i, (_, (a, b), D) in enumerate(leaves):
+            D = _f64(D)
+            if D.shape != (b - a, b - a):
+                raise ValueError(f"leaf {i} has shape {D.shape}, expected {(b - a, b - a)}")
+            if D.strides[1] != 8:
+                D = np.ascontiguousarray(D)
+            self.keep.append(D)
+            lptrs[i] = D.ctypes.data_as(_lib.c_dp)
+            lds[i] = D.strides[0] // 8 if D.shape[0] > 1 else D.shape[1]
+        facs = []
+        for _, _, _, _, up, lo in H.offdiag_blocks():
+            for f in (up, lo):
+                U, V = _f64(f.U), _f64(f.V)
+                self.keep += [U, V]
+                r = U.shape[1]
+                fi = _lib.FactorIn(
+                    format_code(f.fmt), r, U.shape[0], V.shape[0],
+                    U.ctypes.data_as(_lib.c_dp), U.strides[0] // 8, U.strides[1] // 8,
+                    V.ctypes.data_as(_lib.c_dp), V.strides[0] // 8, V.strides[1] // 8)
+                facs.append(fi)
+        nf = 2 * (2 ** depth - 1)
+        if len(facs) != nf:
+            raise ValueError(f"expected {nf} off-diagonal factors, got {len(facs)}")
+        farr = (_lib.FactorIn * max(nf, 1))(*facs)
+        self.keep += [bounds, lds, lptrs, farr]
+        self.desc = _lib.Desc(n, depth, format_code(H.working_format),
+                              bounds.ctypes.data_as(ctypes.POINTER(_lib.c_i64)), lptrs,
+                              lds.ctypes.data_as(ctypes.POINTER(_lib.c_i64)), farr)
+
+
+def descriptor(H) -> _Descriptor:
+    return _Descriptor(H)
+
+
+def _torch():
+    import torch  # plumbing only: device memory and streams
+
+    return torch
+
+
+def _working_code(H, working) -> int:
+    code = format_code(working if working is not None else H.working_format)
+    if code not in _WORKING_DTYPE:
+        raise NotImplementedError(
+            "working precision must be fp64 or fp32 on the B200 path "
+            f"(got {working if working is not None else H.working_format})")
+    return code
+
+
+class HodlrOperator:
+    """Packed, device-resident HODLR matrix (one C-ABI handle)."""
+
+    def __init__(self, H, device: int | None = None, rank: int = 0, nranks: int = 1):
+        L = _lib.lib()
+        if device is None:
+            torch = _torch()
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        self.device = int(device)
+        self.working_format = H.working_format
+        self.n = int(H.n)
+        self.depth = int(H.depth)
+        self.rank, self.nranks = int(rank), int(nranks)
+        d = _Descriptor(H)
+        h = _lib.c_vp()
+        if nranks == 1:
+            st = L.hodlr_create(ctypes.byref(d.desc), self.device, ctypes.byref(h))
+        else:
+            st = L.hodlr_create_sharded(ctypes.byref(d.desc), self.device,
+                                        _lib.Shard(rank, nranks), ctypes.byref(h))
+        _lib.check(st, "hodlr_create")
+        self._h = h
+        self._lock = threading.Lock()
+        info = _lib.Info()
+        _lib.check(L.hodlr_info(h, ctypes.byref(info)), "hodlr_info")
+        self.n_local = int(info.n_local)
+        self.row0 = int(info.row0)
+        self.matrix_bytes = int(info.matrix_bytes)
+        self.device_bytes = int(info.device_bytes)
+        self.launches_per_matvec = int(info.launches_per_matvec)
+        self._finalizer = weakref.finalize(self, L.hodlr_destroy, h)
+
+    # ---------------------------------------------------------------- device
+    def matvec(self, x, working=None, out=None, stream=None):
+        """b = H x for a CUDA tensor x ((n,) or (n, s)), returns a CUDA tensor of
+        the working dtype.  Stream-ordered on ``stream`` (default: current)."""
+        torch = _torch()
+        code = _working_code(self, working)
+        dt = torch.float64 if code == 4 else torch.float32
+        if not (isinstance(x, torch.Tensor) and x.is_cuda):
+            raise TypeError("HodlrOperator.matvec expects a CUDA tensor; use matvec_host for host arrays")
+        vec = x.dim() == 1
+        X = x.reshape(-1, 1) if vec else x
+        if X.dim() != 2 or X.shape[0] != self.n_local:
+            raise ValueError(f"length mismatch: x has {x.shape[0]} rows, operator has {self.n_local}")
+        if X.dtype != dt:
+            X = X.to(dt)  # single RNE rounding fp64 -> fp32 (cvt.rn.f32.f64)
+        if X.stride(1) != 1:
+            X = X.contiguous()
+        s = X.shape[1]
+        B = out if out is not None else torch.empty((self.n_local, s), dtype=dt, device=X.device)
+        if out is not None and (B.shape != (self.n_local, s) or B.dtype != dt or B.stride(1) != 1):
+            raise ValueError("out has the wrong shape / dtype / layout")
+        st = stream if stream is not None else torch.cuda.current_stream(X.device)
+        with self._lock:
+            _lib.check(_lib.lib().hodlr_matvec(
+                self._h, code, X.data_ptr(), X.stride(0), B.data_ptr(), B.stride(0), s, None, 0,
+                st.cuda_stream), "hodlr_matvec")
+        return B[:, 0] if (vec and out is None) else B
+
+    # ---------------------------------------------------------------- host
+    def matvec_host(self, x, working=None) -> np.ndarray:
+        """End-to-end call with host buffers: binary64 in, binary64 out."""
+        code = _working_code(self, working)
+        x = np.asarray(x, dtype=np.float64)
+        vec = x.ndim == 1
+        X = np.ascontiguousarray(x.reshape(-1, 1) if vec else x)
+        if X.ndim != 2 or X.shape[0] != self.n_local:
+            raise ValueError(f"length mismatch: x has {x.shape[0] if x.ndim else 0} rows, "
+                             f"H has {self.n_local}")
+        B = np.empty_like(X)
+        with self._lock:
+            _lib.check(_lib.lib().hodlr_matvec_host(self._h, code, X.ctypes.data, B.ctypes.data,
+                                                     X.shape[1], None), "hodlr_matvec_host")
+        return B[:, 0] if vec else B
+
+    def matvec_host_ptr(self, x_ptr: int, b_ptr: int, s: int, working=None, stream=None) -> None:
+        """Host-pointer variant (pinned buffers), used by the e2e benchmark."""
+        code = _working_code(self, working)
+        _lib.check(_lib.lib().hodlr_matvec_host(self._h, code, x_ptr, b_ptr, s, stream),
+                   "hodlr_matvec_host")
+
+    # ---------------------------------------------------------------- sharded
+    def exchange_count(self, s: int = 1) -> int:
+        c = _lib.c_i64()
+        _lib.check(_lib.lib().hodlr_shard_exchange_count(self._h, s, ctypes.byref(c)))
+        return int(c.value)
+
+    def shard_begin(self, x, send, working=None, stream=None):
+        torch = _torch()
+        code = _working_code(self, working)
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _lib.check(_lib.lib().hodlr_matvec_shard_begin(
+            self._h, code, x.data_ptr(), x.stride(0), x.shape[1],
+            send.data_ptr() if send is not None and send.numel() else None, None, 0,
+            st.cuda_stream), "hodlr_matvec_shard_begin")
+
+    def shard_end(self, x, recv, out, working=None, stream=None):
+        torch = _torch()
+        code = _working_code(self, working)
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _lib.check(_lib.lib().hodlr_matvec_shard_end(
+            self._h, code, x.data_ptr(), x.stride(0),
+            recv.data_ptr() if recv is not None and recv.numel() else None,
+            out.data_ptr(), out.stride(0), x.shape[1], None, 0, st.cuda_stream),
+            "hodlr_matvec_shard_end")
+
+    # ---------------------------------------------------------------- checks
+    def unpack_factor(self, index: int, rows: int, cols: int, rank: int):
+        U = np.empty((rows, rank))
+        V = np.empty((cols, rank))
+        _lib.check(_lib.lib().hodlr_unpack_factor(self._h, index, U.ctypes.data, V.ctypes.data))
+        return U, V
+
+    def unpack_leaf(self, i: int, m: int) -> np.ndarray:
+        D = np.empty((m, m))
+        _lib.check(_lib.lib().hodlr_unpack_leaf(self._h, i, D.ctypes.data))
+        return D
+
+    def close(self):
+        self._finalizer()
+
+
+_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_CACHE_LOCK = threading.Lock()
+
+
+def operator_for(H, device: int | None = None) -> HodlrOperator:
+    """The cached device operator of H (packed on first use)."""
+    with _CACHE_LOCK:
+        op = _CACHE.get(H)
+        if op is None or (device is not None and op.device != device):
+            op = HodlrOperator(H, device)
+            _CACHE[H] = op
+        return op
+
+
+def matvec(H, x, working=None):
+    """Drop-in for the reference's ``linops.matvec(H, x, working)``.
+
+    Host input (numpy / sequence) -> binary64 numpy result of the same shape;
+    CUDA tensor input -> CUDA tensor result in the working dtype.
+    """
+    _working_code(H, working)  # NotImplementedError before any packing
+    try:
+        import torch
+
+        if isinstance(x, torch.Tensor) and x.is_cuda:
+            return operator_for(H, x.device.index).matvec(x, working)
+    except ImportError:  # pragma: no cover - torch is in the image
+        pass
+    xa = np.asarray(x, dtype=np.float64)
+    if xa.ndim == 0 or xa.shape[0] != H.n:
+        raise ValueError(f"length mismatch: x has {xa.shape[0] if xa.ndim else 0} entries, H is {H.n}")
+    return operator_for(H).matvec_host(xa, working)
