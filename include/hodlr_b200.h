@@ -104,8 +104,10 @@ hodlr_status hodlr_workspace_size(const hodlr_handle* h, int64_t s, size_t* byte
  * (HODLR_FMT_FP64 -> double, HODLR_FMT_FP32 -> float).  Stream-ordered: no host
  * synchronisation, no allocation.  ws may be NULL (the handle's own workspace is
  * used; then calls on one handle must not overlap) or a caller buffer of
- * hodlr_workspace_size bytes (then concurrent calls with distinct ws are safe,
- * SPEC.md:403-404).  Sharded handles: see hodlr_matvec_shard_* below. */
+ * hodlr_workspace_size bytes, zero-filled once before its first use and not
+ * modified by the caller afterwards (the fused kernel keeps its per-call
+ * synchronisation state there); concurrent calls with distinct ws are safe
+ * (SPEC.md:403-404).  Sharded handles: see hodlr_matvec_shard_* below. */
 hodlr_status hodlr_matvec(hodlr_handle* h, int32_t working, const void* x, int64_t ldx,
                           void* b, int64_t ldb, int64_t s, void* ws, size_t ws_bytes,
                           void* stream);

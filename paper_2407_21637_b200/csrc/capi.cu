@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -440,16 +441,22 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
     v.t_count = h->t_count;
     v.ext_count = h->ext_count;
 
-    hodlr_status st = sv_prepare(h->nodes, h->chunks, h->leaves, h->chunk_nodes, nlev, h->sv, &h->sv_ok);
-    if (st != HODLR_OK) return cleanup(st);
+    const char* no_sv = getenv("HODLR_B200_DISABLE_FUSED");
+    if (!(no_sv && no_sv[0] == '1')) {
+        hodlr_status st = sv_prepare(h->nodes, h->chunks, h->leaves, h->chunk_nodes, nlev, h->sv, &h->sv_ok);
+        if (st != HODLR_OK) return cleanup(st);
+    }
     *out = h;
     return HODLR_OK;
 }
 
+// Workspace: [fused-path sync state (fixed offset 0, must start zeroed)]
+//            [partials: part_count*s][coefficients: t_count*s]
 template <typename W>
 size_t ws_bytes_for(const hodlr_handle* h, int64_t s) {
-    return (size_t)round_up((h->part_count * s) * sizeof(W), kAlign) +
-           (size_t)round_up((h->t_count * s) * sizeof(W), kAlign) + sv_extra_ws(h->sv, s);
+    return (size_t)round_up((int64_t)sv_extra_ws(h->sv, s), kAlign) +
+           (size_t)round_up((h->part_count * s) * sizeof(W), kAlign) +
+           (size_t)round_up((h->t_count * s) * sizeof(W), kAlign);
 }
 
 int working_bytes(int working) { return working == HODLR_FMT_FP64 ? 8 : working == HODLR_FMT_FP32 ? 4 : 0; }
@@ -457,11 +464,11 @@ int working_bytes(int working) { return working == HODLR_FMT_FP64 ? 8 : working 
 template <typename W>
 void carve(const hodlr_handle* h, int64_t s, void* ws, W** partial, W** tbuf, void** extra) {
     uint8_t* p = (uint8_t*)ws;
+    *extra = p;
+    p += round_up((int64_t)sv_extra_ws(h->sv, s), kAlign);
     *partial = (W*)p;
     p += round_up((h->part_count * s) * sizeof(W), kAlign);
     *tbuf = (W*)p;
-    p += round_up((h->t_count * s) * sizeof(W), kAlign);
-    *extra = p;
 }
 
 hodlr_status check_working(int working) {
@@ -478,8 +485,11 @@ hodlr_status resolve_ws(hodlr_handle* h, int working, int64_t s, void** ws, size
         if (ws_bytes < need) return fail(HODLR_ERR_INVALID, "workspace too small");
         return HODLR_OK;
     }
-    cudaError_t e = h->ws.ensure(std::max<size_t>(need, kAlign));
-    if (e != cudaSuccess) return fail(HODLR_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
+    if (h->ws.bytes < need) {
+        cudaError_t e = h->ws.ensure(std::max<size_t>(need, kAlign));
+        if (e == cudaSuccess) e = cudaMemset(h->ws.p, 0, h->ws.bytes);
+        if (e != cudaSuccess) return fail(HODLR_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
+    }
     *ws = h->ws.p;
     return HODLR_OK;
 }
