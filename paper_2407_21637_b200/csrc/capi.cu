@@ -443,7 +443,9 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
 
     const char* no_sv = getenv("HODLR_B200_DISABLE_FUSED");
     if (!(no_sv && no_sv[0] == '1')) {
-        hodlr_status st = sv_prepare(h->nodes, h->chunks, h->leaves, h->chunk_nodes, nlev, h->sv, &h->sv_ok);
+        SvInput si{&h->nodes, &h->chunks, &h->leaves, &h->chunk_nodes, nlev, (const uint8_t*)h->arena.p,
+                   h->arena_bytes};
+        hodlr_status st = sv_prepare(si, h->sv, &h->sv_ok);
         if (st != HODLR_OK) return cleanup(st);
     }
     *out = h;

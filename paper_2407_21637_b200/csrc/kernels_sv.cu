@@ -1,26 +1,40 @@
-// Single-vector (s = 1) fast path: ONE persistent cooperative kernel per matvec.
+// Single-vector (s = 1) streaming fast path: ONE persistent kernel per matvec.
 //
-// Work list (dynamic, one atomic queue):
-//   items [0, A)    phase A, one per leaf-chunk of M rows: partial V'^T x of every
-//                   level's V' column restricted to the chunk (16-byte loads of the
-//                   narrow factor, in-register up-conversion, warp-shuffle reduce);
-//                   the last chunk of a node to finish reduces the node's partials
-//                   in chunk order (deterministic) into t and publishes a flag.
-//   items [A, A+B)  phase B, one per RB-row block of a leaf: y = D x first (no
-//                   dependency; 16-byte loads of the dense leaf), then wait for the
-//                   t of every ancestor level (flags), then
-//                   b = sum_k U_k t_{k,sib} + y, written once (rows are disjoint: no
-//                   atomics on b).
-// Phase-A items are handed out before any phase-B item and never wait, so with all
-// CTAs co-resident (cooperative launch) the flag waits always make progress.  The
-// leaf product of the first phase-B items hides the reduction latency, so the
-// grid-wide dependency of Alg. 3's level-1 inner product costs no barrier.
-// Per-call state (queue, counters, flags, epoch) lives in the zero-initialised
-// workspace; the last CTA to finish resets it and bumps the epoch.
-#include <cooperative_groups.h>
+// Layout ("leaf slab", built from the quantised level-batched arena at create
+// time): leaf L owns one contiguous region
+//     [ V' columns of every level restricted to the leaf's M rows,
+//       grouped by storage format (q52, bf16, fp16, fp32, fp64), column-major ]
+//     [ U rows of every level, grouped by format, row-major (M x ncols_g) ]
+//     [ dense leaf D, M x M row-major, working format ]
+// so every unit of work is a handful of contiguous byte ranges.
+//
+// Kernel: 1 producer warp + 8 consumer warps per CTA, one CTA per SM
+// (cooperative launch), a ring of kNS shared-memory stages guarded by
+// mbarriers.  The producer pulls work items from one global atomic queue and
+// streams them with cp.async.bulk (TMA bulk copies, complete_tx on the stage's
+// "full" mbarrier); consumers compute from shared memory and release the stage.
+//   item < A        phase A (leaf L): pieces of <= kStage bytes of V' columns
+//                   (+ x_L): partial V'^T x per column -> partial buffer.  After
+//                   the last piece the CTA bumps the counters of the leaf's l
+//                   ancestor nodes; the last leaf of a node reduces the node's
+//                   partials in leaf order (deterministic) into t and publishes
+//                   the node flag (release).
+//   item >= A       phase B (leaf L, RBI rows): D pieces first (y = D x, written
+//                   to b), then a U piece once the t of every ancestor level is
+//                   published: the producer bulk-copies the l coefficient
+//                   vectors next to the U rows; consumers form
+//                   b = U t + y  (rows disjoint -> no atomics on b).
+// U pieces wait in a small producer-side FIFO while their flags are not yet
+// set, so the level-1 grid-wide dependency of Alg. 3 never idles the memory
+// pipe: D pieces of later items keep streaming.  All phase-A items precede all
+// phase-B items in the queue and never wait, so progress is guaranteed with all
+// CTAs co-resident.  Per-call state (queue, counters, flags, epoch) lives in
+// the zero-initialised workspace; the last CTA resets it and bumps the epoch.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "sv.h"
@@ -29,31 +43,56 @@ namespace hodlr {
 
 namespace {
 
-constexpr int kM = 256;        // rows per phase-A chunk (= leaf size of the fast path)
-constexpr int kRB = 32;        // rows per phase-B item
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kM = 256;                 // leaf rows
+constexpr int kNS = 6;                  // ring stages
+constexpr int kStage = 34 * 1024;       // bytes per stage
+constexpr int kConsumers = 8;           // consumer warps
+constexpr int kThreads = 32 * (kConsumers + 1);
 constexpr int kMaxLev = 24;
+constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
+constexpr int kFifo = 32;               // deferred U pieces per CTA
+constexpr int kXB = kM * 8;             // bytes reserved for x_L in a stage
+
+enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_END = 4 };
+
+struct Level {
+    int32_t r, fmt;
+    int32_t col;        // first column of this level inside its format group
+    int32_t slot;       // coefficient slot (elements) inside a U piece
+    int64_t pbase;      // partial buffer base of the level's nodes
+    int64_t tbase;      // coefficient buffer base
+    int32_t tstride;    // padded coefficients per node (multiple of 4)
+    int32_t pad;
+};
+
+struct APiece {
+    int32_t g, col, ncols, pad;
+};
+
+struct SvParams {
+    int32_t depth, nleaves, nnodes;
+    int32_t rbi, rbd, dpieces, napieces;
+    int32_t num_a, num_b;
+    int32_t leaf_fmt;
+    int64_t slab_bytes, us_off, d_off;
+    int32_t gcols[5];              // columns per format group
+    int64_t vgoff[5], ugoff[5];    // byte offsets of the groups inside the V' / U slabs
+    int32_t coef_elems;            // padded coefficient elements per U piece
+    int32_t bitset_words;
+    Level lev[kMaxLev];
+    APiece ap[kMaxPieces];
+    int8_t col_level[512];         // flattened (group, column) -> level (0-based)
+    int16_t col_c[512];            //                            -> rank column
+    int16_t gstart[6];
+};
 
 struct SvSync {
     unsigned epoch, queue, done, pad;
 };
 
-struct SvDev {
-    int32_t* sib;  // [nnodes] node whose t the U of this node consumes
-};
-
-template <typename W>
-struct SvArgs {
-    const W* x;
-    W* b;
-    W* partial;
-    W* tbuf;
-    SvSync* sync;
-    unsigned* counters;  // [nnodes]
-    unsigned* flags;     // [nnodes]
-    const int32_t* sib;
-    int num_a, num_b, items_per_leaf;
+struct PieceHdr {
+    int32_t type, leaf, r0, rows;
+    int32_t g, col, ncols, last;
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -64,20 +103,46 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-
-// 16-byte streaming load (read-once data: do not pollute L1).
-__device__ __forceinline__ uint4 ldg_stream(const void* p) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
-    return v;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
 }
 
-// Unpack a 16-byte vector of format FMT into E = 16/bytes(FMT) values and
-// accumulate dot with xs[0..E).
+__host__ __device__ __forceinline__ int fmt_sz(int f) {
+    return f == HODLR_FMT_Q52 ? 1 : f == HODLR_FMT_FP32 ? 4 : f == HODLR_FMT_FP64 ? 8 : 2;
+}
+
+// ---------------------------------------------------------------- decode + dot
 template <int FMT, typename W>
-__device__ __forceinline__ W dot16_word(uint32_t w, const W* xs, W acc) {
+__device__ __forceinline__ W dot_word(uint32_t w, const W* xs, W acc) {
     if constexpr (FMT == HODLR_FMT_FP32) {
         acc = fma((W)__uint_as_float(w), xs[0], acc);
     } else if constexpr (FMT == HODLR_FMT_BF16) {
@@ -90,7 +155,7 @@ __device__ __forceinline__ W dot16_word(uint32_t w, const W* xs, W acc) {
         float2 f = __half22float2(__half2(r));
         acc = fma((W)f.x, xs[0], acc);
         acc = fma((W)f.y, xs[1], acc);
-    } else {  // q52 (e5m2): byte b -> binary16 bits b << 8
+    } else {  // q52 = e5m2: byte b is the binary16 with bits b << 8
         __half2_raw lo, hi;
         lo.x = (unsigned short)((w << 8) & 0xff00);
         lo.y = (unsigned short)(w & 0xff00);
@@ -112,8 +177,7 @@ __device__ __forceinline__ W dot_f64(uint32_t lo, uint32_t hi, W xv, W acc) {
     else return acc + __double2float_rn(d * (double)xv);
 }
 
-// Unpack a 16-byte vector of format FMT into E = 16/bytes(FMT) values and
-// accumulate their dot product with xs[0..E).
+// 16 bytes of format FMT (E = 16/size values) dotted with xs[0..E).
 template <int FMT, typename W>
 __device__ __forceinline__ W dot16(const uint4& v, const W* xs, W acc) {
     if constexpr (FMT == HODLR_FMT_FP64) {
@@ -121,364 +185,619 @@ __device__ __forceinline__ W dot16(const uint4& v, const W* xs, W acc) {
         acc = dot_f64<W>(v.z, v.w, xs[1], acc);
     } else {
         constexpr int PW = FMT == HODLR_FMT_FP32 ? 1 : FMT == HODLR_FMT_Q52 ? 4 : 2;
-        acc = dot16_word<FMT, W>(v.x, xs + 0 * PW, acc);
-        acc = dot16_word<FMT, W>(v.y, xs + 1 * PW, acc);
-        acc = dot16_word<FMT, W>(v.z, xs + 2 * PW, acc);
-        acc = dot16_word<FMT, W>(v.w, xs + 3 * PW, acc);
+        acc = dot_word<FMT, W>(v.x, xs + 0 * PW, acc);
+        acc = dot_word<FMT, W>(v.y, xs + 1 * PW, acc);
+        acc = dot_word<FMT, W>(v.z, xs + 2 * PW, acc);
+        acc = dot_word<FMT, W>(v.w, xs + 3 * PW, acc);
     }
     return acc;
 }
 
-// Up to 4 columns (same node => same format) dotted with the chunk's x over kM
-// rows: all loads of the group are issued before the math.
+template <int FMT>
+struct FmtInfo {
+    static constexpr int bytes =
+        FMT == HODLR_FMT_Q52 ? 1 : FMT == HODLR_FMT_FP32 ? 4 : FMT == HODLR_FMT_FP64 ? 8 : 2;
+    static constexpr int E = 16 / bytes;  // values per 16-byte vector
+    static constexpr int NV = kM / E;     // vectors per M-row column
+    static constexpr int PER = NV >= 32 ? NV / 32 : 1;
+};
+
+// Phase A: warp-cooperative dot products of `ncols` M-row columns (shared
+// memory) with the stage's x; lane owns the 16-byte vectors lane + 32 i.
 template <int FMT, typename W>
-__device__ __forceinline__ void dot_cols(const uint8_t* col0, int64_t cstride, int ncols,
-                                         const W* xs, int lane, W out[4]) {
-    constexpr int E = 16 / (FMT == HODLR_FMT_FP64 ? 8 : FMT == HODLR_FMT_FP32 ? 4
-                            : FMT == HODLR_FMT_Q52 ? 1 : 2);
-    constexpr int NV = kM / E;                   // 16-byte vectors per column
-    constexpr int PER = NV >= 32 ? NV / 32 : 1;  // per lane
-    const bool active = NV >= 32 || lane < NV;
-    uint4 v[4][PER];
+__device__ __forceinline__ void a_piece_cols(const uint8_t* cols, int ncols, const W* xs, int warp, int lane,
+                                             const SvParams& P, int leaf, int g, int col0, W* partial) {
+    using F = FmtInfo<FMT>;
+    const bool active = F::NV >= 32 || lane < F::NV;
+    W xr[F::PER][F::E];
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int i = 0; i < F::PER; ++i)
 #pragma unroll
-        for (int i = 0; i < PER; ++i)
-            if (c < ncols && active) v[c][i] = ldg_stream(col0 + c * cstride + (int64_t)(lane + 32 * i) * 16);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
+        for (int e = 0; e < F::E; ++e) xr[i][e] = active ? xs[(lane + 32 * i) * F::E + e] : W(0);
+    for (int j = warp; j < ncols; j += kConsumers) {
+        const uint8_t* col = cols + (size_t)j * kM * F::bytes;
         W acc = W(0);
-        if (c < ncols && active) {
+        if (active) {
 #pragma unroll
-            for (int i = 0; i < PER; ++i) acc = dot16<FMT, W>(v[c][i], xs + (lane + 32 * i) * E, acc);
+            for (int i = 0; i < F::PER; ++i) {
+                uint4 v = *reinterpret_cast<const uint4*>(col + (lane + 32 * i) * 16);
+                acc = dot16<FMT, W>(v, xr[i], acc);
+            }
         }
-        out[c] = acc;
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            const int flat = P.gstart[g] + col0 + j;
+            const int k = P.col_level[flat];
+            const int c = P.col_c[flat];
+            const Level& L = P.lev[k];
+            const int sh = P.depth - (k + 1);
+            const int jn = leaf >> sh;
+            const int nch = 1 << sh;
+            partial[L.pbase + ((int64_t)jn * L.r + c) * nch + (leaf - (jn << sh))] = acc;
+        }
     }
 }
 
 template <typename W>
-__device__ __forceinline__ void dot_cols_any(int fmt, const uint8_t* col0, int64_t cstride, int ncols,
-                                             const W* xs, int lane, W out[4]) {
+__device__ __forceinline__ void a_piece(int fmt, const uint8_t* cols, int ncols, const W* xs, int warp, int lane,
+                                        const SvParams& P, int leaf, int col0, W* partial) {
     switch (fmt) {
-        case HODLR_FMT_FP64: dot_cols<HODLR_FMT_FP64, W>(col0, cstride, ncols, xs, lane, out); break;
-        case HODLR_FMT_FP32: dot_cols<HODLR_FMT_FP32, W>(col0, cstride, ncols, xs, lane, out); break;
-        case HODLR_FMT_FP16: dot_cols<HODLR_FMT_FP16, W>(col0, cstride, ncols, xs, lane, out); break;
-        case HODLR_FMT_BF16: dot_cols<HODLR_FMT_BF16, W>(col0, cstride, ncols, xs, lane, out); break;
-        default: dot_cols<HODLR_FMT_Q52, W>(col0, cstride, ncols, xs, lane, out); break;
+        case HODLR_FMT_FP64: a_piece_cols<HODLR_FMT_FP64, W>(cols, ncols, xs, warp, lane, P, leaf, fmt, col0, partial); break;
+        case HODLR_FMT_FP32: a_piece_cols<HODLR_FMT_FP32, W>(cols, ncols, xs, warp, lane, P, leaf, fmt, col0, partial); break;
+        case HODLR_FMT_FP16: a_piece_cols<HODLR_FMT_FP16, W>(cols, ncols, xs, warp, lane, P, leaf, fmt, col0, partial); break;
+        case HODLR_FMT_BF16: a_piece_cols<HODLR_FMT_BF16, W>(cols, ncols, xs, warp, lane, P, leaf, fmt, col0, partial); break;
+        default: a_piece_cols<HODLR_FMT_Q52, W>(cols, ncols, xs, warp, lane, P, leaf, fmt, col0, partial); break;
+    }
+}
+
+// Phase B, leaf part: y = D[rows] x_L (rows of M values, format FMT) -> b.
+template <int FMT, typename W>
+__device__ __forceinline__ void d_piece(const uint8_t* drows, int rows, const W* xs, int warp, int lane, W* b) {
+    using F = FmtInfo<FMT>;
+    W xr[F::PER][F::E];
+#pragma unroll
+    for (int i = 0; i < F::PER; ++i)
+#pragma unroll
+        for (int e = 0; e < F::E; ++e) xr[i][e] = xs[(lane + 32 * i) * F::E + e];
+    for (int r = warp; r < rows; r += kConsumers) {
+        const uint8_t* row = drows + (size_t)r * kM * F::bytes;
+        uint4 v[F::PER];
+#pragma unroll
+        for (int i = 0; i < F::PER; ++i) v[i] = *reinterpret_cast<const uint4*>(row + (lane + 32 * i) * 16);
+        W acc = W(0);
+#pragma unroll
+        for (int i = 0; i < F::PER; ++i) acc = dot16<FMT, W>(v[i], xr[i], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) b[r] = acc;
     }
 }
 
 template <typename W>
-__device__ __forceinline__ W load_elem(int fmt, const uint8_t* col, int i) {
+__device__ __forceinline__ W u_elem(int fmt, const uint8_t* p, int idx) {
     switch (fmt) {
-        case HODLR_FMT_FP64: return (W)__ldg((const double*)col + i);
-        case HODLR_FMT_FP32: return (W)__ldg((const float*)col + i);
-        case HODLR_FMT_FP16: return (W)dec_fp16(__ldg((const unsigned short*)col + i));
-        case HODLR_FMT_BF16: return (W)dec_bf16(__ldg((const unsigned short*)col + i));
-        default: return (W)dec_q52(__ldg(col + i));
+        case HODLR_FMT_FP64: return (W)reinterpret_cast<const double*>(p)[idx];
+        case HODLR_FMT_FP32: return (W)reinterpret_cast<const float*>(p)[idx];
+        case HODLR_FMT_FP16: return (W)dec_fp16(reinterpret_cast<const uint16_t*>(p)[idx]);
+        case HODLR_FMT_BF16: return (W)dec_bf16(reinterpret_cast<const uint16_t*>(p)[idx]);
+        default: return (W)dec_q52(p[idx]);
     }
 }
 
-struct __align__(16) SmemA {
-    int lev_node[kMaxLev];
-    int lev_groups[kMaxLev + 1];  // prefix sums of ceil(rv/4)
-    int last[kMaxLev];
+template <typename W>
+struct SvKernelArgs {
+    const uint8_t* slab;
+    const W* x;
+    W* b;
+    W* partial;
+    W* tbuf;
+    SvSync* sync;
+    unsigned* counters;
+    unsigned* flags;
 };
 
 template <typename W>
-__global__ void __launch_bounds__(kThreads, 1) k_sv_fused(PlanView p, SvArgs<W> a) {
-    __shared__ __align__(16) W xs[kM];
-    __shared__ __align__(16) W ts[512];          // phase-B coefficients (sum of ranks <= 512)
-    __shared__ W red[kWarps][kRB];
-    __shared__ W yrow[kRB];
-    __shared__ SmemA sa;
-    __shared__ int s_item;
-    __shared__ unsigned s_epoch;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nlev = p.nlev;
-    const int total = a.num_a + a.num_b;
+__global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ SvParams P, SvKernelArgs<W> a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* stages = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kNS * kStage);
+    uint64_t* empty = full + kNS;
+    PieceHdr* hdr = reinterpret_cast<PieceHdr*>(empty + kNS);
+    int* misc = reinterpret_cast<int*>(hdr + kNS);  // [0] epoch, [1..kMaxLev] last-arriver flags
+    int* fifo = misc + 64;
+    unsigned* bitset = reinterpret_cast<unsigned*>(fifo + kFifo);
 
-    if (threadIdx.x == 0) s_epoch = ld_acquire(&a.sync->epoch);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int total = P.num_a + P.num_b;
+    const int nlev = P.depth;
+
+    if (threadIdx.x == 0) {
+        misc[0] = (int)ld_acquire(&a.sync->epoch);
+        for (int s = 0; s < kNS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = threadIdx.x; i < P.bitset_words; i += kThreads) bitset[i] = 0u;
     __syncthreads();
-    const unsigned target = s_epoch + 1;
+    const unsigned target = (unsigned)misc[0] + 1u;
 
-    for (;;) {
-        if (threadIdx.x == 0) s_item = (int)atomicAdd(&a.sync->queue, 1u);
-        __syncthreads();
-        const int item = s_item;
-        if (item >= total) break;
-        if (item < a.num_a) {
-            // ------------------------------------------------ phase A
-            const int chunk = item;
-            const ChunkDesc ch = p.chunks[chunk];
-            for (int i = threadIdx.x; i < kM; i += kThreads) xs[i] = a.x[ch.row0 + i];
-            if (threadIdx.x == 0) {
-                int g = 0;
-                for (int lv = 0; lv < nlev; ++lv) {
-                    int id = p.chunk_nodes[chunk * nlev + lv];
-                    sa.lev_node[lv] = id;
-                    sa.lev_groups[lv] = g;
-                    g += (p.nodes[id].rv + 3) >> 2;
-                }
-                sa.lev_groups[nlev] = g;
+    if (warp == 0) {
+        // =========================================================== producer
+        int stage = 0;
+        unsigned phase = 0;
+        int fh = 0, ft = 0;  // deferred-U FIFO head / tail (warp-uniform)
+        auto next_stage = [&]() {
+            if (++stage == kNS) {
+                stage = 0;
+                phase ^= 1u;
             }
-            __syncthreads();
-            const int ngroups = sa.lev_groups[nlev];
-            for (int gi = warp; gi < ngroups; gi += kWarps) {
-                int lv = 0;
-                while (sa.lev_groups[lv + 1] <= gi) ++lv;
-                const NodeDesc& nd = p.nodes[sa.lev_node[lv]];
-                const int c0 = (gi - sa.lev_groups[lv]) * 4;
-                const int nc = min(4, nd.rv - c0);
-                const int64_t cstride = (int64_t)nd.v_ld * fmt_bytes(nd.v_fmt);
-                const uint8_t* col0 = p.arena + nd.v_off + c0 * cstride +
-                                      (int64_t)(ch.row0 - nd.row0) * fmt_bytes(nd.v_fmt);
-                W out[4];
-                dot_cols_any<W>(nd.v_fmt, col0, cstride, nc, xs, lane, out);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) out[c] = warp_sum(out[c]);
-                if (lane < nc) {
-                    W v = lane == 0 ? out[0] : lane == 1 ? out[1] : lane == 2 ? out[2] : out[3];
-                    a.partial[nd.part_off + (int64_t)(c0 + lane) * nd.nchunk + (chunk - nd.chunk0)] = v;
-                }
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                __threadfence();
-                for (int lv = 0; lv < nlev; ++lv) {
-                    const int id = sa.lev_node[lv];
-                    const NodeDesc& nd = p.nodes[id];
-                    unsigned old = atomicAdd(&a.counters[id], 1u);
-                    sa.last[lv] = (old == (unsigned)nd.nchunk - 1) ? 1 : 0;
-                }
-                __threadfence();
-            }
-            __syncthreads();
-            // last arriver of a node: fixed-order reduction over its chunks
-            for (int lv = 0; lv < nlev; ++lv) {
-                if (!sa.last[lv]) continue;
-                const int id = sa.lev_node[lv];
-                const NodeDesc& nd = p.nodes[id];
-                for (int c = warp; c < nd.rv; c += kWarps) {
-                    const W* src = a.partial + nd.part_off + (int64_t)c * nd.nchunk;
-                    // lane-strided in chunk order, then a fixed shuffle tree
-                    W acc = W(0);
-                    for (int j = lane; j < nd.nchunk; j += 32) acc += __ldcg(src + j);
-                    acc = warp_sum(acc);
-                    if (lane == 0) a.tbuf[nd.t_off + c] = acc;
-                }
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    a.counters[id] = 0;
-                    __threadfence();
-                    st_release(&a.flags[id], target);
-                }
-            }
-        } else {
-            // ------------------------------------------------ phase B
-            const int j = item - a.num_a;
-            const int leaf = j / a.items_per_leaf;
-            const int r0 = (j % a.items_per_leaf) * kRB;  // row offset inside the leaf
-            const LeafDesc lf = p.leaves[leaf];
-            for (int i = threadIdx.x; i < kM; i += kThreads) xs[i] = a.x[lf.row0 + i];
-            __syncthreads();
-            // y = D[r0:r0+RB, :] x_leaf  (warp: RB/kWarps rows; 16-B vectors)
-            {
-                constexpr int RPW = kRB / kWarps;
-                const int wb = fmt_bytes(lf.fmt);
-                const uint8_t* d0 = p.arena + lf.off + (int64_t)(r0 + warp * RPW) * lf.ld * wb;
-                const int64_t rstride = (int64_t)lf.ld * wb;
-                W acc[RPW];
-                if (lf.fmt == HODLR_FMT_FP64) {
-                    constexpr int PER = kM / 2 / 32;
-                    uint4 v[RPW][PER];
-#pragma unroll
-                    for (int r = 0; r < RPW; ++r)
-#pragma unroll
-                        for (int i = 0; i < PER; ++i) v[r][i] = ldg_stream(d0 + r * rstride + (lane + 32 * i) * 16);
-#pragma unroll
-                    for (int r = 0; r < RPW; ++r) {
-                        W s = W(0);
-#pragma unroll
-                        for (int i = 0; i < PER; ++i) s = dot16<HODLR_FMT_FP64, W>(v[r][i], xs + (lane + 32 * i) * 2, s);
-                        acc[r] = s;
+        };
+        auto claim = [&]() -> uint8_t* {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            return stages + (size_t)stage * kStage;
+        };
+        // are the coefficients of every level of `leaf` published?
+        auto ready = [&](int leaf) -> bool {
+            bool ok = true;
+            if (lane < nlev) {
+                const int k = lane + 1;
+                const int sib = (1 << k) - 2 + ((leaf >> (nlev - k)) ^ 1);
+                const bool cached = P.bitset_words ? ((bitset[sib >> 5] >> (sib & 31)) & 1u) : false;
+                if (!cached) {
+                    if (ld_acquire(&a.flags[sib]) == target) {
+                        if (P.bitset_words) atomicOr(&bitset[sib >> 5], 1u << (sib & 31));
+                    } else {
+                        ok = false;
                     }
+                }
+            }
+            return __all_sync(0xffffffffu, ok);
+        };
+        auto emit_u = [&](int leaf, int r0) {
+            uint8_t* st = claim();
+            const int wbytes = (int)sizeof(W);
+            const int coef_bytes = P.coef_elems * wbytes;
+            unsigned bytes = (unsigned)coef_bytes;
+            for (int l = 0; l < nlev; ++l)
+                if (P.lev[l].r == 0) bytes -= (unsigned)(P.lev[l].tstride * wbytes);
+            for (int g = 0; g < 5; ++g) bytes += (unsigned)(P.rbi * P.gcols[g] * fmt_sz(g));
+            if (lane == 0) {
+                PieceHdr& h = hdr[stage];
+                h.type = PT_U;
+                h.leaf = leaf;
+                h.r0 = r0;
+                h.rows = P.rbi;
+                mbar_arrive_tx(&full[stage], bytes);
+            }
+            __syncwarp();
+            // coefficients were written by other SMs (generic proxy, release/acquire
+            // on the flag); order them before this SM's async-proxy reads
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            if (lane < nlev) {
+                const Level& L = P.lev[lane];
+                if (L.r > 0) {
+                    const int k = lane + 1;
+                    const int jsib = (leaf >> (nlev - k)) ^ 1;
+                    const W* src = a.tbuf + L.tbase + (int64_t)jsib * L.tstride;
+                    bulk_g2s(st + (size_t)L.slot * wbytes, src, (unsigned)(L.tstride * wbytes), &full[stage]);
+                }
+            } else if (lane >= 24 && lane < 29) {
+                const int g = lane - 24;
+                if (P.gcols[g] > 0) {
+                    const uint8_t* src = a.slab + (int64_t)leaf * P.slab_bytes + P.us_off + P.ugoff[g] +
+                                         (int64_t)r0 * P.gcols[g] * fmt_sz(g);
+                    int off = coef_bytes;
+                    for (int q = 0; q < g; ++q) off += P.rbi * P.gcols[q] * fmt_sz(q);
+                    bulk_g2s(st + off, src, (unsigned)(P.rbi * P.gcols[g] * fmt_sz(g)), &full[stage]);
+                }
+            }
+            __syncwarp();
+            next_stage();
+        };
+        auto flush_fifo = [&](bool block) {
+            while (fh != ft) {
+                const int e = fifo[fh % kFifo];
+                const int leaf = e >> 12, r0 = e & 0xfff;
+                if (!ready(leaf)) {
+                    if (!block) return;
+                    __nanosleep(256);
+                    continue;
+                }
+                emit_u(leaf, r0);
+                ++fh;
+            }
+        };
+
+        int item = 0;
+        if (lane == 0) item = (int)atomicAdd(&a.sync->queue, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        while (item < total) {
+            int nxt = 0;
+            if (lane == 0) nxt = (int)atomicAdd(&a.sync->queue, 1u);  // consumed next round
+            if (item < P.num_a) {
+                const int leaf = item;
+                const uint8_t* base = a.slab + (int64_t)leaf * P.slab_bytes;
+                for (int p = 0; p < P.napieces; ++p) {
+                    const APiece ap = P.ap[p];
+                    uint8_t* st = claim();
+                    const unsigned cb = (unsigned)(ap.ncols * kM * fmt_sz(ap.g));
+                    if (lane == 0) {
+                        PieceHdr& h = hdr[stage];
+                        h.type = PT_A;
+                        h.leaf = leaf;
+                        h.g = ap.g;
+                        h.col = ap.col;
+                        h.ncols = ap.ncols;
+                        h.last = (p == P.napieces - 1);
+                        mbar_arrive_tx(&full[stage], (unsigned)(kM * sizeof(W)) + cb);
+                        bulk_g2s(st, a.x + (int64_t)leaf * kM, (unsigned)(kM * sizeof(W)), &full[stage]);
+                        bulk_g2s(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.col * kM * fmt_sz(ap.g), cb,
+                                 &full[stage]);
+                    }
+                    __syncwarp();
+                    next_stage();
+                }
+            } else {
+                const int bi = item - P.num_a;
+                const int per_leaf = kM / P.rbi;
+                const int leaf = bi / per_leaf;
+                const int r0 = (bi % per_leaf) * P.rbi;
+                const uint8_t* dbase = a.slab + (int64_t)leaf * P.slab_bytes + P.d_off;
+                const int dsz = fmt_sz(P.leaf_fmt);
+                for (int p = 0; p < P.dpieces; ++p) {
+                    uint8_t* st = claim();
+                    const int rr = r0 + p * P.rbd;
+                    const unsigned cb = (unsigned)(P.rbd * kM * dsz);
+                    if (lane == 0) {
+                        PieceHdr& h = hdr[stage];
+                        h.type = PT_D;
+                        h.leaf = leaf;
+                        h.r0 = rr;
+                        h.rows = P.rbd;
+                        mbar_arrive_tx(&full[stage], (unsigned)(kM * sizeof(W)) + cb);
+                        bulk_g2s(st, a.x + (int64_t)leaf * kM, (unsigned)(kM * sizeof(W)), &full[stage]);
+                        bulk_g2s(st + kXB, dbase + (int64_t)rr * kM * dsz, cb, &full[stage]);
+                    }
+                    __syncwarp();
+                    next_stage();
+                }
+                if (nlev == 0) {
+                    // depth 0: no coefficients, b = D x already written
                 } else {
-                    constexpr int PER = kM / 4 / 32;
-                    uint4 v[RPW][PER];
-#pragma unroll
-                    for (int r = 0; r < RPW; ++r)
-#pragma unroll
-                        for (int i = 0; i < PER; ++i) v[r][i] = ldg_stream(d0 + r * rstride + (lane + 32 * i) * 16);
-#pragma unroll
-                    for (int r = 0; r < RPW; ++r) {
-                        W s = W(0);
-#pragma unroll
-                        for (int i = 0; i < PER; ++i) s = dot16<HODLR_FMT_FP32, W>(v[r][i], xs + (lane + 32 * i) * 4, s);
-                        acc[r] = s;
-                    }
-                }
-#pragma unroll
-                for (int r = 0; r < RPW; ++r) {
-                    W s = warp_sum(acc[r]);
-                    if (lane == 0) yrow[warp * RPW + r] = s;
+                    if (ft - fh == kFifo) flush_fifo(true);
+                    if (lane == 0) fifo[ft % kFifo] = (leaf << 12) | r0;
+                    __syncwarp();
+                    ++ft;
+                    flush_fifo(false);
                 }
             }
-            // wait for the coefficients of every level, stage them in smem
-            if (threadIdx.x == 0) {
-                const int chunk = leaf;  // one chunk per leaf on this path
-                int off = 0;
-                for (int lv = 0; lv < nlev; ++lv) {
-                    const int id = p.chunk_nodes[chunk * nlev + lv];
-                    const int src = a.sib[id];
-                    sa.lev_node[lv] = id;
-                    sa.lev_groups[lv] = off;
-                    off += p.nodes[id].ru;
-                    if (ld_acquire(&a.flags[src]) != target) {
-                        unsigned ns = 32;
-                        while (ld_acquire(&a.flags[src]) != target) {
-                            __nanosleep(ns);
-                            ns = min(ns * 2, 256u);
-                        }
-                    }
-                }
-                sa.lev_groups[nlev] = off;
-            }
-            __syncthreads();
-            const int ncoef = sa.lev_groups[nlev];
-            for (int i = threadIdx.x; i < ncoef; i += kThreads) {
-                int lv = 0;
-                while (sa.lev_groups[lv + 1] <= i) ++lv;
-                const NodeDesc& nd = p.nodes[sa.lev_node[lv]];
-                ts[i] = __ldcg(a.tbuf + nd.tsrc_off + (i - sa.lev_groups[lv]));
-            }
-            __syncthreads();
-            // U part: warp w takes coefficients w, w+8, ...; lane = row
-            {
+            item = __shfl_sync(0xffffffffu, nxt, 0);
+        }
+        flush_fifo(true);
+        claim();
+        if (lane == 0) {
+            hdr[stage].type = PT_END;
+            mbar_arrive(&full[stage]);
+        }
+        __syncwarp();
+    } else {
+        // =========================================================== consumers
+        const int cw = warp - 1;
+        const int ctid = threadIdx.x - 32;
+        int stage = 0;
+        unsigned phase = 0;
+        for (;;) {
+            mbar_wait(&full[stage], phase);
+            const PieceHdr h = hdr[stage];
+            const uint8_t* st = stages + (size_t)stage * kStage;
+            if (h.type == PT_END) break;
+            if (h.type == PT_A) {
+                a_piece<W>(h.g, st + kXB, h.ncols, reinterpret_cast<const W*>(st), cw, lane, P, h.leaf, h.col,
+                           a.partial);
+            } else if (h.type == PT_D) {
+                W* brow = a.b + (int64_t)h.leaf * kM + h.r0;
+                const W* xs = reinterpret_cast<const W*>(st);
+                if (P.leaf_fmt == HODLR_FMT_FP64) d_piece<HODLR_FMT_FP64, W>(st + kXB, h.rows, xs, cw, lane, brow);
+                else d_piece<HODLR_FMT_FP32, W>(st + kXB, h.rows, xs, cw, lane, brow);
+            } else {  // PT_U
+                consumer_sync();  // the D pieces of these rows were written by other warps
+                const W* coef = reinterpret_cast<const W*>(st);
+                const int tpr = kConsumers * 32 / h.rows;
+                const int row = ctid / tpr, q = ctid % tpr;
                 W acc = W(0);
-                const int row_in_leaf = r0 + lane;
-                for (int i = warp; i < ncoef; i += kWarps) {
-                    int lv = 0;
-                    while (sa.lev_groups[lv + 1] <= i) ++lv;
-                    const NodeDesc& nd = p.nodes[sa.lev_node[lv]];
-                    const int c = i - sa.lev_groups[lv];
-                    const int64_t cstride = (int64_t)nd.u_ld * fmt_bytes(nd.u_fmt);
-                    const uint8_t* col = p.arena + nd.u_off + c * cstride;
-                    const int r = lf.row0 + row_in_leaf - nd.row0;
-                    acc = fma(load_elem<W>(nd.u_fmt, col, r), ts[i], acc);
+                int off = P.coef_elems * (int)sizeof(W);
+                for (int g = 0; g < 5; ++g) {
+                    const int nc = P.gcols[g];
+                    if (nc == 0) continue;
+                    const uint8_t* ub = st + off + (size_t)row * nc * fmt_sz(g);
+                    for (int j = q; j < nc; j += tpr) {
+                        const int flat = P.gstart[g] + j;
+                        const Level& L = P.lev[P.col_level[flat]];
+                        acc = fma(u_elem<W>(g, ub, j), coef[L.slot + P.col_c[flat]], acc);
+                    }
+                    off += h.rows * nc * fmt_sz(g);
                 }
-                red[warp][lane] = acc;
+                for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (q == 0) {
+                    W* bp = a.b + (int64_t)h.leaf * kM + h.r0 + row;
+                    *bp = acc + *bp;
+                }
             }
-            __syncthreads();
-            if (warp == 0) {
-                W s = W(0);
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) s += red[w][lane];
-                a.b[lf.row0 + r0 + lane] = s + yrow[lane];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (h.type == PT_A && h.last) {
+                // every partial of this leaf is written -> count it into its l nodes
+                consumer_sync();
+                if (ctid == 0) {
+                    __threadfence();
+                    for (int lv = 0; lv < nlev; ++lv) {
+                        const int k = lv + 1;
+                        const int sh = nlev - k;
+                        const int id = (1 << k) - 2 + (h.leaf >> sh);
+                        const unsigned old = atomicAdd(&a.counters[id], 1u);
+                        misc[1 + lv] = (old == (1u << sh) - 1u) ? 1 : 0;
+                    }
+                    __threadfence();
+                }
+                consumer_sync();
+                for (int lv = 0; lv < nlev; ++lv) {
+                    if (!misc[1 + lv]) continue;
+                    const int k = lv + 1;
+                    const int sh = nlev - k;
+                    const int jn = h.leaf >> sh;
+                    const int nch = 1 << sh;
+                    const Level& L = P.lev[lv];
+                    for (int c = cw; c < L.r; c += kConsumers) {
+                        const W* src = a.partial + L.pbase + ((int64_t)jn * L.r + c) * nch;
+                        W acc = W(0);
+                        for (int i = lane; i < nch; i += 32) acc += __ldcg(src + i);
+                        acc = warp_sum(acc);
+                        if (lane == 0) a.tbuf[L.tbase + (int64_t)jn * L.tstride + c] = acc;
+                    }
+                    consumer_sync();
+                    if (ctid == 0) {
+                        const int id = (1 << k) - 2 + jn;
+                        a.counters[id] = 0u;
+                        __threadfence();
+                        st_release(&a.flags[id], target);
+                    }
+                }
+            }
+            if (++stage == kNS) {
+                stage = 0;
+                phase ^= 1u;
             }
         }
-        __syncthreads();
     }
     // ---- teardown: the last CTA resets the queue and publishes the next epoch
+    __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        unsigned old = atomicAdd(&a.sync->done, 1u);
+        const unsigned old = atomicAdd(&a.sync->done, 1u);
         if (old == gridDim.x - 1) {
-            a.sync->queue = 0;
-            a.sync->done = 0;
+            a.sync->queue = 0u;
+            a.sync->done = 0u;
             __threadfence();
             st_release(&a.sync->epoch, target);
         }
     }
 }
 
+size_t smem_bytes(int bitset_words) {
+    return (size_t)kNS * kStage + 2 * kNS * sizeof(uint64_t) + kNS * sizeof(PieceHdr) +
+           (64 + kFifo) * sizeof(int) + (size_t)bitset_words * 4;
+}
+
 }  // namespace
 
-hodlr_status sv_prepare(const std::vector<NodeDesc>& nodes, const std::vector<ChunkDesc>& chunks,
-                        const std::vector<LeafDesc>& leaves, const std::vector<int32_t>& chunk_nodes,
-                        int nlev, SvPlan& sv, bool* ok) {
+// ============================================================== host side
+hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     sv = SvPlan{};
     *ok = false;
-    if (nlev > kMaxLev || leaves.empty()) return HODLR_OK;
-    for (const LeafDesc& l : leaves)
-        if (l.m != kM || (l.fmt != HODLR_FMT_FP64 && l.fmt != HODLR_FMT_FP32)) return HODLR_OK;
-    if (chunks.size() != leaves.size()) return HODLR_OK;
-    for (const NodeDesc& nd : nodes)
-        if (nd.ext_slot >= 0) return HODLR_OK;
-    // sum of ranks a leaf consumes must fit the shared coefficient buffer
-    std::vector<int32_t> sib(nodes.size(), -1);
-    for (size_t c = 0; c < chunks.size(); ++c) {
-        int tot = 0;
-        for (int lv = 0; lv < nlev; ++lv) tot += nodes[chunk_nodes[c * nlev + lv]].ru;
-        if (tot > 512) return HODLR_OK;
+    const auto& nodes = *in.nodes;
+    const auto& leaves = *in.leaves;
+    const int depth = in.nlev;
+    if (depth < 1 || depth > kMaxLev || leaves.empty()) return HODLR_OK;
+    const int nleaves = (int)leaves.size();
+    if (nleaves != (1 << depth) || (int)in.chunks->size() != nleaves) return HODLR_OK;
+    const int lf = leaves[0].fmt;
+    if (lf != HODLR_FMT_FP64 && lf != HODLR_FMT_FP32) return HODLR_OK;
+    for (int i = 0; i < nleaves; ++i)
+        if (leaves[i].m != kM || leaves[i].row0 != i * kM || leaves[i].fmt != lf || leaves[i].ld != kM)
+            return HODLR_OK;
+    if ((int)nodes.size() != (1 << (depth + 1)) - 2) return HODLR_OK;
+    // uniform rank and format per level, node ids level-major
+    SvParams P;
+    memset(&P, 0, sizeof(P));
+    P.depth = depth;
+    P.nleaves = nleaves;
+    P.nnodes = (int)nodes.size();
+    P.leaf_fmt = lf;
+    for (int k = 1; k <= depth; ++k) {
+        const int base = (1 << k) - 2;
+        const NodeDesc& n0 = nodes[base];
+        for (int j = 0; j < (1 << k); ++j) {
+            const NodeDesc& nd = nodes[base + j];
+            if (nd.level != k || nd.ext_slot >= 0 || nd.rv != n0.rv || nd.ru != n0.rv || nd.u_fmt != n0.u_fmt ||
+                nd.v_fmt != n0.u_fmt || nd.nchunk != (1 << (depth - k)) || nd.row0 != j * (kM << (depth - k)) ||
+                nd.part_off != n0.part_off + (int64_t)j * n0.rv * n0.nchunk)
+                return HODLR_OK;
+        }
+        P.lev[k - 1].r = n0.rv;
+        P.lev[k - 1].fmt = n0.u_fmt;
     }
-    // sibling lookup: node whose t_off equals our tsrc_off
-    for (size_t i = 0; i < nodes.size(); ++i) {
-        for (size_t j = 0; j < nodes.size(); ++j) {
-            if (nodes[j].level == nodes[i].level && nodes[j].t_off == nodes[i].tsrc_off && j != i) {
-                sib[i] = (int32_t)j;
-                break;
+    // column lists per format group (level-major inside a group)
+    int flat = 0;
+    for (int g = 0; g < 5; ++g) {
+        P.gstart[g] = (int16_t)flat;
+        int cnt = 0;
+        for (int k = 0; k < depth; ++k) {
+            if (P.lev[k].fmt != g) continue;
+            P.lev[k].col = cnt;
+            for (int c = 0; c < P.lev[k].r; ++c) {
+                if (flat >= 512) return HODLR_OK;
+                P.col_level[flat] = (int8_t)k;
+                P.col_c[flat] = (int16_t)c;
+                ++flat;
+                ++cnt;
             }
         }
-        if (sib[i] < 0 && nodes[i].ru > 0) return HODLR_OK;
-        if (sib[i] < 0) sib[i] = (int32_t)i;  // rank-0 U: any published flag works
+        P.gcols[g] = cnt;
     }
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return HODLR_OK;
-    int sms = 0, occ = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int coop = 0;
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    if (!coop || sms <= 0) return HODLR_OK;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sv_fused<double>, kThreads, 0) != cudaSuccess ||
-        occ < 1)
+    P.gstart[5] = (int16_t)flat;
+    // coefficient slots and partial / coefficient buffers
+    int slot = 0;
+    int64_t tb = 0;
+    for (int k = 0; k < depth; ++k) {
+        Level& L = P.lev[k];
+        L.tstride = (L.r + 3) / 4 * 4;
+        L.slot = slot;
+        slot += L.tstride;
+        L.pbase = nodes[(1 << (k + 1)) - 2].part_off;
+        L.tbase = tb;
+        tb += (int64_t)L.tstride << (k + 1);
+    }
+    P.coef_elems = slot;
+    // slab geometry
+    int64_t vs = 0, us = 0;
+    for (int g = 0; g < 5; ++g) {
+        P.vgoff[g] = vs;
+        vs += (int64_t)P.gcols[g] * kM * fmt_bytes(g);
+        P.ugoff[g] = us;
+        us += (int64_t)P.gcols[g] * kM * fmt_bytes(g);
+    }
+    const int dsz = fmt_bytes(lf);
+    P.us_off = vs;
+    P.d_off = vs + us;
+    P.slab_bytes = vs + us + (int64_t)kM * kM * dsz;
+    // phase-B geometry: D pieces of rbd rows, items / U pieces of rbi rows
+    P.rbd = 1;
+    while (P.rbd * 2 <= kM && kXB + P.rbd * 2 * kM * dsz <= kStage) P.rbd *= 2;
+    int ubytes_row = 0;
+    for (int g = 0; g < 5; ++g) ubytes_row += P.gcols[g] * fmt_bytes(g);
+    P.rbi = 32;
+    while (P.rbi > 8 && P.coef_elems * 8 + P.rbi * ubytes_row > kStage) P.rbi /= 2;
+    if (P.coef_elems * 8 + P.rbi * ubytes_row > kStage) return HODLR_OK;
+    if (P.rbd > P.rbi) P.rbd = P.rbi;
+    if (P.rbi % P.rbd) return HODLR_OK;
+    for (int g = 0; g < 5; ++g)  // bulk copies: 16-byte granules
+        if ((P.rbi * P.gcols[g] * fmt_bytes(g)) % 16) return HODLR_OK;
+    P.dpieces = P.rbi / P.rbd;
+    // phase-A pieces
+    P.napieces = 0;
+    for (int g = 0; g < 5; ++g) {
+        const int cpp = (kStage - kXB) / (kM * fmt_bytes(g));
+        for (int c = 0; c < P.gcols[g]; c += cpp) {
+            if (P.napieces == kMaxPieces) return HODLR_OK;
+            P.ap[P.napieces++] = APiece{g, c, std::min(cpp, P.gcols[g] - c), 0};
+        }
+    }
+    if (P.napieces == 0) return HODLR_OK;  // all ranks zero: generic path
+    P.num_a = nleaves;
+    P.num_b = nleaves * (kM / P.rbi);
+    P.bitset_words = (P.nnodes + 31) / 32;
+    if (smem_bytes(P.bitset_words) > 227 * 1024) P.bitset_words = 0;
+
+    // ---- relayout the quantised level-batched arena into leaf slabs (bytes)
+    std::vector<uint8_t> arena(in.arena_bytes);
+    if (cudaMemcpy(arena.data(), in.d_arena, in.arena_bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
         return HODLR_OK;
-    int occf = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_sv_fused<float>, kThreads, 0);
-    occ = std::min(occ, std::max(occf, 1));
+    std::vector<uint8_t> slab((size_t)P.slab_bytes * nleaves);
+    for (int leaf = 0; leaf < nleaves; ++leaf) {
+        uint8_t* out = slab.data() + (size_t)leaf * P.slab_bytes;
+        for (int g = 0; g < 5; ++g) {
+            const int w = fmt_bytes(g);
+            int col = 0;
+            for (int k = 0; k < depth; ++k) {
+                if (P.lev[k].fmt != g) continue;
+                const int lvl = k + 1;
+                const NodeDesc& nd = nodes[(1 << lvl) - 2 + (leaf >> (depth - lvl))];
+                const int64_t roff = (int64_t)leaf * kM - nd.row0;
+                for (int c = 0; c < nd.rv; ++c, ++col) {
+                    memcpy(out + P.vgoff[g] + (int64_t)col * kM * w,
+                           arena.data() + nd.v_off + ((int64_t)c * nd.v_ld + roff) * w, (size_t)kM * w);
+                    const uint8_t* src = arena.data() + nd.u_off + ((int64_t)c * nd.u_ld + roff) * w;
+                    uint8_t* dst = out + P.us_off + P.ugoff[g] + (int64_t)col * w;
+                    for (int r = 0; r < kM; ++r)
+                        memcpy(dst + (int64_t)r * P.gcols[g] * w, src + (int64_t)r * w, (size_t)w);
+                }
+            }
+        }
+        memcpy(out + P.d_off, arena.data() + leaves[leaf].off, (size_t)kM * kM * dsz);
+    }
+    int dev = 0, sms = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    const size_t smem = smem_bytes(P.bitset_words);
+    if (!coop || sms <= 0 ||
+        cudaFuncSetAttribute(k_stream<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(k_stream<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return HODLR_OK;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stream<double>, kThreads, smem);
+    if (occ < 1) return HODLR_OK;
     void* d = nullptr;
-    if (cudaMalloc(&d, sib.size() * sizeof(int32_t) + 16) != cudaSuccess) return HODLR_OK;
-    cudaMemcpy(d, sib.data(), sib.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (cudaMalloc(&d, slab.size()) != cudaSuccess) return HODLR_OK;
+    if (cudaMemcpy(d, slab.data(), slab.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return HODLR_OK;
+    }
     sv.dev = d;
-    sv.num_items_a = (int)chunks.size();
-    sv.num_items_b = (int)leaves.size() * (kM / kRB);
-    sv.grid = std::min(sms * std::min(occ, 2), sv.num_items_a + sv.num_items_b);
+    sv.dev_bytes = slab.size();
+    sv.slab = (const uint8_t*)d;
+    sv.nleaves = nleaves;
+    sv.nnodes = P.nnodes;
+    sv.depth = depth;
+    sv.rb = P.rbi;
+    sv.num_items_a = P.num_a;
+    sv.num_items_b = P.num_b;
+    sv.grid = std::min(sms, P.num_a + P.num_b);
     sv.launches = 1;
-    sv.extra_ws = sizeof(SvSync) + 2 * nodes.size() * sizeof(unsigned) + 256;
+    sv.tfast_count = tb;
+    sv.extra_ws = (sizeof(SvSync) + 2 * (size_t)P.nnodes * sizeof(unsigned) + 255) / 256 * 256 + (size_t)tb * 8;
+    sv.leaf_fmt = lf;
+    sv.params = new SvParams(P);
     *ok = true;
     return HODLR_OK;
 }
 
 void sv_release(SvPlan& sv) {
     if (sv.dev) cudaFree(sv.dev);
+    delete reinterpret_cast<SvParams*>(sv.params);
     sv = SvPlan{};
 }
 size_t sv_extra_ws(const SvPlan& sv, int64_t) { return sv.extra_ws; }
 int sv_launches(const SvPlan& sv) { return sv.launches; }
 
 template <typename W>
-cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* partial, W* tbuf,
+cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* partial, W* tbuf_unused,
                       void* extra, cudaStream_t st) {
-    SvArgs<W> a;
+    (void)p;
+    (void)tbuf_unused;
+    const SvParams& P = *reinterpret_cast<const SvParams*>(sv.params);
+    if (((uintptr_t)x & 15) || ((uintptr_t)b & 15) || ((uintptr_t)partial & 15))
+        return cudaErrorMisalignedAddress;
+    SvKernelArgs<W> a;
+    a.slab = sv.slab;
     a.x = x;
     a.b = b;
     a.partial = partial;
-    a.tbuf = tbuf;
-    a.sync = (SvSync*)extra;
-    a.counters = (unsigned*)((uint8_t*)extra + sizeof(SvSync));
-    a.flags = a.counters + p.nnodes;
-    a.sib = (const int32_t*)sv.dev;
-    a.num_a = sv.num_items_a;
-    a.num_b = sv.num_items_b;
-    a.items_per_leaf = kM / kRB;
-    PlanView pv = p;
-    void* args[] = {&pv, &a};
-    return cudaLaunchCooperativeKernel((const void*)k_sv_fused<W>, dim3(sv.grid), dim3(kThreads), args, 0, st);
+    uint8_t* e = (uint8_t*)extra;
+    a.sync = (SvSync*)e;
+    a.counters = (unsigned*)(e + sizeof(SvSync));
+    a.flags = a.counters + P.nnodes;
+    const size_t toff = (sizeof(SvSync) + 2 * (size_t)P.nnodes * sizeof(unsigned) + 255) / 256 * 256;
+    a.tbuf = (W*)(e + toff);
+    void* args[] = {(void*)&P, &a};
+    return cudaLaunchCooperativeKernel((const void*)k_stream<W>, dim3(sv.grid), dim3(kThreads), args,
+                                       smem_bytes(P.bitset_words), st);
 }
 
-template cudaError_t sv_matvec<double>(const PlanView&, const SvPlan&, const double*, double*,
-                                       double*, double*, void*, cudaStream_t);
-template cudaError_t sv_matvec<float>(const PlanView&, const SvPlan&, const float*, float*, float*,
-                                      float*, void*, cudaStream_t);
+template cudaError_t sv_matvec<double>(const PlanView&, const SvPlan&, const double*, double*, double*, double*,
+                                       void*, cudaStream_t);
+template cudaError_t sv_matvec<float>(const PlanView&, const SvPlan&, const float*, float*, float*, float*, void*,
+                                      cudaStream_t);
 
 }  // namespace hodlr

@@ -1,4 +1,5 @@
-// Single-vector (s = 1) fast path: one persistent kernel per matvec.
+// Single-vector (s = 1) streaming fast path: one persistent kernel per matvec,
+// fed by cp.async.bulk (TMA bulk copies) from a leaf-slab layout.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -10,19 +11,31 @@
 namespace hodlr {
 
 struct SvPlan {
-    void* dev = nullptr;   // device-side work lists
-    int num_items_a = 0;   // phase-A work items
-    int num_items_b = 0;   // phase-B work items
-    int grid = 0;          // persistent CTAs
+    void* dev = nullptr;     // slab arena (device)
+    size_t dev_bytes = 0;
+    const uint8_t* slab = nullptr;
+    void* params = nullptr;  // host copy of the kernel parameter block
+    int nleaves = 0, nnodes = 0, depth = 0;
+    int rb = 0;                 // rows per phase-B item
+    int num_items_a = 0, num_items_b = 0;
+    int grid = 0;
     int launches = 1;
-    size_t extra_ws = 0;   // bytes of workspace beyond partials/coefficients (per s=1)
-    const void* items = nullptr;
-    const void* sync = nullptr;
+    int64_t tfast_count = 0;    // padded coefficient buffer (elements)
+    size_t extra_ws = 0;        // bytes of workspace for sync state + coefficients
+    int leaf_fmt = 4;
 };
 
-hodlr_status sv_prepare(const std::vector<NodeDesc>& nodes, const std::vector<ChunkDesc>& chunks,
-                        const std::vector<LeafDesc>& leaves, const std::vector<int32_t>& chunk_nodes,
-                        int nlev, SvPlan& sv, bool* ok);
+struct SvInput {
+    const std::vector<NodeDesc>* nodes;
+    const std::vector<ChunkDesc>* chunks;
+    const std::vector<LeafDesc>* leaves;
+    const std::vector<int32_t>* chunk_nodes;
+    int nlev;
+    const uint8_t* d_arena;     // generic (level-batched) arena, already quantised
+    size_t arena_bytes;
+};
+
+hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok);
 void sv_release(SvPlan& sv);
 size_t sv_extra_ws(const SvPlan& sv, int64_t s);
 int sv_launches(const SvPlan& sv);
