@@ -43,7 +43,7 @@ def make_op(H, fused=True):
 @pytest.mark.parametrize("working,fmts", FMT_SETS)
 def test_fused_matches_oracle(cuda, working, fmts):
     torch = cuda
-    H = random_hodlr(2048, 3, fmts, [(1, 24), (0, 17), (3, 9)], working, seed=len(fmts[0]) + len(working))
+    H = random_hodlr(2048, 3, fmts, [24, 17, 3], working, seed=len(fmts[0]) + len(working))
     op = make_op(H)
     assert op.launches_per_matvec == 1, "fused path not selected"
     x = np.random.default_rng(1).standard_normal(H.n)
@@ -118,3 +118,27 @@ def test_cfg1_built_by_harness_matches_reference_golden(cuda):
     assert rel(b, b_ref) <= 1e-12
     beta = np.linalg.norm(b - kx) / (normA * np.linalg.norm(x))
     assert beta <= 10 * matvec_bound(4, 1e-8)
+
+
+def test_variable_ranks_take_generic_path(cuda):
+    """Per-block ranks that differ inside a level (the cfg3 situation) are served
+    by the generic kernels; results still match the oracle."""
+    torch = cuda
+    H = random_hodlr(2048, 3, ["fp32", "bf16", "q52"], [(1, 24), (0, 17), (3, 9)], "fp64", seed=11)
+    op = make_op(H)
+    assert op.launches_per_matvec == 3
+    x = np.random.default_rng(5).standard_normal(H.n)
+    b = op.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel(b, matvec_oracle(H, x)) <= 1e-12
+
+
+@pytest.mark.parametrize("depth", [1, 2, 5])
+def test_fused_depths(cuda, depth):
+    torch = cuda
+    fm = ["fp32", "fp16", "bf16", "q52", "fp64"][:depth]
+    H = random_hodlr(256 << depth, depth, fm, [7, 5, 9, 3, 4][:depth], "fp64", seed=depth)
+    op = make_op(H)
+    assert op.launches_per_matvec == 1
+    x = np.random.default_rng(6).standard_normal(H.n)
+    b = op.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel(b, matvec_oracle(H, x)) <= 1e-12
