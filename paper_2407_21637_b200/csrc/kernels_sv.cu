@@ -46,7 +46,7 @@ namespace {
 constexpr int kM = 256;                 // leaf rows
 constexpr int kNS = 6;                  // ring stages
 constexpr int kStage = 34 * 1024;       // bytes per stage
-constexpr int kConsumers = 8;           // consumer warps
+constexpr int kConsumers = 16;          // consumer warps
 constexpr int kThreads = 32 * (kConsumers + 1);
 constexpr int kMaxLev = 24;
 constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
@@ -214,26 +214,40 @@ __device__ __forceinline__ void a_piece_cols(const uint8_t* cols, int ncols, con
     for (int i = 0; i < F::PER; ++i)
 #pragma unroll
         for (int e = 0; e < F::E; ++e) xr[i][e] = active ? xs[(lane + 32 * i) * F::E + e] : W(0);
-    for (int j = warp; j < ncols; j += kConsumers) {
+    for (int j = warp; j < ncols; j += 2 * kConsumers) {
+        const int j2 = j + kConsumers;
+        const bool two = j2 < ncols;
         const uint8_t* col = cols + (size_t)j * kM * F::bytes;
-        W acc = W(0);
+        const uint8_t* col2 = cols + (size_t)(two ? j2 : j) * kM * F::bytes;
+        W acc = W(0), acc2 = W(0);
         if (active) {
+            uint4 v[F::PER], v2[F::PER];
 #pragma unroll
             for (int i = 0; i < F::PER; ++i) {
-                uint4 v = *reinterpret_cast<const uint4*>(col + (lane + 32 * i) * 16);
-                acc = dot16<FMT, W>(v, xr[i], acc);
+                v[i] = *reinterpret_cast<const uint4*>(col + (lane + 32 * i) * 16);
+                v2[i] = *reinterpret_cast<const uint4*>(col2 + (lane + 32 * i) * 16);
+            }
+#pragma unroll
+            for (int i = 0; i < F::PER; ++i) {
+                acc = dot16<FMT, W>(v[i], xr[i], acc);
+                acc2 = dot16<FMT, W>(v2[i], xr[i], acc2);
             }
         }
-        acc = warp_sum(acc);
-        if (lane == 0) {
-            const int flat = P.gstart[g] + col0 + j;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+        }
+        if (lane < 2 && (lane == 0 || two)) {
+            const int jj = lane == 0 ? j : j2;
+            const int flat = P.gstart[g] + col0 + jj;
             const int k = P.col_level[flat];
             const int c = P.col_c[flat];
             const Level& L = P.lev[k];
             const int sh = P.depth - (k + 1);
             const int jn = leaf >> sh;
             const int nch = 1 << sh;
-            partial[L.pbase + ((int64_t)jn * L.r + c) * nch + (leaf - (jn << sh))] = acc;
+            partial[L.pbase + ((int64_t)jn * L.r + c) * nch + (leaf - (jn << sh))] = lane == 0 ? acc : acc2;
         }
     }
 }
@@ -304,7 +318,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
     PieceHdr* hdr = reinterpret_cast<PieceHdr*>(empty + kNS);
     int* misc = reinterpret_cast<int*>(hdr + kNS);  // [0] epoch, [1..kMaxLev] last-arriver flags
     int* fifo = misc + 64;
-    unsigned* bitset = reinterpret_cast<unsigned*>(fifo + kFifo);
+    int16_t* cidx = reinterpret_cast<int16_t*>(fifo + kFifo);  // [512]: U column -> coefficient slot
+    unsigned* bitset = reinterpret_cast<unsigned*>(cidx + 512);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int total = P.num_a + P.num_b;
@@ -319,6 +334,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = threadIdx.x; i < P.bitset_words; i += kThreads) bitset[i] = 0u;
+    for (int i = threadIdx.x; i < P.gstart[5]; i += kThreads)
+        cidx[i] = (int16_t)(P.lev[P.col_level[i]].slot + P.col_c[i]);
     __syncthreads();
     const unsigned target = (unsigned)misc[0] + 1u;
 
@@ -511,11 +528,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                     const int nc = P.gcols[g];
                     if (nc == 0) continue;
                     const uint8_t* ub = st + off + (size_t)row * nc * fmt_sz(g);
-                    for (int j = q; j < nc; j += tpr) {
-                        const int flat = P.gstart[g] + j;
-                        const Level& L = P.lev[P.col_level[flat]];
-                        acc = fma(u_elem<W>(g, ub, j), coef[L.slot + P.col_c[flat]], acc);
-                    }
+                    const int16_t* ci = cidx + P.gstart[g];
+                    for (int j = q; j < nc; j += tpr) acc = fma(u_elem<W>(g, ub, j), coef[ci[j]], acc);
                     off += h.rows * nc * fmt_sz(g);
                 }
                 for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -586,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
 
 size_t smem_bytes(int bitset_words) {
     return (size_t)kNS * kStage + 2 * kNS * sizeof(uint64_t) + kNS * sizeof(PieceHdr) +
-           (64 + kFifo) * sizeof(int) + (size_t)bitset_words * 4;
+           (64 + kFifo) * sizeof(int) + 512 * sizeof(int16_t) + (size_t)bitset_words * 4;
 }
 
 }  // namespace
