@@ -47,7 +47,9 @@ constexpr int kM = 256;                 // leaf rows
 constexpr int kNS = 6;                  // ring stages
 constexpr int kStage = 34 * 1024;       // bytes per stage
 constexpr int kConsumers = 16;          // consumer warps
-constexpr int kThreads = 32 * (kConsumers + 1);
+constexpr int kThreads = 32 * (kConsumers + 2);  // + producer + reducer
+constexpr int kEvQ = 16;                // pending phase-A completion events
+constexpr int kZeroSlot = 4;            // zero coefficients for padded U columns
 constexpr int kMaxLev = 24;
 constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
 constexpr int kFifo = 32;               // deferred U pieces per CTA
@@ -75,7 +77,12 @@ struct SvParams {
     int32_t num_a, num_b;
     int32_t leaf_fmt;
     int64_t slab_bytes, us_off, d_off;
-    int32_t gcols[5];              // columns per format group
+    int32_t gcols[5];              // columns per format group (V' slab)
+    int32_t gpad[5];               // U slab row length per group, padded to 4 columns
+    int32_t gstart_pad[5];         // first padded U column of each group
+    int32_t ucols_total;
+    int32_t tpr_shift;             // log2(threads per U row)
+    int32_t ubytes[2];             // U-piece transaction bytes for fp32 / fp64 working
     int64_t vgoff[5], ugoff[5];    // byte offsets of the groups inside the V' / U slabs
     int32_t coef_elems;            // padded coefficient elements per U piece
     int32_t bitset_words;
@@ -84,6 +91,7 @@ struct SvParams {
     int8_t col_level[512];         // flattened (group, column) -> level (0-based)
     int16_t col_c[512];            //                            -> rank column
     int16_t gstart[6];
+    int16_t ucidx[512];            // padded U column -> coefficient slot (zero slot for padding)
 };
 
 struct SvSync {
@@ -233,13 +241,14 @@ __device__ __forceinline__ void a_piece_cols(const uint8_t* cols, int ncols, con
                 acc2 = dot16<FMT, W>(v2[i], xr[i], acc2);
             }
         }
+        // transposed reduction: lanes 0-15 finish column j, lanes 16-31 column j2
+        const bool hi = lane & 16;
+        W v = hi ? acc2 : acc;
+        v += __shfl_xor_sync(0xffffffffu, hi ? acc : acc2, 16);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
-        }
-        if (lane < 2 && (lane == 0 || two)) {
-            const int jj = lane == 0 ? j : j2;
+        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((lane & 15) == 0 && (!hi || two)) {
+            const int jj = hi ? j2 : j;
             const int flat = P.gstart[g] + col0 + jj;
             const int k = P.col_level[flat];
             const int c = P.col_c[flat];
@@ -247,7 +256,7 @@ __device__ __forceinline__ void a_piece_cols(const uint8_t* cols, int ncols, con
             const int sh = P.depth - (k + 1);
             const int jn = leaf >> sh;
             const int nch = 1 << sh;
-            partial[L.pbase + ((int64_t)jn * L.r + c) * nch + (leaf - (jn << sh))] = lane == 0 ? acc : acc2;
+            partial[L.pbase + ((int64_t)jn * L.r + c) * nch + (leaf - (jn << sh))] = v;
         }
     }
 }
@@ -297,9 +306,55 @@ __device__ __forceinline__ W u_elem(int fmt, const uint8_t* p, int idx) {
     }
 }
 
+// U piece: 4 consecutive columns j..j+3 of one row (format g, padded row) times
+// their coefficients (slot indices packed 4 x int16 in one 8-byte word).
+template <typename W>
+__device__ __forceinline__ W u_dot4(int g, const uint8_t* ub, int j, const int16_t* ci, const W* coef, W acc) {
+    const uint2 iw = *reinterpret_cast<const uint2*>(ci + j);
+    const int i0 = (int)(int16_t)(iw.x & 0xffff), i1 = (int)(int16_t)(iw.x >> 16);
+    const int i2 = (int)(int16_t)(iw.y & 0xffff), i3 = (int)(int16_t)(iw.y >> 16);
+    W u0, u1, u2, u3;
+    switch (g) {
+        case HODLR_FMT_FP64: {
+            const double4 v = *reinterpret_cast<const double4*>(ub + (size_t)j * 8);
+            u0 = (W)v.x; u1 = (W)v.y; u2 = (W)v.z; u3 = (W)v.w;
+            break;
+        }
+        case HODLR_FMT_FP32: {
+            const float4 v = *reinterpret_cast<const float4*>(ub + (size_t)j * 4);
+            u0 = (W)v.x; u1 = (W)v.y; u2 = (W)v.z; u3 = (W)v.w;
+            break;
+        }
+        case HODLR_FMT_FP16: {
+            const uint2 v = *reinterpret_cast<const uint2*>(ub + (size_t)j * 2);
+            u0 = (W)dec_fp16(v.x & 0xffff); u1 = (W)dec_fp16(v.x >> 16);
+            u2 = (W)dec_fp16(v.y & 0xffff); u3 = (W)dec_fp16(v.y >> 16);
+            break;
+        }
+        case HODLR_FMT_BF16: {
+            const uint2 v = *reinterpret_cast<const uint2*>(ub + (size_t)j * 2);
+            u0 = (W)__uint_as_float(v.x << 16); u1 = (W)__uint_as_float(v.x & 0xffff0000u);
+            u2 = (W)__uint_as_float(v.y << 16); u3 = (W)__uint_as_float(v.y & 0xffff0000u);
+            break;
+        }
+        default: {
+            const uint32_t v = *reinterpret_cast<const uint32_t*>(ub + j);
+            u0 = (W)dec_q52(v & 0xff); u1 = (W)dec_q52((v >> 8) & 0xff);
+            u2 = (W)dec_q52((v >> 16) & 0xff); u3 = (W)dec_q52(v >> 24);
+            break;
+        }
+    }
+    acc = fma(u0, coef[i0], acc);
+    acc = fma(u1, coef[i1], acc);
+    acc = fma(u2, coef[i2], acc);
+    acc = fma(u3, coef[i3], acc);
+    return acc;
+}
+
 template <typename W>
 struct SvKernelArgs {
     const uint8_t* slab;
+    const uint8_t* zeros;  // 32 zero bytes (coefficient of padded U columns)
     const W* x;
     W* b;
     W* partial;
@@ -309,41 +364,52 @@ struct SvKernelArgs {
     unsigned* flags;
 };
 
+// shared-memory bookkeeping next to the stage ring
+struct SmemCtl {
+    uint64_t full[kNS], empty[kNS];
+    PieceHdr hdr[kNS];
+    unsigned epoch;
+    volatile int ev_tail;          // phase-A completion events pushed by the producer
+    volatile int ev_head;          // ... and retired by the reducer warp
+    int ev_leaf[kEvQ];
+    unsigned ev_done[kEvQ];        // consumer warps finished with the event's leaf
+    int fifo[kFifo];
+    alignas(16) int16_t cidx[512];  // U column (padded groups) -> coefficient slot
+};
+
 template <typename W>
 __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ SvParams P, SvKernelArgs<W> a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* stages = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kNS * kStage);
-    uint64_t* empty = full + kNS;
-    PieceHdr* hdr = reinterpret_cast<PieceHdr*>(empty + kNS);
-    int* misc = reinterpret_cast<int*>(hdr + kNS);  // [0] epoch, [1..kMaxLev] last-arriver flags
-    int* fifo = misc + 64;
-    int16_t* cidx = reinterpret_cast<int16_t*>(fifo + kFifo);  // [512]: U column -> coefficient slot
-    unsigned* bitset = reinterpret_cast<unsigned*>(cidx + 512);
+    SmemCtl& C = *reinterpret_cast<SmemCtl*>(smem + kNS * kStage);
+    unsigned* bitset = reinterpret_cast<unsigned*>(&C + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int total = P.num_a + P.num_b;
     const int nlev = P.depth;
 
     if (threadIdx.x == 0) {
-        misc[0] = (int)ld_acquire(&a.sync->epoch);
+        C.epoch = ld_acquire(&a.sync->epoch);
+        C.ev_tail = 0;
+        C.ev_head = 0;
         for (int s = 0; s < kNS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumers);
+            mbar_init(&C.full[s], 1);
+            mbar_init(&C.empty[s], kConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int i = threadIdx.x; i < kEvQ; i += kThreads) C.ev_done[i] = 0u;
     for (int i = threadIdx.x; i < P.bitset_words; i += kThreads) bitset[i] = 0u;
-    for (int i = threadIdx.x; i < P.gstart[5]; i += kThreads)
-        cidx[i] = (int16_t)(P.lev[P.col_level[i]].slot + P.col_c[i]);
+    for (int i = threadIdx.x; i < P.ucols_total; i += kThreads) C.cidx[i] = P.ucidx[i];
     __syncthreads();
-    const unsigned target = (unsigned)misc[0] + 1u;
+    const unsigned target = C.epoch + 1u;
 
     if (warp == 0) {
         // =========================================================== producer
         int stage = 0;
         unsigned phase = 0;
         int fh = 0, ft = 0;  // deferred-U FIFO head / tail (warp-uniform)
+        int ev = 0;          // phase-A events pushed
         auto next_stage = [&]() {
             if (++stage == kNS) {
                 stage = 0;
@@ -351,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
             }
         };
         auto claim = [&]() -> uint8_t* {
-            mbar_wait(&empty[stage], phase ^ 1u);
+            mbar_wait(&C.empty[stage], phase ^ 1u);
             return stages + (size_t)stage * kStage;
         };
         // are the coefficients of every level of `leaf` published?
@@ -375,21 +441,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
             uint8_t* st = claim();
             const int wbytes = (int)sizeof(W);
             const int coef_bytes = P.coef_elems * wbytes;
-            unsigned bytes = (unsigned)coef_bytes;
-            for (int l = 0; l < nlev; ++l)
-                if (P.lev[l].r == 0) bytes -= (unsigned)(P.lev[l].tstride * wbytes);
-            for (int g = 0; g < 5; ++g) bytes += (unsigned)(P.rbi * P.gcols[g] * fmt_sz(g));
             if (lane == 0) {
-                PieceHdr& h = hdr[stage];
+                PieceHdr& h = C.hdr[stage];
                 h.type = PT_U;
                 h.leaf = leaf;
                 h.r0 = r0;
                 h.rows = P.rbi;
-                mbar_arrive_tx(&full[stage], bytes);
+                mbar_arrive_tx(&C.full[stage], (unsigned)P.ubytes[sizeof(W) == 8 ? 1 : 0]);
             }
             __syncwarp();
-            // coefficients were written by other SMs (generic proxy, release/acquire
-            // on the flag); order them before this SM's async-proxy reads
+            // coefficients were written by other SMs (generic proxy, release/acquire on
+            // the flag); order them before this SM's async-proxy reads
             asm volatile("fence.proxy.async.global;" ::: "memory");
             if (lane < nlev) {
                 const Level& L = P.lev[lane];
@@ -397,24 +459,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                     const int k = lane + 1;
                     const int jsib = (leaf >> (nlev - k)) ^ 1;
                     const W* src = a.tbuf + L.tbase + (int64_t)jsib * L.tstride;
-                    bulk_g2s(st + (size_t)L.slot * wbytes, src, (unsigned)(L.tstride * wbytes), &full[stage]);
+                    bulk_g2s(st + (size_t)L.slot * wbytes, src, (unsigned)(L.tstride * wbytes), &C.full[stage]);
                 }
             } else if (lane >= 24 && lane < 29) {
                 const int g = lane - 24;
-                if (P.gcols[g] > 0) {
+                if (P.gpad[g] > 0) {
                     const uint8_t* src = a.slab + (int64_t)leaf * P.slab_bytes + P.us_off + P.ugoff[g] +
-                                         (int64_t)r0 * P.gcols[g] * fmt_sz(g);
-                    int off = coef_bytes;
-                    for (int q = 0; q < g; ++q) off += P.rbi * P.gcols[q] * fmt_sz(q);
-                    bulk_g2s(st + off, src, (unsigned)(P.rbi * P.gcols[g] * fmt_sz(g)), &full[stage]);
+                                         (int64_t)r0 * P.gpad[g] * fmt_sz(g);
+                    int off = coef_bytes + kZeroSlot * wbytes;
+                    for (int q = 0; q < g; ++q) off += P.rbi * P.gpad[q] * fmt_sz(q);
+                    bulk_g2s(st + off, src, (unsigned)(P.rbi * P.gpad[g] * fmt_sz(g)), &C.full[stage]);
                 }
+            } else if (lane == 31) {
+                bulk_g2s(st + coef_bytes, a.zeros, (unsigned)(kZeroSlot * wbytes), &C.full[stage]);
             }
             __syncwarp();
             next_stage();
         };
         auto flush_fifo = [&](bool block) {
             while (fh != ft) {
-                const int e = fifo[fh % kFifo];
+                const int e = C.fifo[fh % kFifo];
                 const int leaf = e >> 12, r0 = e & 0xfff;
                 if (!ready(leaf)) {
                     if (!block) return;
@@ -424,6 +488,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                 emit_u(leaf, r0);
                 ++fh;
             }
+        };
+        auto push_event = [&](int leaf) {  // lane 0
+            while (ev - C.ev_head >= kEvQ) __nanosleep(64);
+            C.ev_leaf[ev % kEvQ] = leaf;
+            __threadfence_block();
+            C.ev_tail = ev + 1;
         };
 
         int item = 0;
@@ -435,22 +505,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
             if (item < P.num_a) {
                 const int leaf = item;
                 const uint8_t* base = a.slab + (int64_t)leaf * P.slab_bytes;
+                if (lane == 0) push_event(leaf);
+                ++ev;
+                __syncwarp();
                 for (int p = 0; p < P.napieces; ++p) {
                     const APiece ap = P.ap[p];
                     uint8_t* st = claim();
                     const unsigned cb = (unsigned)(ap.ncols * kM * fmt_sz(ap.g));
                     if (lane == 0) {
-                        PieceHdr& h = hdr[stage];
+                        PieceHdr& h = C.hdr[stage];
                         h.type = PT_A;
                         h.leaf = leaf;
                         h.g = ap.g;
                         h.col = ap.col;
                         h.ncols = ap.ncols;
                         h.last = (p == P.napieces - 1);
-                        mbar_arrive_tx(&full[stage], (unsigned)(kM * sizeof(W)) + cb);
-                        bulk_g2s(st, a.x + (int64_t)leaf * kM, (unsigned)(kM * sizeof(W)), &full[stage]);
+                        mbar_arrive_tx(&C.full[stage], (unsigned)(kM * sizeof(W)) + cb);
+                        bulk_g2s(st, a.x + (int64_t)leaf * kM, (unsigned)(kM * sizeof(W)), &C.full[stage]);
                         bulk_g2s(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.col * kM * fmt_sz(ap.g), cb,
-                                 &full[stage]);
+                                 &C.full[stage]);
                     }
                     __syncwarp();
                     next_stage();
@@ -467,46 +540,97 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                     const int rr = r0 + p * P.rbd;
                     const unsigned cb = (unsigned)(P.rbd * kM * dsz);
                     if (lane == 0) {
-                        PieceHdr& h = hdr[stage];
+                        PieceHdr& h = C.hdr[stage];
                         h.type = PT_D;
                         h.leaf = leaf;
                         h.r0 = rr;
                         h.rows = P.rbd;
-                        mbar_arrive_tx(&full[stage], (unsigned)(kM * sizeof(W)) + cb);
-                        bulk_g2s(st, a.x + (int64_t)leaf * kM, (unsigned)(kM * sizeof(W)), &full[stage]);
-                        bulk_g2s(st + kXB, dbase + (int64_t)rr * kM * dsz, cb, &full[stage]);
+                        mbar_arrive_tx(&C.full[stage], (unsigned)(kM * sizeof(W)) + cb);
+                        bulk_g2s(st, a.x + (int64_t)leaf * kM, (unsigned)(kM * sizeof(W)), &C.full[stage]);
+                        bulk_g2s(st + kXB, dbase + (int64_t)rr * kM * dsz, cb, &C.full[stage]);
                     }
                     __syncwarp();
                     next_stage();
                 }
-                if (nlev == 0) {
-                    // depth 0: no coefficients, b = D x already written
-                } else {
-                    if (ft - fh == kFifo) flush_fifo(true);
-                    if (lane == 0) fifo[ft % kFifo] = (leaf << 12) | r0;
-                    __syncwarp();
-                    ++ft;
-                    flush_fifo(false);
-                }
+                if (ft - fh == kFifo) flush_fifo(true);
+                if (lane == 0) C.fifo[ft % kFifo] = (leaf << 12) | r0;
+                __syncwarp();
+                ++ft;
+                flush_fifo(false);
             }
             item = __shfl_sync(0xffffffffu, nxt, 0);
         }
         flush_fifo(true);
         claim();
         if (lane == 0) {
-            hdr[stage].type = PT_END;
-            mbar_arrive(&full[stage]);
+            C.hdr[stage].type = PT_END;
+            mbar_arrive(&C.full[stage]);
+            while (ev - C.ev_head >= kEvQ) __nanosleep(64);
+            C.ev_leaf[ev % kEvQ] = -1;  // reducer: done
+            __threadfence_block();
+            C.ev_tail = ev + 1;
         }
         __syncwarp();
+    } else if (warp == 1) {
+        // =========================================================== reducer
+        // Retires phase-A events in order: once all consumer warps finished the
+        // leaf's partials, bump the counters of its l ancestor nodes; for every
+        // node whose last leaf this was, reduce the node's partials in leaf order
+        // (deterministic) into t and publish the node flag.
+        for (int ev = 0;; ++ev) {
+            while (C.ev_tail <= ev) __nanosleep(64);
+            const int leaf = C.ev_leaf[ev % kEvQ];
+            if (leaf < 0) break;
+            while (*(volatile unsigned*)&C.ev_done[ev % kEvQ] < (unsigned)kConsumers) __nanosleep(32);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            bool last = false;
+            if (lane < nlev) {
+                const int k = lane + 1;
+                const int sh = nlev - k;
+                const int id = (1 << k) - 2 + (leaf >> sh);
+                unsigned old;
+                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.counters + id) : "memory");
+                last = old == (1u << sh) - 1u;
+            }
+            unsigned mask = __ballot_sync(0xffffffffu, last);
+            while (mask) {
+                const int lv = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int k = lv + 1;
+                const int sh = nlev - k;
+                const int jn = leaf >> sh;
+                const int nch = 1 << sh;
+                const Level& L = P.lev[lv];
+                for (int c = 0; c < L.r; ++c) {
+                    const W* src = a.partial + L.pbase + ((int64_t)jn * L.r + c) * nch;
+                    W acc = W(0);
+                    for (int i = lane; i < nch; i += 32) acc += __ldcg(src + i);
+                    acc = warp_sum(acc);
+                    if (lane == 0) a.tbuf[L.tbase + (int64_t)jn * L.tstride + c] = acc;
+                }
+                if (lane == 0) {
+                    a.counters[(1 << k) - 2 + jn] = 0u;
+                    st_release(&a.flags[(1 << k) - 2 + jn], target);
+                }
+                __syncwarp();
+            }
+            if (lane == 0) {
+                C.ev_done[ev % kEvQ] = 0u;
+                __threadfence_block();
+                C.ev_head = ev + 1;
+            }
+            __syncwarp();
+        }
     } else {
         // =========================================================== consumers
-        const int cw = warp - 1;
-        const int ctid = threadIdx.x - 32;
+        const int cw = warp - 2;
+        const int ctid = threadIdx.x - 64;
         int stage = 0;
         unsigned phase = 0;
+        int ev = 0;
         for (;;) {
-            mbar_wait(&full[stage], phase);
-            const PieceHdr h = hdr[stage];
+            mbar_wait(&C.full[stage], phase);
+            const PieceHdr h = C.hdr[stage];
             const uint8_t* st = stages + (size_t)stage * kStage;
             if (h.type == PT_END) break;
             if (h.type == PT_A) {
@@ -519,64 +643,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                 else d_piece<HODLR_FMT_FP32, W>(st + kXB, h.rows, xs, cw, lane, brow);
             } else {  // PT_U
                 consumer_sync();  // the D pieces of these rows were written by other warps
+                const int row = ctid >> P.tpr_shift, q = ctid & ((1 << P.tpr_shift) - 1);
+                W* bp = a.b + (int64_t)h.leaf * kM + h.r0 + row;
+                const W bold = q == 0 ? *bp : W(0);
                 const W* coef = reinterpret_cast<const W*>(st);
-                const int tpr = kConsumers * 32 / h.rows;
-                const int row = ctid / tpr, q = ctid % tpr;
                 W acc = W(0);
-                int off = P.coef_elems * (int)sizeof(W);
+                int off = (P.coef_elems + kZeroSlot) * (int)sizeof(W);
                 for (int g = 0; g < 5; ++g) {
-                    const int nc = P.gcols[g];
+                    const int nc = P.gpad[g];
                     if (nc == 0) continue;
                     const uint8_t* ub = st + off + (size_t)row * nc * fmt_sz(g);
-                    const int16_t* ci = cidx + P.gstart[g];
-                    for (int j = q; j < nc; j += tpr) acc = fma(u_elem<W>(g, ub, j), coef[ci[j]], acc);
+                    const int16_t* ci = C.cidx + P.gstart_pad[g];
+                    for (int j = 4 * q; j < nc; j += 4 << P.tpr_shift)
+                        acc = u_dot4<W>(g, ub, j, ci, coef, acc);
                     off += h.rows * nc * fmt_sz(g);
                 }
-                for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (q == 0) {
-                    W* bp = a.b + (int64_t)h.leaf * kM + h.r0 + row;
-                    *bp = acc + *bp;
-                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+                    if (o < (1 << P.tpr_shift)) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (q == 0) *bp = acc + bold;
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (lane == 0) mbar_arrive(&C.empty[stage]);
             if (h.type == PT_A && h.last) {
-                // every partial of this leaf is written -> count it into its l nodes
-                consumer_sync();
-                if (ctid == 0) {
-                    __threadfence();
-                    for (int lv = 0; lv < nlev; ++lv) {
-                        const int k = lv + 1;
-                        const int sh = nlev - k;
-                        const int id = (1 << k) - 2 + (h.leaf >> sh);
-                        const unsigned old = atomicAdd(&a.counters[id], 1u);
-                        misc[1 + lv] = (old == (1u << sh) - 1u) ? 1 : 0;
-                    }
-                    __threadfence();
+                // this warp's partials of the leaf are written: tell the reducer
+                if (lane == 0) {
+                    asm volatile("fence.acq_rel.cta;" ::: "memory");
+                    atomicAdd(&C.ev_done[ev % kEvQ], 1u);
                 }
-                consumer_sync();
-                for (int lv = 0; lv < nlev; ++lv) {
-                    if (!misc[1 + lv]) continue;
-                    const int k = lv + 1;
-                    const int sh = nlev - k;
-                    const int jn = h.leaf >> sh;
-                    const int nch = 1 << sh;
-                    const Level& L = P.lev[lv];
-                    for (int c = cw; c < L.r; c += kConsumers) {
-                        const W* src = a.partial + L.pbase + ((int64_t)jn * L.r + c) * nch;
-                        W acc = W(0);
-                        for (int i = lane; i < nch; i += 32) acc += __ldcg(src + i);
-                        acc = warp_sum(acc);
-                        if (lane == 0) a.tbuf[L.tbase + (int64_t)jn * L.tstride + c] = acc;
-                    }
-                    consumer_sync();
-                    if (ctid == 0) {
-                        const int id = (1 << k) - 2 + jn;
-                        a.counters[id] = 0u;
-                        __threadfence();
-                        st_release(&a.flags[id], target);
-                    }
-                }
+                ++ev;
             }
             if (++stage == kNS) {
                 stage = 0;
@@ -587,20 +682,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
     // ---- teardown: the last CTA resets the queue and publishes the next epoch
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned old = atomicAdd(&a.sync->done, 1u);
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&a.sync->done) : "memory");
         if (old == gridDim.x - 1) {
             a.sync->queue = 0u;
             a.sync->done = 0u;
-            __threadfence();
             st_release(&a.sync->epoch, target);
         }
     }
 }
 
 size_t smem_bytes(int bitset_words) {
-    return (size_t)kNS * kStage + 2 * kNS * sizeof(uint64_t) + kNS * sizeof(PieceHdr) +
-           (64 + kFifo) * sizeof(int) + 512 * sizeof(int16_t) + (size_t)bitset_words * 4;
+    return (size_t)kNS * kStage + sizeof(SmemCtl) + (size_t)bitset_words * 4;
 }
 
 }  // namespace
@@ -673,14 +766,28 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         tb += (int64_t)L.tstride << (k + 1);
     }
     P.coef_elems = slot;
-    // slab geometry
+    // slab geometry (U rows padded to 4-column groups; padding -> zero coefficient)
     int64_t vs = 0, us = 0;
+    int upad = 0;
     for (int g = 0; g < 5; ++g) {
         P.vgoff[g] = vs;
         vs += (int64_t)P.gcols[g] * kM * fmt_bytes(g);
+        P.gpad[g] = (P.gcols[g] + 3) / 4 * 4;
+        P.gstart_pad[g] = upad;
+        for (int j = 0; j < P.gpad[g]; ++j) {
+            if (upad + j >= 512) return HODLR_OK;
+            if (j < P.gcols[g]) {
+                const int f = P.gstart[g] + j;
+                P.ucidx[upad + j] = (int16_t)(P.lev[P.col_level[f]].slot + P.col_c[f]);
+            } else {
+                P.ucidx[upad + j] = (int16_t)P.coef_elems;  // zero slot
+            }
+        }
+        upad += P.gpad[g];
         P.ugoff[g] = us;
-        us += (int64_t)P.gcols[g] * kM * fmt_bytes(g);
+        us += (int64_t)P.gpad[g] * kM * fmt_bytes(g);
     }
+    P.ucols_total = upad;
     const int dsz = fmt_bytes(lf);
     P.us_off = vs;
     P.d_off = vs + us;
@@ -689,14 +796,23 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     P.rbd = 1;
     while (P.rbd * 2 <= kM && kXB + P.rbd * 2 * kM * dsz <= kStage) P.rbd *= 2;
     int ubytes_row = 0;
-    for (int g = 0; g < 5; ++g) ubytes_row += P.gcols[g] * fmt_bytes(g);
+    for (int g = 0; g < 5; ++g) ubytes_row += P.gpad[g] * fmt_bytes(g);
+    const int cfix = (P.coef_elems + kZeroSlot) * 8;
     P.rbi = 32;
-    while (P.rbi > 8 && P.coef_elems * 8 + P.rbi * ubytes_row > kStage) P.rbi /= 2;
-    if (P.coef_elems * 8 + P.rbi * ubytes_row > kStage) return HODLR_OK;
+    const int min_rbi = kConsumers;  // U-piece reduction: <= 32 threads per row
+    while (P.rbi > min_rbi && cfix + P.rbi * ubytes_row > kStage) P.rbi /= 2;
+    if (cfix + P.rbi * ubytes_row > kStage) return HODLR_OK;
+    P.tpr_shift = 0;
+    while ((1 << P.tpr_shift) * P.rbi < kConsumers * 32) ++P.tpr_shift;
+    if ((1 << P.tpr_shift) * P.rbi != kConsumers * 32 || P.tpr_shift > 5) return HODLR_OK;
+    for (int wi = 0; wi < 2; ++wi) {
+        const int wb = wi ? 8 : 4;
+        P.ubytes[wi] = (P.coef_elems + kZeroSlot) * wb + P.rbi * ubytes_row;
+    }
     if (P.rbd > P.rbi) P.rbd = P.rbi;
     if (P.rbi % P.rbd) return HODLR_OK;
     for (int g = 0; g < 5; ++g)  // bulk copies: 16-byte granules
-        if ((P.rbi * P.gcols[g] * fmt_bytes(g)) % 16) return HODLR_OK;
+        if ((P.rbi * P.gpad[g] * fmt_bytes(g)) % 16) return HODLR_OK;
     P.dpieces = P.rbi / P.rbd;
     // phase-A pieces
     P.napieces = 0;
@@ -734,7 +850,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
                     const uint8_t* src = arena.data() + nd.u_off + ((int64_t)c * nd.u_ld + roff) * w;
                     uint8_t* dst = out + P.us_off + P.ugoff[g] + (int64_t)col * w;
                     for (int r = 0; r < kM; ++r)
-                        memcpy(dst + (int64_t)r * P.gcols[g] * w, src + (int64_t)r * w, (size_t)w);
+                        memcpy(dst + (int64_t)r * P.gpad[g] * w, src + (int64_t)r * w, (size_t)w);
                 }
             }
         }
@@ -753,6 +869,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stream<double>, kThreads, smem);
     if (occ < 1) return HODLR_OK;
     void* d = nullptr;
+    slab.resize(slab.size() + 256, 0);  // + zero coefficients for padded U columns
     if (cudaMalloc(&d, slab.size()) != cudaSuccess) return HODLR_OK;
     if (cudaMemcpy(d, slab.data(), slab.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
         cudaFree(d);
@@ -795,6 +912,7 @@ cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* 
         return cudaErrorMisalignedAddress;
     SvKernelArgs<W> a;
     a.slab = sv.slab;
+    a.zeros = sv.slab + sv.dev_bytes - 256;
     a.x = x;
     a.b = b;
     a.partial = partial;
