@@ -47,7 +47,8 @@ constexpr int kM = 256;                 // leaf rows
 constexpr int kNS = 6;                  // ring stages
 constexpr int kStage = 34 * 1024;       // bytes per stage
 constexpr int kConsumers = 16;          // consumer warps
-constexpr int kThreads = 32 * (kConsumers + 2);  // + producer + reducer
+constexpr int kReducers = 4;            // reducer warps (phase-A node reductions)
+constexpr int kThreads = 32 * (kConsumers + 1 + kReducers);  // + producer + reducers
 constexpr int kEvQ = 16;                // pending phase-A completion events
 constexpr int kZeroSlot = 4;            // zero coefficients for padded U columns
 constexpr int kMaxLev = 24;
@@ -142,6 +143,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
+}
+__device__ __forceinline__ void reducer_sync() {
+    asm volatile("bar.sync 2, %0;" ::"n"(kReducers * 32) : "memory");
 }
 
 __host__ __device__ __forceinline__ int fmt_sz(int f) {
@@ -373,7 +377,7 @@ struct SmemCtl {
     volatile int ev_head;          // ... and retired by the reducer warp
     int ev_leaf[kEvQ];
     unsigned ev_done[kEvQ];        // consumer warps finished with the event's leaf
-    int fifo[kFifo];
+    int fifo[kFifo + 4];
     alignas(16) int16_t cidx[512];  // U column (padded groups) -> coefficient slot
 };
 
@@ -571,28 +575,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
             C.ev_tail = ev + 1;
         }
         __syncwarp();
-    } else if (warp == 1) {
-        // =========================================================== reducer
-        // Retires phase-A events in order: once all consumer warps finished the
+    } else if (warp <= kReducers) {
+        // =========================================================== reducers
+        // Retire phase-A events in order: once all consumer warps finished the
         // leaf's partials, bump the counters of its l ancestor nodes; for every
         // node whose last leaf this was, reduce the node's partials in leaf order
-        // (deterministic) into t and publish the node flag.
+        // (fixed thread mapping -> deterministic) into t and publish the flag.
+        const int rt = threadIdx.x - 32;  // 0 .. 32*kReducers-1
+        int* last_mask = reinterpret_cast<int*>(&C.fifo[0]) + kFifo;  // scratch word after the FIFO
         for (int ev = 0;; ++ev) {
             while (C.ev_tail <= ev) __nanosleep(64);
             const int leaf = C.ev_leaf[ev % kEvQ];
             if (leaf < 0) break;
             while (*(volatile unsigned*)&C.ev_done[ev % kEvQ] < (unsigned)kConsumers) __nanosleep(32);
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            bool last = false;
-            if (lane < nlev) {
-                const int k = lane + 1;
-                const int sh = nlev - k;
-                const int id = (1 << k) - 2 + (leaf >> sh);
-                unsigned old;
-                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.counters + id) : "memory");
-                last = old == (1u << sh) - 1u;
+            if (warp == 1) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                bool last = false;
+                if (lane < nlev) {
+                    const int k = lane + 1;
+                    const int sh = nlev - k;
+                    const int id = (1 << k) - 2 + (leaf >> sh);
+                    unsigned old;
+                    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.counters + id) : "memory");
+                    last = old == (1u << sh) - 1u;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, last);
+                if (lane == 0) *last_mask = (int)m;
             }
-            unsigned mask = __ballot_sync(0xffffffffu, last);
+            reducer_sync();
+            unsigned mask = (unsigned)*last_mask;
             while (mask) {
                 const int lv = __ffs(mask) - 1;
                 mask &= mask - 1;
@@ -601,30 +612,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                 const int jn = leaf >> sh;
                 const int nch = 1 << sh;
                 const Level& L = P.lev[lv];
-                for (int c = 0; c < L.r; ++c) {
-                    const W* src = a.partial + L.pbase + ((int64_t)jn * L.r + c) * nch;
-                    W acc = W(0);
-                    for (int i = lane; i < nch; i += 32) acc += __ldcg(src + i);
-                    acc = warp_sum(acc);
-                    if (lane == 0) a.tbuf[L.tbase + (int64_t)jn * L.tstride + c] = acc;
+                if (L.r > 0) {
+                    int tpc = 32;  // threads per column (power of two, divides 32)
+                    while (tpc > 1 && tpc * L.r > 32 * kReducers) tpc >>= 1;
+                    const int cpr = 32 * kReducers / tpc;  // columns per round
+                    for (int c0 = 0; c0 < L.r; c0 += cpr) {
+                        const int c = c0 + rt / tpc, sl = rt % tpc;
+                        W a0 = W(0), a1 = W(0), a2 = W(0), a3 = W(0);
+                        if (c < L.r) {
+                            const W* src = a.partial + L.pbase + ((int64_t)jn * L.r + c) * nch;
+                            int i = sl;
+                            for (; i + 3 * tpc < nch; i += 4 * tpc) {
+                                a0 += __ldcg(src + i);
+                                a1 += __ldcg(src + i + tpc);
+                                a2 += __ldcg(src + i + 2 * tpc);
+                                a3 += __ldcg(src + i + 3 * tpc);
+                            }
+                            for (; i < nch; i += tpc) a0 += __ldcg(src + i);
+                        }
+                        W v = (a0 + a1) + (a2 + a3);
+                        for (int o = tpc >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                        if (sl == 0 && c < L.r) a.tbuf[L.tbase + (int64_t)jn * L.tstride + c] = v;
+                    }
                 }
-                if (lane == 0) {
+                reducer_sync();
+                if (rt == 0) {
                     a.counters[(1 << k) - 2 + jn] = 0u;
                     st_release(&a.flags[(1 << k) - 2 + jn], target);
                 }
-                __syncwarp();
             }
-            if (lane == 0) {
+            if (rt == 0) {
                 C.ev_done[ev % kEvQ] = 0u;
                 __threadfence_block();
                 C.ev_head = ev + 1;
             }
-            __syncwarp();
+            reducer_sync();
         }
     } else {
         // =========================================================== consumers
-        const int cw = warp - 2;
-        const int ctid = threadIdx.x - 64;
+        const int cw = warp - 1 - kReducers;
+        const int ctid = threadIdx.x - 32 * (1 + kReducers);
         int stage = 0;
         unsigned phase = 0;
         int ev = 0;
