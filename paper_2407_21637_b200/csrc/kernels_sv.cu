@@ -44,16 +44,17 @@ namespace hodlr {
 namespace {
 
 constexpr int kM = 256;                 // leaf rows
-constexpr int kNS = 6;                  // ring stages
+constexpr int kNS = 3;                  // ring stages per CTA
+constexpr int kCtasPerSm = 2;           // independent pipelines per SM
 constexpr int kStage = 34 * 1024;       // bytes per stage
-constexpr int kConsumers = 16;          // consumer warps
-constexpr int kReducers = 4;            // reducer warps (phase-A node reductions)
+constexpr int kConsumers = 8;           // consumer warps
+constexpr int kReducers = 2;            // reducer warps (phase-A node reductions)
 constexpr int kThreads = 32 * (kConsumers + 1 + kReducers);  // + producer + reducers
 constexpr int kEvQ = 16;                // pending phase-A completion events
 constexpr int kZeroSlot = 4;            // zero coefficients for padded U columns
 constexpr int kMaxLev = 24;
 constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
-constexpr int kFifo = 32;               // deferred U pieces per CTA
+constexpr int kFifo = 16;               // deferred U pieces per CTA
 constexpr int kXB = kM * 8;             // bytes reserved for x_L in a stage
 
 enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_END = 4 };
@@ -100,7 +101,7 @@ struct SvSync {
 };
 
 struct PieceHdr {
-    int32_t type, leaf, r0, rows;
+    int32_t type, leaf, r0, rows, slot, pad0, pad1, pad2;
     int32_t g, col, ncols, last;
 };
 
@@ -286,16 +287,30 @@ __device__ __forceinline__ void d_piece(const uint8_t* drows, int rows, const W*
     for (int i = 0; i < F::PER; ++i)
 #pragma unroll
         for (int e = 0; e < F::E; ++e) xr[i][e] = xs[(lane + 32 * i) * F::E + e];
-    for (int r = warp; r < rows; r += kConsumers) {
+    for (int r = warp; r < rows; r += 2 * kConsumers) {
+        const int r2 = r + kConsumers;
+        const bool two = r2 < rows;
         const uint8_t* row = drows + (size_t)r * kM * F::bytes;
-        uint4 v[F::PER];
+        const uint8_t* row2 = drows + (size_t)(two ? r2 : r) * kM * F::bytes;
+        uint4 v[F::PER], v2[F::PER];
 #pragma unroll
-        for (int i = 0; i < F::PER; ++i) v[i] = *reinterpret_cast<const uint4*>(row + (lane + 32 * i) * 16);
-        W acc = W(0);
+        for (int i = 0; i < F::PER; ++i) {
+            v[i] = *reinterpret_cast<const uint4*>(row + (lane + 32 * i) * 16);
+            v2[i] = *reinterpret_cast<const uint4*>(row2 + (lane + 32 * i) * 16);
+        }
+        W acc = W(0), acc2 = W(0);
 #pragma unroll
-        for (int i = 0; i < F::PER; ++i) acc = dot16<FMT, W>(v[i], xr[i], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) b[r] = acc;
+        for (int i = 0; i < F::PER; ++i) {
+            acc = dot16<FMT, W>(v[i], xr[i], acc);
+            acc2 = dot16<FMT, W>(v2[i], xr[i], acc2);
+        }
+        const bool hi = lane & 16;
+        W s = hi ? acc2 : acc;
+        s += __shfl_xor_sync(0xffffffffu, hi ? acc : acc2, 16);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) b[r] = s;
+        if (lane == 16 && two) b[r2] = s;
     }
 }
 
@@ -369,6 +384,7 @@ struct SvKernelArgs {
 };
 
 // shared-memory bookkeeping next to the stage ring
+template <typename W>
 struct SmemCtl {
     uint64_t full[kNS], empty[kNS];
     PieceHdr hdr[kNS];
@@ -378,14 +394,15 @@ struct SmemCtl {
     int ev_leaf[kEvQ];
     unsigned ev_done[kEvQ];        // consumer warps finished with the event's leaf
     int fifo[kFifo + 4];
+    alignas(16) W ybuf[kFifo][32];  // leaf products y = D x of pending phase-B items
     alignas(16) int16_t cidx[512];  // U column (padded groups) -> coefficient slot
 };
 
 template <typename W>
-__global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ SvParams P, SvKernelArgs<W> a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_constant__ SvParams P, SvKernelArgs<W> a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* stages = smem;
-    SmemCtl& C = *reinterpret_cast<SmemCtl*>(smem + kNS * kStage);
+    SmemCtl<W>& C = *reinterpret_cast<SmemCtl<W>*>(smem + kNS * kStage);
     unsigned* bitset = reinterpret_cast<unsigned*>(&C + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -441,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
             }
             return __all_sync(0xffffffffu, ok);
         };
-        auto emit_u = [&](int leaf, int r0) {
+        auto emit_u = [&](int leaf, int r0, int slot) {
             uint8_t* st = claim();
             const int wbytes = (int)sizeof(W);
             const int coef_bytes = P.coef_elems * wbytes;
@@ -451,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                 h.leaf = leaf;
                 h.r0 = r0;
                 h.rows = P.rbi;
+                h.slot = slot;
                 mbar_arrive_tx(&C.full[stage], (unsigned)P.ubytes[sizeof(W) == 8 ? 1 : 0]);
             }
             __syncwarp();
@@ -489,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                     __nanosleep(256);
                     continue;
                 }
-                emit_u(leaf, r0);
+                emit_u(leaf, r0, fh % kFifo);
                 ++fh;
             }
         };
@@ -539,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                 const int r0 = (bi % per_leaf) * P.rbi;
                 const uint8_t* dbase = a.slab + (int64_t)leaf * P.slab_bytes + P.d_off;
                 const int dsz = fmt_sz(P.leaf_fmt);
+                if (ft - fh == kFifo) flush_fifo(true);  // frees the y slot this item will use
                 for (int p = 0; p < P.dpieces; ++p) {
                     uint8_t* st = claim();
                     const int rr = r0 + p * P.rbd;
@@ -549,6 +568,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                         h.leaf = leaf;
                         h.r0 = rr;
                         h.rows = P.rbd;
+                        h.slot = ft % kFifo;
+                        h.pad0 = p * P.rbd;  // row offset inside the item
                         mbar_arrive_tx(&C.full[stage], (unsigned)(kM * sizeof(W)) + cb);
                         bulk_g2s(st, a.x + (int64_t)leaf * kM, (unsigned)(kM * sizeof(W)), &C.full[stage]);
                         bulk_g2s(st + kXB, dbase + (int64_t)rr * kM * dsz, cb, &C.full[stage]);
@@ -556,7 +577,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                     __syncwarp();
                     next_stage();
                 }
-                if (ft - fh == kFifo) flush_fifo(true);
                 if (lane == 0) C.fifo[ft % kFifo] = (leaf << 12) | r0;
                 __syncwarp();
                 ++ft;
@@ -664,7 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                 a_piece<W>(h.g, st + kXB, h.ncols, reinterpret_cast<const W*>(st), cw, lane, P, h.leaf, h.col,
                            a.partial);
             } else if (h.type == PT_D) {
-                W* brow = a.b + (int64_t)h.leaf * kM + h.r0;
+                W* brow = &C.ybuf[h.slot][h.pad0];
                 const W* xs = reinterpret_cast<const W*>(st);
                 if (P.leaf_fmt == HODLR_FMT_FP64) d_piece<HODLR_FMT_FP64, W>(st + kXB, h.rows, xs, cw, lane, brow);
                 else d_piece<HODLR_FMT_FP32, W>(st + kXB, h.rows, xs, cw, lane, brow);
@@ -672,7 +692,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
                 consumer_sync();  // the D pieces of these rows were written by other warps
                 const int row = ctid >> P.tpr_shift, q = ctid & ((1 << P.tpr_shift) - 1);
                 W* bp = a.b + (int64_t)h.leaf * kM + h.r0 + row;
-                const W bold = q == 0 ? *bp : W(0);
                 const W* coef = reinterpret_cast<const W*>(st);
                 W acc = W(0);
                 int off = (P.coef_elems + kZeroSlot) * (int)sizeof(W);
@@ -688,7 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1)
                     if (o < (1 << P.tpr_shift)) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (q == 0) *bp = acc + bold;
+                if (q == 0) *bp = acc + C.ybuf[h.slot][row];  // b written once: U t + D x
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&C.empty[stage]);
@@ -720,7 +739,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(const __grid_constant__ 
 }
 
 size_t smem_bytes(int bitset_words) {
-    return (size_t)kNS * kStage + sizeof(SmemCtl) + (size_t)bitset_words * 4;
+    return (size_t)kNS * kStage + sizeof(SmemCtl<double>) + (size_t)bitset_words * 4;
 }
 
 }  // namespace
@@ -911,7 +930,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     sv.rb = P.rbi;
     sv.num_items_a = P.num_a;
     sv.num_items_b = P.num_b;
-    sv.grid = std::min(sms, P.num_a + P.num_b);
+    sv.grid = std::min(sms * std::min(occ, kCtasPerSm), P.num_a + P.num_b);
     sv.launches = 1;
     sv.tfast_count = tb;
     sv.extra_ws = (sizeof(SvSync) + 2 * (size_t)P.nnodes * sizeof(unsigned) + 255) / 256 * 256 + (size_t)tb * 8;
