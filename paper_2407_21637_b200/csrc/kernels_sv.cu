@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -58,6 +59,16 @@ constexpr int kFifo = 16;               // deferred U pieces per CTA
 constexpr int kXB = kM * 8;             // bytes reserved for x_L in a stage
 
 enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_END = 4 };
+
+#ifdef HODLR_PROFILE
+// per-CTA cycle accounting (debug build only): [0] producer empty-wait, [1] producer
+// fifo-block, [2] consumer full-wait, [3..5] consumer busy A/D/U, [6] kernel total
+#define PROF_T(v) long long v = clock64()
+#define PROF_ADD(i, dt) if (lane == 0) atomicAdd((unsigned long long*)&prof[i], (unsigned long long)(dt))
+#else
+#define PROF_T(v)
+#define PROF_ADD(i, dt)
+#endif
 
 struct Level {
     int32_t r, fmt;
@@ -97,7 +108,7 @@ struct SvParams {
 };
 
 struct SvSync {
-    unsigned epoch, queue, done, pad;
+    unsigned epoch, queue, done, published;  // published: node flags set this call
 };
 
 struct PieceHdr {
@@ -402,6 +413,11 @@ template <typename W>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_constant__ SvParams P, SvKernelArgs<W> a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* stages = smem;
+#ifdef HODLR_PROFILE
+    __shared__ long long prof[8];
+    if (threadIdx.x < 8) prof[threadIdx.x] = 0;
+    const long long t_kernel = clock64();
+#endif
     SmemCtl<W>& C = *reinterpret_cast<SmemCtl<W>*>(smem + kNS * kStage);
     unsigned* bitset = reinterpret_cast<unsigned*>(&C + 1);
 
@@ -438,11 +454,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             }
         };
         auto claim = [&]() -> uint8_t* {
+            PROF_T(t0);
             mbar_wait(&C.empty[stage], phase ^ 1u);
+            PROF_ADD(0, clock64() - t0);
             return stages + (size_t)stage * kStage;
         };
         // are the coefficients of every level of `leaf` published?
+        bool all_ready = false;  // every node of this call published: no more polls
         auto ready = [&](int leaf) -> bool {
+            if (all_ready) return true;
+            unsigned pub = 0;
+            if (lane == 0) pub = ld_acquire(&a.sync->published);
+            if (__shfl_sync(0xffffffffu, pub, 0) == (unsigned)P.nnodes) {
+                all_ready = true;
+                return true;
+            }
             bool ok = true;
             if (lane < nlev) {
                 const int k = lane + 1;
@@ -504,7 +530,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 const int leaf = e >> 12, r0 = e & 0xfff;
                 if (!ready(leaf)) {
                     if (!block) return;
+                    PROF_T(t0);
                     __nanosleep(256);
+                    PROF_ADD(1, clock64() - t0);
                     continue;
                 }
                 emit_u(leaf, r0, fh % kFifo);
@@ -518,12 +546,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             C.ev_tail = ev + 1;
         };
 
-        int item = 0;
-        if (lane == 0) item = (int)atomicAdd(&a.sync->queue, 1u);
+        // work items, fetched two ahead so the atomic's latency hides behind emission
+        int item = 0, n1 = 0, n2 = 0;
+        if (lane == 0) {
+            item = (int)atomicAdd(&a.sync->queue, 1u);
+            n1 = (int)atomicAdd(&a.sync->queue, 1u);
+        }
         item = __shfl_sync(0xffffffffu, item, 0);
         while (item < total) {
-            int nxt = 0;
-            if (lane == 0) nxt = (int)atomicAdd(&a.sync->queue, 1u);  // consumed next round
+            if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);  // consumed two rounds later
             if (item < P.num_a) {
                 const int leaf = item;
                 const uint8_t* base = a.slab + (int64_t)leaf * P.slab_bytes;
@@ -582,7 +613,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 ++ft;
                 flush_fifo(false);
             }
-            item = __shfl_sync(0xffffffffu, nxt, 0);
+            item = __shfl_sync(0xffffffffu, n1, 0);
+            n1 = n2;
         }
         flush_fifo(true);
         claim();
@@ -659,6 +691,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 if (rt == 0) {
                     a.counters[(1 << k) - 2 + jn] = 0u;
                     st_release(&a.flags[(1 << k) - 2 + jn], target);
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&a.sync->published) : "memory");
                 }
             }
             if (rt == 0) {
@@ -676,7 +709,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         unsigned phase = 0;
         int ev = 0;
         for (;;) {
+            PROF_T(tw);
             mbar_wait(&C.full[stage], phase);
+            PROF_T(tb);
+            PROF_ADD(2, tb - tw);
             const PieceHdr h = C.hdr[stage];
             const uint8_t* st = stages + (size_t)stage * kStage;
             if (h.type == PT_END) break;
@@ -711,6 +747,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&C.empty[stage]);
+            PROF_ADD(2 + h.type, clock64() - tb);
             if (h.type == PT_A && h.last) {
                 // this warp's partials of the leaf are written: tell the reducer
                 if (lane == 0) {
@@ -727,12 +764,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     }
     // ---- teardown: the last CTA resets the queue and publishes the next epoch
     __syncthreads();
+#ifdef HODLR_PROFILE
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 101 || blockIdx.x == 250))
+        printf("PROF cta %d: total %lld prod_empty %lld prod_fifo %lld cons_wait %lld busyA %lld busyD %lld busyU %lld (consumer sums over %d warps)\n",
+               blockIdx.x, clock64() - t_kernel, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], kConsumers);
+#endif
     if (threadIdx.x == 0) {
         unsigned old;
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&a.sync->done) : "memory");
         if (old == gridDim.x - 1) {
             a.sync->queue = 0u;
             a.sync->done = 0u;
+            a.sync->published = 0u;
             st_release(&a.sync->epoch, target);
         }
     }
