@@ -55,7 +55,6 @@ constexpr int kEvQ = 16;                // pending phase-A completion events
 constexpr int kZeroSlot = 4;            // zero coefficients for padded U columns
 constexpr int kMaxLev = 24;
 constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
-constexpr int kFifo = 16;               // deferred U pieces per CTA
 constexpr int kXB = kM * 8;             // bytes reserved for x_L in a stage
 
 enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_END = 4 };
@@ -87,7 +86,7 @@ struct APiece {
 struct SvParams {
     int32_t depth, nleaves, nnodes;
     int32_t rbi, rbd, dpieces, napieces;
-    int32_t num_a, num_b;
+    int32_t num_a, num_d, num_u;
     int32_t leaf_fmt;
     int64_t slab_bytes, us_off, d_off;
     int32_t gcols[5];              // columns per format group (V' slab)
@@ -96,9 +95,9 @@ struct SvParams {
     int32_t ucols_total;
     int32_t tpr_shift;             // log2(threads per U row)
     int32_t ubytes[2];             // U-piece transaction bytes for fp32 / fp64 working
+    int32_t uy_off[2];             // offset of the staged y rows inside a U piece
     int64_t vgoff[5], ugoff[5];    // byte offsets of the groups inside the V' / U slabs
     int32_t coef_elems;            // padded coefficient elements per U piece
-    int32_t bitset_words;
     Level lev[kMaxLev];
     APiece ap[kMaxPieces];
     int8_t col_level[512];         // flattened (group, column) -> level (0-based)
@@ -108,7 +107,8 @@ struct SvParams {
 };
 
 struct SvSync {
-    unsigned epoch, queue, done, published;  // published: node flags set this call
+    unsigned epoch, queue, done, published;  // published: nodes whose t exists (this call)
+    unsigned leaves_done, pad[3];            // leaves whose D results are all in b
 };
 
 struct PieceHdr {
@@ -390,22 +390,20 @@ struct SvKernelArgs {
     W* partial;
     W* tbuf;
     SvSync* sync;
-    unsigned* counters;
-    unsigned* flags;
+    unsigned* counters;    // [nnodes]: leaves counted into each node (last arriver reduces)
+    unsigned* dcount;      // [nleaves]: consumer-warp arrivals of the leaf's D pieces
 };
 
 // shared-memory bookkeeping next to the stage ring
-template <typename W>
 struct SmemCtl {
     uint64_t full[kNS], empty[kNS];
     PieceHdr hdr[kNS];
     unsigned epoch;
     volatile int ev_tail;          // phase-A completion events pushed by the producer
-    volatile int ev_head;          // ... and retired by the reducer warp
+    volatile int ev_head;          // ... and retired by the reducer warps
     int ev_leaf[kEvQ];
     unsigned ev_done[kEvQ];        // consumer warps finished with the event's leaf
-    int fifo[kFifo + 4];
-    alignas(16) W ybuf[kFifo][32];  // leaf products y = D x of pending phase-B items
+    int last_mask;
     alignas(16) int16_t cidx[512];  // U column (padded groups) -> coefficient slot
 };
 
@@ -418,12 +416,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     if (threadIdx.x < 8) prof[threadIdx.x] = 0;
     const long long t_kernel = clock64();
 #endif
-    SmemCtl<W>& C = *reinterpret_cast<SmemCtl<W>*>(smem + kNS * kStage);
-    unsigned* bitset = reinterpret_cast<unsigned*>(&C + 1);
+    SmemCtl& C = *reinterpret_cast<SmemCtl*>(smem + kNS * kStage);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int total = P.num_a + P.num_b;
     const int nlev = P.depth;
+    const int nq = P.num_d + P.num_u;  // dynamic queue: D items, then U items
+    const unsigned d_expect = (unsigned)(P.dpieces * (kM / P.rbi) * kConsumers);  // per leaf
 
     if (threadIdx.x == 0) {
         C.epoch = ld_acquire(&a.sync->epoch);
@@ -436,7 +434,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = threadIdx.x; i < kEvQ; i += kThreads) C.ev_done[i] = 0u;
-    for (int i = threadIdx.x; i < P.bitset_words; i += kThreads) bitset[i] = 0u;
     for (int i = threadIdx.x; i < P.ucols_total; i += kThreads) C.cidx[i] = P.ucidx[i];
     __syncthreads();
     const unsigned target = C.epoch + 1u;
@@ -445,8 +442,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         // =========================================================== producer
         int stage = 0;
         unsigned phase = 0;
-        int fh = 0, ft = 0;  // deferred-U FIFO head / tail (warp-uniform)
-        int ev = 0;          // phase-A events pushed
+        int ev = 0;  // phase-A events pushed
         auto next_stage = [&]() {
             if (++stage == kNS) {
                 stage = 0;
@@ -459,136 +455,57 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             PROF_ADD(0, clock64() - t0);
             return stages + (size_t)stage * kStage;
         };
-        // are the coefficients of every level of `leaf` published?
-        bool all_ready = false;  // every node of this call published: no more polls
-        auto ready = [&](int leaf) -> bool {
-            if (all_ready) return true;
-            unsigned pub = 0;
-            if (lane == 0) pub = ld_acquire(&a.sync->published);
-            if (__shfl_sync(0xffffffffu, pub, 0) == (unsigned)P.nnodes) {
-                all_ready = true;
-                return true;
-            }
-            bool ok = true;
-            if (lane < nlev) {
-                const int k = lane + 1;
-                const int sib = (1 << k) - 2 + ((leaf >> (nlev - k)) ^ 1);
-                const bool cached = P.bitset_words ? ((bitset[sib >> 5] >> (sib & 31)) & 1u) : false;
-                if (!cached) {
-                    if (ld_acquire(&a.flags[sib]) == target) {
-                        if (P.bitset_words) atomicOr(&bitset[sib >> 5], 1u << (sib & 31));
-                    } else {
-                        ok = false;
-                    }
-                }
-            }
-            return __all_sync(0xffffffffu, ok);
-        };
-        auto emit_u = [&](int leaf, int r0, int slot) {
-            uint8_t* st = claim();
-            const int wbytes = (int)sizeof(W);
-            const int coef_bytes = P.coef_elems * wbytes;
-            if (lane == 0) {
-                PieceHdr& h = C.hdr[stage];
-                h.type = PT_U;
-                h.leaf = leaf;
-                h.r0 = r0;
-                h.rows = P.rbi;
-                h.slot = slot;
-                mbar_arrive_tx(&C.full[stage], (unsigned)P.ubytes[sizeof(W) == 8 ? 1 : 0]);
-            }
-            __syncwarp();
-            // coefficients were written by other SMs (generic proxy, release/acquire on
-            // the flag); order them before this SM's async-proxy reads
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            if (lane < nlev) {
-                const Level& L = P.lev[lane];
-                if (L.r > 0) {
-                    const int k = lane + 1;
-                    const int jsib = (leaf >> (nlev - k)) ^ 1;
-                    const W* src = a.tbuf + L.tbase + (int64_t)jsib * L.tstride;
-                    bulk_g2s(st + (size_t)L.slot * wbytes, src, (unsigned)(L.tstride * wbytes), &C.full[stage]);
-                }
-            } else if (lane >= 24 && lane < 29) {
-                const int g = lane - 24;
-                if (P.gpad[g] > 0) {
-                    const uint8_t* src = a.slab + (int64_t)leaf * P.slab_bytes + P.us_off + P.ugoff[g] +
-                                         (int64_t)r0 * P.gpad[g] * fmt_sz(g);
-                    int off = coef_bytes + kZeroSlot * wbytes;
-                    for (int q = 0; q < g; ++q) off += P.rbi * P.gpad[q] * fmt_sz(q);
-                    bulk_g2s(st + off, src, (unsigned)(P.rbi * P.gpad[g] * fmt_sz(g)), &C.full[stage]);
-                }
-            } else if (lane == 31) {
-                bulk_g2s(st + coef_bytes, a.zeros, (unsigned)(kZeroSlot * wbytes), &C.full[stage]);
-            }
-            __syncwarp();
-            next_stage();
-        };
-        auto flush_fifo = [&](bool block) {
-            while (fh != ft) {
-                const int e = C.fifo[fh % kFifo];
-                const int leaf = e >> 12, r0 = e & 0xfff;
-                if (!ready(leaf)) {
-                    if (!block) return;
-                    PROF_T(t0);
-                    __nanosleep(256);
-                    PROF_ADD(1, clock64() - t0);
-                    continue;
-                }
-                emit_u(leaf, r0, fh % kFifo);
-                ++fh;
-            }
-        };
         auto push_event = [&](int leaf) {  // lane 0
             while (ev - C.ev_head >= kEvQ) __nanosleep(64);
             C.ev_leaf[ev % kEvQ] = leaf;
             __threadfence_block();
             C.ev_tail = ev + 1;
         };
+        bool coef_ready = false, d_ready = false;
 
-        // work items, fetched two ahead so the atomic's latency hides behind emission
-        int item = 0, n1 = 0, n2 = 0;
-        if (lane == 0) {
-            item = (int)atomicAdd(&a.sync->queue, 1u);
-            n1 = (int)atomicAdd(&a.sync->queue, 1u);
-        }
-        item = __shfl_sync(0xffffffffu, item, 0);
-        while (item < total) {
-            if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);  // consumed two rounds later
-            if (item < P.num_a) {
-                const int leaf = item;
-                const uint8_t* base = a.slab + (int64_t)leaf * P.slab_bytes;
-                if (lane == 0) push_event(leaf);
-                ++ev;
-                __syncwarp();
-                for (int p = 0; p < P.napieces; ++p) {
-                    const APiece ap = P.ap[p];
-                    uint8_t* st = claim();
-                    const unsigned cb = (unsigned)(ap.ncols * kM * fmt_sz(ap.g));
-                    if (lane == 0) {
-                        PieceHdr& h = C.hdr[stage];
-                        h.type = PT_A;
-                        h.leaf = leaf;
-                        h.g = ap.g;
-                        h.col = ap.col;
-                        h.ncols = ap.ncols;
-                        h.last = (p == P.napieces - 1);
-                        mbar_arrive_tx(&C.full[stage], (unsigned)(kM * sizeof(W)) + cb);
-                        bulk_g2s(st, a.x + (int64_t)leaf * kM, (unsigned)(kM * sizeof(W)), &C.full[stage]);
-                        bulk_g2s(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.col * kM * fmt_sz(ap.g), cb,
-                                 &C.full[stage]);
-                    }
-                    __syncwarp();
-                    next_stage();
+        // ---- phase A: leaves dealt round-robin, every CTA starts with its share
+        for (int leaf = blockIdx.x; leaf < P.num_a; leaf += gridDim.x) {
+            const uint8_t* base = a.slab + (int64_t)leaf * P.slab_bytes;
+            if (lane == 0) push_event(leaf);
+            ++ev;
+            __syncwarp();
+            for (int p = 0; p < P.napieces; ++p) {
+                const APiece ap = P.ap[p];
+                uint8_t* st = claim();
+                const unsigned cb = (unsigned)(ap.ncols * kM * fmt_sz(ap.g));
+                if (lane == 0) {
+                    PieceHdr& h = C.hdr[stage];
+                    h.type = PT_A;
+                    h.leaf = leaf;
+                    h.g = ap.g;
+                    h.col = ap.col;
+                    h.ncols = ap.ncols;
+                    h.last = (p == P.napieces - 1);
+                    mbar_arrive_tx(&C.full[stage], (unsigned)(kM * sizeof(W)) + cb);
+                    bulk_g2s(st, a.x + (int64_t)leaf * kM, (unsigned)(kM * sizeof(W)), &C.full[stage]);
+                    bulk_g2s(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.col * kM * fmt_sz(ap.g), cb, &C.full[stage]);
                 }
-            } else {
-                const int bi = item - P.num_a;
-                const int per_leaf = kM / P.rbi;
-                const int leaf = bi / per_leaf;
-                const int r0 = (bi % per_leaf) * P.rbi;
+                __syncwarp();
+                next_stage();
+            }
+        }
+        // ---- phases B (D items) and C (U items) from one atomic queue, two ahead
+        int n1 = 0, n2 = 0;
+        if (lane == 0) {
+            n1 = (int)atomicAdd(&a.sync->queue, 1u);
+            n2 = (int)atomicAdd(&a.sync->queue, 1u);
+        }
+        const int per_leaf = kM / P.rbi;
+        for (;;) {
+            const int q = __shfl_sync(0xffffffffu, n1, 0);
+            if (q >= nq) break;
+            n1 = n2;
+            if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);
+            if (q < P.num_d) {
+                const int leaf = q / per_leaf;
+                const int r0 = (q % per_leaf) * P.rbi;
                 const uint8_t* dbase = a.slab + (int64_t)leaf * P.slab_bytes + P.d_off;
                 const int dsz = fmt_sz(P.leaf_fmt);
-                if (ft - fh == kFifo) flush_fifo(true);  // frees the y slot this item will use
                 for (int p = 0; p < P.dpieces; ++p) {
                     uint8_t* st = claim();
                     const int rr = r0 + p * P.rbd;
@@ -599,8 +516,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                         h.leaf = leaf;
                         h.r0 = rr;
                         h.rows = P.rbd;
-                        h.slot = ft % kFifo;
-                        h.pad0 = p * P.rbd;  // row offset inside the item
                         mbar_arrive_tx(&C.full[stage], (unsigned)(kM * sizeof(W)) + cb);
                         bulk_g2s(st, a.x + (int64_t)leaf * kM, (unsigned)(kM * sizeof(W)), &C.full[stage]);
                         bulk_g2s(st + kXB, dbase + (int64_t)rr * kM * dsz, cb, &C.full[stage]);
@@ -608,21 +523,78 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     __syncwarp();
                     next_stage();
                 }
-                if (lane == 0) C.fifo[ft % kFifo] = (leaf << 12) | r0;
+            } else {
+                const int u = q - P.num_d;
+                const int leaf = u / per_leaf;
+                const int r0 = (u % per_leaf) * P.rbi;
+                // the coefficients of every node, and this leaf's D results, must exist
+                PROF_T(tr0);
+                if (!coef_ready) {
+                    unsigned pub = 0;
+                    if (lane == 0)
+                        while ((pub = ld_acquire(&a.sync->published)) != (unsigned)P.nnodes) __nanosleep(128);
+                    coef_ready = true;
+                }
+                if (!d_ready) {
+                    if (lane == 0) {
+                        if (ld_acquire(&a.sync->leaves_done) == (unsigned)P.nleaves) {
+                            d_ready = true;
+                        } else {
+                            while (ld_acquire(&a.dcount[leaf]) != d_expect) __nanosleep(64);
+                        }
+                    }
+                    d_ready = __shfl_sync(0xffffffffu, d_ready, 0);
+                }
+                PROF_ADD(6, clock64() - tr0);
                 __syncwarp();
-                ++ft;
-                flush_fifo(false);
+                uint8_t* st = claim();
+                const int wbytes = (int)sizeof(W);
+                const int coef_bytes = P.coef_elems * wbytes;
+                const int yoff = P.uy_off[sizeof(W) == 8 ? 1 : 0];
+                if (lane == 0) {
+                    PieceHdr& h = C.hdr[stage];
+                    h.type = PT_U;
+                    h.leaf = leaf;
+                    h.r0 = r0;
+                    h.rows = P.rbi;
+                    mbar_arrive_tx(&C.full[stage], (unsigned)P.ubytes[sizeof(W) == 8 ? 1 : 0]);
+                }
+                __syncwarp();
+                // coefficients and y were written by other SMs (generic proxy, made
+                // visible by the acquires above); order them before the async-proxy reads
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                if (lane < nlev) {
+                    const Level& L = P.lev[lane];
+                    if (L.r > 0) {
+                        const int k = lane + 1;
+                        const int jsib = (leaf >> (nlev - k)) ^ 1;
+                        const W* src = a.tbuf + L.tbase + (int64_t)jsib * L.tstride;
+                        bulk_g2s(st + (size_t)L.slot * wbytes, src, (unsigned)(L.tstride * wbytes), &C.full[stage]);
+                    }
+                } else if (lane >= 24 && lane < 29) {
+                    const int g = lane - 24;
+                    if (P.gpad[g] > 0) {
+                        const uint8_t* src = a.slab + (int64_t)leaf * P.slab_bytes + P.us_off + P.ugoff[g] +
+                                             (int64_t)r0 * P.gpad[g] * fmt_sz(g);
+                        int off = coef_bytes + kZeroSlot * wbytes;
+                        for (int g2 = 0; g2 < g; ++g2) off += P.rbi * P.gpad[g2] * fmt_sz(g2);
+                        bulk_g2s(st + off, src, (unsigned)(P.rbi * P.gpad[g] * fmt_sz(g)), &C.full[stage]);
+                    }
+                } else if (lane == 30) {
+                    bulk_g2s(st + yoff, a.b + (int64_t)leaf * kM + r0, (unsigned)(P.rbi * wbytes), &C.full[stage]);
+                } else if (lane == 31) {
+                    bulk_g2s(st + coef_bytes, a.zeros, (unsigned)(kZeroSlot * wbytes), &C.full[stage]);
+                }
+                __syncwarp();
+                next_stage();
             }
-            item = __shfl_sync(0xffffffffu, n1, 0);
-            n1 = n2;
         }
-        flush_fifo(true);
         claim();
         if (lane == 0) {
             C.hdr[stage].type = PT_END;
             mbar_arrive(&C.full[stage]);
             while (ev - C.ev_head >= kEvQ) __nanosleep(64);
-            C.ev_leaf[ev % kEvQ] = -1;  // reducer: done
+            C.ev_leaf[ev % kEvQ] = -1;  // reducers: done
             __threadfence_block();
             C.ev_tail = ev + 1;
         }
@@ -632,16 +604,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         // Retire phase-A events in order: once all consumer warps finished the
         // leaf's partials, bump the counters of its l ancestor nodes; for every
         // node whose last leaf this was, reduce the node's partials in leaf order
-        // (fixed thread mapping -> deterministic) into t and publish the flag.
+        // (fixed thread mapping -> deterministic) into t and count it published.
         const int rt = threadIdx.x - 32;  // 0 .. 32*kReducers-1
-        int* last_mask = reinterpret_cast<int*>(&C.fifo[0]) + kFifo;  // scratch word after the FIFO
         for (int ev = 0;; ++ev) {
-            while (C.ev_tail <= ev) __nanosleep(64);
+            if (rt == 0)
+                while (C.ev_tail <= ev) __nanosleep(256);
+            reducer_sync();
             const int leaf = C.ev_leaf[ev % kEvQ];
             if (leaf < 0) break;
-            while (*(volatile unsigned*)&C.ev_done[ev % kEvQ] < (unsigned)kConsumers) __nanosleep(32);
+            if (rt == 0)
+                while (*(volatile unsigned*)&C.ev_done[ev % kEvQ] < (unsigned)kConsumers) __nanosleep(64);
             if (warp == 1) {
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                if (lane == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                __syncwarp();
                 bool last = false;
                 if (lane < nlev) {
                     const int k = lane + 1;
@@ -652,10 +627,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     last = old == (1u << sh) - 1u;
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, last);
-                if (lane == 0) *last_mask = (int)m;
+                if (lane == 0) C.last_mask = (int)m;
             }
             reducer_sync();
-            unsigned mask = (unsigned)*last_mask;
+            unsigned mask = (unsigned)C.last_mask;
+            int published = 0;
             while (mask) {
                 const int lv = __ffs(mask) - 1;
                 mask &= mask - 1;
@@ -670,36 +646,37 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     const int cpr = 32 * kReducers / tpc;  // columns per round
                     for (int c0 = 0; c0 < L.r; c0 += cpr) {
                         const int c = c0 + rt / tpc, sl = rt % tpc;
-                        W a0 = W(0), a1 = W(0), a2 = W(0), a3 = W(0);
+                        W acc = W(0);
                         if (c < L.r) {
                             const W* src = a.partial + L.pbase + ((int64_t)jn * L.r + c) * nch;
-                            int i = sl;
-                            for (; i + 3 * tpc < nch; i += 4 * tpc) {
-                                a0 += __ldcg(src + i);
-                                a1 += __ldcg(src + i + tpc);
-                                a2 += __ldcg(src + i + 2 * tpc);
-                                a3 += __ldcg(src + i + 3 * tpc);
+                            constexpr int B = 8;  // loads in flight per thread
+                            for (int i0 = sl; i0 < nch; i0 += B * tpc) {
+                                W v[B];
+#pragma unroll
+                                for (int u = 0; u < B; ++u) {
+                                    const int i = i0 + u * tpc;
+                                    v[u] = i < nch ? __ldcg(src + i) : W(0);
+                                }
+#pragma unroll
+                                for (int u = 0; u < B; ++u) acc += v[u];
                             }
-                            for (; i < nch; i += tpc) a0 += __ldcg(src + i);
                         }
-                        W v = (a0 + a1) + (a2 + a3);
-                        for (int o = tpc >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                        if (sl == 0 && c < L.r) a.tbuf[L.tbase + (int64_t)jn * L.tstride + c] = v;
+                        for (int o = tpc >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                        if (sl == 0 && c < L.r) a.tbuf[L.tbase + (int64_t)jn * L.tstride + c] = acc;
                     }
                 }
-                reducer_sync();
-                if (rt == 0) {
-                    a.counters[(1 << k) - 2 + jn] = 0u;
-                    st_release(&a.flags[(1 << k) - 2 + jn], target);
-                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&a.sync->published) : "memory");
-                }
+                if (rt == 0) a.counters[(1 << k) - 2 + jn] = 0u;
+                ++published;
             }
+            reducer_sync();
             if (rt == 0) {
+                if (published)
+                    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->published), "r"(published)
+                                 : "memory");
                 C.ev_done[ev % kEvQ] = 0u;
                 __threadfence_block();
                 C.ev_head = ev + 1;
             }
-            reducer_sync();
         }
     } else {
         // =========================================================== consumers
@@ -720,15 +697,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 a_piece<W>(h.g, st + kXB, h.ncols, reinterpret_cast<const W*>(st), cw, lane, P, h.leaf, h.col,
                            a.partial);
             } else if (h.type == PT_D) {
-                W* brow = &C.ybuf[h.slot][h.pad0];
+                W* brow = a.b + (int64_t)h.leaf * kM + h.r0;
                 const W* xs = reinterpret_cast<const W*>(st);
                 if (P.leaf_fmt == HODLR_FMT_FP64) d_piece<HODLR_FMT_FP64, W>(st + kXB, h.rows, xs, cw, lane, brow);
                 else d_piece<HODLR_FMT_FP32, W>(st + kXB, h.rows, xs, cw, lane, brow);
-            } else {  // PT_U
-                consumer_sync();  // the D pieces of these rows were written by other warps
+            } else {  // PT_U: b = U t + y (y = D x, staged from b)
                 const int row = ctid >> P.tpr_shift, q = ctid & ((1 << P.tpr_shift) - 1);
-                W* bp = a.b + (int64_t)h.leaf * kM + h.r0 + row;
                 const W* coef = reinterpret_cast<const W*>(st);
+                const W* ys = reinterpret_cast<const W*>(st + P.uy_off[sizeof(W) == 8 ? 1 : 0]);
                 W acc = W(0);
                 int off = (P.coef_elems + kZeroSlot) * (int)sizeof(W);
                 for (int g = 0; g < 5; ++g) {
@@ -736,25 +712,30 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     if (nc == 0) continue;
                     const uint8_t* ub = st + off + (size_t)row * nc * fmt_sz(g);
                     const int16_t* ci = C.cidx + P.gstart_pad[g];
-                    for (int j = 4 * q; j < nc; j += 4 << P.tpr_shift)
-                        acc = u_dot4<W>(g, ub, j, ci, coef, acc);
+                    for (int j = 4 * q; j < nc; j += 4 << P.tpr_shift) acc = u_dot4<W>(g, ub, j, ci, coef, acc);
                     off += h.rows * nc * fmt_sz(g);
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1)
                     if (o < (1 << P.tpr_shift)) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (q == 0) *bp = acc + C.ybuf[h.slot][row];  // b written once: U t + D x
+                if (q == 0) a.b[(int64_t)h.leaf * kM + h.r0 + row] = acc + ys[row];  // levels, then leaf
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&C.empty[stage]);
             PROF_ADD(2 + h.type, clock64() - tb);
             if (h.type == PT_A && h.last) {
-                // this warp's partials of the leaf are written: tell the reducer
+                // this warp's partials of the leaf are written: tell the reducers
                 if (lane == 0) {
                     asm volatile("fence.acq_rel.cta;" ::: "memory");
                     atomicAdd(&C.ev_done[ev % kEvQ], 1u);
                 }
                 ++ev;
+            } else if (h.type == PT_D && lane == 0) {
+                // this warp's rows of y are in b: count it toward the leaf's D completion
+                unsigned old;
+                asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.dcount + h.leaf) : "memory");
+                if (old == d_expect - 1u)
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&a.sync->leaves_done) : "memory");
             }
             if (++stage == kNS) {
                 stage = 0;
@@ -762,27 +743,39 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             }
         }
     }
-    // ---- teardown: the last CTA resets the queue and publishes the next epoch
+    // ---- teardown: the last CTA resets the per-call state and bumps the epoch
     __syncthreads();
 #ifdef HODLR_PROFILE
     if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 101 || blockIdx.x == 250))
-        printf("PROF cta %d: total %lld prod_empty %lld prod_fifo %lld cons_wait %lld busyA %lld busyD %lld busyU %lld (consumer sums over %d warps)\n",
-               blockIdx.x, clock64() - t_kernel, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], kConsumers);
+        printf("PROF cta %d: total %lld prod_empty %lld wait_ready %lld | cons_wait %lld busyA %lld busyD %lld busyU %lld (consumer sums over %d warps)\n",
+               blockIdx.x, clock64() - t_kernel, prof[0], prof[6], prof[2], prof[3], prof[4], prof[5], kConsumers);
 #endif
+    __shared__ unsigned s_last;
     if (threadIdx.x == 0) {
         unsigned old;
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&a.sync->done) : "memory");
-        if (old == gridDim.x - 1) {
+        s_last = old == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        for (int i = threadIdx.x; i < P.nleaves; i += kThreads) a.dcount[i] = 0u;
+        __syncthreads();
+        if (threadIdx.x == 0) {
             a.sync->queue = 0u;
             a.sync->done = 0u;
             a.sync->published = 0u;
+            a.sync->leaves_done = 0u;
+            __threadfence();
             st_release(&a.sync->epoch, target);
         }
     }
 }
 
-size_t smem_bytes(int bitset_words) {
-    return (size_t)kNS * kStage + sizeof(SmemCtl<double>) + (size_t)bitset_words * 4;
+size_t smem_bytes() { return (size_t)kNS * kStage + sizeof(SmemCtl); }
+
+// workspace head: SvSync, node counters, leaf D counters (zeroed once, reset per call)
+size_t sv_sync_bytes(int nnodes, int nleaves) {
+    return (sizeof(SvSync) + ((size_t)nnodes + nleaves) * sizeof(unsigned) + 255) / 256 * 256;
 }
 
 }  // namespace
@@ -889,14 +882,15 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     const int cfix = (P.coef_elems + kZeroSlot) * 8;
     P.rbi = 32;
     const int min_rbi = kConsumers;  // U-piece reduction: <= 32 threads per row
-    while (P.rbi > min_rbi && cfix + P.rbi * ubytes_row > kStage) P.rbi /= 2;
-    if (cfix + P.rbi * ubytes_row > kStage) return HODLR_OK;
+    while (P.rbi > min_rbi && cfix + P.rbi * (ubytes_row + 8) > kStage) P.rbi /= 2;
+    if (cfix + P.rbi * (ubytes_row + 8) > kStage) return HODLR_OK;
     P.tpr_shift = 0;
     while ((1 << P.tpr_shift) * P.rbi < kConsumers * 32) ++P.tpr_shift;
     if ((1 << P.tpr_shift) * P.rbi != kConsumers * 32 || P.tpr_shift > 5) return HODLR_OK;
     for (int wi = 0; wi < 2; ++wi) {
         const int wb = wi ? 8 : 4;
-        P.ubytes[wi] = (P.coef_elems + kZeroSlot) * wb + P.rbi * ubytes_row;
+        P.uy_off[wi] = (P.coef_elems + kZeroSlot) * wb + P.rbi * ubytes_row;  // 16-B multiple
+        P.ubytes[wi] = P.uy_off[wi] + P.rbi * wb;
     }
     if (P.rbd > P.rbi) P.rbd = P.rbi;
     if (P.rbi % P.rbd) return HODLR_OK;
@@ -914,9 +908,8 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     }
     if (P.napieces == 0) return HODLR_OK;  // all ranks zero: generic path
     P.num_a = nleaves;
-    P.num_b = nleaves * (kM / P.rbi);
-    P.bitset_words = (P.nnodes + 31) / 32;
-    if (smem_bytes(P.bitset_words) > 227 * 1024) P.bitset_words = 0;
+    P.num_d = nleaves * (kM / P.rbi);
+    P.num_u = nleaves * (kM / P.rbi);
 
     // ---- relayout the quantised level-batched arena into leaf slabs (bytes)
     std::vector<uint8_t> arena(in.arena_bytes);
@@ -949,7 +942,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    const size_t smem = smem_bytes(P.bitset_words);
+    const size_t smem = smem_bytes();
     if (!coop || sms <= 0 ||
         cudaFuncSetAttribute(k_stream<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
         cudaFuncSetAttribute(k_stream<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -972,11 +965,11 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     sv.depth = depth;
     sv.rb = P.rbi;
     sv.num_items_a = P.num_a;
-    sv.num_items_b = P.num_b;
-    sv.grid = std::min(sms * std::min(occ, kCtasPerSm), P.num_a + P.num_b);
+    sv.num_items_b = P.num_d + P.num_u;
+    sv.grid = std::min(sms * std::min(occ, kCtasPerSm), P.num_a + P.num_d + P.num_u);
     sv.launches = 1;
     sv.tfast_count = tb;
-    sv.extra_ws = (sizeof(SvSync) + 2 * (size_t)P.nnodes * sizeof(unsigned) + 255) / 256 * 256 + (size_t)tb * 8;
+    sv.extra_ws = sv_sync_bytes(P.nnodes, P.nleaves) + (size_t)tb * 8;
     sv.leaf_fmt = lf;
     sv.params = new SvParams(P);
     *ok = true;
@@ -1008,12 +1001,12 @@ cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* 
     uint8_t* e = (uint8_t*)extra;
     a.sync = (SvSync*)e;
     a.counters = (unsigned*)(e + sizeof(SvSync));
-    a.flags = a.counters + P.nnodes;
-    const size_t toff = (sizeof(SvSync) + 2 * (size_t)P.nnodes * sizeof(unsigned) + 255) / 256 * 256;
+    a.dcount = a.counters + P.nnodes;
+    const size_t toff = sv_sync_bytes(P.nnodes, P.nleaves);
     a.tbuf = (W*)(e + toff);
     void* args[] = {(void*)&P, &a};
     return cudaLaunchCooperativeKernel((const void*)k_stream<W>, dim3(sv.grid), dim3(kThreads), args,
-                                       smem_bytes(P.bitset_words), st);
+                                       smem_bytes(), st);
 }
 
 template cudaError_t sv_matvec<double>(const PlanView&, const SvPlan&, const double*, double*, double*, double*,
