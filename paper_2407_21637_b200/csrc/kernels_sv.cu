@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             __threadfence_block();
             C.ev_tail = ev + 1;
         };
-        bool coef_ready = false, d_ready = false;
+        bool coef_ready = false;
 
         // ---- phase A: leaves dealt round-robin, every CTA starts with its share
         for (int leaf = blockIdx.x; leaf < P.num_a; leaf += gridDim.x) {
@@ -535,16 +535,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                         while ((pub = ld_acquire(&a.sync->published)) != (unsigned)P.nnodes) __nanosleep(128);
                     coef_ready = true;
                 }
-                if (!d_ready) {
-                    if (lane == 0) {
-                        if (ld_acquire(&a.sync->leaves_done) == (unsigned)P.nleaves) {
-                            d_ready = true;
-                        } else {
-                            while (ld_acquire(&a.dcount[leaf]) != d_expect) __nanosleep(64);
-                        }
-                    }
-                    d_ready = __shfl_sync(0xffffffffu, d_ready, 0);
-                }
+                if (lane == 0)
+                    while (ld_acquire(&a.dcount[leaf]) != d_expect) __nanosleep(64);
                 PROF_ADD(6, clock64() - tr0);
                 __syncwarp();
                 uint8_t* st = claim();
@@ -731,11 +723,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 }
                 ++ev;
             } else if (h.type == PT_D && lane == 0) {
-                // this warp's rows of y are in b: count it toward the leaf's D completion
-                unsigned old;
-                asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.dcount + h.leaf) : "memory");
-                if (old == d_expect - 1u)
-                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&a.sync->leaves_done) : "memory");
+                // this warp's rows of y are in b (ordered by the __syncwarp above):
+                // count it toward the leaf's D completion, fire-and-forget
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.dcount + h.leaf) : "memory");
             }
             if (++stage == kNS) {
                 stage = 0;
