@@ -51,6 +51,7 @@ constexpr int kStage = 34 * 1024;       // bytes per stage
 constexpr int kConsumers = 8;           // consumer warps
 constexpr int kReducers = 2;            // reducer warps (phase-A node reductions)
 constexpr int kThreads = 32 * (kConsumers + 1 + kReducers);  // + producer + reducers
+constexpr int kDList = 64;              // D items per CTA between completion publishes
 constexpr int kEvQ = 16;                // pending phase-A completion events
 constexpr int kZeroSlot = 4;            // zero coefficients for padded U columns
 constexpr int kMaxLev = 24;
@@ -404,6 +405,8 @@ struct SmemCtl {
     int ev_leaf[kEvQ];
     unsigned ev_done[kEvQ];        // consumer warps finished with the event's leaf
     int last_mask;
+    unsigned d_done;               // consumer-warp completions of this CTA's D pieces
+    int dlist[kDList];             // leaves of D items emitted but not yet published
     alignas(16) int16_t cidx[512];  // U column (padded groups) -> coefficient slot
 };
 
@@ -421,12 +424,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nlev = P.depth;
     const int nq = P.num_d + P.num_u;  // dynamic queue: D items, then U items
-    const unsigned d_expect = (unsigned)(P.dpieces * (kM / P.rbi) * kConsumers);  // per leaf
+    const unsigned d_expect = (unsigned)(kM / P.rbi);  // D items per leaf
 
     if (threadIdx.x == 0) {
         C.epoch = ld_acquire(&a.sync->epoch);
         C.ev_tail = 0;
         C.ev_head = 0;
+        C.d_done = 0u;
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&C.full[s], 1);
             mbar_init(&C.empty[s], kConsumers);
@@ -462,6 +466,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             C.ev_tail = ev + 1;
         };
         bool coef_ready = false;
+        int nd_items = 0;          // D items in C.dlist
+        unsigned d_pieces = 0;     // D pieces emitted by this CTA
+        // Wait until this CTA's consumers finished every emitted D piece (their b
+        // stores are ordered by the CTA-scope release on C.d_done), then publish
+        // each listed D item with one GPU-scope release.
+        auto publish_d = [&]() {
+            if (nd_items == 0) return;
+            if (lane == 0) {
+                while (*(volatile unsigned*)&C.d_done < d_pieces * kConsumers) __nanosleep(64);
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            }
+            __syncwarp();
+            for (int i = lane; i < nd_items; i += 32)
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.dcount + C.dlist[i]) : "memory");
+            __syncwarp();
+            nd_items = 0;
+        };
 
         // ---- phase A: leaves dealt round-robin, every CTA starts with its share
         for (int leaf = blockIdx.x; leaf < P.num_a; leaf += gridDim.x) {
@@ -506,6 +527,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 const int r0 = (q % per_leaf) * P.rbi;
                 const uint8_t* dbase = a.slab + (int64_t)leaf * P.slab_bytes + P.d_off;
                 const int dsz = fmt_sz(P.leaf_fmt);
+                if (nd_items == kDList) publish_d();
+                if (lane == 0) C.dlist[nd_items] = leaf;
+                __syncwarp();
+                ++nd_items;
+                d_pieces += (unsigned)P.dpieces;
                 for (int p = 0; p < P.dpieces; ++p) {
                     uint8_t* st = claim();
                     const int rr = r0 + p * P.rbd;
@@ -528,6 +554,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 const int leaf = u / per_leaf;
                 const int r0 = (u % per_leaf) * P.rbi;
                 // the coefficients of every node, and this leaf's D results, must exist
+                publish_d();  // own D items first (another CTA's U item may wait on them)
                 PROF_T(tr0);
                 if (!coef_ready) {
                     unsigned pub = 0;
@@ -581,7 +608,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 next_stage();
             }
         }
+        publish_d();
         claim();
+#ifdef HODLR_PROFILE
+        if (lane == 0) prof[1] = clock64() - t_kernel;
+#endif
         if (lane == 0) {
             C.hdr[stage].type = PT_END;
             mbar_arrive(&C.full[stage]);
@@ -684,7 +715,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             PROF_ADD(2, tb - tw);
             const PieceHdr h = C.hdr[stage];
             const uint8_t* st = stages + (size_t)stage * kStage;
-            if (h.type == PT_END) break;
+            if (h.type == PT_END) {
+#ifdef HODLR_PROFILE
+                if (ctid == 0) prof[7] = clock64() - t_kernel;
+#endif
+                break;
+            }
             if (h.type == PT_A) {
                 a_piece<W>(h.g, st + kXB, h.ncols, reinterpret_cast<const W*>(st), cw, lane, P, h.leaf, h.col,
                            a.partial);
@@ -724,8 +760,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 ++ev;
             } else if (h.type == PT_D && lane == 0) {
                 // this warp's rows of y are in b (ordered by the __syncwarp above):
-                // count it toward the leaf's D completion, fire-and-forget
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.dcount + h.leaf) : "memory");
+                // CTA-scope release; the producer publishes GPU-wide per D item
+                asm volatile("fence.acq_rel.cta;" ::: "memory");
+                atomicAdd(&C.d_done, 1u);
             }
             if (++stage == kNS) {
                 stage = 0;
@@ -737,8 +774,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     __syncthreads();
 #ifdef HODLR_PROFILE
     if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 101 || blockIdx.x == 250))
-        printf("PROF cta %d: total %lld prod_empty %lld wait_ready %lld | cons_wait %lld busyA %lld busyD %lld busyU %lld (consumer sums over %d warps)\n",
-               blockIdx.x, clock64() - t_kernel, prof[0], prof[6], prof[2], prof[3], prof[4], prof[5], kConsumers);
+        printf("PROF cta %d: total %lld END_emitted %lld END_seen %lld prod_empty %lld wait_ready %lld | cons_wait %lld busyA %lld busyD %lld busyU %lld (consumer sums over %d warps)\n",
+               blockIdx.x, clock64() - t_kernel, prof[1], prof[7], prof[0], prof[6], prof[2], prof[3], prof[4], prof[5], kConsumers);
 #endif
     __shared__ unsigned s_last;
     if (threadIdx.x == 0) {
