@@ -147,6 +147,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -406,7 +417,8 @@ struct SmemCtl {
     unsigned ev_done[kEvQ];        // consumer warps finished with the event's leaf
     int last_mask;
     unsigned d_done;               // consumer-warp completions of this CTA's D pieces
-    int dlist[kDList];             // leaves of D items emitted but not yet published
+    int dlist[kDList];             // leaves of D items emitted but not yet published (FIFO)
+    unsigned dend[kDList];         // ... and the cumulative D-piece count at their end
     alignas(16) int16_t cidx[512];  // U column (padded groups) -> coefficient slot
 };
 
@@ -453,12 +465,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 phase ^= 1u;
             }
         };
-        auto claim = [&]() -> uint8_t* {
-            PROF_T(t0);
-            mbar_wait(&C.empty[stage], phase ^ 1u);
-            PROF_ADD(0, clock64() - t0);
-            return stages + (size_t)stage * kStage;
-        };
         auto push_event = [&](int leaf) {  // lane 0
             while (ev - C.ev_head >= kEvQ) __nanosleep(64);
             C.ev_leaf[ev % kEvQ] = leaf;
@@ -466,22 +472,34 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             C.ev_tail = ev + 1;
         };
         bool coef_ready = false;
-        int nd_items = 0;          // D items in C.dlist
+        int dh = 0, dt = 0;        // D-item FIFO head / tail (warp-uniform)
         unsigned d_pieces = 0;     // D pieces emitted by this CTA
-        // Wait until this CTA's consumers finished every emitted D piece (their b
-        // stores are ordered by the CTA-scope release on C.d_done), then publish
-        // each listed D item with one GPU-scope release.
-        auto publish_d = [&]() {
-            if (nd_items == 0) return;
-            if (lane == 0) {
-                while (*(volatile unsigned*)&C.d_done < d_pieces * kConsumers) __nanosleep(64);
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        // Publish, in order, every listed D item whose pieces this CTA's consumers
+        // have finished (their b stores are ordered by the CTA-scope release on
+        // C.d_done): one GPU-scope release per item.  block: wait for all.
+        auto publish_d = [&](bool block) {
+            while (dh != dt) {
+                int n = 0;
+                if (lane == 0) {
+                    const unsigned done = *(volatile unsigned*)&C.d_done;
+                    while (dh + n != dt && done >= C.dend[(dh + n) % kDList] * kConsumers) ++n;
+                    if (n) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                }
+                n = __shfl_sync(0xffffffffu, n, 0);
+                for (int i = lane; i < n; i += 32)
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.dcount + C.dlist[(dh + i) % kDList])
+                                 : "memory");
+                dh += n;
+                __syncwarp();
+                if (!block || dh == dt) return;
+                if (n == 0) __nanosleep(64);
             }
-            __syncwarp();
-            for (int i = lane; i < nd_items; i += 32)
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.dcount + C.dlist[i]) : "memory");
-            __syncwarp();
-            nd_items = 0;
+        };
+        auto claim = [&]() -> uint8_t* {
+            PROF_T(t0);
+            while (!mbar_test(&C.empty[stage], phase ^ 1u)) publish_d(false);
+            PROF_ADD(0, clock64() - t0);
+            return stages + (size_t)stage * kStage;
         };
 
         // ---- phase A: leaves dealt round-robin, every CTA starts with its share
@@ -527,11 +545,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 const int r0 = (q % per_leaf) * P.rbi;
                 const uint8_t* dbase = a.slab + (int64_t)leaf * P.slab_bytes + P.d_off;
                 const int dsz = fmt_sz(P.leaf_fmt);
-                if (nd_items == kDList) publish_d();
-                if (lane == 0) C.dlist[nd_items] = leaf;
-                __syncwarp();
-                ++nd_items;
+                if (dt - dh == kDList) publish_d(true);
                 d_pieces += (unsigned)P.dpieces;
+                if (lane == 0) {
+                    C.dlist[dt % kDList] = leaf;
+                    C.dend[dt % kDList] = d_pieces;
+                }
+                __syncwarp();
+                ++dt;
                 for (int p = 0; p < P.dpieces; ++p) {
                     uint8_t* st = claim();
                     const int rr = r0 + p * P.rbd;
@@ -554,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 const int leaf = u / per_leaf;
                 const int r0 = (u % per_leaf) * P.rbi;
                 // the coefficients of every node, and this leaf's D results, must exist
-                publish_d();  // own D items first (another CTA's U item may wait on them)
+                publish_d(true);  // own D items first (another CTA's U item may wait on them)
                 PROF_T(tr0);
                 if (!coef_ready) {
                     unsigned pub = 0;
@@ -608,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 next_stage();
             }
         }
-        publish_d();
+        publish_d(true);
         claim();
 #ifdef HODLR_PROFILE
         if (lane == 0) prof[1] = clock64() - t_kernel;
