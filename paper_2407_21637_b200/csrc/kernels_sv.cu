@@ -297,18 +297,18 @@ __device__ __forceinline__ void col_block(const uint8_t* blk, int ncols, int war
             }
         }
     }
-    for (int k = 0; c < ncols; c += kConsumers, ++k) {
+    for (; c < ncols; c += kConsumers) {  // tail: fixed accumulator (no dynamic register indexing)
         const W m = mul(c);
         const uint8_t* p = blk + ((size_t)c * kRB + 2 * lane) * sz;
         if constexpr (FMT == HODLR_FMT_FP64) {
             const double2 t = *reinterpret_cast<const double2*>(p);
-            acc[k][0] = madd_d<W>(t.x, m, acc[k][0]);
-            acc[k][1] = madd_d<W>(t.y, m, acc[k][1]);
+            acc[0][0] = madd_d<W>(t.x, m, acc[0][0]);
+            acc[0][1] = madd_d<W>(t.y, m, acc[0][1]);
         } else {
             float a, b;
             load2<FMT>(p, a, b);
-            acc[k][0] = madd<W>(a, m, acc[k][0]);
-            acc[k][1] = madd<W>(b, m, acc[k][1]);
+            acc[0][0] = madd<W>(a, m, acc[0][0]);
+            acc[0][1] = madd<W>(b, m, acc[0][1]);
         }
     }
 }
