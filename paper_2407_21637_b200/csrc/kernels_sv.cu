@@ -350,6 +350,9 @@ struct SmemCtl {
     int dlist[kDList];             // leaves of B items emitted but not yet published (FIFO)
     unsigned dend[kDList];         // ... and the cumulative B-item count at their end
     alignas(16) int16_t cidx[kMaxCols];  // flattened U column -> coefficient slot
+    int64_t pbase_c[kMaxCols];     // flattened V' column -> partial buffer base (level pbase + c*nch)
+    int32_t pstride_c[kMaxCols];   //                     -> r * nch (stride between nodes)
+    int8_t psh_c[kMaxCols];        //                     -> log2(nch)
 };
 
 template <typename W>
@@ -380,8 +383,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = threadIdx.x; i < kEvQ; i += kThreads) C.ev_done[i] = 0u;
-    for (int i = threadIdx.x; i < P.gstart[5]; i += kThreads)
-        C.cidx[i] = (int16_t)(P.lev[P.col_level[i]].slot + P.col_c[i]);
+    for (int i = threadIdx.x; i < P.gstart[5]; i += kThreads) {
+        const Level& L = P.lev[P.col_level[i]];
+        const int sh = nlev - (P.col_level[i] + 1);
+        C.cidx[i] = (int16_t)(L.slot + P.col_c[i]);
+        C.pbase_c[i] = L.pbase + ((int64_t)P.col_c[i] << sh);
+        C.pstride_c[i] = L.r << sh;
+        C.psh_c[i] = (int8_t)sh;
+    }
     __syncthreads();
     const unsigned target = C.epoch + 1u;
 
@@ -482,6 +491,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 }
                 __syncwarp();
                 ++dt;
+                publish_d(false);  // eagerly: C items of other CTAs may be waiting
                 for (int p = 0; p < P.dpieces; ++p) {
                     uint8_t* st = claim();
                     const int c0 = p * P.dcols;
@@ -681,12 +691,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
 #pragma unroll
                         for (int w = 1; w < kConsumers; ++w) s += red[w * vp + c];
                         const int flat = P.gstart[ap.g] + c;
-                        const int k = P.col_level[flat];
-                        const int cc = P.col_c[flat];
-                        const Level& L = P.lev[k];
-                        const int sh = nlev - (k + 1);
+                        const int sh = C.psh_c[flat];
                         const int jn = h.leaf >> sh;
-                        a.partial[L.pbase + ((int64_t)jn * L.r + cc) * (1 << sh) + (h.leaf - (jn << sh))] = s;
+                        a.partial[C.pbase_c[flat] + (int64_t)jn * C.pstride_c[flat] + (h.leaf - (jn << sh))] = s;
                     }
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
