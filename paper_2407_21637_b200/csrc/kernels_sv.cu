@@ -51,16 +51,15 @@ constexpr int kNS = 3;                  // ring stages per CTA
 constexpr int kCtasPerSm = 2;           // independent pipelines per SM
 constexpr int kStage = 34 * 1024;       // bytes per stage
 constexpr int kConsumers = 8;           // consumer warps (= column subsets of B/C pieces)
-constexpr int kReducers = 2;            // reducer warps
-constexpr int kThreads = 32 * (kConsumers + 1 + kReducers);
+constexpr int kThreads = 32 * (kConsumers + 1);  // + producer warp
 constexpr int kDList = 64;              // B items per CTA between completion publishes
-constexpr int kEvQ = 16;                // pending phase-A completion events
+constexpr int kMaxRPieces = 256;        // node-reduction pieces
 constexpr int kMaxLev = 24;
 constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
 constexpr int kMaxCols = 512;           // columns (sum of ranks) per leaf
 constexpr int kXB = 2048;               // bytes reserved for the x segment of a stage
 
-enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_END = 4 };
+enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_R = 5, PT_END = 4 };
 
 #ifdef HODLR_PROFILE
 #define PROF_T(v) long long v = clock64()
@@ -82,10 +81,17 @@ struct APiece {
     int32_t g, r0, nrows, last_of_group;
 };
 
+// Node reduction: level lv, nodes [j0, j1), rank columns [c0, c1) (whole nodes,
+// or one node split by columns); its partials are contiguous.
+struct RPiece {
+    int16_t lv, pad;
+    int32_t j0, j1, c0, c1;
+};
+
 struct SvParams {
     int32_t depth, nleaves, nnodes;
     int32_t leaf_fmt;
-    int32_t num_a, num_d, num_u;
+    int32_t num_a, num_d, num_u, num_r, pos_r;  // queue: B items with R items at pos_r, then C
     int32_t napieces, dpieces, dcols;     // phase-B pieces per item and columns per piece
     int64_t slab_bytes, ds_off, us_off;
     int64_t dblock_bytes, ublock_bytes;
@@ -95,14 +101,17 @@ struct SvParams {
     int32_t u_y_off[2], u_data_off[2], u_bytes[2];  // U piece layout for fp32 / fp64 working
     Level lev[kMaxLev];
     APiece ap[kMaxPieces];
+    RPiece rp[kMaxRPieces];
     int8_t col_level[kMaxCols];           // flattened (group, column) -> level (0-based)
     int16_t col_c[kMaxCols];              //                            -> rank column
     int16_t gstart[6];
 };
 
 struct SvSync {
-    unsigned epoch, queue, done, published;  // published: nodes whose t exists (this call)
-    unsigned pad[4];
+    unsigned epoch, queue, done;
+    unsigned a_done;     // phase-A leaves whose partials are written (this call)
+    unsigned r_done;     // node-reduction pieces whose coefficients are written
+    unsigned pad[3];
 };
 
 struct PieceHdr {
@@ -157,9 +166,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
 }
-__device__ __forceinline__ void reducer_sync() {
-    asm volatile("bar.sync 2, %0;" ::"n"(kReducers * 32) : "memory");
-}
+__host__ __device__ __forceinline__ int64_t round_up16_d(int64_t v) { return (v + 15) / 16 * 16; }
 __host__ __device__ __forceinline__ int fmt_sz(int f) {
     return f == HODLR_FMT_Q52 ? 1 : f == HODLR_FMT_FP32 ? 4 : f == HODLR_FMT_FP64 ? 8 : 2;
 }
@@ -330,10 +337,9 @@ struct SvKernelArgs {
     const uint8_t* slab;
     const W* x;
     W* b;
-    W* partial;
+    W* partial;            // fast-path layout: level bases P.lev[].pbase
     W* tbuf;
     SvSync* sync;
-    unsigned* counters;    // [nnodes]: leaves counted into each node (last arriver reduces)
     unsigned* dcount;      // [nleaves]: phase-B items of the leaf whose y is in b
 };
 
@@ -341,12 +347,7 @@ struct SmemCtl {
     uint64_t full[kNS], empty[kNS];
     PieceHdr hdr[kNS];
     unsigned epoch;
-    volatile int ev_tail;          // phase-A completion events pushed by the producer
-    volatile int ev_head;          // ... and retired by the reducer warps
-    int ev_leaf[kEvQ];
-    unsigned ev_done[kEvQ];        // consumer warps finished with the event's leaf
-    int last_mask;
-    unsigned d_done;               // phase-B items of this CTA whose y is stored
+    unsigned a_cnt, r_cnt, d_cnt;  // consumer completions (A items, R pieces, B items)
     int dlist[kDList];             // leaves of B items emitted but not yet published (FIFO)
     unsigned dend[kDList];         // ... and the cumulative B-item count at their end
     alignas(16) int16_t cidx[kMaxCols];  // flattened U column -> coefficient slot
@@ -367,22 +368,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     SmemCtl& C = *reinterpret_cast<SmemCtl*>(smem + kNS * kStage);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nlev = P.depth;
-    const int nq = P.num_d + P.num_u;        // dynamic queue: B items, then C items
-    constexpr int kBlocks = kM / kRB;        // row blocks per leaf
+    const int nq = P.num_d + P.num_r + P.num_u;  // dynamic queue: B (R inserted at pos_r), then C
+    constexpr int kBlocks = kM / kRB;            // row blocks per leaf
     const unsigned d_expect = (unsigned)kBlocks;
 
     if (threadIdx.x == 0) {
         C.epoch = ld_acquire(&a.sync->epoch);
-        C.ev_tail = 0;
-        C.ev_head = 0;
-        C.d_done = 0u;
+        C.a_cnt = C.r_cnt = C.d_cnt = 0u;
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&C.full[s], 1);
             mbar_init(&C.empty[s], kConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = threadIdx.x; i < kEvQ; i += kThreads) C.ev_done[i] = 0u;
     for (int i = threadIdx.x; i < P.gstart[5]; i += kThreads) {
         const Level& L = P.lev[P.col_level[i]];
         const int sh = nlev - (P.col_level[i] + 1);
@@ -398,34 +396,41 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         // =========================================================== producer
         int stage = 0;
         unsigned phase = 0;
-        int ev = 0;
-        int dh = 0, dt = 0;       // B-item FIFO head / tail (warp-uniform)
-        unsigned d_items = 0;     // B items emitted by this CTA
-        // publish, in order, every listed B item whose y this CTA's consumers have
-        // stored (ordered by the CTA-scope release on C.d_done): one GPU-scope
-        // release per item.  block: wait for all of them.
-        auto publish_d = [&](bool block) {
-            while (dh != dt) {
+        unsigned a_pub = 0, r_pub = 0;  // completions published GPU-wide
+        int dh = 0, dt = 0;             // B-item FIFO head / tail (warp-uniform)
+        unsigned d_items = 0;           // B items emitted by this CTA
+        unsigned a_items = 0, r_items = 0;
+        // Publish this CTA's finished work GPU-wide.  Consumers signal completion
+        // with CTA-scope releases on C.*_cnt (after the data's stores); one fence
+        // plus one release reduction per batch makes it visible.  block: wait until
+        // everything emitted so far is published.
+        auto publish = [&](bool block) {
+            for (;;) {
                 int n = 0;
+                unsigned na = 0, nr = 0;
                 if (lane == 0) {
-                    const unsigned done = *(volatile unsigned*)&C.d_done;
-                    while (dh + n != dt && done >= C.dend[(dh + n) % kDList]) ++n;
-                    if (n) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    const unsigned dd = *(volatile unsigned*)&C.d_cnt;
+                    while (dh + n != dt && dd >= C.dend[(dh + n) % kDList]) ++n;
+                    na = *(volatile unsigned*)&C.a_cnt - a_pub;
+                    nr = *(volatile unsigned*)&C.r_cnt - r_pub;
+                    if (n || na || nr) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    if (na) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->a_done), "r"(na) : "memory");
+                    if (nr) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->r_done), "r"(nr) : "memory");
                 }
                 n = __shfl_sync(0xffffffffu, n, 0);
+                a_pub += __shfl_sync(0xffffffffu, na, 0);
+                r_pub += __shfl_sync(0xffffffffu, nr, 0);
                 for (int i = lane; i < n; i += 32)
                     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.dcount + C.dlist[(dh + i) % kDList])
                                  : "memory");
                 dh += n;
                 __syncwarp();
-                if (!block || dh == dt) return;
-                if (n == 0) __nanosleep(64);
+                if (!block || (dh == dt && a_pub == a_items && r_pub == r_items)) return;
+                __nanosleep(64);
             }
         };
         auto claim = [&]() -> uint8_t* {
-            PROF_T(t0);
-            while (!mbar_test(&C.empty[stage], phase ^ 1u)) publish_d(false);
-            PROF_ADD(0, clock64() - t0);
+            while (!mbar_test(&C.empty[stage], phase ^ 1u)) publish(false);
             return stages + (size_t)stage * kStage;
         };
         auto next_stage = [&]() {
@@ -434,20 +439,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 phase ^= 1u;
             }
         };
-        auto push_event = [&](int leaf) {  // lane 0
-            while (ev - C.ev_head >= kEvQ) __nanosleep(64);
-            C.ev_leaf[ev % kEvQ] = leaf;
-            __threadfence_block();
-            C.ev_tail = ev + 1;
+        auto wait_count = [&](const unsigned* ctr, unsigned want) {  // lane 0
+            while (ld_acquire(ctr) != want) __nanosleep(128);
         };
-        bool coef_ready = false;
+        bool a_ready = false, r_ready = false;
 
         // ---- phase A: leaves dealt round-robin, every CTA starts with its share
         for (int leaf = blockIdx.x; leaf < P.num_a; leaf += gridDim.x) {
             const uint8_t* base = a.slab + (int64_t)leaf * P.slab_bytes;
-            if (lane == 0) push_event(leaf);
-            ++ev;
-            __syncwarp();
+            ++a_items;
             for (int p = 0; p < P.napieces; ++p) {
                 const APiece ap = P.ap[p];
                 uint8_t* st = claim();
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 next_stage();
             }
         }
-        // ---- phases B and C from one atomic queue, fetched two ahead
+        // ---- B, R, C items from one atomic queue, fetched two ahead
         int n1 = 0, n2 = 0;
         if (lane == 0) {
             n1 = (int)atomicAdd(&a.sync->queue, 1u);
@@ -480,10 +480,40 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             if (q >= nq) break;
             n1 = n2;
             if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);
-            if (q < P.num_d) {
-                const int leaf = q / kBlocks, rb = q % kBlocks;
+            publish(false);
+            if (q >= P.pos_r && q < P.pos_r + P.num_r) {
+                // ---- R: reduce node partials (needs every leaf's partials)
+                const RPiece rp = P.rp[q - P.pos_r];
+                const Level& L = P.lev[rp.lv];
+                const int nch = 1 << (nlev - 1 - rp.lv);
+                if (!a_ready) {
+                    publish(true);  // own A items first
+                    if (lane == 0) wait_count(&a.sync->a_done, (unsigned)P.num_a);
+                    a_ready = true;
+                }
+                __syncwarp();
+                ++r_items;
+                uint8_t* st = claim();
+                const int64_t cnt = (int64_t)(rp.j1 - rp.j0) * (rp.c1 - rp.c0) * nch;
+                const unsigned bytes = (unsigned)round_up16_d(cnt * (int64_t)sizeof(W));
+                if (lane == 0) {
+                    PieceHdr& h = C.hdr[stage];
+                    h.type = PT_R;
+                    h.a = q - P.pos_r;
+                    mbar_arrive_tx(&C.full[stage], bytes);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    bulk_g2s(st, a.partial + L.pbase + ((int64_t)rp.j0 * L.r + rp.c0) * nch, bytes, &C.full[stage]);
+                }
+                __syncwarp();
+                next_stage();
+                continue;
+            }
+            const int qb = q < P.pos_r ? q : q - P.num_r;
+            if (qb < P.num_d) {
+                // ---- B: y = D x for one 64-row block
+                const int leaf = qb / kBlocks, rb = qb % kBlocks;
                 const uint8_t* blk = a.slab + (int64_t)leaf * P.slab_bytes + P.ds_off + (int64_t)rb * P.dblock_bytes;
-                if (dt - dh == kDList) publish_d(true);
+                if (dt - dh == kDList) publish(true);
                 ++d_items;
                 if (lane == 0) {
                     C.dlist[dt % kDList] = leaf;
@@ -491,7 +521,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 }
                 __syncwarp();
                 ++dt;
-                publish_d(false);  // eagerly: C items of other CTAs may be waiting
                 for (int p = 0; p < P.dpieces; ++p) {
                     uint8_t* st = claim();
                     const int c0 = p * P.dcols;
@@ -513,18 +542,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     next_stage();
                 }
             } else {
-                const int u = q - P.num_d;
+                // ---- C: b = U t + y for one 64-row block
+                const int u = qb - P.num_d;
                 const int leaf = u / kBlocks, rb = u % kBlocks;
-                publish_d(true);  // own B items first (another CTA's C item may wait on them)
-                PROF_T(tr0);
-                if (!coef_ready) {
-                    if (lane == 0)
-                        while (ld_acquire(&a.sync->published) != (unsigned)P.nnodes) __nanosleep(128);
-                    coef_ready = true;
+                if (!r_ready) {
+                    publish(true);  // own B and R items first
+                    if (lane == 0) wait_count(&a.sync->r_done, (unsigned)P.num_r);
+                    r_ready = true;
                 }
-                if (lane == 0)
-                    while (ld_acquire(&a.dcount[leaf]) != d_expect) __nanosleep(64);
-                PROF_ADD(6, clock64() - tr0);
+                if (lane == 0) wait_count(&a.dcount[leaf], d_expect);
                 __syncwarp();
                 uint8_t* st = claim();
                 const int wi = sizeof(W) == 8 ? 1 : 0;
@@ -560,99 +586,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 next_stage();
             }
         }
-        publish_d(true);
+        publish(true);
         claim();
         if (lane == 0) {
             C.hdr[stage].type = PT_END;
             mbar_arrive(&C.full[stage]);
-            while (ev - C.ev_head >= kEvQ) __nanosleep(64);
-            C.ev_leaf[ev % kEvQ] = -1;  // reducers: done
-            __threadfence_block();
-            C.ev_tail = ev + 1;
         }
         __syncwarp();
-    } else if (warp <= kReducers) {
-        // =========================================================== reducers
-        const int rt = threadIdx.x - 32;
-        for (int ev = 0;; ++ev) {
-            if (rt == 0)
-                while (C.ev_tail <= ev) __nanosleep(256);
-            reducer_sync();
-            const int leaf = C.ev_leaf[ev % kEvQ];
-            if (leaf < 0) break;
-            if (rt == 0)
-                while (*(volatile unsigned*)&C.ev_done[ev % kEvQ] < (unsigned)kConsumers) __nanosleep(64);
-            if (warp == 1) {
-                if (lane == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                __syncwarp();
-                bool last = false;
-                if (lane < nlev) {
-                    const int k = lane + 1;
-                    const int sh = nlev - k;
-                    const int id = (1 << k) - 2 + (leaf >> sh);
-                    unsigned old;
-                    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.counters + id) : "memory");
-                    last = old == (1u << sh) - 1u;
-                }
-                const unsigned m = __ballot_sync(0xffffffffu, last);
-                if (lane == 0) C.last_mask = (int)m;
-            }
-            reducer_sync();
-            unsigned mask = (unsigned)C.last_mask;
-            int published = 0;
-            while (mask) {
-                const int lv = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int k = lv + 1;
-                const int sh = nlev - k;
-                const int jn = leaf >> sh;
-                const int nch = 1 << sh;
-                const Level& L = P.lev[lv];
-                if (L.r > 0) {
-                    int tpc = 32;  // threads per column (power of two, divides 32)
-                    while (tpc > 1 && tpc * L.r > 32 * kReducers) tpc >>= 1;
-                    const int cpr = 32 * kReducers / tpc;
-                    for (int c0 = 0; c0 < L.r; c0 += cpr) {
-                        const int c = c0 + rt / tpc, sl = rt % tpc;
-                        W acc = W(0);
-                        if (c < L.r) {
-                            const W* src = a.partial + L.pbase + ((int64_t)jn * L.r + c) * nch;
-                            constexpr int B = 8;
-                            for (int i0 = sl; i0 < nch; i0 += B * tpc) {
-                                W v[B];
-#pragma unroll
-                                for (int u = 0; u < B; ++u) {
-                                    const int i = i0 + u * tpc;
-                                    v[u] = i < nch ? __ldcg(src + i) : W(0);
-                                }
-#pragma unroll
-                                for (int u = 0; u < B; ++u) acc += v[u];
-                            }
-                        }
-                        for (int o = tpc >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                        if (sl == 0 && c < L.r) a.tbuf[L.tbase + (int64_t)jn * L.tstride + c] = acc;
-                    }
-                }
-                if (rt == 0) a.counters[(1 << k) - 2 + jn] = 0u;
-                ++published;
-            }
-            reducer_sync();
-            if (rt == 0) {
-                if (published)
-                    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->published), "r"(published)
-                                 : "memory");
-                C.ev_done[ev % kEvQ] = 0u;
-                __threadfence_block();
-                C.ev_head = ev + 1;
-            }
-        }
     } else {
         // =========================================================== consumers
-        const int cw = warp - 1 - kReducers;
-        const int ctid = threadIdx.x - 32 * (1 + kReducers);
+        const int cw = warp - 1;
+        const int ctid = threadIdx.x - 32;
         int stage = 0;
         unsigned phase = 0;
-        int ev = 0;
         W aacc[2][4];   // phase A: column sums of the current format group
         W bacc[4][2];   // phases B / C: row sums (2 rows per lane, 4 chains)
 #pragma unroll
@@ -662,10 +608,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
 #pragma unroll
         for (int k = 0; k < 4; ++k) bacc[k][0] = bacc[k][1] = W(0);
         for (;;) {
-            PROF_T(tw);
             mbar_wait(&C.full[stage], phase);
-            PROF_T(tb);
-            PROF_ADD(2, tb - tw);
             const PieceHdr h = C.hdr[stage];
             uint8_t* st = stages + (size_t)stage * kStage;
             if (h.type == PT_END) break;
@@ -718,14 +661,37 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                         for (int w = 1; w < kConsumers; ++w) s += red[w * kRB + ctid];
                         a.b[(int64_t)h.leaf * kM + h.a * kRB + ctid] = s;  // y = D x
                     }
-                    consumer_sync();
-                    if (ctid == 0) {  // all of y's stores precede this (barrier above)
-                        asm volatile("fence.acq_rel.cta;" ::: "memory");
-                        atomicAdd(&C.d_done, 1u);
-                    }
 #pragma unroll
                     for (int k = 0; k < 4; ++k) bacc[k][0] = bacc[k][1] = W(0);
+                    scratch = true;
                 }
+            } else if (h.type == PT_R) {
+                // t for (node, column) pairs: fixed-order sums over the node's leaves
+                const RPiece rp = P.rp[h.a];
+                const Level& L = P.lev[rp.lv];
+                const int nch = 1 << (nlev - 1 - rp.lv);
+                const int ncol = rp.c1 - rp.c0;
+                const int npairs = (rp.j1 - rp.j0) * ncol;
+                const W* v = reinterpret_cast<const W*>(st);
+                if (nch >= 32) {
+                    for (int p = cw; p < npairs; p += kConsumers) {
+                        W s = W(0);
+                        for (int i = lane; i < nch; i += 32) s += v[(int64_t)p * nch + i];
+                        s = warp_sum(s);
+                        if (lane == 0) {
+                            const int j = rp.j0 + p / ncol, c = rp.c0 + p % ncol;
+                            a.tbuf[L.tbase + (int64_t)j * L.tstride + c] = s;
+                        }
+                    }
+                } else {
+                    for (int p = ctid; p < npairs; p += kConsumers * 32) {
+                        W s = v[(int64_t)p * nch];
+                        for (int i = 1; i < nch; ++i) s += v[(int64_t)p * nch + i];
+                        const int j = rp.j0 + p / ncol, c = rp.c0 + p % ncol;
+                        a.tbuf[L.tbase + (int64_t)j * L.tstride + c] = s;
+                    }
+                }
+                scratch = true;
             } else {  // PT_U: b = U t + y
                 const int wi = sizeof(W) == 8 ? 1 : 0;
                 const W* coef = reinterpret_cast<const W*>(st);
@@ -752,19 +718,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 for (int k = 0; k < 4; ++k) bacc[k][0] = bacc[k][1] = W(0);
                 scratch = true;
             }
-            if (scratch) consumer_sync();  // scratch reads done before the stage is refilled
+            if (scratch) {
+                consumer_sync();  // scratch reads and the item's global stores are done
+                if (ctid == 0) {
+                    const bool a_end = h.type == PT_A && h.last;
+                    const bool d_end = h.type == PT_D && h.last;
+                    const bool r_end = h.type == PT_R;
+                    if (a_end || d_end || r_end) {
+                        asm volatile("fence.acq_rel.cta;" ::: "memory");
+                        atomicAdd(a_end ? &C.a_cnt : d_end ? &C.d_cnt : &C.r_cnt, 1u);
+                    }
+                }
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&C.empty[stage]);
-            PROF_ADD(2 + h.type, clock64() - tb);
-            if (h.type == PT_A && h.last) {
-                // this warp's partials of the leaf are written (ordered by the barrier
-                // above): tell the reducers
-                if (lane == 0) {
-                    asm volatile("fence.acq_rel.cta;" ::: "memory");
-                    atomicAdd(&C.ev_done[ev % kEvQ], 1u);
-                }
-                ++ev;
-            }
             if (++stage == kNS) {
                 stage = 0;
                 phase ^= 1u;
@@ -773,11 +740,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     }
     // ---- teardown: the last CTA resets the per-call state and bumps the epoch
     __syncthreads();
-#ifdef HODLR_PROFILE
-    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 101 || blockIdx.x == 250))
-        printf("PROF cta %d: total %lld prod_empty %lld wait_ready %lld | cons_wait %lld busyA %lld busyD %lld busyU %lld (sums over %d warps)\n",
-               blockIdx.x, clock64() - t_kernel, prof[0], prof[6], prof[2], prof[3], prof[4], prof[5], kConsumers);
-#endif
     __shared__ unsigned s_last;
     if (threadIdx.x == 0) {
         unsigned old;
@@ -791,7 +753,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         if (threadIdx.x == 0) {
             a.sync->queue = 0u;
             a.sync->done = 0u;
-            a.sync->published = 0u;
+            a.sync->a_done = 0u;
+            a.sync->r_done = 0u;
             __threadfence();
             st_release(&a.sync->epoch, target);
         }
@@ -800,9 +763,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
 
 size_t smem_bytes() { return (size_t)kNS * kStage + sizeof(SmemCtl); }
 
-// workspace head: SvSync, node counters, leaf B counters (zeroed once, reset per call)
-size_t sv_sync_bytes(int nnodes, int nleaves) {
-    return (sizeof(SvSync) + ((size_t)nnodes + nleaves) * sizeof(unsigned) + 255) / 256 * 256;
+// workspace: [SvSync | leaf B counters] (zeroed once, reset per call) [partials] [coefficients]
+size_t sv_sync_bytes(int nleaves) {
+    return (sizeof(SvSync) + (size_t)nleaves * sizeof(unsigned) + 255) / 256 * 256;
 }
 
 int64_t round_up16(int64_t v) { return (v + 15) / 16 * 16; }
@@ -868,13 +831,14 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     if (flat == 0) return HODLR_OK;  // all ranks zero: generic path
     // coefficient slots and partial / coefficient buffers
     int slot = 0;
-    int64_t tb = 0;
+    int64_t tb = 0, pb = 0;
     for (int k = 0; k < depth; ++k) {
         Level& L = P.lev[k];
         L.tstride = (L.r + 3) / 4 * 4;
         L.slot = slot;
         slot += L.tstride;
-        L.pbase = nodes[(1 << (k + 1)) - 2].part_off;
+        L.pbase = pb;  // level partials: [node][column][leaf of node], 32-byte aligned
+        pb += ((int64_t)L.r * nleaves + 3) / 4 * 4;
         L.tbase = tb;
         tb += (int64_t)L.tstride << (k + 1);
     }
@@ -927,6 +891,34 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     P.num_a = nleaves;
     P.num_d = nleaves * (kM / kRB);
     P.num_u = nleaves * (kM / kRB);
+    // node-reduction pieces (R items): a level's partials are [node][column][leaf]
+    P.num_r = 0;
+    for (int k = 0; k < depth; ++k) {
+        const Level& L = P.lev[k];
+        if (L.r == 0) continue;
+        const int nodes_k = 1 << (k + 1);
+        const int64_t nch = nleaves >> (k + 1);
+        const int64_t node_bytes = (int64_t)L.r * nch * 8;
+        auto add = [&](int j0, int j1, int c0, int c1) {
+            if (P.num_r == kMaxRPieces) return false;
+            if ((L.pbase + ((int64_t)j0 * L.r + c0) * nch) % 4) return false;  // 16-B aligned source
+            P.rp[P.num_r++] = RPiece{(int16_t)k, 0, j0, j1, c0, c1};
+            return true;
+        };
+        if (node_bytes <= kStage) {
+            int per = (int)std::min<int64_t>(nodes_k, kStage / node_bytes);
+            if (per >= 4) per = per / 4 * 4;
+            for (int j0 = 0; j0 < nodes_k; j0 += per)
+                if (!add(j0, std::min(nodes_k, j0 + per), 0, L.r)) return HODLR_OK;
+        } else {
+            const int cols = (int)(kStage / (nch * 8));
+            if (cols < 1) return HODLR_OK;
+            for (int j = 0; j < nodes_k; ++j)
+                for (int c0 = 0; c0 < L.r; c0 += cols)
+                    if (!add(j, j + 1, c0, std::min(L.r, c0 + cols))) return HODLR_OK;
+        }
+    }
+    P.pos_r = P.num_d * 3 / 5;  // R items run in the middle of phase B, long before phase C
 
     // ---- relayout the quantised level-batched arena into leaf slabs (bytes)
     std::vector<uint8_t> arena(in.arena_bytes);
@@ -991,7 +983,8 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     sv.grid = std::min(sms * std::min(occ, kCtasPerSm), P.num_a + P.num_d + P.num_u);
     sv.launches = 1;
     sv.tfast_count = tb;
-    sv.extra_ws = sv_sync_bytes(P.nnodes, P.nleaves) + (size_t)tb * 8;
+    sv.extra_ws = sv_sync_bytes(P.nleaves) + (size_t)(pb + tb) * 8;
+    sv.part_count = pb;
     sv.leaf_fmt = lf;
     sv.params = new SvParams(P);
     *ok = true;
@@ -1018,12 +1011,12 @@ cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* 
     a.slab = sv.slab;
     a.x = x;
     a.b = b;
-    a.partial = partial;
+    (void)partial;
     uint8_t* e = (uint8_t*)extra;
     a.sync = (SvSync*)e;
-    a.counters = (unsigned*)(e + sizeof(SvSync));
-    a.dcount = a.counters + P.nnodes;
-    a.tbuf = (W*)(e + sv_sync_bytes(P.nnodes, P.nleaves));
+    a.dcount = (unsigned*)(e + sizeof(SvSync));
+    a.partial = (W*)(e + sv_sync_bytes(P.nleaves));
+    a.tbuf = (W*)(e + sv_sync_bytes(P.nleaves) + sv.part_count * 8);
     void* args[] = {(void*)&P, &a};
     return cudaLaunchCooperativeKernel((const void*)k_stream<W>, dim3(sv.grid), dim3(kThreads), args, smem_bytes(), st);
 }

@@ -21,6 +21,7 @@ struct SvPlan {
     int grid = 0;
     int launches = 1;
     int64_t tfast_count = 0;    // padded coefficient buffer (elements)
+    int64_t part_count = 0;     // fast-path partial buffer (elements)
     size_t extra_ws = 0;        // bytes of workspace for sync state + coefficients
     int leaf_fmt = 4;
 };
