@@ -51,7 +51,7 @@ constexpr int kNS = 3;                  // ring stages per CTA
 constexpr int kCtasPerSm = 2;           // independent pipelines per SM
 constexpr int kStage = 34 * 1024;       // bytes per stage
 constexpr int kConsumers = 8;           // consumer warps (= column subsets of B/C pieces)
-constexpr int kThreads = 32 * (kConsumers + 2);  // + producer and publisher warps
+constexpr int kThreads = 32 * (kConsumers + 1);  // + producer warp
 constexpr int kDList = 64;              // B items per CTA between completion publishes
 constexpr int kMaxRPieces = 256;        // node-reduction pieces
 constexpr int kMaxLev = 24;
@@ -348,11 +348,7 @@ struct SmemCtl {
     PieceHdr hdr[kNS];
     unsigned epoch;
     unsigned a_cnt, r_cnt, d_cnt;  // consumer completions (A items, R pieces, B items)
-    volatile unsigned a_pub, r_pub;  // ... published GPU-wide by the publisher warp
-    volatile int d_tail, d_head;   // B-item FIFO: pushed by the producer, popped when published
-    volatile int prod_done;        // producer finished emitting
-    unsigned a_emit, r_emit;       // A items / R pieces emitted (valid once prod_done)
-    int dlist[kDList];             // leaves of B items emitted but not yet published
+    int dlist[kDList];             // leaves of B items emitted but not yet published (FIFO)
     unsigned dend[kDList];         // ... and the cumulative B-item count at their end
     alignas(16) int16_t cidx[kMaxCols];  // flattened U column -> coefficient slot
     int64_t pbase_c[kMaxCols];     // flattened V' column -> partial buffer base (level pbase + c*nch)
@@ -379,9 +375,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     if (threadIdx.x == 0) {
         C.epoch = ld_acquire(&a.sync->epoch);
         C.a_cnt = C.r_cnt = C.d_cnt = 0u;
-        C.a_pub = C.r_pub = 0u;
-        C.d_tail = C.d_head = 0;
-        C.prod_done = 0;
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&C.full[s], 1);
             mbar_init(&C.empty[s], kConsumers);
@@ -403,17 +396,41 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         // =========================================================== producer
         int stage = 0;
         unsigned phase = 0;
-        int dt = 0;                     // B items pushed to the publish FIFO
+        unsigned a_pub = 0, r_pub = 0;  // completions published GPU-wide
+        int dh = 0, dt = 0;             // B-item FIFO head / tail (warp-uniform)
         unsigned d_items = 0;           // B items emitted by this CTA
         unsigned a_items = 0, r_items = 0;
-        // wait until the publisher warp has made everything emitted so far visible
-        auto drain_published = [&]() {
-            if (lane == 0)
-                while (C.a_pub != a_items || C.r_pub != r_items || C.d_head != dt) __nanosleep(64);
-            __syncwarp();
+        // Publish this CTA's finished work GPU-wide.  Consumers signal completion
+        // with CTA-scope releases on C.*_cnt (after the data's stores); one fence
+        // plus one release reduction per batch makes it visible.  block: wait until
+        // everything emitted so far is published.
+        auto publish = [&](bool block) {
+            for (;;) {
+                int n = 0;
+                unsigned na = 0, nr = 0;
+                if (lane == 0) {
+                    const unsigned dd = *(volatile unsigned*)&C.d_cnt;
+                    while (dh + n != dt && dd >= C.dend[(dh + n) % kDList]) ++n;
+                    na = *(volatile unsigned*)&C.a_cnt - a_pub;
+                    nr = *(volatile unsigned*)&C.r_cnt - r_pub;
+                    if (n || na || nr) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    if (na) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->a_done), "r"(na) : "memory");
+                    if (nr) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->r_done), "r"(nr) : "memory");
+                }
+                n = __shfl_sync(0xffffffffu, n, 0);
+                a_pub += __shfl_sync(0xffffffffu, na, 0);
+                r_pub += __shfl_sync(0xffffffffu, nr, 0);
+                for (int i = lane; i < n; i += 32)
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.dcount + C.dlist[(dh + i) % kDList])
+                                 : "memory");
+                dh += n;
+                __syncwarp();
+                if (!block || (dh == dt && a_pub == a_items && r_pub == r_items)) return;
+                __nanosleep(64);
+            }
         };
         auto claim = [&]() -> uint8_t* {
-            mbar_wait(&C.empty[stage], phase ^ 1u);
+            while (!mbar_test(&C.empty[stage], phase ^ 1u)) publish(false);
             return stages + (size_t)stage * kStage;
         };
         auto next_stage = [&]() {
@@ -463,13 +480,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             if (q >= nq) break;
             n1 = n2;
             if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);
+            publish(false);
             if (q >= P.pos_r && q < P.pos_r + P.num_r) {
                 // ---- R: reduce node partials (needs every leaf's partials)
                 const RPiece rp = P.rp[q - P.pos_r];
                 const Level& L = P.lev[rp.lv];
                 const int nch = 1 << (nlev - 1 - rp.lv);
                 if (!a_ready) {
-                    drain_published();  // own A items first
+                    publish(true);  // own A items first
                     if (lane == 0) wait_count(&a.sync->a_done, (unsigned)P.num_a);
                     a_ready = true;
                 }
@@ -495,13 +513,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 // ---- B: y = D x for one 64-row block
                 const int leaf = qb / kBlocks, rb = qb % kBlocks;
                 const uint8_t* blk = a.slab + (int64_t)leaf * P.slab_bytes + P.ds_off + (int64_t)rb * P.dblock_bytes;
+                if (dt - dh == kDList) publish(true);
                 ++d_items;
                 if (lane == 0) {
-                    while (dt - C.d_head >= kDList) __nanosleep(64);  // FIFO full
                     C.dlist[dt % kDList] = leaf;
                     C.dend[dt % kDList] = d_items;
-                    __threadfence_block();
-                    C.d_tail = dt + 1;
                 }
                 __syncwarp();
                 ++dt;
@@ -530,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 const int u = qb - P.num_d;
                 const int leaf = u / kBlocks, rb = u % kBlocks;
                 if (!r_ready) {
-                    drain_published();  // own B and R items first
+                    publish(true);  // own B and R items first
                     if (lane == 0) wait_count(&a.sync->r_done, (unsigned)P.num_r);
                     r_ready = true;
                 }
@@ -570,63 +586,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 next_stage();
             }
         }
+        publish(true);
         claim();
         if (lane == 0) {
             C.hdr[stage].type = PT_END;
             mbar_arrive(&C.full[stage]);
-            C.a_emit = a_items;
-            C.r_emit = r_items;
-            __threadfence_block();
-            C.prod_done = 1;
         }
         __syncwarp();
-    } else if (warp == 1) {
-        // =========================================================== publisher
-        // Makes this CTA's finished work visible GPU-wide.  Consumers signal with
-        // CTA-scope releases on C.*_cnt after the work's global stores; one GPU
-        // fence plus release reductions per batch publish it (kept off the
-        // producer: a GPU-scope fence costs microseconds under full HBM load).
-        int dh = 0;
-        unsigned a_pub = 0, r_pub = 0;
-        for (;;) {
-            int n = 0;
-            unsigned na = 0, nr = 0;
-            bool done = false;
-            if (lane == 0) {
-                done = C.prod_done != 0;  // read first: then every item below is already listed
-                const int dt = C.d_tail;
-                const unsigned dd = *(volatile unsigned*)&C.d_cnt;
-                while (dh + n != dt && dd >= C.dend[(dh + n) % kDList]) ++n;
-                na = *(volatile unsigned*)&C.a_cnt - a_pub;
-                nr = *(volatile unsigned*)&C.r_cnt - r_pub;
-                if (n || na || nr) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                if (na) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->a_done), "r"(na) : "memory");
-                if (nr) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->r_done), "r"(nr) : "memory");
-                done = done && dh + n == dt && a_pub + na == C.a_emit && r_pub + nr == C.r_emit;
-            }
-            n = __shfl_sync(0xffffffffu, n, 0);
-            na = __shfl_sync(0xffffffffu, na, 0);
-            nr = __shfl_sync(0xffffffffu, nr, 0);
-            done = __shfl_sync(0xffffffffu, done, 0);
-            for (int i = lane; i < n; i += 32)
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.dcount + C.dlist[(dh + i) % kDList])
-                             : "memory");
-            __syncwarp();
-            dh += n;
-            a_pub += na;
-            r_pub += nr;
-            if (lane == 0 && (n || na || nr)) {
-                C.a_pub = a_pub;
-                C.r_pub = r_pub;
-                C.d_head = dh;
-            }
-            if (done) break;
-            if (!(n || na || nr)) __nanosleep(128);
-        }
     } else {
         // =========================================================== consumers
-        const int cw = warp - 2;
-        const int ctid = threadIdx.x - 64;
+        const int cw = warp - 1;
+        const int ctid = threadIdx.x - 32;
         int stage = 0;
         unsigned phase = 0;
         W aacc[2][4];   // phase A: column sums of the current format group
