@@ -404,15 +404,25 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         // with CTA-scope releases on C.*_cnt (after the data's stores); one fence
         // plus one release reduction per batch makes it visible.  block: wait until
         // everything emitted so far is published.
-        auto publish = [&](bool block) {
+        // Publish this CTA's finished work GPU-wide.  Consumers signal completion
+        // with CTA-scope releases on C.*_cnt after the work's global stores; one
+        // GPU fence plus release reductions publishes a batch.  A GPU-scope fence
+        // costs microseconds under full HBM load, so fences are rare: phase A is
+        // published once when all of this CTA's leaves are done (R items wait on
+        // it); B items and R pieces only once, when this CTA turns to phase C
+        // (or the B FIFO fills).  block: wait until the requested work is done.
+        auto publish = [&](bool block, bool with_bd) {
             for (;;) {
                 int n = 0;
                 unsigned na = 0, nr = 0;
                 if (lane == 0) {
-                    const unsigned dd = *(volatile unsigned*)&C.d_cnt;
-                    while (dh + n != dt && dd >= C.dend[(dh + n) % kDList]) ++n;
-                    na = *(volatile unsigned*)&C.a_cnt - a_pub;
-                    nr = *(volatile unsigned*)&C.r_cnt - r_pub;
+                    const unsigned ac = *(volatile unsigned*)&C.a_cnt;
+                    if (ac == a_items) na = ac - a_pub;  // all-or-nothing: one fence for phase A
+                    if (with_bd) {
+                        const unsigned dd = *(volatile unsigned*)&C.d_cnt;
+                        while (dh + n != dt && dd >= C.dend[(dh + n) % kDList]) ++n;
+                        nr = *(volatile unsigned*)&C.r_cnt - r_pub;
+                    }
                     if (n || na || nr) asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     if (na) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->a_done), "r"(na) : "memory");
                     if (nr) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->r_done), "r"(nr) : "memory");
@@ -425,12 +435,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                                  : "memory");
                 dh += n;
                 __syncwarp();
-                if (!block || (dh == dt && a_pub == a_items && r_pub == r_items)) return;
+                const bool a_ok = a_pub == a_items;
+                const bool bd_ok = !with_bd || (dh == dt && r_pub == r_items);
+                if (!block || (a_ok && bd_ok)) return;
                 __nanosleep(64);
             }
         };
         auto claim = [&]() -> uint8_t* {
-            while (!mbar_test(&C.empty[stage], phase ^ 1u)) publish(false);
+            while (!mbar_test(&C.empty[stage], phase ^ 1u)) if (a_pub != a_items) publish(false, false);
             return stages + (size_t)stage * kStage;
         };
         auto next_stage = [&]() {
@@ -443,6 +455,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             while (ld_acquire(ctr) != want) __nanosleep(128);
         };
         bool a_ready = false, r_ready = false;
+#ifdef HODLR_PROFILE
+        bool first_c = true;
+#endif
 
         // ---- phase A: leaves dealt round-robin, every CTA starts with its share
         for (int leaf = blockIdx.x; leaf < P.num_a; leaf += gridDim.x) {
@@ -468,6 +483,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 next_stage();
             }
         }
+#ifdef HODLR_PROFILE
+        if (lane == 0) prof[4] = clock64() - t_kernel;  // A emitted
+#endif
         // ---- B, R, C items from one atomic queue, fetched two ahead
         int n1 = 0, n2 = 0;
         if (lane == 0) {
@@ -480,14 +498,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             if (q >= nq) break;
             n1 = n2;
             if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);
-            publish(false);
+            if (a_pub != a_items) publish(false, false);
             if (q >= P.pos_r && q < P.pos_r + P.num_r) {
                 // ---- R: reduce node partials (needs every leaf's partials)
                 const RPiece rp = P.rp[q - P.pos_r];
                 const Level& L = P.lev[rp.lv];
                 const int nch = 1 << (nlev - 1 - rp.lv);
                 if (!a_ready) {
-                    publish(true);  // own A items first
+                    publish(true, false);  // own A items first
                     if (lane == 0) wait_count(&a.sync->a_done, (unsigned)P.num_a);
                     a_ready = true;
                 }
@@ -513,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 // ---- B: y = D x for one 64-row block
                 const int leaf = qb / kBlocks, rb = qb % kBlocks;
                 const uint8_t* blk = a.slab + (int64_t)leaf * P.slab_bytes + P.ds_off + (int64_t)rb * P.dblock_bytes;
-                if (dt - dh == kDList) publish(true);
+                if (dt - dh == kDList) publish(true, true);
                 ++d_items;
                 if (lane == 0) {
                     C.dlist[dt % kDList] = leaf;
@@ -545,13 +563,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 // ---- C: b = U t + y for one 64-row block
                 const int u = qb - P.num_d;
                 const int leaf = u / kBlocks, rb = u % kBlocks;
+#ifdef HODLR_PROFILE
+                if (first_c && lane == 0) prof[5] = clock64() - t_kernel;  // first C item
+#endif
                 if (!r_ready) {
-                    publish(true);  // own B and R items first
+                    publish(true, true);  // own B and R items first
                     if (lane == 0) wait_count(&a.sync->r_done, (unsigned)P.num_r);
                     r_ready = true;
                 }
                 if (lane == 0) wait_count(&a.dcount[leaf], d_expect);
                 __syncwarp();
+#ifdef HODLR_PROFILE
+                if (first_c && lane == 0) prof[6] = clock64() - t_kernel;  // first C item ready
+                first_c = false;
+#endif
                 uint8_t* st = claim();
                 const int wi = sizeof(W) == 8 ? 1 : 0;
                 const int wbytes = (int)sizeof(W);
@@ -586,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 next_stage();
             }
         }
-        publish(true);
+        publish(true, true);
         claim();
         if (lane == 0) {
             C.hdr[stage].type = PT_END;
@@ -608,10 +633,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
 #pragma unroll
         for (int k = 0; k < 4; ++k) bacc[k][0] = bacc[k][1] = W(0);
         for (;;) {
+            PROF_T(tw);
             mbar_wait(&C.full[stage], phase);
             const PieceHdr h = C.hdr[stage];
             uint8_t* st = stages + (size_t)stage * kStage;
             if (h.type == PT_END) break;
+            PROF_ADD(h.type == PT_R ? 0 : h.type, clock64() - tw);  // [1] A [2] D [3] U [0] R
             bool scratch = false;  // the stage was reused as reduction scratch
             if (h.type == PT_A) {
                 const APiece ap = P.ap[h.a];
@@ -740,6 +767,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     }
     // ---- teardown: the last CTA resets the per-call state and bumps the epoch
     __syncthreads();
+#ifdef HODLR_PROFILE
+    if (threadIdx.x == 0 && (blockIdx.x % 50) == 0)
+        printf("PROF cta %3d total %lld | A_emitted %lld firstC %lld firstC_ready %lld | cons_wait(sum 8 warps) A %lld D %lld U %lld R %lld\n",
+               blockIdx.x, clock64() - t_kernel, prof[4], prof[5], prof[6], prof[1], prof[2], prof[3], prof[0]);
+#endif
     __shared__ unsigned s_last;
     if (threadIdx.x == 0) {
         unsigned old;

@@ -40,11 +40,11 @@ def main():
     dt = torch.float64 if H.working_format.name == "fp64" else torch.float32
     xd = torch.from_numpy(x).cuda().to(dt)
     bd = torch.empty_like(xd)
-    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    flush = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
     times = []
     st = torch.cuda.current_stream()
     for i in range(args.iters):
-        flush.fill_(float(i))
+        flush.sum()  # read-only L2 flush: evicts the matrix, leaves no dirty lines
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         op.matvec(xd, out=bd.view(-1, 1))
