@@ -418,10 +418,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 if (lane == 0) {
                     const unsigned ac = *(volatile unsigned*)&C.a_cnt;
                     if (ac == a_items) na = ac - a_pub;  // all-or-nothing: one fence for phase A
+                    nr = *(volatile unsigned*)&C.r_cnt - r_pub;  // R pieces gate every C item: eager
                     if (with_bd) {
                         const unsigned dd = *(volatile unsigned*)&C.d_cnt;
                         while (dh + n != dt && dd >= C.dend[(dh + n) % kDList]) ++n;
-                        nr = *(volatile unsigned*)&C.r_cnt - r_pub;
                     }
                     if (n || na || nr) asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     if (na) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->a_done), "r"(na) : "memory");
@@ -436,13 +436,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 dh += n;
                 __syncwarp();
                 const bool a_ok = a_pub == a_items;
-                const bool bd_ok = !with_bd || (dh == dt && r_pub == r_items);
+                const bool bd_ok = !with_bd || (dh == dt && r_pub == r_items);  // (R waited on only here)
                 if (!block || (a_ok && bd_ok)) return;
                 __nanosleep(64);
             }
         };
         auto claim = [&]() -> uint8_t* {
-            while (!mbar_test(&C.empty[stage], phase ^ 1u)) if (a_pub != a_items) publish(false, false);
+            while (!mbar_test(&C.empty[stage], phase ^ 1u))
+                if (a_pub != a_items || r_pub != r_items) publish(false, false);
             return stages + (size_t)stage * kStage;
         };
         auto next_stage = [&]() {
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             if (q >= nq) break;
             n1 = n2;
             if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);
-            if (a_pub != a_items) publish(false, false);
+            if (a_pub != a_items || r_pub != r_items) publish(false, false);
             if (q >= P.pos_r && q < P.pos_r + P.num_r) {
                 // ---- R: reduce node partials (needs every leaf's partials)
                 const RPiece rp = P.rp[q - P.pos_r];
@@ -768,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     // ---- teardown: the last CTA resets the per-call state and bumps the epoch
     __syncthreads();
 #ifdef HODLR_PROFILE
-    if (threadIdx.x == 0 && (blockIdx.x % 50) == 0)
+    if (threadIdx.x == 0)
         printf("PROF cta %3d total %lld | A_emitted %lld firstC %lld firstC_ready %lld | cons_wait(sum 8 warps) A %lld D %lld U %lld R %lld\n",
                blockIdx.x, clock64() - t_kernel, prof[4], prof[5], prof[6], prof[1], prof[2], prof[3], prof[0]);
 #endif
