@@ -52,7 +52,7 @@ constexpr int kCtasPerSm = 2;           // independent pipelines per SM
 constexpr int kStage = 34 * 1024;       // bytes per stage
 constexpr int kConsumers = 8;           // consumer warps (= column subsets of B/C pieces)
 constexpr int kThreads = 32 * (kConsumers + 1);  // + producer warp
-constexpr int kDList = 64;              // B items per CTA between completion publishes
+constexpr int kFifo = 8;                // BC items whose U piece waits for the coefficients
 constexpr int kMaxRPieces = 256;        // node-reduction pieces
 constexpr int kMaxLev = 24;
 constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
@@ -91,14 +91,14 @@ struct RPiece {
 struct SvParams {
     int32_t depth, nleaves, nnodes;
     int32_t leaf_fmt;
-    int32_t num_a, num_d, num_u, num_r, pos_r;  // queue: B items with R items at pos_r, then C
+    int32_t num_a, num_d, num_r, pos_r;   // queue: BC items with the R pieces at pos_r
     int32_t napieces, dpieces, dcols;     // phase-B pieces per item and columns per piece
     int64_t slab_bytes, ds_off, us_off;
     int64_t dblock_bytes, ublock_bytes;
     int32_t gcols[5], vpad[5];
     int64_t vgoff[5], ugoff[5];           // V' sub-slab offsets / U sub-block offsets in a block
     int32_t coef_elems;
-    int32_t u_y_off[2], u_data_off[2], u_bytes[2];  // U piece layout for fp32 / fp64 working
+    int32_t u_data_off[2], u_bytes[2];    // U piece layout for fp32 / fp64 working
     Level lev[kMaxLev];
     APiece ap[kMaxPieces];
     RPiece rp[kMaxRPieces];
@@ -340,16 +340,15 @@ struct SvKernelArgs {
     W* partial;            // fast-path layout: level bases P.lev[].pbase
     W* tbuf;
     SvSync* sync;
-    unsigned* dcount;      // [nleaves]: phase-B items of the leaf whose y is in b
 };
 
 struct SmemCtl {
     uint64_t full[kNS], empty[kNS];
     PieceHdr hdr[kNS];
     unsigned epoch;
-    unsigned a_cnt, r_cnt, d_cnt;  // consumer completions (A items, R pieces, B items)
-    int dlist[kDList];             // leaves of B items emitted but not yet published (FIFO)
-    unsigned dend[kDList];         // ... and the cumulative B-item count at their end
+    unsigned a_cnt, r_cnt;         // consumer completions (A leaves, R pieces)
+    int fifo[kFifo];               // deferred U pieces: (leaf << 8) | row block
+    alignas(16) double ybuf[kFifo][kRB];  // y = D x of those items (working type)
     alignas(16) int16_t cidx[kMaxCols];  // flattened U column -> coefficient slot
     int64_t pbase_c[kMaxCols];     // flattened V' column -> partial buffer base (level pbase + c*nch)
     int32_t pstride_c[kMaxCols];   //                     -> r * nch (stride between nodes)
@@ -368,13 +367,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     SmemCtl& C = *reinterpret_cast<SmemCtl*>(smem + kNS * kStage);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nlev = P.depth;
-    const int nq = P.num_d + P.num_r + P.num_u;  // dynamic queue: B (R inserted at pos_r), then C
+    const int nq = P.num_d + P.num_r;            // dynamic queue: BC items with R pieces at pos_r
     constexpr int kBlocks = kM / kRB;            // row blocks per leaf
-    const unsigned d_expect = (unsigned)kBlocks;
 
     if (threadIdx.x == 0) {
         C.epoch = ld_acquire(&a.sync->epoch);
-        C.a_cnt = C.r_cnt = C.d_cnt = 0u;
+        C.a_cnt = C.r_cnt = 0u;
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&C.full[s], 1);
             mbar_init(&C.empty[s], kConsumers);
@@ -397,53 +395,34 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         int stage = 0;
         unsigned phase = 0;
         unsigned a_pub = 0, r_pub = 0;  // completions published GPU-wide
-        int dh = 0, dt = 0;             // B-item FIFO head / tail (warp-uniform)
-        unsigned d_items = 0;           // B items emitted by this CTA
         unsigned a_items = 0, r_items = 0;
-        // Publish this CTA's finished work GPU-wide.  Consumers signal completion
-        // with CTA-scope releases on C.*_cnt (after the data's stores); one fence
-        // plus one release reduction per batch makes it visible.  block: wait until
-        // everything emitted so far is published.
-        // Publish this CTA's finished work GPU-wide.  Consumers signal completion
-        // with CTA-scope releases on C.*_cnt after the work's global stores; one
-        // GPU fence plus release reductions publishes a batch.  A GPU-scope fence
-        // costs microseconds under full HBM load, so fences are rare: phase A is
-        // published once when all of this CTA's leaves are done (R items wait on
-        // it); B items and R pieces only once, when this CTA turns to phase C
-        // (or the B FIFO fills).  block: wait until the requested work is done.
-        auto publish = [&](bool block, bool with_bd) {
+        int fh = 0, ft = 0;             // deferred-U FIFO (warp-uniform); slot = index % kFifo
+        // Publish this CTA's finished phase-A leaves (once, all together) and R
+        // pieces GPU-wide.  Consumers signal with CTA-scope releases on C.*_cnt
+        // after the work's global stores; one GPU fence plus a release reduction
+        // publishes a batch (a GPU-scope fence costs microseconds under full HBM
+        // load, so there are only a handful per matvec).  block: wait for all.
+        auto publish = [&](bool block) {
             for (;;) {
-                int n = 0;
                 unsigned na = 0, nr = 0;
                 if (lane == 0) {
                     const unsigned ac = *(volatile unsigned*)&C.a_cnt;
-                    if (ac == a_items) na = ac - a_pub;  // all-or-nothing: one fence for phase A
-                    nr = *(volatile unsigned*)&C.r_cnt - r_pub;  // R pieces gate every C item: eager
-                    if (with_bd) {
-                        const unsigned dd = *(volatile unsigned*)&C.d_cnt;
-                        while (dh + n != dt && dd >= C.dend[(dh + n) % kDList]) ++n;
-                    }
-                    if (n || na || nr) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    if (ac == a_items) na = ac - a_pub;
+                    nr = *(volatile unsigned*)&C.r_cnt - r_pub;
+                    if (na || nr) asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     if (na) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->a_done), "r"(na) : "memory");
                     if (nr) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->r_done), "r"(nr) : "memory");
                 }
-                n = __shfl_sync(0xffffffffu, n, 0);
                 a_pub += __shfl_sync(0xffffffffu, na, 0);
                 r_pub += __shfl_sync(0xffffffffu, nr, 0);
-                for (int i = lane; i < n; i += 32)
-                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.dcount + C.dlist[(dh + i) % kDList])
-                                 : "memory");
-                dh += n;
-                __syncwarp();
-                const bool a_ok = a_pub == a_items;
-                const bool bd_ok = !with_bd || (dh == dt && r_pub == r_items);  // (R waited on only here)
-                if (!block || (a_ok && bd_ok)) return;
+                if (!block || (a_pub == a_items && r_pub == r_items)) return;
                 __nanosleep(64);
             }
         };
+        auto pending = [&]() { return a_pub != a_items || r_pub != r_items; };
         auto claim = [&]() -> uint8_t* {
             while (!mbar_test(&C.empty[stage], phase ^ 1u))
-                if (a_pub != a_items || r_pub != r_items) publish(false, false);
+                if (pending()) publish(false);
             return stages + (size_t)stage * kStage;
         };
         auto next_stage = [&]() {
@@ -452,13 +431,62 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 phase ^= 1u;
             }
         };
-        auto wait_count = [&](const unsigned* ctr, unsigned want) {  // lane 0
-            while (ld_acquire(ctr) != want) __nanosleep(128);
+        // coefficients of every node exist?  (checked without blocking until the
+        // deferred-U FIFO is full; the result is cached)
+        bool r_ready = false;
+        auto check_r = [&](bool block) {
+            if (r_ready) return;
+            unsigned v = 0;
+            if (lane == 0) {
+                v = ld_acquire(&a.sync->r_done);
+                while (block && v != (unsigned)P.num_r) {
+                    __nanosleep(128);
+                    v = ld_acquire(&a.sync->r_done);
+                }
+            }
+            r_ready = __shfl_sync(0xffffffffu, v, 0) == (unsigned)P.num_r;
+            if (r_ready) asm volatile("fence.proxy.async.global;" ::: "memory");  // t read by TMA below
         };
-        bool a_ready = false, r_ready = false;
-#ifdef HODLR_PROFILE
-        bool first_c = true;
-#endif
+        auto emit_u = [&](int leaf, int rb, int slot) {
+            uint8_t* st = claim();
+            const int wi = sizeof(W) == 8 ? 1 : 0;
+            const int wbytes = (int)sizeof(W);
+            if (lane == 0) {
+                PieceHdr& h = C.hdr[stage];
+                h.type = PT_U;
+                h.leaf = leaf;
+                h.a = rb;
+                h.b = slot;
+                mbar_arrive_tx(&C.full[stage], (unsigned)P.u_bytes[wi]);
+            }
+            __syncwarp();
+            if (lane < nlev) {
+                const Level& L = P.lev[lane];
+                if (L.r > 0) {
+                    const int k = lane + 1;
+                    const int jsib = (leaf >> (nlev - k)) ^ 1;
+                    const W* src = a.tbuf + L.tbase + (int64_t)jsib * L.tstride;
+                    bulk_g2s(st + (size_t)L.slot * wbytes, src, (unsigned)(L.tstride * wbytes), &C.full[stage]);
+                }
+            } else if (lane == 31) {
+                bulk_g2s(st + P.u_data_off[wi],
+                         a.slab + (int64_t)leaf * P.slab_bytes + P.us_off + (int64_t)rb * P.ublock_bytes,
+                         (unsigned)P.ublock_bytes, &C.full[stage]);
+            }
+            __syncwarp();
+            next_stage();
+        };
+        auto flush_u = [&](bool block) {
+            if (fh == ft) return;
+            if (block && !r_ready) publish(true);  // never block while holding unpublished work
+            check_r(block);
+            if (!r_ready) return;
+            while (fh != ft) {
+                const int e = C.fifo[fh % kFifo];
+                emit_u(e >> 8, e & 0xff, fh % kFifo);
+                ++fh;
+            }
+        };
 
         // ---- phase A: leaves dealt round-robin, every CTA starts with its share
         for (int leaf = blockIdx.x; leaf < P.num_a; leaf += gridDim.x) {
@@ -484,10 +512,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 next_stage();
             }
         }
-#ifdef HODLR_PROFILE
-        if (lane == 0) prof[4] = clock64() - t_kernel;  // A emitted
-#endif
-        // ---- B, R, C items from one atomic queue, fetched two ahead
+        // ---- R pieces and BC items (leaf, 64-row block) from one atomic queue
         int n1 = 0, n2 = 0;
         if (lane == 0) {
             n1 = (int)atomicAdd(&a.sync->queue, 1u);
@@ -499,16 +524,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             if (q >= nq) break;
             n1 = n2;
             if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);
-            if (a_pub != a_items || r_pub != r_items) publish(false, false);
+            if (pending()) publish(false);
             if (q >= P.pos_r && q < P.pos_r + P.num_r) {
                 // ---- R: reduce node partials (needs every leaf's partials)
                 const RPiece rp = P.rp[q - P.pos_r];
                 const Level& L = P.lev[rp.lv];
                 const int nch = 1 << (nlev - 1 - rp.lv);
-                if (!a_ready) {
-                    publish(true, false);  // own A items first
-                    if (lane == 0) wait_count(&a.sync->a_done, (unsigned)P.num_a);
-                    a_ready = true;
+                publish(true);  // own A leaves first (and anything else pending)
+                if (lane == 0) {
+                    while (ld_acquire(&a.sync->a_done) != (unsigned)P.num_a) __nanosleep(128);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 __syncwarp();
                 ++r_items;
@@ -520,99 +545,45 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     h.type = PT_R;
                     h.a = q - P.pos_r;
                     mbar_arrive_tx(&C.full[stage], bytes);
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
                     bulk_g2s(st, a.partial + L.pbase + ((int64_t)rp.j0 * L.r + rp.c0) * nch, bytes, &C.full[stage]);
                 }
                 __syncwarp();
                 next_stage();
                 continue;
             }
+            // ---- BC: y = D x now (kept in this CTA's y slot), b = U t + y once t exists
             const int qb = q < P.pos_r ? q : q - P.num_r;
-            if (qb < P.num_d) {
-                // ---- B: y = D x for one 64-row block
-                const int leaf = qb / kBlocks, rb = qb % kBlocks;
-                const uint8_t* blk = a.slab + (int64_t)leaf * P.slab_bytes + P.ds_off + (int64_t)rb * P.dblock_bytes;
-                if (dt - dh == kDList) publish(true, true);
-                ++d_items;
-                if (lane == 0) {
-                    C.dlist[dt % kDList] = leaf;
-                    C.dend[dt % kDList] = d_items;
-                }
-                __syncwarp();
-                ++dt;
-                for (int p = 0; p < P.dpieces; ++p) {
-                    uint8_t* st = claim();
-                    const int c0 = p * P.dcols;
-                    const int nc = min(P.dcols, kM - c0);
-                    const unsigned cb = (unsigned)(nc * kRB * dsz);
-                    const unsigned xb = (unsigned)(nc * sizeof(W));
-                    if (lane == 0) {
-                        PieceHdr& h = C.hdr[stage];
-                        h.type = PT_D;
-                        h.leaf = leaf;
-                        h.a = rb;
-                        h.b = c0;
-                        h.last = (p == P.dpieces - 1);
-                        mbar_arrive_tx(&C.full[stage], xb + cb);
-                        bulk_g2s(st, a.x + (int64_t)leaf * kM + c0, xb, &C.full[stage]);
-                        bulk_g2s(st + kXB, blk + (int64_t)c0 * kRB * dsz, cb, &C.full[stage]);
-                    }
-                    __syncwarp();
-                    next_stage();
-                }
-            } else {
-                // ---- C: b = U t + y for one 64-row block
-                const int u = qb - P.num_d;
-                const int leaf = u / kBlocks, rb = u % kBlocks;
-#ifdef HODLR_PROFILE
-                if (first_c && lane == 0) prof[5] = clock64() - t_kernel;  // first C item
-#endif
-                if (!r_ready) {
-                    publish(true, true);  // own B and R items first
-                    if (lane == 0) wait_count(&a.sync->r_done, (unsigned)P.num_r);
-                    r_ready = true;
-                }
-                if (lane == 0) wait_count(&a.dcount[leaf], d_expect);
-                __syncwarp();
-#ifdef HODLR_PROFILE
-                if (first_c && lane == 0) prof[6] = clock64() - t_kernel;  // first C item ready
-                first_c = false;
-#endif
+            const int leaf = qb / kBlocks, rb = qb % kBlocks;
+            if (ft - fh == kFifo) flush_u(true);  // frees the y slot this item will use
+            const int slot = ft % kFifo;
+            const uint8_t* blk = a.slab + (int64_t)leaf * P.slab_bytes + P.ds_off + (int64_t)rb * P.dblock_bytes;
+            for (int p = 0; p < P.dpieces; ++p) {
                 uint8_t* st = claim();
-                const int wi = sizeof(W) == 8 ? 1 : 0;
-                const int wbytes = (int)sizeof(W);
+                const int c0 = p * P.dcols;
+                const int nc = min(P.dcols, kM - c0);
+                const unsigned cb = (unsigned)(nc * kRB * dsz);
+                const unsigned xb = (unsigned)(nc * sizeof(W));
                 if (lane == 0) {
                     PieceHdr& h = C.hdr[stage];
-                    h.type = PT_U;
+                    h.type = PT_D;
                     h.leaf = leaf;
                     h.a = rb;
-                    mbar_arrive_tx(&C.full[stage], (unsigned)P.u_bytes[wi]);
-                }
-                __syncwarp();
-                // t and y were written by other SMs (generic proxy, made visible by the
-                // acquires above); order them before the async-proxy reads
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                if (lane < nlev) {
-                    const Level& L = P.lev[lane];
-                    if (L.r > 0) {
-                        const int k = lane + 1;
-                        const int jsib = (leaf >> (nlev - k)) ^ 1;
-                        const W* src = a.tbuf + L.tbase + (int64_t)jsib * L.tstride;
-                        bulk_g2s(st + (size_t)L.slot * wbytes, src, (unsigned)(L.tstride * wbytes), &C.full[stage]);
-                    }
-                } else if (lane == 30) {
-                    bulk_g2s(st + P.u_y_off[wi], a.b + (int64_t)leaf * kM + rb * kRB, (unsigned)(kRB * wbytes),
-                             &C.full[stage]);
-                } else if (lane == 31) {
-                    bulk_g2s(st + P.u_data_off[wi],
-                             a.slab + (int64_t)leaf * P.slab_bytes + P.us_off + (int64_t)rb * P.ublock_bytes,
-                             (unsigned)P.ublock_bytes, &C.full[stage]);
+                    h.b = c0;
+                    h.last = (p == P.dpieces - 1) ? 1 + slot : 0;
+                    mbar_arrive_tx(&C.full[stage], xb + cb);
+                    bulk_g2s(st, a.x + (int64_t)leaf * kM + c0, xb, &C.full[stage]);
+                    bulk_g2s(st + kXB, blk + (int64_t)c0 * kRB * dsz, cb, &C.full[stage]);
                 }
                 __syncwarp();
                 next_stage();
             }
+            if (lane == 0) C.fifo[ft % kFifo] = (leaf << 8) | rb;
+            __syncwarp();
+            ++ft;
+            flush_u(false);
         }
-        publish(true, true);
+        flush_u(true);
+        publish(true);
         claim();
         if (lane == 0) {
             C.hdr[stage].type = PT_END;
@@ -687,7 +658,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                         W s = red[ctid];
 #pragma unroll
                         for (int w = 1; w < kConsumers; ++w) s += red[w * kRB + ctid];
-                        a.b[(int64_t)h.leaf * kM + h.a * kRB + ctid] = s;  // y = D x
+                        reinterpret_cast<W*>(C.ybuf[h.last - 1])[ctid] = s;  // y = D x, kept for the U piece
                     }
 #pragma unroll
                     for (int k = 0; k < 4; ++k) bacc[k][0] = bacc[k][1] = W(0);
@@ -723,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             } else {  // PT_U: b = U t + y
                 const int wi = sizeof(W) == 8 ? 1 : 0;
                 const W* coef = reinterpret_cast<const W*>(st);
-                const W* ys = reinterpret_cast<const W*>(st + P.u_y_off[wi]);
+                const W* ys = reinterpret_cast<const W*>(C.ybuf[h.b]);
                 const uint8_t* ub = st + P.u_data_off[wi];
                 for (int g = 0; g < 5; ++g) {
                     const int nc = P.gcols[g];
@@ -750,11 +721,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 consumer_sync();  // scratch reads and the item's global stores are done
                 if (ctid == 0) {
                     const bool a_end = h.type == PT_A && h.last;
-                    const bool d_end = h.type == PT_D && h.last;
                     const bool r_end = h.type == PT_R;
-                    if (a_end || d_end || r_end) {
+                    if (a_end || r_end) {
                         asm volatile("fence.acq_rel.cta;" ::: "memory");
-                        atomicAdd(a_end ? &C.a_cnt : d_end ? &C.d_cnt : &C.r_cnt, 1u);
+                        atomicAdd(a_end ? &C.a_cnt : &C.r_cnt, 1u);
                     }
                 }
             }
@@ -781,8 +751,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     }
     __syncthreads();
     if (s_last) {
-        for (int i = threadIdx.x; i < P.nleaves; i += kThreads) a.dcount[i] = 0u;
-        __syncthreads();
         if (threadIdx.x == 0) {
             a.sync->queue = 0u;
             a.sync->done = 0u;
@@ -913,17 +881,15 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     P.dcols = (kStage - kXB) / (kRB * dsz);
     P.dcols = std::min(kM, P.dcols / 8 * 8);
     P.dpieces = (kM + P.dcols - 1) / P.dcols;
-    // phase-C piece: coefficients | y (64) | U block | reduction scratch (8 x 64)
+    // U piece: coefficients | U block | reduction scratch (8 x 64)
     for (int wi = 0; wi < 2; ++wi) {
         const int wb = wi ? 8 : 4;
-        P.u_y_off[wi] = (int)round_up16((int64_t)P.coef_elems * wb);
-        P.u_data_off[wi] = P.u_y_off[wi] + kRB * wb;
+        P.u_data_off[wi] = (int)round_up16((int64_t)P.coef_elems * wb);
         P.u_bytes[wi] = (int)(P.u_data_off[wi] + P.ublock_bytes);
         if (P.u_bytes[wi] + kConsumers * kRB * wb > kStage) return HODLR_OK;
     }
     P.num_a = nleaves;
     P.num_d = nleaves * (kM / kRB);
-    P.num_u = nleaves * (kM / kRB);
     // node-reduction pieces (R items): a level's partials are [node][column][leaf]
     P.num_r = 0;
     for (int k = 0; k < depth; ++k) {
@@ -951,7 +917,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
                     if (!add(j, j + 1, c0, std::min(L.r, c0 + cols))) return HODLR_OK;
         }
     }
-    P.pos_r = P.num_d * 3 / 5;  // R items run in the middle of phase B, long before phase C
+    P.pos_r = P.num_d / 6;  // after every CTA's phase-A leaves, well before the U pieces need t
 
     // ---- relayout the quantised level-batched arena into leaf slabs (bytes)
     std::vector<uint8_t> arena(in.arena_bytes);
@@ -1012,11 +978,11 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     sv.depth = depth;
     sv.rb = kRB;
     sv.num_items_a = P.num_a;
-    sv.num_items_b = P.num_d + P.num_u;
-    sv.grid = std::min(sms * std::min(occ, kCtasPerSm), P.num_a + P.num_d + P.num_u);
+    sv.num_items_b = P.num_d + P.num_r;
+    sv.grid = std::min(sms * std::min(occ, kCtasPerSm), P.num_a + P.num_d + P.num_r);
     sv.launches = 1;
     sv.tfast_count = tb;
-    sv.extra_ws = sv_sync_bytes(P.nleaves) + (size_t)(pb + tb) * 8;
+    sv.extra_ws = sv_sync_bytes(P.nleaves) + (size_t)(pb + tb) * 8;  // (leaf counters unused now)
     sv.part_count = pb;
     sv.leaf_fmt = lf;
     sv.params = new SvParams(P);
@@ -1047,7 +1013,6 @@ cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* 
     (void)partial;
     uint8_t* e = (uint8_t*)extra;
     a.sync = (SvSync*)e;
-    a.dcount = (unsigned*)(e + sizeof(SvSync));
     a.partial = (W*)(e + sv_sync_bytes(P.nleaves));
     a.tbuf = (W*)(e + sv_sync_bytes(P.nleaves) + sv.part_count * 8);
     void* args[] = {(void*)&P, &a};
