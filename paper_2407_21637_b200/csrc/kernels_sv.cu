@@ -46,7 +46,8 @@ namespace hodlr {
 namespace {
 
 constexpr int kM = 256;                 // leaf rows
-constexpr int kRB = 64;                 // rows of a phase-B / phase-C item
+constexpr int kRB = 32;                 // rows of a BC item (one leaf row block)
+constexpr int kRPL = kRB / 32;          // rows per lane in B / C pieces
 constexpr int kNS = 3;                  // ring stages per CTA
 constexpr int kCtasPerSm = 2;           // independent pipelines per SM
 constexpr int kStage = 34 * 1024;       // bytes per stage
@@ -282,47 +283,54 @@ __device__ __forceinline__ void a_piece(int g, const uint8_t* rows, int nrows, i
 // Column-major block (ncols x 64 rows) of format FMT: lane owns rows 2l, 2l+1,
 // warp w takes columns w, w + 8, ...; the multiplier of column c is mul(c)
 // (x or a coefficient).  4 independent accumulator pairs break the FMA chains.
+template <int FMT, typename W>
+__device__ __forceinline__ void col_elem(const uint8_t* p, W m, W acc[kRPL]) {
+    if constexpr (FMT == HODLR_FMT_FP64) {
+        if constexpr (kRPL == 2) {
+            const double2 t = *reinterpret_cast<const double2*>(p);
+            acc[0] = madd_d<W>(t.x, m, acc[0]);
+            acc[1] = madd_d<W>(t.y, m, acc[1]);
+        } else {
+            acc[0] = madd_d<W>(*reinterpret_cast<const double*>(p), m, acc[0]);
+        }
+    } else if constexpr (kRPL == 2) {
+        float a, b;
+        load2<FMT>(p, a, b);
+        acc[0] = madd<W>(a, m, acc[0]);
+        acc[1] = madd<W>(b, m, acc[1]);
+    } else {
+        float a;
+        if constexpr (FMT == HODLR_FMT_FP32) a = *reinterpret_cast<const float*>(p);
+        else if constexpr (FMT == HODLR_FMT_BF16) a = __uint_as_float((uint32_t)(*reinterpret_cast<const uint16_t*>(p)) << 16);
+        else if constexpr (FMT == HODLR_FMT_FP16) a = dec_fp16(*reinterpret_cast<const uint16_t*>(p));
+        else a = dec_q52(*p);
+        acc[0] = madd<W>(a, m, acc[0]);
+    }
+}
+
+// Column-major block (ncols x kRB rows) of format FMT: lane owns rows
+// kRPL*l .. kRPL*l + kRPL-1, warp w takes columns w, w + 8, ...; the multiplier
+// of column c is mul(c) (x or a coefficient).  4 accumulator sets break the
+// FMA chains.
 template <int FMT, typename W, typename MulF>
-__device__ __forceinline__ void col_block(const uint8_t* blk, int ncols, int warp, int lane, MulF mul, W acc[4][2]) {
+__device__ __forceinline__ void col_block(const uint8_t* blk, int ncols, int warp, int lane, MulF mul,
+                                          W acc[4][kRPL]) {
     constexpr int sz = FMT == HODLR_FMT_Q52 ? 1 : FMT == HODLR_FMT_FP32 ? 4 : FMT == HODLR_FMT_FP64 ? 8 : 2;
     int c = warp;
     for (; c + 3 * kConsumers < ncols; c += 4 * kConsumers) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int cc = c + k * kConsumers;
-            const W m = mul(cc);
-            const uint8_t* p = blk + ((size_t)cc * kRB + 2 * lane) * sz;
-            if constexpr (FMT == HODLR_FMT_FP64) {
-                const double2 t = *reinterpret_cast<const double2*>(p);
-                acc[k][0] = madd_d<W>(t.x, m, acc[k][0]);
-                acc[k][1] = madd_d<W>(t.y, m, acc[k][1]);
-            } else {
-                float a, b;
-                load2<FMT>(p, a, b);
-                acc[k][0] = madd<W>(a, m, acc[k][0]);
-                acc[k][1] = madd<W>(b, m, acc[k][1]);
-            }
+            col_elem<FMT, W>(blk + ((size_t)cc * kRB + kRPL * lane) * sz, mul(cc), acc[k]);
         }
     }
-    for (; c < ncols; c += kConsumers) {  // tail: fixed accumulator (no dynamic register indexing)
-        const W m = mul(c);
-        const uint8_t* p = blk + ((size_t)c * kRB + 2 * lane) * sz;
-        if constexpr (FMT == HODLR_FMT_FP64) {
-            const double2 t = *reinterpret_cast<const double2*>(p);
-            acc[0][0] = madd_d<W>(t.x, m, acc[0][0]);
-            acc[0][1] = madd_d<W>(t.y, m, acc[0][1]);
-        } else {
-            float a, b;
-            load2<FMT>(p, a, b);
-            acc[0][0] = madd<W>(a, m, acc[0][0]);
-            acc[0][1] = madd<W>(b, m, acc[0][1]);
-        }
-    }
+    for (; c < ncols; c += kConsumers)  // tail: fixed accumulator set (no dynamic register indexing)
+        col_elem<FMT, W>(blk + ((size_t)c * kRB + kRPL * lane) * sz, mul(c), acc[0]);
 }
 
 template <typename W, typename MulF>
 __device__ __forceinline__ void col_block_any(int fmt, const uint8_t* blk, int ncols, int warp, int lane, MulF mul,
-                                              W acc[4][2]) {
+                                              W acc[4][kRPL]) {
     switch (fmt) {
         case HODLR_FMT_FP64: col_block<HODLR_FMT_FP64, W>(blk, ncols, warp, lane, mul, acc); break;
         case HODLR_FMT_FP32: col_block<HODLR_FMT_FP32, W>(blk, ncols, warp, lane, mul, acc); break;
@@ -597,13 +605,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         int stage = 0;
         unsigned phase = 0;
         W aacc[2][4];   // phase A: column sums of the current format group
-        W bacc[4][2];   // phases B / C: row sums (2 rows per lane, 4 chains)
+        W bacc[4][kRPL];  // BC items: row sums (kRPL rows per lane, 4 chains)
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
             for (int e = 0; e < 4; ++e) aacc[i][e] = W(0);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) bacc[k][0] = bacc[k][1] = W(0);
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int r = 0; r < kRPL; ++r) bacc[k][r] = W(0);
         for (;;) {
             PROF_T(tw);
             mbar_wait(&C.full[stage], phase);
@@ -651,8 +661,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 if (h.last) {
                     W* red = reinterpret_cast<W*>(st);
                     consumer_sync();
-                    red[cw * kRB + 2 * lane] = (bacc[0][0] + bacc[1][0]) + (bacc[2][0] + bacc[3][0]);
-                    red[cw * kRB + 2 * lane + 1] = (bacc[0][1] + bacc[1][1]) + (bacc[2][1] + bacc[3][1]);
+#pragma unroll
+                    for (int r = 0; r < kRPL; ++r)
+                        red[cw * kRB + kRPL * lane + r] = (bacc[0][r] + bacc[1][r]) + (bacc[2][r] + bacc[3][r]);
                     consumer_sync();
                     if (ctid < kRB) {
                         W s = red[ctid];
@@ -661,7 +672,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                         reinterpret_cast<W*>(C.ybuf[h.last - 1])[ctid] = s;  // y = D x, kept for the U piece
                     }
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) bacc[k][0] = bacc[k][1] = W(0);
+                    for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int r = 0; r < kRPL; ++r) bacc[k][r] = W(0);
                     scratch = true;
                 }
             } else if (h.type == PT_R) {
@@ -704,8 +717,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     col_block_any<W>(g, ub + P.ugoff[g], nc, cw, lane, mul, bacc);
                 }
                 W* red = reinterpret_cast<W*>(st + P.u_bytes[wi]);  // scratch after the piece's data
-                red[cw * kRB + 2 * lane] = (bacc[0][0] + bacc[1][0]) + (bacc[2][0] + bacc[3][0]);
-                red[cw * kRB + 2 * lane + 1] = (bacc[0][1] + bacc[1][1]) + (bacc[2][1] + bacc[3][1]);
+#pragma unroll
+                for (int r = 0; r < kRPL; ++r)
+                    red[cw * kRB + kRPL * lane + r] = (bacc[0][r] + bacc[1][r]) + (bacc[2][r] + bacc[3][r]);
                 consumer_sync();
                 if (ctid < kRB) {
                     W s = red[ctid];
@@ -714,7 +728,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     a.b[(int64_t)h.leaf * kM + h.a * kRB + ctid] = s + ys[ctid];  // levels, then the leaf
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) bacc[k][0] = bacc[k][1] = W(0);
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int r = 0; r < kRPL; ++r) bacc[k][r] = W(0);
                 scratch = true;
             }
             if (scratch) {
