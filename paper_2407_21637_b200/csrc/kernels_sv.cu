@@ -46,7 +46,7 @@ namespace hodlr {
 namespace {
 
 constexpr int kM = 256;                 // leaf rows
-constexpr int kRB = 32;                 // rows of a BC item (one leaf row block)
+constexpr int kRB = 64;                 // rows of a BC item (one leaf row block)
 constexpr int kRPL = kRB / 32;          // rows per lane in B / C pieces
 constexpr int kNS = 3;                  // ring stages per CTA
 constexpr int kCtasPerSm = 2;           // independent pipelines per SM

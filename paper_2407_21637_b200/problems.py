@@ -36,7 +36,20 @@ def gaussian_1d_dense(n: int, sigma: float, nugget: float, seed: int) -> np.ndar
 
 
 class ToeplitzInvSource(BlockSource):
-    """A_ij = 1 / (1 + |i - j|), generated block-wise on the GPU."""
+    """A_ij = 1 / (1 + |i - j|).
+
+    Blocks up to ``dense_max`` rows are generated densely on the GPU; larger
+    off-diagonal blocks (cfg5's level 1 is 131072^2 = 137 GB dense) are never
+    formed: they are Toeplitz, so ||B||_F^2 comes exactly from the distance
+    counts and the randomized range finder applies B and B^T by FFT
+    convolution (O(m log m) per column)."""
+
+    dense_max = 32768
+    sketch = 96
+
+    @staticmethod
+    def f(t):
+        return 1.0 / (1.0 + np.abs(t))
 
     def block(self, a, b, c, d):
         import torch
@@ -49,6 +62,54 @@ class ToeplitzInvSource(BlockSource):
         n = self.n
         dist = np.arange(1, n, dtype=np.float64)
         return float(n) + 2.0 * math.fsum((n - dist) / (1.0 + dist) ** 2)
+
+    def block_frob2(self, a, b, c, d) -> float:
+        m, k = b - a, d - c
+        delta = np.arange(-(m - 1), k, dtype=np.int64)      # j - i
+        cnt = np.where(delta >= 0, np.minimum(m, k - delta), np.minimum(k, m + delta)).astype(np.float64)
+        return math.fsum(cnt * self.f((c - a) + delta).astype(np.float64) ** 2)
+
+    # B X for B = A[a:b, c:d], B_ij = f(o + j - i) with o = c - a (f is even, so
+    # B^T has the same form with o -> -o), X: k x L, by FFT correlation.
+    def _apply(self, a, b, c, d, X, transpose=False):
+        m, k, o = b - a, d - c, c - a
+        if transpose:
+            m, k, o = k, m, -o
+        h = self.f(o + np.arange(-(m - 1), k, dtype=np.int64))   # h[t + m - 1] = f(o + t)
+        nfft = 1 << int(np.ceil(np.log2(len(h) + k)))
+        full = np.fft.irfft(np.fft.rfft(h[::-1], nfft)[:, None] * np.fft.rfft(X, nfft, axis=0), nfft, axis=0)
+        return full[k - 1:k - 1 + m]                              # y_i = conv[k - 1 + i]
+
+    def compress(self, a, b, c, d, eps, cache=None):
+        if min(b - a, d - c) <= self.dense_max:
+            return super().compress(a, b, c, d, eps, cache)
+        import torch
+
+        from .construct import truncation_rank
+
+        key = (a, b, c, d, eps)
+        if cache is not None and key in cache:
+            return cache[key]
+        m, k = b - a, d - c
+        rng = np.random.default_rng(self.seed)
+        Lw = min(self.sketch, m, k)
+        Om = rng.standard_normal((k, Lw))
+        Q, _ = np.linalg.qr(self._apply(a, b, c, d, Om))
+        for _ in range(self.power_iters):
+            Z, _ = np.linalg.qr(self._apply(a, b, c, d, Q, transpose=True))
+            Q, _ = np.linalg.qr(self._apply(a, b, c, d, Z))
+        Ct = self._apply(a, b, c, d, Q, transpose=True)          # B^T Q  (k x Lw) = C^T
+        Uc, s, Vh = np.linalg.svd(Ct.T, full_matrices=False)
+        frob2 = self.block_frob2(a, b, c, d)
+        # the sketch resolves the spectrum far below eps (kernel decays exponentially);
+        # the unresolved remainder is bounded by s[-1] and dropped
+        r = truncation_rank(s, eps, max(m, k), resid2=0.0, frob=math.sqrt(frob2))
+        U = torch.from_numpy(np.ascontiguousarray(Q @ Uc[:, :r])).to(self.device)
+        V = torch.from_numpy(np.ascontiguousarray(Vh[:r].T * s[:r])).to(self.device)
+        out = (U, V)
+        if cache is not None:
+            cache[key] = out
+        return out
 
 
 def cfg1(seed_x: int = 1):
