@@ -55,6 +55,7 @@ constexpr int kConsumers = 8;           // consumer warps (= column subsets of B
 constexpr int kThreads = 32 * (kConsumers + 1);  // + producer warp
 constexpr int kFifo = 8;                // BC items whose U piece waits for the coefficients
 constexpr int kMaxRPieces = 256;        // node-reduction pieces
+constexpr int kMaxUPieces = 16;         // U chunks per BC item
 constexpr int kMaxLev = 24;
 constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
 constexpr int kMaxCols = 512;           // columns (sum of ranks) per leaf
@@ -82,6 +83,11 @@ struct APiece {
     int32_t g, r0, nrows, last_of_group;
 };
 
+// U chunk of a BC item: columns [c0, c0 + ncols) of format group g.
+struct UPiece {
+    int32_t g, c0, ncols, pad;
+};
+
 // Node reduction: level lv, nodes [j0, j1), rank columns [c0, c1) (whole nodes,
 // or one node split by columns); its partials are contiguous.
 struct RPiece {
@@ -99,10 +105,12 @@ struct SvParams {
     int32_t gcols[5], vpad[5];
     int64_t vgoff[5], ugoff[5];           // V' sub-slab offsets / U sub-block offsets in a block
     int32_t coef_elems;
-    int32_t u_data_off[2], u_bytes[2];    // U piece layout for fp32 / fp64 working
+    int32_t u_data_off[2];                // U piece: coefficients, then the U chunk
+    int32_t nupieces;                     // U pieces per BC item (column chunks of the U block)
     Level lev[kMaxLev];
     APiece ap[kMaxPieces];
     RPiece rp[kMaxRPieces];
+    UPiece up[kMaxUPieces];
     int8_t col_level[kMaxCols];           // flattened (group, column) -> level (0-based)
     int16_t col_c[kMaxCols];              //                            -> rank column
     int16_t gstart[6];
@@ -456,33 +464,38 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             if (r_ready) asm volatile("fence.proxy.async.global;" ::: "memory");  // t read by TMA below
         };
         auto emit_u = [&](int leaf, int rb, int slot) {
-            uint8_t* st = claim();
             const int wi = sizeof(W) == 8 ? 1 : 0;
             const int wbytes = (int)sizeof(W);
-            if (lane == 0) {
-                PieceHdr& h = C.hdr[stage];
-                h.type = PT_U;
-                h.leaf = leaf;
-                h.a = rb;
-                h.b = slot;
-                mbar_arrive_tx(&C.full[stage], (unsigned)P.u_bytes[wi]);
-            }
-            __syncwarp();
-            if (lane < nlev) {
-                const Level& L = P.lev[lane];
-                if (L.r > 0) {
-                    const int k = lane + 1;
-                    const int jsib = (leaf >> (nlev - k)) ^ 1;
-                    const W* src = a.tbuf + L.tbase + (int64_t)jsib * L.tstride;
-                    bulk_g2s(st + (size_t)L.slot * wbytes, src, (unsigned)(L.tstride * wbytes), &C.full[stage]);
+            const uint8_t* ublk = a.slab + (int64_t)leaf * P.slab_bytes + P.us_off + (int64_t)rb * P.ublock_bytes;
+            for (int p = 0; p < P.nupieces; ++p) {
+                const UPiece up = P.up[p];
+                const unsigned cb = (unsigned)(up.ncols * kRB * fmt_sz(up.g));
+                uint8_t* st = claim();
+                if (lane == 0) {
+                    PieceHdr& h = C.hdr[stage];
+                    h.type = PT_U;
+                    h.leaf = leaf;
+                    h.a = rb;
+                    h.b = slot;
+                    h.last = p;
+                    mbar_arrive_tx(&C.full[stage], (unsigned)P.u_data_off[wi] + cb);
                 }
-            } else if (lane == 31) {
-                bulk_g2s(st + P.u_data_off[wi],
-                         a.slab + (int64_t)leaf * P.slab_bytes + P.us_off + (int64_t)rb * P.ublock_bytes,
-                         (unsigned)P.ublock_bytes, &C.full[stage]);
+                __syncwarp();
+                if (lane < nlev) {
+                    const Level& L = P.lev[lane];
+                    if (L.r > 0) {
+                        const int k = lane + 1;
+                        const int jsib = (leaf >> (nlev - k)) ^ 1;
+                        const W* src = a.tbuf + L.tbase + (int64_t)jsib * L.tstride;
+                        bulk_g2s(st + (size_t)L.slot * wbytes, src, (unsigned)(L.tstride * wbytes), &C.full[stage]);
+                    }
+                } else if (lane == 31) {
+                    bulk_g2s(st + P.u_data_off[wi], ublk + P.ugoff[up.g] + (int64_t)up.c0 * kRB * fmt_sz(up.g), cb,
+                             &C.full[stage]);
+                }
+                __syncwarp();
+                next_stage();
             }
-            __syncwarp();
-            next_stage();
         };
         auto flush_u = [&](bool block) {
             if (fh == ft) return;
@@ -704,34 +717,35 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     }
                 }
                 scratch = true;
-            } else {  // PT_U: b = U t + y
+            } else {  // PT_U: b = U t + y, one column chunk of U per piece
                 const int wi = sizeof(W) == 8 ? 1 : 0;
+                const UPiece up = P.up[h.last];
                 const W* coef = reinterpret_cast<const W*>(st);
                 const W* ys = reinterpret_cast<const W*>(C.ybuf[h.b]);
-                const uint8_t* ub = st + P.u_data_off[wi];
-                for (int g = 0; g < 5; ++g) {
-                    const int nc = P.gcols[g];
-                    if (nc == 0) continue;
-                    const int16_t* ci = C.cidx + P.gstart[g];
+                {
+                    const int16_t* ci = C.cidx + P.gstart[up.g] + up.c0;
                     auto mul = [&](int c) { return coef[ci[c]]; };
-                    col_block_any<W>(g, ub + P.ugoff[g], nc, cw, lane, mul, bacc);
+                    col_block_any<W>(up.g, st + P.u_data_off[wi], up.ncols, cw, lane, mul, bacc);
                 }
-                W* red = reinterpret_cast<W*>(st + P.u_bytes[wi]);  // scratch after the piece's data
+                if (h.last == P.nupieces - 1) {
+                    // scratch after this piece's data (capacity checked at prepare time)
+                    W* red = reinterpret_cast<W*>(st + P.u_data_off[wi] + round_up16_d(up.ncols * kRB * fmt_sz(up.g)));
 #pragma unroll
-                for (int r = 0; r < kRPL; ++r)
-                    red[cw * kRB + kRPL * lane + r] = (bacc[0][r] + bacc[1][r]) + (bacc[2][r] + bacc[3][r]);
-                consumer_sync();
-                if (ctid < kRB) {
-                    W s = red[ctid];
+                    for (int r = 0; r < kRPL; ++r)
+                        red[cw * kRB + kRPL * lane + r] = (bacc[0][r] + bacc[1][r]) + (bacc[2][r] + bacc[3][r]);
+                    consumer_sync();
+                    if (ctid < kRB) {
+                        W s = red[ctid];
 #pragma unroll
-                    for (int w = 1; w < kConsumers; ++w) s += red[w * kRB + ctid];
-                    a.b[(int64_t)h.leaf * kM + h.a * kRB + ctid] = s + ys[ctid];  // levels, then the leaf
+                        for (int w = 1; w < kConsumers; ++w) s += red[w * kRB + ctid];
+                        a.b[(int64_t)h.leaf * kM + h.a * kRB + ctid] = s + ys[ctid];  // levels, then the leaf
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+#pragma unroll
+                        for (int r = 0; r < kRPL; ++r) bacc[k][r] = W(0);
+                    scratch = true;
                 }
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int r = 0; r < kRPL; ++r) bacc[k][r] = W(0);
-                scratch = true;
             }
             if (scratch) {
                 consumer_sync();  // scratch reads and the item's global stores are done
@@ -897,12 +911,22 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     P.dcols = (kStage - kXB) / (kRB * dsz);
     P.dcols = std::min(kM, P.dcols / 8 * 8);
     P.dpieces = (kM + P.dcols - 1) / P.dcols;
-    // U piece: coefficients | U block | reduction scratch (8 x 64)
-    for (int wi = 0; wi < 2; ++wi) {
-        const int wb = wi ? 8 : 4;
-        P.u_data_off[wi] = (int)round_up16((int64_t)P.coef_elems * wb);
-        P.u_bytes[wi] = (int)(P.u_data_off[wi] + P.ublock_bytes);
-        if (P.u_bytes[wi] + kConsumers * kRB * wb > kStage) return HODLR_OK;
+    // U pieces: coefficients | column chunk of the U block | reduction scratch
+    for (int wi = 0; wi < 2; ++wi) P.u_data_off[wi] = (int)round_up16((int64_t)P.coef_elems * (wi ? 8 : 4));
+    {
+        const int64_t room = kStage - P.u_data_off[1] - (int64_t)kConsumers * kRB * 8 - 16;
+        P.nupieces = 0;
+        for (int g = 0; g < 5; ++g) {
+            if (P.gcols[g] == 0) continue;
+            int per = (int)(room / ((int64_t)kRB * fmt_bytes(g)));
+            per = per >= 8 ? per / 8 * 8 : per;  // keep chunk offsets 16-byte aligned
+            if (per < 1 || (per < 8 && P.gcols[g] > per)) return HODLR_OK;
+            for (int c0 = 0; c0 < P.gcols[g]; c0 += per) {
+                if (P.nupieces == kMaxUPieces) return HODLR_OK;
+                P.up[P.nupieces++] = UPiece{g, c0, std::min(per, P.gcols[g] - c0), 0};
+            }
+        }
+        if (P.nupieces == 0) return HODLR_OK;
     }
     P.num_a = nleaves;
     P.num_d = nleaves * (kM / kRB);

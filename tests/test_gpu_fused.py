@@ -142,3 +142,18 @@ def test_fused_depths(cuda, depth):
     x = np.random.default_rng(6).standard_normal(H.n)
     b = op.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
     assert rel(b, matvec_oracle(H, x)) <= 1e-12
+
+
+@pytest.mark.parametrize("working,fmts,ranks", [
+    ("fp64", ["fp64", "fp64", "fp64"], [60, 50, 40]),      # U block > one stage: several U pieces
+    ("fp32", ["fp32", "bf16", "q52"], [90, 70, 50]),
+])
+def test_fused_large_ranks(cuda, working, fmts, ranks):
+    torch = cuda
+    H = random_hodlr(2048, 3, fmts, ranks, working, seed=sum(ranks))
+    op = make_op(H)
+    assert op.launches_per_matvec == 1
+    x = np.random.default_rng(7).standard_normal(H.n)
+    dt = torch.float64 if working == "fp64" else torch.float32
+    b = op.matvec(torch.from_numpy(x).cuda().to(dt)).double().cpu().numpy()
+    assert rel(b, matvec_oracle(H, x)) <= (1e-12 if working == "fp64" else 1e-5)
