@@ -15,7 +15,7 @@
 // four output columns and walks the rows.  Partial sums stay in registers for
 // all pieces of a work item; warps combine once per item through shared memory.
 //
-// Schedule (one CTA per pipeline, kCtasPerSm per SM, cooperative launch):
+// Schedule (one CTA per pipeline, kCtasPerSm per SM; no co-residency needed):
 //   producer warp  pulls work and streams it with cp.async.bulk (1-D TMA,
 //                  complete_tx on the stage's "full" mbarrier) into a ring of
 //                  kNS stages;
@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -383,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     SmemCtl& C = *reinterpret_cast<SmemCtl*>(smem + kNS * kStage);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nlev = P.depth;
-    const int nq = P.num_d + P.num_r;            // dynamic queue: BC items with R pieces at pos_r
+    const int nq = P.num_a + P.num_d + P.num_r;  // queue: A leaves, then BC items with R pieces at pos_r
     constexpr int kBlocks = kM / kRB;            // row blocks per leaf
 
     if (threadIdx.x == 0) {
@@ -509,31 +510,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             }
         };
 
-        // ---- phase A: leaves dealt round-robin, every CTA starts with its share
-        for (int leaf = blockIdx.x; leaf < P.num_a; leaf += gridDim.x) {
-            const uint8_t* base = a.slab + (int64_t)leaf * P.slab_bytes;
-            ++a_items;
-            for (int p = 0; p < P.napieces; ++p) {
-                const APiece ap = P.ap[p];
-                uint8_t* st = claim();
-                const unsigned cb = (unsigned)(ap.nrows * P.vpad[ap.g] * fmt_sz(ap.g));
-                const unsigned xb = (unsigned)(ap.nrows * sizeof(W));
-                if (lane == 0) {
-                    PieceHdr& h = C.hdr[stage];
-                    h.type = PT_A;
-                    h.leaf = leaf;
-                    h.a = p;
-                    h.last = (p == P.napieces - 1);
-                    mbar_arrive_tx(&C.full[stage], xb + cb);
-                    bulk_g2s(st, a.x + (int64_t)leaf * kM + ap.r0, xb, &C.full[stage]);
-                    bulk_g2s(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.r0 * P.vpad[ap.g] * fmt_sz(ap.g), cb,
-                             &C.full[stage]);
-                }
-                __syncwarp();
-                next_stage();
-            }
-        }
-        // ---- R pieces and BC items (leaf, 64-row block) from one atomic queue
+        // ---- one atomic queue, fetched two ahead:  [A leaves][BC items, R pieces at pos_r]
+        // Every cross-CTA wait (R on all A leaves, U on all R pieces) targets work
+        // that sits EARLIER in the queue, i.e. was already taken by a running CTA,
+        // so progress never depends on CTAs being co-resident.
         int n1 = 0, n2 = 0;
         if (lane == 0) {
             n1 = (int)atomicAdd(&a.sync->queue, 1u);
@@ -546,9 +526,36 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             n1 = n2;
             if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);
             if (pending()) publish(false);
-            if (q >= P.pos_r && q < P.pos_r + P.num_r) {
+            if (q < P.num_a) {
+                // ---- A: partial V'^T x of one leaf
+                const int leaf = q;
+                const uint8_t* base = a.slab + (int64_t)leaf * P.slab_bytes;
+                ++a_items;
+                for (int p = 0; p < P.napieces; ++p) {
+                    const APiece ap = P.ap[p];
+                    uint8_t* st = claim();
+                    const unsigned cb = (unsigned)(ap.nrows * P.vpad[ap.g] * fmt_sz(ap.g));
+                    const unsigned xb = (unsigned)(ap.nrows * sizeof(W));
+                    if (lane == 0) {
+                        PieceHdr& h = C.hdr[stage];
+                        h.type = PT_A;
+                        h.leaf = leaf;
+                        h.a = p;
+                        h.last = (p == P.napieces - 1);
+                        mbar_arrive_tx(&C.full[stage], xb + cb);
+                        bulk_g2s(st, a.x + (int64_t)leaf * kM + ap.r0, xb, &C.full[stage]);
+                        bulk_g2s(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.r0 * P.vpad[ap.g] * fmt_sz(ap.g), cb,
+                                 &C.full[stage]);
+                    }
+                    __syncwarp();
+                    next_stage();
+                }
+                continue;
+            }
+            const int qq = q - P.num_a;
+            if (qq >= P.pos_r && qq < P.pos_r + P.num_r) {
                 // ---- R: reduce node partials (needs every leaf's partials)
-                const RPiece rp = P.rp[q - P.pos_r];
+                const RPiece rp = P.rp[qq - P.pos_r];
                 const Level& L = P.lev[rp.lv];
                 const int nch = 1 << (nlev - 1 - rp.lv);
                 publish(true);  // own A leaves first (and anything else pending)
@@ -564,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 if (lane == 0) {
                     PieceHdr& h = C.hdr[stage];
                     h.type = PT_R;
-                    h.a = q - P.pos_r;
+                    h.a = qq - P.pos_r;
                     mbar_arrive_tx(&C.full[stage], bytes);
                     bulk_g2s(st, a.partial + L.pbase + ((int64_t)rp.j0 * L.r + rp.c0) * nch, bytes, &C.full[stage]);
                 }
@@ -573,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 continue;
             }
             // ---- BC: y = D x now (kept in this CTA's y slot), b = U t + y once t exists
-            const int qb = q < P.pos_r ? q : q - P.num_r;
+            const int qb = qq < P.pos_r ? qq : qq - P.num_r;
             const int leaf = qb / kBlocks, rb = qb % kBlocks;
             if (ft - fh == kFifo) flush_u(true);  // frees the y slot this item will use
             const int slot = ft % kFifo;
@@ -957,7 +964,9 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
                     if (!add(j, j + 1, c0, std::min(L.r, c0 + cols))) return HODLR_OK;
         }
     }
-    P.pos_r = P.num_d / 6;  // after every CTA's phase-A leaves, well before the U pieces need t
+    // R pieces: late enough that the A leaves are (nearly) done, early enough that
+    // they are taken before any running CTA could fill its deferred-U FIFO
+    P.pos_r = std::min(P.num_d / 6, kFifo * 16);  // (assumes >= 16 CTAs can run at once)
 
     // ---- relayout the quantised level-batched arena into leaf slabs (bytes)
     std::vector<uint8_t> arena(in.arena_bytes);
@@ -997,7 +1006,8 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
     const size_t smem = smem_bytes();
-    if (!coop || sms <= 0 ||
+    (void)coop;
+    if (sms <= 0 ||
         cudaFuncSetAttribute(k_stream<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
         cudaFuncSetAttribute(k_stream<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return HODLR_OK;
@@ -1020,6 +1030,10 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     sv.num_items_a = P.num_a;
     sv.num_items_b = P.num_d + P.num_r;
     sv.grid = std::min(sms * std::min(occ, kCtasPerSm), P.num_a + P.num_d + P.num_r);
+    if (const char* g = getenv("HODLR_B200_GRID")) sv.grid = std::min(sv.grid, atoi(g));
+    if (getenv("HODLR_B200_VERBOSE"))
+        fprintf(stderr, "[hodlr_b200] fused path: grid %d (sms %d occ %d) smem %zu items A %d BC %d R %d U pieces %d\n",
+                sv.grid, sms, occ, smem, P.num_a, P.num_d, P.num_r, P.nupieces);
     sv.launches = 1;
     sv.tfast_count = tb;
     sv.extra_ws = sv_sync_bytes(P.nleaves) + (size_t)(pb + tb) * 8;  // (leaf counters unused now)
@@ -1056,7 +1070,7 @@ cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* 
     a.partial = (W*)(e + sv_sync_bytes(P.nleaves));
     a.tbuf = (W*)(e + sv_sync_bytes(P.nleaves) + sv.part_count * 8);
     void* args[] = {(void*)&P, &a};
-    return cudaLaunchCooperativeKernel((const void*)k_stream<W>, dim3(sv.grid), dim3(kThreads), args, smem_bytes(), st);
+    return cudaLaunchKernel((const void*)k_stream<W>, dim3(sv.grid), dim3(kThreads), args, smem_bytes(), st);
 }
 
 template cudaError_t sv_matvec<double>(const PlanView&, const SvPlan&, const double*, double*, double*, double*,
