@@ -51,7 +51,7 @@ constexpr int kRB = 64;                 // rows of a BC item (one leaf row block
 constexpr int kRPL = kRB / 32;          // rows per lane in B / C pieces
 constexpr int kNS = 3;                  // ring stages per CTA
 constexpr int kCtasPerSm = 2;           // independent pipelines per SM
-constexpr int kStage = 34 * 1024;       // bytes per stage
+constexpr int kStage = 33280;           // bytes per stage (= 512 B of x + a 64 x 64 fp64 D block)
 constexpr int kConsumers = 8;           // consumer warps (= column subsets of B/C pieces)
 constexpr int kThreads = 32 * (kConsumers + 1);  // + producer warp
 constexpr int kFifo = 8;                // BC items whose U piece waits for the coefficients
@@ -60,7 +60,8 @@ constexpr int kMaxUPieces = 16;         // U chunks per BC item
 constexpr int kMaxLev = 24;
 constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
 constexpr int kMaxCols = 512;           // columns (sum of ranks) per leaf
-constexpr int kXB = 2048;               // bytes reserved for the x segment of a stage
+constexpr int kXB = 2048;               // x segment of an A piece (<= 256 rows)
+constexpr int kXD = 512;                // x segment of a D piece (<= 64 fp64 columns)
 
 enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_R = 5, PT_END = 4 };
 
@@ -367,7 +368,7 @@ struct SmemCtl {
     int fifo[kFifo];               // deferred U pieces: (leaf << 8) | row block
     alignas(16) double ybuf[kFifo][kRB];  // y = D x of those items (working type)
     alignas(16) int16_t cidx[kMaxCols];  // flattened U column -> coefficient slot
-    int64_t pbase_c[kMaxCols];     // flattened V' column -> partial buffer base (level pbase + c*nch)
+    int32_t pbase_c[kMaxCols];     // flattened V' column -> partial buffer base (level pbase + c*nch)
     int32_t pstride_c[kMaxCols];   //                     -> r * nch (stride between nodes)
     int8_t psh_c[kMaxCols];        //                     -> log2(nch)
 };
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         const Level& L = P.lev[P.col_level[i]];
         const int sh = nlev - (P.col_level[i] + 1);
         C.cidx[i] = (int16_t)(L.slot + P.col_c[i]);
-        C.pbase_c[i] = L.pbase + ((int64_t)P.col_c[i] << sh);
+        C.pbase_c[i] = (int32_t)(L.pbase + ((int64_t)P.col_c[i] << sh));
         C.pstride_c[i] = L.r << sh;
         C.psh_c[i] = (int8_t)sh;
     }
@@ -600,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     h.last = (p == P.dpieces - 1) ? 1 + slot : 0;
                     mbar_arrive_tx(&C.full[stage], xb + cb);
                     bulk_g2s(st, a.x + (int64_t)leaf * kM + c0, xb, &C.full[stage]);
-                    bulk_g2s(st + kXB, blk + (int64_t)c0 * kRB * dsz, cb, &C.full[stage]);
+                    bulk_g2s(st + kXD, blk + (int64_t)c0 * kRB * dsz, cb, &C.full[stage]);
                 }
                 __syncwarp();
                 next_stage();
@@ -665,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                         const int flat = P.gstart[ap.g] + c;
                         const int sh = C.psh_c[flat];
                         const int jn = h.leaf >> sh;
-                        a.partial[C.pbase_c[flat] + (int64_t)jn * C.pstride_c[flat] + (h.leaf - (jn << sh))] = s;
+                        a.partial[(int64_t)C.pbase_c[flat] + (int64_t)jn * C.pstride_c[flat] + (h.leaf - (jn << sh))] = s;
                     }
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
@@ -677,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 const W* xs = reinterpret_cast<const W*>(st);
                 const int nc = min(P.dcols, kM - h.b);
                 auto mul = [&](int c) { return xs[c]; };
-                col_block_any<W>(P.leaf_fmt, st + kXB, nc, cw, lane, mul, bacc);
+                col_block_any<W>(P.leaf_fmt, st + kXD, nc, cw, lane, mul, bacc);
                 if (h.last) {
                     W* red = reinterpret_cast<W*>(st);
                     consumer_sync();
@@ -881,6 +882,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         tb += (int64_t)L.tstride << (k + 1);
     }
     P.coef_elems = slot;
+    if (pb >= (int64_t(1) << 31)) return HODLR_OK;  // int32 partial indices in shared tables
     // slab geometry
     const int dsz = fmt_bytes(lf);
     int64_t vs = 0;
@@ -915,7 +917,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     for (int g = 0; g < 5; ++g)
         if ((size_t)kConsumers * P.vpad[g] * 8 > (size_t)kStage) return HODLR_OK;
     // phase-B pieces: column blocks of a 64-row block
-    P.dcols = (kStage - kXB) / (kRB * dsz);
+    P.dcols = (kStage - kXD) / (kRB * dsz);
     P.dcols = std::min(kM, P.dcols / 8 * 8);
     P.dpieces = (kM + P.dcols - 1) / P.dcols;
     // U pieces: coefficients | column chunk of the U block | reduction scratch
