@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded (multi-GPU) code path even at one rank")
     return ap.parse_args()
 
 
@@ -169,7 +171,17 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, world, rank)
-    if world > 1 or args.gpus > 1:
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not launched by torchrun: relaunch one rank per GPU
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if world > 1 or args.sharded:
         from paper_2407_21637_b200 import dist
 
         return dist.bench_sharded(args, build_workload, alg_bytes, peaks, ClockSampler)

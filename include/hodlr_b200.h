@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HODLR_B200_ABI_VERSION 1
+#define HODLR_B200_ABI_VERSION 2
 
 typedef enum {
     HODLR_OK = 0,
@@ -119,18 +119,29 @@ hodlr_status hodlr_matvec(hodlr_handle* h, int32_t working, const void* x, int64
 hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x_host,
                                double* b_host, int64_t s, void* stream);
 
-/* Sharded matvec in three stream-ordered steps around one all-gather:
- *   1. shard_begin: local subtree partial coefficients + this rank's partial
- *      V^T x coefficients of every external level -> `send` (device,
+/* Sharded matvec: three stream-ordered steps around one all-gather.
+ *   1. shard_begin: this rank's partial V'^T x coefficients of every external
+ *      level (1..log2 nranks), over its own rows -> `send` (device,
  *      hodlr_shard_exchange_count(h, s) elements of the working type);
- *   2. caller all-gathers `send` from every rank, in rank order, into `recv`
- *      (nranks * count elements), e.g. ncclAllGather over NVLink;
- *   3. shard_end: fixed-order reduction of the gathered coefficients, then
- *      b_local = sum_k U_k t_k + D x for this rank's rows. */
+ *   2. the caller starts an all-gather of `send` from every rank, in rank
+ *      order, into `recv` (nranks * count elements), e.g. ncclAllGather over
+ *      NVLink, and meanwhile calls
+ *      shard_local: b_local = D x + sum_{k > L} U_k t_k, the communication-free
+ *      subtree part (the single-vector fused kernel when it applies), which
+ *      overlaps the exchange;
+ *   3. once `recv` is complete on `stream`, shard_end: fixed-order (rank order)
+ *      reduction of the gathered coefficients of the sibling subtrees, then
+ *      b_local += sum_{k <= L} U_k t_k.
+ * shard_local must precede shard_end on the same b_local.  The three calls
+ * share the handle's workspace (or `ws`) and must not interleave with another
+ * matvec on the same workspace. */
 hodlr_status hodlr_shard_exchange_count(const hodlr_handle* h, int64_t s, int64_t* count);
 hodlr_status hodlr_matvec_shard_begin(hodlr_handle* h, int32_t working, const void* x_local,
                                       int64_t ldx, int64_t s, void* send, void* ws,
                                       size_t ws_bytes, void* stream);
+hodlr_status hodlr_matvec_shard_local(hodlr_handle* h, int32_t working, const void* x_local,
+                                      int64_t ldx, void* b_local, int64_t ldb, int64_t s,
+                                      void* ws, size_t ws_bytes, void* stream);
 hodlr_status hodlr_matvec_shard_end(hodlr_handle* h, int32_t working, const void* x_local,
                                     int64_t ldx, const void* recv, void* b_local, int64_t ldb,
                                     int64_t s, void* ws, size_t ws_bytes, void* stream);

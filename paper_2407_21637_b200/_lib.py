@@ -16,7 +16,7 @@ c_i32, c_i64, c_sz, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctyp
 c_dp = ctypes.POINTER(ctypes.c_double)
 
 HODLR_OK, HODLR_ERR_INVALID, HODLR_ERR_UNSUPPORTED, HODLR_ERR_CUDA = 0, 1, 2, 3
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class FactorIn(ctypes.Structure):
@@ -52,6 +52,8 @@ EXPORTS = {
     "hodlr_matvec_host": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i64, c_vp]),
     "hodlr_shard_exchange_count": (c_i32, [c_vp, c_i64, ctypes.POINTER(c_i64)]),
     "hodlr_matvec_shard_begin": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_i64, c_vp, c_vp, c_sz, c_vp]),
+    "hodlr_matvec_shard_local": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_sz,
+                                         c_vp]),
     "hodlr_matvec_shard_end": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp,
                                        c_sz, c_vp]),
     "hodlr_quantize": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_vp]),

@@ -326,6 +326,11 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
     }
     h->part_count = part;
     h->t_count = tcount;
+    for (int k = 1; k <= L; ++k)  // kernels_shard.cu relies on external nodes being ids 0..L-1
+        if (h->nodes[k - 1].level != k || h->nodes[k - 1].ext_slot < 0) {
+            delete h;
+            return fail(HODLR_ERR_INVALID, "internal: external node order");
+        }
 
     // ---- arena layout: [leaves][q52][bf16][fp16][fp32][fp64], 256-B aligned
     int64_t seg_byte_off[kNumFormats];
@@ -443,10 +448,27 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
 
     const char* no_sv = getenv("HODLR_B200_DISABLE_FUSED");
     if (!(no_sv && no_sv[0] == '1')) {
-        SvInput si{&h->nodes, &h->chunks, &h->leaves, &h->chunk_nodes, nlev, (const uint8_t*)h->arena.p,
+        // sharded handles: the fused kernel runs the rank's subtree (levels
+        // L+1..l renumbered 1..l-L); external levels run in kernels_shard.cu
+        std::vector<NodeDesc> sub;
+        for (const NodeDesc& nd : h->nodes)
+            if (nd.level > L) {
+                sub.push_back(nd);
+                sub.back().level -= L;
+            }
+        SvInput si{&sub, &h->chunks, &h->leaves, &h->chunk_nodes, depth - L, (const uint8_t*)h->arena.p,
                    h->arena_bytes};
         hodlr_status st = sv_prepare(si, h->sv, &h->sv_ok);
         if (st != HODLR_OK) return cleanup(st);
+        if (h->sv_ok && P > 1) {
+            // leave a few SMs to the all-gather kernel that overlaps the
+            // subtree (the persistent kernel would otherwise hold every SM)
+            int sms = 148, reserve = 4;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+            if (const char* r = getenv("HODLR_B200_SHARD_RESERVE_SMS")) reserve = atoi(r);
+            reserve = std::max(0, std::min(reserve, sms - 1));
+            h->sv.grid = std::max(1, std::min(h->sv.grid, 2 * (sms - reserve)));
+        }
     }
     *out = h;
     return HODLR_OK;
@@ -454,11 +476,18 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
 
 // Workspace: [fused-path sync state (fixed offset 0, must start zeroed)]
 //            [partials: part_count*s][coefficients: t_count*s]
+//            [sharded only: k_ext_v per-block partials | discarded send | ticket]
+template <typename W>
+size_t ext_ws_bytes(const hodlr_handle* h, int64_t s) {
+    if (h->nranks == 1 || h->ext_count == 0) return 0;
+    return (size_t)round_up((int64_t)ext_v_blocks(h->n_local) * h->ext_count * s * sizeof(W), kAlign) +
+           (size_t)round_up(h->ext_count * s * sizeof(W), kAlign) + kAlign;
+}
 template <typename W>
 size_t ws_bytes_for(const hodlr_handle* h, int64_t s) {
     return (size_t)round_up((int64_t)sv_extra_ws(h->sv, s), kAlign) +
            (size_t)round_up((h->part_count * s) * sizeof(W), kAlign) +
-           (size_t)round_up((h->t_count * s) * sizeof(W), kAlign);
+           (size_t)round_up((h->t_count * s) * sizeof(W), kAlign) + ext_ws_bytes<W>(h, s);
 }
 
 int working_bytes(int working) { return working == HODLR_FMT_FP64 ? 8 : working == HODLR_FMT_FP32 ? 4 : 0; }
@@ -471,6 +500,24 @@ void carve(const hodlr_handle* h, int64_t s, void* ws, W** partial, W** tbuf, vo
     *partial = (W*)p;
     p += round_up((h->part_count * s) * sizeof(W), kAlign);
     *tbuf = (W*)p;
+}
+
+template <typename W>
+struct ExtWs {
+    W* scratch;
+    W* dummy_send;
+    unsigned* ticket;
+};
+template <typename W>
+ExtWs<W> carve_ext(const hodlr_handle* h, int64_t s, void* ws) {
+    uint8_t* p = (uint8_t*)ws + ws_bytes_for<W>(h, s) - ext_ws_bytes<W>(h, s);
+    ExtWs<W> e;
+    e.scratch = (W*)p;
+    p += round_up((int64_t)ext_v_blocks(h->n_local) * h->ext_count * s * sizeof(W), kAlign);
+    e.dummy_send = (W*)p;
+    p += round_up(h->ext_count * s * sizeof(W), kAlign);
+    e.ticket = (unsigned*)p;
+    return e;
 }
 
 hodlr_status check_working(int working) {
@@ -511,6 +558,25 @@ hodlr_status run_local(hodlr_handle* h, const W* x, int64_t ldx, W* b, int64_t l
     }
     if (e != cudaSuccess) return fail(HODLR_ERR_CUDA, std::string("matvec launch: ") + cudaGetErrorString(e));
     return HODLR_OK;
+}
+
+template <typename W>
+cudaError_t shard_local_impl(hodlr_handle* h, const W* x, int64_t ldx, W* b, int64_t ldb, int64_t s, void* ws,
+                             cudaStream_t st) {
+    W *partial, *tbuf;
+    void* extra;
+    carve<W>(h, s, ws, &partial, &tbuf, &extra);
+    if (h->sv_ok && s == 1 && ldx == 1 && ldb == 1) return sv_matvec<W>(h->view, h->sv, x, b, partial, tbuf, extra, st);
+    // generic: the whole local plan with the external coefficients set to 0
+    // (their products add exact zeros); the external partials go to a
+    // discarded buffer, shard_begin owns the real ones.
+    W* dummy = h->ext_count ? carve_ext<W>(h, s, ws).dummy_send : nullptr;
+    cudaError_t e = gen_begin<W>(h->view, x, ldx, s, partial, tbuf, dummy, st);
+    for (const ExtDesc& x_ : h->ext)
+        if (e == cudaSuccess && x_.rank > 0)
+            e = cudaMemsetAsync(tbuf + x_.tdst * s, 0, (size_t)x_.rank * s * sizeof(W), st);
+    if (e == cudaSuccess) e = gen_end<W>(h->view, x, ldx, tbuf, b, ldb, s, h->max_chunk_rows, st);
+    return e;
 }
 
 }  // namespace
@@ -619,17 +685,30 @@ hodlr_status hodlr_matvec_shard_begin(hodlr_handle* h, int32_t working, const vo
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     if (working == HODLR_FMT_FP64) {
-        double *partial, *tbuf;
-        void* extra;
-        carve<double>(h, s, ws, &partial, &tbuf, &extra);
-        e = gen_begin<double>(h->view, (const double*)x_local, ldx, s, partial, tbuf, (double*)send, st);
+        ExtWs<double> x = carve_ext<double>(h, s, ws);
+        e = ext_begin<double>(h->view, (const double*)x_local, ldx, s, x.scratch, x.ticket, (double*)send, st);
     } else {
-        float *partial, *tbuf;
-        void* extra;
-        carve<float>(h, s, ws, &partial, &tbuf, &extra);
-        e = gen_begin<float>(h->view, (const float*)x_local, ldx, s, partial, tbuf, (float*)send, st);
+        ExtWs<float> x = carve_ext<float>(h, s, ws);
+        e = ext_begin<float>(h->view, (const float*)x_local, ldx, s, x.scratch, x.ticket, (float*)send, st);
     }
     if (e != cudaSuccess) return fail(HODLR_ERR_CUDA, std::string("shard_begin: ") + cudaGetErrorString(e));
+    return HODLR_OK;
+}
+
+hodlr_status hodlr_matvec_shard_local(hodlr_handle* h, int32_t working, const void* x_local,
+                                      int64_t ldx, void* b_local, int64_t ldb, int64_t s,
+                                      void* ws, size_t ws_bytes, void* stream) {
+    if (!h) return fail(HODLR_ERR_INVALID, "null handle");
+    hodlr_status stc = check_working(working);
+    if (stc != HODLR_OK) return stc;
+    if (s < 1 || ldx < s || ldb < s || !x_local || !b_local) return fail(HODLR_ERR_INVALID, "bad x / b / s");
+    hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes);
+    if (r != HODLR_OK) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = working == HODLR_FMT_FP64
+                        ? shard_local_impl<double>(h, (const double*)x_local, ldx, (double*)b_local, ldb, s, ws, st)
+                        : shard_local_impl<float>(h, (const float*)x_local, ldx, (float*)b_local, ldb, s, ws, st);
+    if (e != cudaSuccess) return fail(HODLR_ERR_CUDA, std::string("shard_local: ") + cudaGetErrorString(e));
     return HODLR_OK;
 }
 
@@ -649,18 +728,12 @@ hodlr_status hodlr_matvec_shard_end(hodlr_handle* h, int32_t working, const void
         double *partial, *tbuf;
         void* extra;
         carve<double>(h, s, ws, &partial, &tbuf, &extra);
-        e = gen_ext<double>(h->view, s, (const double*)recv, tbuf, st);
-        if (e == cudaSuccess)
-            e = gen_end<double>(h->view, (const double*)x_local, ldx, tbuf, (double*)b_local, ldb, s,
-                                h->max_chunk_rows, st);
+        e = ext_finish<double>(h->view, s, (const double*)recv, tbuf, (double*)b_local, ldb, st);
     } else {
         float *partial, *tbuf;
         void* extra;
         carve<float>(h, s, ws, &partial, &tbuf, &extra);
-        e = gen_ext<float>(h->view, s, (const float*)recv, tbuf, st);
-        if (e == cudaSuccess)
-            e = gen_end<float>(h->view, (const float*)x_local, ldx, tbuf, (float*)b_local, ldb, s,
-                               h->max_chunk_rows, st);
+        e = ext_finish<float>(h->view, s, (const float*)recv, tbuf, (float*)b_local, ldb, st);
     }
     if (e != cudaSuccess) return fail(HODLR_ERR_CUDA, std::string("shard_end: ") + cudaGetErrorString(e));
     return HODLR_OK;
@@ -744,7 +817,7 @@ hodlr_status hodlr_info(const hodlr_handle* h, hodlr_info_t* info) {
     info->device_bytes = (int64_t)h->arena_bytes;
     info->depth = h->depth;
     info->leaf_fmt = h->leaf_fmt;
-    info->launches_per_matvec = h->sv_ok ? sv_launches(h->sv) : 3;
+    info->launches_per_matvec = (h->sv_ok ? sv_launches(h->sv) : 3) + (h->nranks > 1 && h->ext_count ? 3 : 0);
     info->num_levels_external = h->L;
     return HODLR_OK;
 }

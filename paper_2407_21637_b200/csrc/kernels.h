@@ -27,4 +27,13 @@ template <typename W>
 cudaError_t gen_end(const PlanView& p, const W* x, int64_t ldx, const W* tbuf, W* b, int64_t ldb,
                     int64_t s, int max_chunk_rows, cudaStream_t st);
 
+// Sharded path, external levels (kernels_shard.cu).
+int ext_v_blocks(int64_t n_local);
+template <typename W>
+cudaError_t ext_begin(const PlanView& p, const W* x, int64_t ldx, int64_t s, W* scratch, unsigned* ticket,
+                      W* send, cudaStream_t st);
+template <typename W>
+cudaError_t ext_finish(const PlanView& p, int64_t s, const W* recv, W* tbuf, W* b, int64_t ldb,
+                       cudaStream_t st);
+
 }  // namespace hodlr

@@ -61,7 +61,6 @@ constexpr int kMaxLev = 24;
 constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
 constexpr int kMaxCols = 512;           // columns (sum of ranks) per leaf
 constexpr int kXB = 2048;               // x segment of an A piece (<= 256 rows)
-constexpr int kXD = 512;                // x segment of a D piece (<= 64 fp64 columns)
 
 enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_R = 5, PT_END = 4 };
 
@@ -101,7 +100,8 @@ struct SvParams {
     int32_t depth, nleaves, nnodes;
     int32_t leaf_fmt;
     int32_t num_a, num_d, num_r, pos_r;   // queue: BC items with the R pieces at pos_r
-    int32_t napieces, dpieces, dcols;     // phase-B pieces per item and columns per piece
+    int32_t napieces;
+    int32_t dpieces_w[2], dcols_w[2];      // phase-B pieces per item / columns per piece, [fp32, fp64 working]
     int64_t slab_bytes, ds_off, us_off;
     int64_t dblock_bytes, ublock_bytes;
     int32_t gcols[5], vpad[5];
@@ -586,10 +586,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             if (ft - fh == kFifo) flush_u(true);  // frees the y slot this item will use
             const int slot = ft % kFifo;
             const uint8_t* blk = a.slab + (int64_t)leaf * P.slab_bytes + P.ds_off + (int64_t)rb * P.dblock_bytes;
-            for (int p = 0; p < P.dpieces; ++p) {
+            const int dcols = P.dcols_w[sizeof(W) == 8], dpieces = P.dpieces_w[sizeof(W) == 8];
+            const int xoff = dcols * (int)sizeof(W);  // x segment, then the D columns (16-B aligned)
+            for (int p = 0; p < dpieces; ++p) {
                 uint8_t* st = claim();
-                const int c0 = p * P.dcols;
-                const int nc = min(P.dcols, kM - c0);
+                const int c0 = p * dcols;
+                const int nc = min(dcols, kM - c0);
                 const unsigned cb = (unsigned)(nc * kRB * dsz);
                 const unsigned xb = (unsigned)(nc * sizeof(W));
                 if (lane == 0) {
@@ -598,10 +600,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     h.leaf = leaf;
                     h.a = rb;
                     h.b = c0;
-                    h.last = (p == P.dpieces - 1) ? 1 + slot : 0;
+                    h.last = (p == dpieces - 1) ? 1 + slot : 0;
                     mbar_arrive_tx(&C.full[stage], xb + cb);
                     bulk_g2s(st, a.x + (int64_t)leaf * kM + c0, xb, &C.full[stage]);
-                    bulk_g2s(st + kXD, blk + (int64_t)c0 * kRB * dsz, cb, &C.full[stage]);
+                    bulk_g2s(st + xoff, blk + (int64_t)c0 * kRB * dsz, cb, &C.full[stage]);
                 }
                 __syncwarp();
                 next_stage();
@@ -676,9 +678,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 }
             } else if (h.type == PT_D) {
                 const W* xs = reinterpret_cast<const W*>(st);
-                const int nc = min(P.dcols, kM - h.b);
+                const int dcols = P.dcols_w[sizeof(W) == 8];
+                const int nc = min(dcols, kM - h.b);
                 auto mul = [&](int c) { return xs[c]; };
-                col_block_any<W>(P.leaf_fmt, st + kXD, nc, cw, lane, mul, bacc);
+                col_block_any<W>(P.leaf_fmt, st + dcols * (int)sizeof(W), nc, cw, lane, mul, bacc);
                 if (h.last) {
                     W* red = reinterpret_cast<W*>(st);
                     consumer_sync();
@@ -917,9 +920,15 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     for (int g = 0; g < 5; ++g)
         if ((size_t)kConsumers * P.vpad[g] * 8 > (size_t)kStage) return HODLR_OK;
     // phase-B pieces: column blocks of a 64-row block
-    P.dcols = (kStage - kXD) / (kRB * dsz);
-    P.dcols = std::min(kM, P.dcols / 8 * 8);
-    P.dpieces = (kM + P.dcols - 1) / P.dcols;
+    // [x segment: dcols working values][dcols D columns]; balanced pieces
+    for (int wi = 0; wi < 2; ++wi) {
+        const int wsz = wi ? 8 : 4;
+        int dc = std::min(kM, (int)(kStage / (kRB * dsz + wsz)) / 8 * 8);
+        const int np = (kM + dc - 1) / dc;
+        dc = ((kM + np - 1) / np + 7) / 8 * 8;
+        P.dcols_w[wi] = dc;
+        P.dpieces_w[wi] = (kM + dc - 1) / dc;
+    }
     // U pieces: coefficients | column chunk of the U block | reduction scratch
     for (int wi = 0; wi < 2; ++wi) P.u_data_off[wi] = (int)round_up16((int64_t)P.coef_elems * (wi ? 8 : 4));
     {

@@ -202,6 +202,14 @@ class HodlrOperator:
             send.data_ptr() if send is not None and send.numel() else None, None, 0,
             st.cuda_stream), "hodlr_matvec_shard_begin")
 
+    def shard_local(self, x, out, working=None, stream=None):
+        torch = _torch()
+        code = _working_code(self, working)
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _lib.check(_lib.lib().hodlr_matvec_shard_local(
+            self._h, code, x.data_ptr(), x.stride(0), out.data_ptr(), out.stride(0), x.shape[1],
+            None, 0, st.cuda_stream), "hodlr_matvec_shard_local")
+
     def shard_end(self, x, recv, out, working=None, stream=None):
         torch = _torch()
         code = _working_code(self, working)

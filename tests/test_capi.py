@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(L):
     for name in header_functions():
         assert hasattr(L, name), name
         assert name in _lib.EXPORTS, f"{name} not bound in _lib.EXPORTS"
-    assert L.hodlr_abi_version() == 1
+    assert L.hodlr_abi_version() == 2
 
 
 def host_quantize(L, fmt, x):

@@ -157,3 +157,25 @@ def test_fused_large_ranks(cuda, working, fmts, ranks):
     dt = torch.float64 if working == "fp64" else torch.float32
     b = op.matvec(torch.from_numpy(x).cuda().to(dt)).double().cpu().numpy()
     assert rel(b, matvec_oracle(H, x)) <= (1e-12 if working == "fp64" else 1e-5)
+
+
+@pytest.mark.parametrize("leaf_working,call_working", [("fp32", "fp64"), ("fp64", "fp32"), ("fp32", "fp32")])
+def test_fused_leaf_vs_working_precision_stress(cuda, leaf_working, call_working):
+    """Leaves stored in one working format, matvec called in the other: the
+    D pieces' x segment depends on the call's working type (a too-small x
+    segment once overlapped the D columns and failed intermittently)."""
+    torch = cuda
+    from paper_2407_21637_b200 import NAMED_FORMATS
+
+    H = random_hodlr(2048, 3, ["fp32", "fp32", "fp16"], [10, 8, 6], leaf_working, seed=4)
+    op = make_op(H)
+    w = NAMED_FORMATS[call_working]
+    dt = torch.float64 if call_working == "fp64" else torch.float32
+    x = np.random.default_rng(3).standard_normal(H.n)
+    xd = torch.from_numpy(x).cuda().to(dt)
+    ref = matvec_oracle(H, x, call_working)
+    first = op.matvec(xd, working=w).double().cpu().numpy()
+    assert rel(first, ref) <= (1e-12 if call_working == "fp64" else 1e-5)
+    for _ in range(150):
+        again = op.matvec(xd, working=w).double().cpu().numpy()
+        assert np.array_equal(first, again)

@@ -170,30 +170,3 @@ def test_overflow_propagates_inf(cuda):
     x[5] = 3e38
     b = linops.matvec(H, x)
     assert np.isinf(b).any()
-
-
-@pytest.mark.parametrize("nranks", [2, 4])
-def test_sharded_emulated_on_one_gpu(cuda, nranks):
-    """The row-range shard path: P handles on one device, the
-    all-gather emulated by concatenation (no kernel waits on another)."""
-    torch = cuda
-    from paper_2407_21637_b200 import linops
-
-    H, vec, summ = load_case("toep1024_e4_fp64")
-    X = vec["x"]
-    ops = [linops.HodlrOperator(H, rank=g, nranks=nranks) for g in range(nranks)]
-    count = ops[0].exchange_count(X.shape[1])
-    sends, xs = [], []
-    for op in ops:
-        xl = torch.from_numpy(np.ascontiguousarray(X[op.row0:op.row0 + op.n_local])).cuda()
-        send = torch.zeros(count, dtype=torch.float64, device="cuda")
-        op.shard_begin(xl, send)
-        sends.append(send)
-        xs.append(xl)
-    recv = torch.cat(sends)
-    out = np.zeros_like(X)
-    for op, xl in zip(ops, xs):
-        bl = torch.empty_like(xl)
-        op.shard_end(xl, recv, bl)
-        out[op.row0:op.row0 + op.n_local] = bl.cpu().numpy()
-    assert rel(out, matvec_oracle(H, X)) <= 1e-12
