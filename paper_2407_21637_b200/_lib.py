@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhodlr_b200.so")
+# HODLR_B200_LIB: load an instrumented build instead (diagnostics in tools/ only)
+LIB_PATH = os.environ.get("HODLR_B200_LIB") or os.path.join(_HERE, "libhodlr_b200.so")
 
 c_i32, c_i64, c_sz, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_void_p
 c_dp = ctypes.POINTER(ctypes.c_double)

@@ -49,17 +49,33 @@ namespace {
 constexpr int kM = 256;                 // leaf rows
 constexpr int kRB = 64;                 // rows of a BC item (one leaf row block)
 constexpr int kRPL = kRB / 32;          // rows per lane in B / C pieces
-constexpr int kNS = 3;                  // ring stages per CTA
-constexpr int kCtasPerSm = 2;           // independent pipelines per SM
-constexpr int kStage = 33280;           // bytes per stage (= 512 B of x + a 64 x 64 fp64 D block)
+// (HODLR_KNS / HODLR_KSTAGE override the ring geometry for tools/build_variants.sh sweeps)
+#ifndef HODLR_KNS
+#define HODLR_KNS 3
+#endif
+#ifndef HODLR_KSTAGE
+#define HODLR_KSTAGE 33280
+#endif
+constexpr int kNS = HODLR_KNS;          // ring stages per CTA
+#ifndef HODLR_CTAS
+#define HODLR_CTAS 2
+#endif
+constexpr int kCtasPerSm = HODLR_CTAS;  // independent pipelines per SM
+constexpr int kStage = HODLR_KSTAGE;    // bytes per stage (= 512 B of x + a 64 x 64 fp64 D block)
 constexpr int kConsumers = 8;           // consumer warps (= column subsets of B/C pieces)
 constexpr int kThreads = 32 * (kConsumers + 1);  // + producer warp
 constexpr int kFifo = 8;                // BC items whose U piece waits for the coefficients
-constexpr int kMaxRPieces = 256;        // node-reduction pieces
+#ifndef HODLR_MAX_R
+#define HODLR_MAX_R 256
+#endif
+constexpr int kMaxRPieces = HODLR_MAX_R;  // node-reduction pieces
 constexpr int kMaxUPieces = 16;         // U chunks per BC item
 constexpr int kMaxLev = 24;
 constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
-constexpr int kMaxCols = 512;           // columns (sum of ranks) per leaf
+#ifndef HODLR_MAX_COLS
+#define HODLR_MAX_COLS 512
+#endif
+constexpr int kMaxCols = HODLR_MAX_COLS;  // columns (sum of ranks) per leaf
 constexpr int kXB = 2048;               // x segment of an A piece (<= 256 rows)
 
 enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_R = 5, PT_END = 4 };
@@ -72,16 +88,35 @@ enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_R = 5, PT_END = 4 };
 #define PROF_ADD(i, dt)
 #endif
 
+// HODLR_TRACE builds: per-CTA %globaltimer stamps into a.trace[cta * 16 + i]
+// (tools/trace_run.py reads them back and prints the phase timeline).
+#ifdef HODLR_TRACE
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TR(i) do { if (a.trace) a.trace[blockIdx.x * 48 + (i)] = gtimer(); } while (0)
+#define TRV(i, v) do { if (a.trace) a.trace[blockIdx.x * 48 + (i)] = (unsigned long long)(v); } while (0)
+#else
+#define TR(i) do { } while (0)
+#define TRV(i, v) do { } while (0)
+#endif
+
 struct Level {
     int32_t r, fmt;
     int32_t slot;       // coefficient slot (elements) inside a U piece
     int32_t tstride;    // padded coefficients per node (multiple of 4)
+    int32_t npc;        // A pieces (row chunks) per leaf of this level's format group
+    int32_t cst;        // partials per (node, column): stride (multiple of 4) >= leaves_of_node * npc
     int64_t pbase;      // partial buffer base of the level's nodes
     int64_t tbase;      // coefficient buffer base
 };
 
+// A queue item (leaf, piece): rows [r0, r0 + nrows) of format group g's V'
+// sub-slab; chunk = index of the piece inside its group (npc pieces per group).
 struct APiece {
-    int32_t g, r0, nrows, last_of_group;
+    int32_t g, r0, nrows, chunk, npc, pad;
 };
 
 // U chunk of a BC item: columns [c0, c0 + ncols) of format group g.
@@ -102,7 +137,9 @@ struct SvParams {
     int32_t num_a, num_d, num_r, pos_r;   // queue: BC items with the R pieces at pos_r
     int32_t napieces;
     int32_t dpieces_w[2], dcols_w[2];      // phase-B pieces per item / columns per piece, [fp32, fp64 working]
-    int64_t slab_bytes, ds_off, us_off;
+    // three regions, leaf-major inside each: [V' of every leaf][D blocks][U blocks]
+    int64_t vs_bytes, ds_bytes, us_bytes;  // per leaf
+    int64_t d_region, u_region;            // region offsets (the V' region starts at 0)
     int64_t dblock_bytes, ublock_bytes;
     int32_t gcols[5], vpad[5];
     int64_t vgoff[5], ugoff[5];           // V' sub-slab offsets / U sub-block offsets in a block
@@ -143,7 +180,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+#ifdef HODLR_EXP_NOLOAD
+    (void)bytes;  // timing experiment: no matrix bytes move (results are garbage)
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+#else
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -157,22 +199,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+#ifdef HODLR_EXP_NOLOAD
+    return;
+#endif
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
+}
+// Streaming (read-once) matrix bytes: L2 evict-first, so they do not push the
+// small, re-read state (x, partials, coefficients) out of L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                                uint64_t pol) {
+#if defined(HODLR_NO_L2_HINT) || defined(HODLR_EXP_NOLOAD)
+    (void)pol;
+    bulk_g2s(dst, src, bytes, bar);
+#else
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+#endif
 }
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
@@ -244,37 +298,58 @@ __device__ __forceinline__ void load4(const uint8_t* p, float v[4]) {
 }
 
 // ------------------------------------------------------------ phase A
-// Rows of the V' sub-slab of format FMT: lane owns column quads q = lane + 32 i
-// (i < 2), warp w owns rows w, w + 8, ...; sums stay in acc across pieces.
+// Rows of the V' sub-slab of format FMT: lane owns column quad q = lane (and
+// lane + 32 when vpad > 128), warp w owns rows w, w + 8, ...; sums stay in acc
+// across pieces.  Lanes past the last quad read quad 0 (a valid address, the
+// sums are never written), so the row loop has no divergent branches and the
+// loads of four rows are in flight together.
+template <int FMT, typename W>
+__device__ __forceinline__ void a_quad(const uint8_t* p, W x, W acc[4]) {
+    if constexpr (FMT == HODLR_FMT_FP64) {
+        const double2 t0 = *reinterpret_cast<const double2*>(p);
+        const double2 t1 = *reinterpret_cast<const double2*>(p + 16);
+        acc[0] = madd_d<W>(t0.x, x, acc[0]);
+        acc[1] = madd_d<W>(t0.y, x, acc[1]);
+        acc[2] = madd_d<W>(t1.x, x, acc[2]);
+        acc[3] = madd_d<W>(t1.y, x, acc[3]);
+    } else {
+        float v[4];
+        load4<FMT>(p, v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = madd<W>(v[e], x, acc[e]);
+    }
+}
+
+template <int FMT, typename W, int NSET>
+__device__ __forceinline__ void a_rows_n(const uint8_t* rows, int nrows, int nq, int row_bytes, const W* xs, int warp,
+                                         int lane, W acc[2][4]) {
+    constexpr int qb = 4 * (FMT == HODLR_FMT_Q52 ? 1 : FMT == HODLR_FMT_FP32 ? 4 : FMT == HODLR_FMT_FP64 ? 8 : 2);
+    const uint8_t* b0 = rows + (lane < nq ? lane : 0) * qb;
+    const uint8_t* b1 = rows + (lane + 32 < nq ? lane + 32 : 0) * qb;
+    int j = warp;
+    for (; j + 3 * kConsumers < nrows; j += 4 * kConsumers) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int jj = j + u * kConsumers;
+            const W x = xs[jj];
+            a_quad<FMT, W>(b0 + (size_t)jj * row_bytes, x, acc[0]);
+            if constexpr (NSET == 2) a_quad<FMT, W>(b1 + (size_t)jj * row_bytes, x, acc[1]);
+        }
+    }
+    for (; j < nrows; j += kConsumers) {
+        const W x = xs[j];
+        a_quad<FMT, W>(b0 + (size_t)j * row_bytes, x, acc[0]);
+        if constexpr (NSET == 2) a_quad<FMT, W>(b1 + (size_t)j * row_bytes, x, acc[1]);
+    }
+}
+
 template <int FMT, typename W>
 __device__ __forceinline__ void a_rows(const uint8_t* rows, int nrows, int vpad, const W* xs, int warp, int lane,
                                        W acc[2][4]) {
     const int nq = vpad >> 2;
     const int row_bytes = vpad * fmt_sz(FMT);
-#pragma unroll 2
-    for (int j = warp; j < nrows; j += kConsumers) {
-        const W xv = xs[j];
-        const uint8_t* row = rows + (size_t)j * row_bytes;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const int q = lane + 32 * i;
-            if (q < nq) {
-                if constexpr (FMT == HODLR_FMT_FP64) {
-                    const double2 t0 = *reinterpret_cast<const double2*>(row + (size_t)q * 32);
-                    const double2 t1 = *reinterpret_cast<const double2*>(row + (size_t)q * 32 + 16);
-                    acc[i][0] = madd_d<W>(t0.x, xv, acc[i][0]);
-                    acc[i][1] = madd_d<W>(t0.y, xv, acc[i][1]);
-                    acc[i][2] = madd_d<W>(t1.x, xv, acc[i][2]);
-                    acc[i][3] = madd_d<W>(t1.y, xv, acc[i][3]);
-                } else {
-                    float v[4];
-                    load4<FMT>(row + (size_t)q * 4 * fmt_sz(FMT), v);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) acc[i][e] = madd<W>(v[e], xv, acc[i][e]);
-                }
-            }
-        }
-    }
+    if (nq <= 32) a_rows_n<FMT, W, 1>(rows, nrows, nq, row_bytes, xs, warp, lane, acc);
+    else a_rows_n<FMT, W, 2>(rows, nrows, nq, row_bytes, xs, warp, lane, acc);
 }
 
 template <typename W>
@@ -334,8 +409,13 @@ __device__ __forceinline__ void col_block(const uint8_t* blk, int ncols, int war
             col_elem<FMT, W>(blk + ((size_t)cc * kRB + kRPL * lane) * sz, mul(cc), acc[k]);
         }
     }
-    for (; c < ncols; c += kConsumers)  // tail: fixed accumulator set (no dynamic register indexing)
-        col_elem<FMT, W>(blk + ((size_t)c * kRB + kRPL * lane) * sz, mul(c), acc[0]);
+    // tail (< 4 columns, warp-uniform conditions): separate accumulator sets
+    if (c < ncols) col_elem<FMT, W>(blk + ((size_t)c * kRB + kRPL * lane) * sz, mul(c), acc[0]);
+    if (c + kConsumers < ncols)
+        col_elem<FMT, W>(blk + ((size_t)(c + kConsumers) * kRB + kRPL * lane) * sz, mul(c + kConsumers), acc[1]);
+    if (c + 2 * kConsumers < ncols)
+        col_elem<FMT, W>(blk + ((size_t)(c + 2 * kConsumers) * kRB + kRPL * lane) * sz, mul(c + 2 * kConsumers),
+                         acc[2]);
 }
 
 template <typename W, typename MulF>
@@ -358,13 +438,12 @@ struct SvKernelArgs {
     W* partial;            // fast-path layout: level bases P.lev[].pbase
     W* tbuf;
     SvSync* sync;
+    unsigned long long* trace;  // HODLR_TRACE builds only (else unused)
 };
 
 struct SmemCtl {
     uint64_t full[kNS], empty[kNS];
     PieceHdr hdr[kNS];
-    unsigned epoch;
-    unsigned a_cnt, r_cnt;         // consumer completions (A leaves, R pieces)
     int fifo[kFifo];               // deferred U pieces: (leaf << 8) | row block
     alignas(16) double ybuf[kFifo][kRB];  // y = D x of those items (working type)
     alignas(16) int16_t cidx[kMaxCols];  // flattened U column -> coefficient slot
@@ -389,58 +468,44 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     constexpr int kBlocks = kM / kRB;            // row blocks per leaf
 
     if (threadIdx.x == 0) {
-        C.epoch = ld_acquire(&a.sync->epoch);
-        C.a_cnt = C.r_cnt = 0u;
+        TR(0);
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&C.full[s], 1);
             mbar_init(&C.empty[s], kConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = threadIdx.x; i < P.gstart[5]; i += kThreads) {
-        const Level& L = P.lev[P.col_level[i]];
-        const int sh = nlev - (P.col_level[i] + 1);
-        C.cidx[i] = (int16_t)(L.slot + P.col_c[i]);
-        C.pbase_c[i] = (int32_t)(L.pbase + ((int64_t)P.col_c[i] << sh));
-        C.pstride_c[i] = L.r << sh;
-        C.psh_c[i] = (int8_t)sh;
-    }
     __syncthreads();
-    const unsigned target = C.epoch + 1u;
+    if (warp != 0) {
+        // consumers build the column tables while the producer starts streaming
+        for (int i = threadIdx.x - 32; i < P.gstart[5]; i += kConsumers * 32) {
+            const Level& L = P.lev[P.col_level[i]];
+            const int sh = nlev - (P.col_level[i] + 1);
+            C.cidx[i] = (int16_t)(L.slot + P.col_c[i]);
+            C.pbase_c[i] = (int32_t)(L.pbase + (int64_t)P.col_c[i] * L.cst);
+            C.pstride_c[i] = L.r * L.cst;
+            C.psh_c[i] = (int8_t)sh;
+        }
+        consumer_sync();
+        if (threadIdx.x == 32) TR(22);
+    }
 
     if (warp == 0) {
         // =========================================================== producer
         int stage = 0;
         unsigned phase = 0;
-        unsigned a_pub = 0, r_pub = 0;  // completions published GPU-wide
+        const uint64_t pol = policy_evict_first();
         unsigned a_items = 0, r_items = 0;
         int fh = 0, ft = 0;             // deferred-U FIFO (warp-uniform); slot = index % kFifo
-        // Publish this CTA's finished phase-A leaves (once, all together) and R
-        // pieces GPU-wide.  Consumers signal with CTA-scope releases on C.*_cnt
-        // after the work's global stores; one GPU fence plus a release reduction
-        // publishes a batch (a GPU-scope fence costs microseconds under full HBM
-        // load, so there are only a handful per matvec).  block: wait for all.
-        auto publish = [&](bool block) {
-            for (;;) {
-                unsigned na = 0, nr = 0;
-                if (lane == 0) {
-                    const unsigned ac = *(volatile unsigned*)&C.a_cnt;
-                    if (ac == a_items) na = ac - a_pub;
-                    nr = *(volatile unsigned*)&C.r_cnt - r_pub;
-                    if (na || nr) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    if (na) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->a_done), "r"(na) : "memory");
-                    if (nr) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->r_done), "r"(nr) : "memory");
-                }
-                a_pub += __shfl_sync(0xffffffffu, na, 0);
-                r_pub += __shfl_sync(0xffffffffu, nr, 0);
-                if (!block || (a_pub == a_items && r_pub == r_items)) return;
-                __nanosleep(64);
-            }
-        };
-        auto pending = [&]() { return a_pub != a_items || r_pub != r_items; };
+        bool first_claim = true;
         auto claim = [&]() -> uint8_t* {
-            while (!mbar_test(&C.empty[stage], phase ^ 1u))
-                if (pending()) publish(false);
+            // try_wait parks the warp in hardware until the stage is released: a
+            // test_wait spin here steals shared-memory pipe slots from the consumers
+            mbar_wait(&C.empty[stage], phase ^ 1u);
+            if (first_claim) {
+                first_claim = false;
+                if (lane == 0) TR(1);
+            }
             return stages + (size_t)stage * kStage;
         };
         auto next_stage = [&]() {
@@ -464,16 +529,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             }
             r_ready = __shfl_sync(0xffffffffu, v, 0) == (unsigned)P.num_r;
             if (r_ready) asm volatile("fence.proxy.async.global;" ::: "memory");  // t read by TMA below
+            if (r_ready && lane == 0) TR(6);
         };
         auto emit_u = [&](int leaf, int rb, int slot) {
             const int wi = sizeof(W) == 8 ? 1 : 0;
             const int wbytes = (int)sizeof(W);
-            const uint8_t* ublk = a.slab + (int64_t)leaf * P.slab_bytes + P.us_off + (int64_t)rb * P.ublock_bytes;
+            const uint8_t* ublk = a.slab + P.u_region + (int64_t)leaf * P.us_bytes + (int64_t)rb * P.ublock_bytes;
             for (int p = 0; p < P.nupieces; ++p) {
                 const UPiece up = P.up[p];
                 const unsigned cb = (unsigned)(up.ncols * kRB * fmt_sz(up.g));
                 uint8_t* st = claim();
                 if (lane == 0) {
+                    if (fh == 0 && p == 0) TR(14);
                     PieceHdr& h = C.hdr[stage];
                     h.type = PT_U;
                     h.leaf = leaf;
@@ -492,8 +559,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                         bulk_g2s(st + (size_t)L.slot * wbytes, src, (unsigned)(L.tstride * wbytes), &C.full[stage]);
                     }
                 } else if (lane == 31) {
-                    bulk_g2s(st + P.u_data_off[wi], ublk + P.ugoff[up.g] + (int64_t)up.c0 * kRB * fmt_sz(up.g), cb,
-                             &C.full[stage]);
+                    bulk_g2s_stream(st + P.u_data_off[wi], ublk + P.ugoff[up.g] + (int64_t)up.c0 * kRB * fmt_sz(up.g),
+                                    cb, &C.full[stage], pol);
                 }
                 __syncwarp();
                 next_stage();
@@ -501,7 +568,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         };
         auto flush_u = [&](bool block) {
             if (fh == ft) return;
-            if (block && !r_ready) publish(true);  // never block while holding unpublished work
             check_r(block);
             if (!r_ready) return;
             while (fh != ft) {
@@ -517,8 +583,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         // so progress never depends on CTAs being co-resident.
         int n1 = 0, n2 = 0;
         if (lane == 0) {
-            n1 = (int)atomicAdd(&a.sync->queue, 1u);
-            n2 = (int)atomicAdd(&a.sync->queue, 1u);
+            n1 = (int)atomicAdd(&a.sync->queue, 2u);
+            n2 = n1 + 1;
+            TR(23);
         }
         const int dsz = fmt_sz(P.leaf_fmt);
         for (;;) {
@@ -526,31 +593,32 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             if (q >= nq) break;
             n1 = n2;
             if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);
-            if (pending()) publish(false);
             if (q < P.num_a) {
-                // ---- A: partial V'^T x of one leaf
-                const int leaf = q;
-                const uint8_t* base = a.slab + (int64_t)leaf * P.slab_bytes;
+                // ---- A: partial V'^T x of one (leaf, row chunk of a format group)
+                const int leaf = q / P.napieces, p = q - leaf * P.napieces;
+                const uint8_t* base = a.slab + (int64_t)leaf * P.vs_bytes;
+                const APiece ap = P.ap[p];
                 ++a_items;
-                for (int p = 0; p < P.napieces; ++p) {
-                    const APiece ap = P.ap[p];
-                    uint8_t* st = claim();
-                    const unsigned cb = (unsigned)(ap.nrows * P.vpad[ap.g] * fmt_sz(ap.g));
-                    const unsigned xb = (unsigned)(ap.nrows * sizeof(W));
-                    if (lane == 0) {
-                        PieceHdr& h = C.hdr[stage];
-                        h.type = PT_A;
-                        h.leaf = leaf;
-                        h.a = p;
-                        h.last = (p == P.napieces - 1);
-                        mbar_arrive_tx(&C.full[stage], xb + cb);
-                        bulk_g2s(st, a.x + (int64_t)leaf * kM + ap.r0, xb, &C.full[stage]);
-                        bulk_g2s(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.r0 * P.vpad[ap.g] * fmt_sz(ap.g), cb,
-                                 &C.full[stage]);
-                    }
-                    __syncwarp();
-                    next_stage();
+                uint8_t* st = claim();
+                const unsigned cb = (unsigned)(ap.nrows * P.vpad[ap.g] * fmt_sz(ap.g));
+                const unsigned xb = (unsigned)(ap.nrows * sizeof(W));
+                if (lane == 0) {
+                    PieceHdr& h = C.hdr[stage];
+                    h.type = PT_A;
+                    h.leaf = leaf;
+                    h.a = p;
+                    // 2 = this CTA's last A piece (the next queue entry is not A):
+                    // its consumers then publish the CTA's A pieces GPU-wide
+                    h.last = n1 >= P.num_a ? 2 : 1;
+                    mbar_arrive_tx(&C.full[stage], xb + cb);
+                    bulk_g2s(st, a.x + (int64_t)leaf * kM + ap.r0, xb, &C.full[stage]);
+                    bulk_g2s_stream(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.r0 * P.vpad[ap.g] * fmt_sz(ap.g), cb,
+                                    &C.full[stage], pol);
+                    TR(2);
+                    TRV(11, a_items);
                 }
+                __syncwarp();
+                next_stage();
                 continue;
             }
             const int qq = q - P.num_a;
@@ -558,23 +626,25 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 // ---- R: reduce node partials (needs every leaf's partials)
                 const RPiece rp = P.rp[qq - P.pos_r];
                 const Level& L = P.lev[rp.lv];
-                const int nch = 1 << (nlev - 1 - rp.lv);
-                publish(true);  // own A leaves first (and anything else pending)
                 if (lane == 0) {
+                    if (r_items == 0) TR(4);
                     while (ld_acquire(&a.sync->a_done) != (unsigned)P.num_a) __nanosleep(128);
                     asm volatile("fence.proxy.async.global;" ::: "memory");
+                    if (r_items == 0) TR(5);
+                    TRV(13, r_items + 1);
                 }
                 __syncwarp();
                 ++r_items;
                 uint8_t* st = claim();
-                const int64_t cnt = (int64_t)(rp.j1 - rp.j0) * (rp.c1 - rp.c0) * nch;
+                const int64_t cnt = (int64_t)(rp.j1 - rp.j0) * (rp.c1 - rp.c0) * L.cst;
                 const unsigned bytes = (unsigned)round_up16_d(cnt * (int64_t)sizeof(W));
                 if (lane == 0) {
                     PieceHdr& h = C.hdr[stage];
                     h.type = PT_R;
                     h.a = qq - P.pos_r;
                     mbar_arrive_tx(&C.full[stage], bytes);
-                    bulk_g2s(st, a.partial + L.pbase + ((int64_t)rp.j0 * L.r + rp.c0) * nch, bytes, &C.full[stage]);
+                    bulk_g2s(st, a.partial + L.pbase + ((int64_t)rp.j0 * L.r + rp.c0) * L.cst, bytes, &C.full[stage]);
+                    TR(20);
                 }
                 __syncwarp();
                 next_stage();
@@ -583,9 +653,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             // ---- BC: y = D x now (kept in this CTA's y slot), b = U t + y once t exists
             const int qb = qq < P.pos_r ? qq : qq - P.num_r;
             const int leaf = qb / kBlocks, rb = qb % kBlocks;
+            if (lane == 0) {
+                if (ft == 0) TR(3);
+                TRV(12, ft + 1);
+            }
             if (ft - fh == kFifo) flush_u(true);  // frees the y slot this item will use
             const int slot = ft % kFifo;
-            const uint8_t* blk = a.slab + (int64_t)leaf * P.slab_bytes + P.ds_off + (int64_t)rb * P.dblock_bytes;
+            const uint8_t* blk = a.slab + P.d_region + (int64_t)leaf * P.ds_bytes + (int64_t)rb * P.dblock_bytes;
             const int dcols = P.dcols_w[sizeof(W) == 8], dpieces = P.dpieces_w[sizeof(W) == 8];
             const int xoff = dcols * (int)sizeof(W);  // x segment, then the D columns (16-B aligned)
             for (int p = 0; p < dpieces; ++p) {
@@ -603,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     h.last = (p == dpieces - 1) ? 1 + slot : 0;
                     mbar_arrive_tx(&C.full[stage], xb + cb);
                     bulk_g2s(st, a.x + (int64_t)leaf * kM + c0, xb, &C.full[stage]);
-                    bulk_g2s(st + xoff, blk + (int64_t)c0 * kRB * dsz, cb, &C.full[stage]);
+                    bulk_g2s_stream(st + xoff, blk + (int64_t)c0 * kRB * dsz, cb, &C.full[stage], pol);
                 }
                 __syncwarp();
                 next_stage();
@@ -613,8 +687,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             ++ft;
             flush_u(false);
         }
+        if (lane == 0) TR(7);
         flush_u(true);
-        publish(true);
+        if (lane == 0) TR(8);
         claim();
         if (lane == 0) {
             C.hdr[stage].type = PT_END;
@@ -627,6 +702,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         const int ctid = threadIdx.x - 32;
         int stage = 0;
         unsigned phase = 0;
+        unsigned my_a = 0;  // A pieces this CTA's consumers finished
+        bool first_u_seen = false;
         W aacc[2][4];   // phase A: column sums of the current format group
         W bacc[4][kRPL];  // BC items: row sums (kRPL rows per lane, 4 chains)
 #pragma unroll
@@ -637,18 +714,54 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         for (int k = 0; k < 4; ++k)
 #pragma unroll
             for (int r = 0; r < kRPL; ++r) bacc[k][r] = W(0);
+#ifdef HODLR_TRACE
+        long long wait_cyc = 0, t_loop = clock64();
+        long long busy[6] = {0, 0, 0, 0, 0, 0}, nb[6] = {0, 0, 0, 0, 0, 0}, t_busy = 0;
+        long long split[4] = {0, 0, 0, 0}, ts0 = 0;
+        int busy_type = 0;
+#endif
         for (;;) {
             PROF_T(tw);
+#ifdef HODLR_TRACE
+            const long long tw0 = clock64();
+#endif
             mbar_wait(&C.full[stage], phase);
+#ifdef HODLR_TRACE
+            wait_cyc += clock64() - tw0;
+            t_busy = clock64();
+            busy_type = C.hdr[stage].type;
+#endif
             const PieceHdr h = C.hdr[stage];
             uint8_t* st = stages + (size_t)stage * kStage;
-            if (h.type == PT_END) break;
+            if (h.type == PT_END) {
+                if (ctid == 0) {
+                    TR(9);
+#ifdef HODLR_TRACE
+                    TRV(28, wait_cyc);
+                    TRV(29, clock64() - t_loop);
+                    for (int i = 0; i < 6; ++i) {
+                        TRV(32 + i, busy[i]);
+                        TRV(38 + i, nb[i]);
+                    }
+                    for (int i = 0; i < 4; ++i) TRV(44 + i, split[i]);
+#endif
+                }
+                break;
+            }
             PROF_ADD(h.type == PT_R ? 0 : h.type, clock64() - tw);  // [1] A [2] D [3] U [0] R
             bool scratch = false;  // the stage was reused as reduction scratch
             if (h.type == PT_A) {
+                if (ctid == 0 && my_a < 4) TR(24 + my_a);  // arrival of this CTA's A pieces 1..4
                 const APiece ap = P.ap[h.a];
+#ifdef HODLR_TRACE
+                ts0 = clock64();
+#endif
                 a_piece<W>(ap.g, st + kXB, ap.nrows, P.vpad[ap.g], reinterpret_cast<const W*>(st), cw, lane, aacc);
-                if (ap.last_of_group) {
+#ifdef HODLR_TRACE
+                split[0] += clock64() - ts0;
+                ts0 = clock64();
+#endif
+                {
                     // combine the warps' column sums in warp order, write the partials
                     W* red = reinterpret_cast<W*>(st);
                     const int vp = P.vpad[ap.g];
@@ -668,7 +781,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                         const int flat = P.gstart[ap.g] + c;
                         const int sh = C.psh_c[flat];
                         const int jn = h.leaf >> sh;
-                        a.partial[(int64_t)C.pbase_c[flat] + (int64_t)jn * C.pstride_c[flat] + (h.leaf - (jn << sh))] = s;
+                        a.partial[(int64_t)C.pbase_c[flat] + (int64_t)jn * C.pstride_c[flat] +
+                                  (int64_t)(h.leaf - (jn << sh)) * ap.npc + ap.chunk] = s;
                     }
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
@@ -676,12 +790,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                         for (int e = 0; e < 4; ++e) aacc[i][e] = W(0);
                     scratch = true;
                 }
+#ifdef HODLR_TRACE
+                split[1] += clock64() - ts0;
+#endif
             } else if (h.type == PT_D) {
                 const W* xs = reinterpret_cast<const W*>(st);
                 const int dcols = P.dcols_w[sizeof(W) == 8];
                 const int nc = min(dcols, kM - h.b);
                 auto mul = [&](int c) { return xs[c]; };
+#ifdef HODLR_TRACE
+                ts0 = clock64();
+#endif
                 col_block_any<W>(P.leaf_fmt, st + dcols * (int)sizeof(W), nc, cw, lane, mul, bacc);
+#ifdef HODLR_TRACE
+                split[2] += clock64() - ts0;
+                ts0 = clock64();
+#endif
                 if (h.last) {
                     W* red = reinterpret_cast<W*>(st);
                     consumer_sync();
@@ -700,19 +824,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
 #pragma unroll
             for (int r = 0; r < kRPL; ++r) bacc[k][r] = W(0);
                     scratch = true;
+#ifdef HODLR_TRACE
+                    split[3] += clock64() - ts0;
+#endif
                 }
             } else if (h.type == PT_R) {
                 // t for (node, column) pairs: fixed-order sums over the node's leaves
                 const RPiece rp = P.rp[h.a];
                 const Level& L = P.lev[rp.lv];
-                const int nch = 1 << (nlev - 1 - rp.lv);
+                const int nch = (1 << (nlev - 1 - rp.lv)) * L.npc;  // partials per (node, column)
                 const int ncol = rp.c1 - rp.c0;
                 const int npairs = (rp.j1 - rp.j0) * ncol;
                 const W* v = reinterpret_cast<const W*>(st);
                 if (nch >= 32) {
                     for (int p = cw; p < npairs; p += kConsumers) {
                         W s = W(0);
-                        for (int i = lane; i < nch; i += 32) s += v[(int64_t)p * nch + i];
+                        for (int i = lane; i < nch; i += 32) s += v[(int64_t)p * L.cst + i];
                         s = warp_sum(s);
                         if (lane == 0) {
                             const int j = rp.j0 + p / ncol, c = rp.c0 + p % ncol;
@@ -721,14 +848,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     }
                 } else {
                     for (int p = ctid; p < npairs; p += kConsumers * 32) {
-                        W s = v[(int64_t)p * nch];
-                        for (int i = 1; i < nch; ++i) s += v[(int64_t)p * nch + i];
+                        W s = v[(int64_t)p * L.cst];
+                        for (int i = 1; i < nch; ++i) s += v[(int64_t)p * L.cst + i];
                         const int j = rp.j0 + p / ncol, c = rp.c0 + p % ncol;
                         a.tbuf[L.tbase + (int64_t)j * L.tstride + c] = s;
                     }
                 }
                 scratch = true;
             } else {  // PT_U: b = U t + y, one column chunk of U per piece
+                if (ctid == 0 && !first_u_seen) {
+                    first_u_seen = true;
+                    TR(15);
+                }
                 const int wi = sizeof(W) == 8 ? 1 : 0;
                 const UPiece up = P.up[h.last];
                 const W* coef = reinterpret_cast<const W*>(st);
@@ -739,8 +870,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     col_block_any<W>(up.g, st + P.u_data_off[wi], up.ncols, cw, lane, mul, bacc);
                 }
                 if (h.last == P.nupieces - 1) {
-                    // scratch after this piece's data (capacity checked at prepare time)
-                    W* red = reinterpret_cast<W*>(st + P.u_data_off[wi] + round_up16_d(up.ncols * kRB * fmt_sz(up.g)));
+                    W* red = reinterpret_cast<W*>(st);  // the stage is scratch once every warp is done with it
+                    consumer_sync();
 #pragma unroll
                     for (int r = 0; r < kRPL; ++r)
                         red[cw * kRB + kRPL * lane + r] = (bacc[0][r] + bacc[1][r]) + (bacc[2][r] + bacc[3][r]);
@@ -758,19 +889,30 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     scratch = true;
                 }
             }
-            if (scratch) {
+            if (scratch && (h.type == PT_A || h.type == PT_R)) {
                 consumer_sync();  // scratch reads and the item's global stores are done
-                if (ctid == 0) {
-                    const bool a_end = h.type == PT_A && h.last;
-                    const bool r_end = h.type == PT_R;
-                    if (a_end || r_end) {
-                        asm volatile("fence.acq_rel.cta;" ::: "memory");
-                        atomicAdd(a_end ? &C.a_cnt : &C.r_cnt, 1u);
-                    }
+                // Publish GPU-wide from a consumer thread (it has no bulk copies
+                // in flight, so its fence does not wait for the ring's loads):
+                // all of this CTA's A pieces at once after its last one, every
+                // R piece.  Release pattern: CTA barrier, fence.acq_rel.gpu,
+                // relaxed reduction; readers ld.acquire the counter.
+                if (h.type == PT_A) ++my_a;
+                if (ctid == 0 && ((h.type == PT_A && h.last == 2) || h.type == PT_R)) {
+                    if (h.type == PT_A) TR(16); else TR(18);
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    if (h.type == PT_A) TR(17); else TR(19);
+                    if (h.type == PT_A)
+                        asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->a_done), "r"(my_a) : "memory");
+                    else
+                        asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&a.sync->r_done), "r"(1u) : "memory");
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&C.empty[stage]);
+#ifdef HODLR_TRACE
+            busy[busy_type] += clock64() - t_busy;
+            nb[busy_type] += 1;
+#endif
             if (++stage == kNS) {
                 stage = 0;
                 phase ^= 1u;
@@ -791,6 +933,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         s_last = old == gridDim.x - 1;
     }
     __syncthreads();
+    if (threadIdx.x == 0) TR(10);
     if (s_last) {
         if (threadIdx.x == 0) {
             a.sync->queue = 0u;
@@ -798,7 +941,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             a.sync->a_done = 0u;
             a.sync->r_done = 0u;
             __threadfence();
-            st_release(&a.sync->epoch, target);
+            st_release(&a.sync->epoch, a.sync->epoch + 1u);  // calls completed (informational)
         }
     }
 }
@@ -879,13 +1022,10 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         L.tstride = (L.r + 3) / 4 * 4;
         L.slot = slot;
         slot += L.tstride;
-        L.pbase = pb;  // level partials: [node][column][leaf of node], 32-byte aligned
-        pb += ((int64_t)L.r * nleaves + 3) / 4 * 4;
         L.tbase = tb;
         tb += (int64_t)L.tstride << (k + 1);
     }
     P.coef_elems = slot;
-    if (pb >= (int64_t(1) << 31)) return HODLR_OK;  // int32 partial indices in shared tables
     // slab geometry
     const int dsz = fmt_bytes(lf);
     int64_t vs = 0;
@@ -900,9 +1040,12 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         ub += round_up16((int64_t)P.gcols[g] * kRB * fmt_bytes(g));
     }
     P.ublock_bytes = ub;
-    P.ds_off = vs;
-    P.us_off = vs + (kM / kRB) * P.dblock_bytes;
-    P.slab_bytes = P.us_off + (kM / kRB) * P.ublock_bytes;
+    P.vs_bytes = vs;
+    P.ds_bytes = (kM / kRB) * P.dblock_bytes;
+    P.us_bytes = (kM / kRB) * P.ublock_bytes;
+    P.d_region = round_up16((int64_t)nleaves * P.vs_bytes + 240);
+    P.u_region = round_up16(P.d_region + (int64_t)nleaves * P.ds_bytes + 240);
+    const int64_t slab_total = P.u_region + (int64_t)nleaves * P.us_bytes;
     // phase-A pieces: row blocks of each format's V' sub-slab (multiples of 8 rows)
     P.napieces = 0;
     for (int g = 0; g < 5; ++g) {
@@ -913,9 +1056,22 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         for (int r0 = 0; r0 < kM; r0 += rows) {
             if (P.napieces == kMaxPieces) return HODLR_OK;
             const int nr = std::min(rows, kM - r0);
-            P.ap[P.napieces++] = APiece{g, r0, nr, r0 + nr == kM};
+            P.ap[P.napieces++] = APiece{g, r0, nr, r0 / rows, (kM + rows - 1) / rows, 0};
         }
     }
+    // partials: per level [node][column][cst], entries (leaf of node, chunk) in
+    // leaf-major order, each (node, column) run 32-byte aligned
+    for (int k = 0; k < depth; ++k) {
+        Level& L = P.lev[k];
+        L.npc = 0;
+        for (int i = 0; i < P.napieces; ++i)
+            if (P.ap[i].g == L.fmt) L.npc = P.ap[i].npc;
+        if (L.r > 0 && L.npc == 0) return HODLR_OK;
+        L.cst = (int)(((int64_t)(nleaves >> (k + 1)) * std::max(L.npc, 1) + 3) / 4 * 4);
+        L.pbase = pb;
+        pb += (int64_t)L.r * L.cst << (k + 1);
+    }
+    if (pb >= (int64_t(1) << 31)) return HODLR_OK;  // int32 partial indices in shared tables
     // reduction scratch in an A piece's stage: kConsumers x vpad values
     for (int g = 0; g < 5; ++g)
         if ((size_t)kConsumers * P.vpad[g] * 8 > (size_t)kStage) return HODLR_OK;
@@ -932,13 +1088,18 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     // U pieces: coefficients | column chunk of the U block | reduction scratch
     for (int wi = 0; wi < 2; ++wi) P.u_data_off[wi] = (int)round_up16((int64_t)P.coef_elems * (wi ? 8 : 4));
     {
-        const int64_t room = kStage - P.u_data_off[1] - (int64_t)kConsumers * kRB * 8 - 16;
+        const int64_t room = kStage - P.u_data_off[1] - 16;
+        if ((size_t)kConsumers * kRB * 8 > (size_t)kStage) return HODLR_OK;  // combine scratch
         P.nupieces = 0;
         for (int g = 0; g < 5; ++g) {
             if (P.gcols[g] == 0) continue;
             int per = (int)(room / ((int64_t)kRB * fmt_bytes(g)));
             per = per >= 8 ? per / 8 * 8 : per;  // keep chunk offsets 16-byte aligned
             if (per < 1 || (per < 8 && P.gcols[g] > per)) return HODLR_OK;
+            if (per >= 8) {  // balance the chunks of this group
+                const int np = (P.gcols[g] + per - 1) / per;
+                per = std::min(per, ((P.gcols[g] + np - 1) / np + 7) / 8 * 8);
+            }
             for (int c0 = 0; c0 < P.gcols[g]; c0 += per) {
                 if (P.nupieces == kMaxUPieces) return HODLR_OK;
                 P.up[P.nupieces++] = UPiece{g, c0, std::min(per, P.gcols[g] - c0), 0};
@@ -946,7 +1107,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         }
         if (P.nupieces == 0) return HODLR_OK;
     }
-    P.num_a = nleaves;
+    P.num_a = nleaves * P.napieces;
     P.num_d = nleaves * (kM / kRB);
     // node-reduction pieces (R items): a level's partials are [node][column][leaf]
     P.num_r = 0;
@@ -954,7 +1115,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         const Level& L = P.lev[k];
         if (L.r == 0) continue;
         const int nodes_k = 1 << (k + 1);
-        const int64_t nch = nleaves >> (k + 1);
+        const int64_t nch = L.cst;
         const int64_t node_bytes = (int64_t)L.r * nch * 8;
         auto add = [&](int j0, int j1, int c0, int c1) {
             if (P.num_r == kMaxRPieces) return false;
@@ -983,9 +1144,11 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     std::vector<uint8_t> arena(in.arena_bytes);
     if (cudaMemcpy(arena.data(), in.d_arena, in.arena_bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
         return HODLR_OK;
-    std::vector<uint8_t> slab((size_t)P.slab_bytes * nleaves, 0);
+    std::vector<uint8_t> slab((size_t)slab_total, 0);
     for (int leaf = 0; leaf < nleaves; ++leaf) {
-        uint8_t* out = slab.data() + (size_t)leaf * P.slab_bytes;
+        uint8_t* out_v = slab.data() + (size_t)leaf * P.vs_bytes;
+        uint8_t* out_d = slab.data() + P.d_region + (size_t)leaf * P.ds_bytes;
+        uint8_t* out_u = slab.data() + P.u_region + (size_t)leaf * P.us_bytes;
         for (int g = 0; g < 5; ++g) {
             const int w = fmt_bytes(g);
             int col = 0;
@@ -998,9 +1161,9 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
                     const uint8_t* vsrc = arena.data() + nd.v_off + ((int64_t)c * nd.v_ld + roff) * w;
                     const uint8_t* usrc = arena.data() + nd.u_off + ((int64_t)c * nd.u_ld + roff) * w;
                     for (int r = 0; r < kM; ++r)  // V' row-major
-                        memcpy(out + P.vgoff[g] + ((int64_t)r * P.vpad[g] + col) * w, vsrc + (int64_t)r * w, (size_t)w);
+                        memcpy(out_v + P.vgoff[g] + ((int64_t)r * P.vpad[g] + col) * w, vsrc + (int64_t)r * w, (size_t)w);
                     for (int rb = 0; rb < kM / kRB; ++rb)  // U column-major per 64-row block
-                        memcpy(out + P.us_off + rb * P.ublock_bytes + P.ugoff[g] + (int64_t)col * kRB * w,
+                        memcpy(out_u + rb * P.ublock_bytes + P.ugoff[g] + (int64_t)col * kRB * w,
                                usrc + (int64_t)rb * kRB * w, (size_t)kRB * w);
                 }
             }
@@ -1009,7 +1172,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         for (int rb = 0; rb < kM / kRB; ++rb)
             for (int c = 0; c < kM; ++c)
                 for (int r = 0; r < kRB; ++r)
-                    memcpy(out + P.ds_off + rb * P.dblock_bytes + ((int64_t)c * kRB + r) * dsz,
+                    memcpy(out_d + rb * P.dblock_bytes + ((int64_t)c * kRB + r) * dsz,
                            dsrc + ((int64_t)(rb * kRB + r) * kM + c) * dsz, (size_t)dsz);
     }
     int dev = 0, sms = 0, coop = 0;
@@ -1080,8 +1243,36 @@ cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* 
     a.sync = (SvSync*)e;
     a.partial = (W*)(e + sv_sync_bytes(P.nleaves));
     a.tbuf = (W*)(e + sv_sync_bytes(P.nleaves) + sv.part_count * 8);
+    a.trace = nullptr;
+#ifdef HODLR_TRACE
+    static unsigned long long* trace_buf = nullptr;
+    static int trace_cap = 0;
+    if (trace_cap < sv.grid) {
+        if (trace_buf) cudaFree(trace_buf);
+        cudaMalloc(&trace_buf, (size_t)sv.grid * 48 * 8);
+        trace_cap = sv.grid;
+    }
+    cudaMemsetAsync(trace_buf, 0, (size_t)sv.grid * 48 * 8, st);
+    a.trace = trace_buf;
+#endif
     void* args[] = {(void*)&P, &a};
-    return cudaLaunchKernel((const void*)k_stream<W>, dim3(sv.grid), dim3(kThreads), args, smem_bytes(), st);
+    cudaError_t err = cudaLaunchKernel((const void*)k_stream<W>, dim3(sv.grid), dim3(kThreads), args, smem_bytes(), st);
+#ifdef HODLR_TRACE
+    if (err == cudaSuccess) {
+        std::vector<unsigned long long> h((size_t)sv.grid * 48);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost);
+        if (const char* f = getenv("HODLR_B200_TRACE_FILE")) {
+            if (FILE* fp = fopen(f, "wb")) {
+                int hdr[4] = {sv.grid, 48, P.num_a, P.num_r};
+                fwrite(hdr, sizeof(hdr), 1, fp);
+                fwrite(h.data(), 8, h.size(), fp);
+                fclose(fp);
+            }
+        }
+    }
+#endif
+    return err;
 }
 
 template cudaError_t sv_matvec<double>(const PlanView&, const SvPlan&, const double*, double*, double*, double*,
