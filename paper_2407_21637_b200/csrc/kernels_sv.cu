@@ -113,10 +113,13 @@ struct Level {
     int64_t tbase;      // coefficient buffer base
 };
 
-// A queue item (leaf, piece): rows [r0, r0 + nrows) of format group g's V'
-// sub-slab; chunk = index of the piece inside its group (npc pieces per group).
+// A piece: rows [r0, r0 + nrows) of format group g's V' sub-slab.  A queue
+// item is one piece (few leaves per CTA: the A phase spreads over every CTA)
+// or a whole leaf (many leaves: 1/npc the partials).  Partials of a group are
+// written at its item's last piece of that group (last_of_group), into slot
+// chunk of npc slots per leaf.
 struct APiece {
-    int32_t g, r0, nrows, chunk, npc, pad;
+    int32_t g, r0, nrows, chunk, npc, last_of_group;
 };
 
 // U chunk of a BC item: columns [c0, c0 + ncols) of format group g.
@@ -136,6 +139,7 @@ struct SvParams {
     int32_t leaf_fmt;
     int32_t num_a, num_d, num_r, pos_r;   // queue: BC items with the R pieces at pos_r
     int32_t napieces;
+    int32_t a_group;                      // pieces per A queue item: 1 or napieces (whole leaf)
     int32_t dpieces_w[2], dcols_w[2];      // phase-B pieces per item / columns per piece, [fp32, fp64 working]
     // three regions, leaf-major inside each: [V' of every leaf][D blocks][U blocks]
     int64_t vs_bytes, ds_bytes, us_bytes;  // per leaf
@@ -594,31 +598,34 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             n1 = n2;
             if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);
             if (q < P.num_a) {
-                // ---- A: partial V'^T x of one (leaf, row chunk of a format group)
-                const int leaf = q / P.napieces, p = q - leaf * P.napieces;
+                // ---- A: partial V'^T x of one (leaf, piece) or one whole leaf
+                const int per_leaf = P.napieces / P.a_group;
+                const int leaf = q / per_leaf, p0 = (q - leaf * per_leaf) * P.a_group;
                 const uint8_t* base = a.slab + (int64_t)leaf * P.vs_bytes;
-                const APiece ap = P.ap[p];
                 ++a_items;
-                uint8_t* st = claim();
-                const unsigned cb = (unsigned)(ap.nrows * P.vpad[ap.g] * fmt_sz(ap.g));
-                const unsigned xb = (unsigned)(ap.nrows * sizeof(W));
-                if (lane == 0) {
-                    PieceHdr& h = C.hdr[stage];
-                    h.type = PT_A;
-                    h.leaf = leaf;
-                    h.a = p;
-                    // 2 = this CTA's last A piece (the next queue entry is not A):
-                    // its consumers then publish the CTA's A pieces GPU-wide
-                    h.last = n1 >= P.num_a ? 2 : 1;
-                    mbar_arrive_tx(&C.full[stage], xb + cb);
-                    bulk_g2s(st, a.x + (int64_t)leaf * kM + ap.r0, xb, &C.full[stage]);
-                    bulk_g2s_stream(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.r0 * P.vpad[ap.g] * fmt_sz(ap.g), cb,
-                                    &C.full[stage], pol);
-                    TR(2);
-                    TRV(11, a_items);
+                for (int p = p0; p < p0 + P.a_group; ++p) {
+                    const APiece ap = P.ap[p];
+                    uint8_t* st = claim();
+                    const unsigned cb = (unsigned)(ap.nrows * P.vpad[ap.g] * fmt_sz(ap.g));
+                    const unsigned xb = (unsigned)(ap.nrows * sizeof(W));
+                    if (lane == 0) {
+                        PieceHdr& h = C.hdr[stage];
+                        h.type = PT_A;
+                        h.leaf = leaf;
+                        h.a = p;
+                        // item end: 1; 2 = also this CTA's last A item (the next queue
+                        // entry is not A): its consumers then publish the CTA's A items
+                        h.last = p + 1 < p0 + P.a_group ? 0 : n1 >= P.num_a ? 2 : 1;
+                        mbar_arrive_tx(&C.full[stage], xb + cb);
+                        bulk_g2s(st, a.x + (int64_t)leaf * kM + ap.r0, xb, &C.full[stage]);
+                        bulk_g2s_stream(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.r0 * P.vpad[ap.g] * fmt_sz(ap.g),
+                                        cb, &C.full[stage], pol);
+                        TR(2);
+                        TRV(11, a_items);
+                    }
+                    __syncwarp();
+                    next_stage();
                 }
-                __syncwarp();
-                next_stage();
                 continue;
             }
             const int qq = q - P.num_a;
@@ -761,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 split[0] += clock64() - ts0;
                 ts0 = clock64();
 #endif
-                {
+                if (ap.last_of_group) {
                     // combine the warps' column sums in warp order, write the partials
                     W* red = reinterpret_cast<W*>(st);
                     const int vp = P.vpad[ap.g];
@@ -889,14 +896,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                     scratch = true;
                 }
             }
-            if (scratch && (h.type == PT_A || h.type == PT_R)) {
+            if (scratch && ((h.type == PT_A && h.last) || h.type == PT_R)) {
                 consumer_sync();  // scratch reads and the item's global stores are done
                 // Publish GPU-wide from a consumer thread (it has no bulk copies
                 // in flight, so its fence does not wait for the ring's loads):
                 // all of this CTA's A pieces at once after its last one, every
                 // R piece.  Release pattern: CTA barrier, fence.acq_rel.gpu,
                 // relaxed reduction; readers ld.acquire the counter.
-                if (h.type == PT_A) ++my_a;
+                if (h.type == PT_A && h.last) ++my_a;
                 if (ctid == 0 && ((h.type == PT_A && h.last == 2) || h.type == PT_R)) {
                     if (h.type == PT_A) TR(16); else TR(18);
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -1056,7 +1063,22 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         for (int r0 = 0; r0 < kM; r0 += rows) {
             if (P.napieces == kMaxPieces) return HODLR_OK;
             const int nr = std::min(rows, kM - r0);
-            P.ap[P.napieces++] = APiece{g, r0, nr, r0 / rows, (kM + rows - 1) / rows, 0};
+            P.ap[P.napieces++] = APiece{g, r0, nr, r0 / rows, (kM + rows - 1) / rows, r0 + nr == kM};
+        }
+    }
+    // A items: single pieces while leaves are scarce (cfg2: 256 leaves for ~300
+    // CTAs), whole leaves once every CTA gets a few (1/npc the partials)
+    int sms_now = 148, dev_now = 0;
+    cudaGetDevice(&dev_now);
+    cudaDeviceGetAttribute(&sms_now, cudaDevAttrMultiProcessorCount, dev_now);
+    P.a_group = nleaves >= 2 * kCtasPerSm * sms_now ? P.napieces : 1;
+    if (getenv("HODLR_B200_A_GROUP")) P.a_group = atoi(getenv("HODLR_B200_A_GROUP")) > 1 ? P.napieces : 1;
+    for (int i = 0; i < P.napieces; ++i) {
+        if (P.a_group > 1) {
+            P.ap[i].chunk = 0;
+            P.ap[i].npc = 1;
+        } else {
+            P.ap[i].last_of_group = 1;
         }
     }
     // partials: per level [node][column][cst], entries (leaf of node, chunk) in
@@ -1107,7 +1129,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         }
         if (P.nupieces == 0) return HODLR_OK;
     }
-    P.num_a = nleaves * P.napieces;
+    P.num_a = nleaves * (P.napieces / P.a_group);
     P.num_d = nleaves * (kM / kRB);
     // node-reduction pieces (R items): a level's partials are [node][column][leaf]
     P.num_r = 0;
