@@ -288,12 +288,16 @@ def build_adaptive(source, tree, eps: float, working=FP64, available=(), svd_cac
         fmt = chosen[k - 1]
         row = []
         shared = None
+        batch = None
+        if hasattr(source, "compress_level") and not same_blocks_per_level:
+            rects = [(*lvl[2 * i], *lvl[2 * i + 1]) for i in range(2 ** (k - 1))]
+            batch = source.compress_level(rects, eps, svd_cache)
         for i in range(2 ** (k - 1)):
             if same_blocks_per_level and shared is not None:
                 row.append(shared)
                 continue
             (a, b), (c, d) = lvl[2 * i], lvl[2 * i + 1]
-            Uu, Vu = source.compress(a, b, c, d, eps, svd_cache)
+            Uu, Vu = batch[i] if batch is not None else source.compress(a, b, c, d, eps, svd_cache)
             if symmetric:
                 # lower = upper^T = (V/s)(s)(U)^T : re-normalise so lower.U is orthonormal
                 if gpu:

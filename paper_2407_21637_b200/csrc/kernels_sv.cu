@@ -77,6 +77,7 @@ constexpr int kMaxPieces = 32;          // phase-A pieces per leaf
 #endif
 constexpr int kMaxCols = HODLR_MAX_COLS;  // columns (sum of ranks) per leaf
 constexpr int kXB = 2048;               // x segment of an A piece (<= 256 rows)
+constexpr int kMaxAG = 12;              // phase-A column groups
 
 enum { PT_A = 1, PT_D = 2, PT_U = 3, PT_R = 5, PT_END = 4 };
 
@@ -119,7 +120,14 @@ struct Level {
 // written at its item's last piece of that group (last_of_group), into slot
 // chunk of npc slots per leaf.
 struct APiece {
-    int32_t g, r0, nrows, chunk, npc, last_of_group;
+    int32_t g, r0, nrows, chunk, npc, last_of_group;  // g: A group (index into SvParams::ag)
+};
+
+// Phase-A column group: whole levels of one storage format, <= 256 columns
+// (lanes own <= 2 column quads), stored as a row-major M x vpad V' sub-slab.
+struct AGroup {
+    int32_t fmt, c0, ncols, vpad;  // c0: first column inside the format's flat list
+    int64_t voff;                  // sub-slab offset inside a leaf's V' region
 };
 
 // U chunk of a BC item: columns [c0, c0 + ncols) of format group g.
@@ -145,8 +153,10 @@ struct SvParams {
     int64_t vs_bytes, ds_bytes, us_bytes;  // per leaf
     int64_t d_region, u_region;            // region offsets (the V' region starts at 0)
     int64_t dblock_bytes, ublock_bytes;
-    int32_t gcols[5], vpad[5];
-    int64_t vgoff[5], ugoff[5];           // V' sub-slab offsets / U sub-block offsets in a block
+    int32_t gcols[5];                     // columns per storage format (U block, flat index)
+    int64_t ugoff[5];                     // U sub-block offsets in a block
+    AGroup ag[kMaxAG];                    // V' sub-slabs (phase A column groups)
+    int32_t nag;
     int32_t coef_elems;
     int32_t u_data_off[2];                // U piece: coefficients, then the U chunk
     int32_t nupieces;                     // U pieces per BC item (column chunks of the U block)
@@ -606,7 +616,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 for (int p = p0; p < p0 + P.a_group; ++p) {
                     const APiece ap = P.ap[p];
                     uint8_t* st = claim();
-                    const unsigned cb = (unsigned)(ap.nrows * P.vpad[ap.g] * fmt_sz(ap.g));
+                    const AGroup& G = P.ag[ap.g];
+                    const unsigned cb = (unsigned)(ap.nrows * G.vpad * fmt_sz(G.fmt));
                     const unsigned xb = (unsigned)(ap.nrows * sizeof(W));
                     if (lane == 0) {
                         PieceHdr& h = C.hdr[stage];
@@ -618,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                         h.last = p + 1 < p0 + P.a_group ? 0 : n1 >= P.num_a ? 2 : 1;
                         mbar_arrive_tx(&C.full[stage], xb + cb);
                         bulk_g2s(st, a.x + (int64_t)leaf * kM + ap.r0, xb, &C.full[stage]);
-                        bulk_g2s_stream(st + kXB, base + P.vgoff[ap.g] + (int64_t)ap.r0 * P.vpad[ap.g] * fmt_sz(ap.g),
+                        bulk_g2s_stream(st + kXB, base + G.voff + (int64_t)ap.r0 * G.vpad * fmt_sz(G.fmt),
                                         cb, &C.full[stage], pol);
                         TR(2);
                         TRV(11, a_items);
@@ -763,7 +774,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
 #ifdef HODLR_TRACE
                 ts0 = clock64();
 #endif
-                a_piece<W>(ap.g, st + kXB, ap.nrows, P.vpad[ap.g], reinterpret_cast<const W*>(st), cw, lane, aacc);
+                const AGroup& G = P.ag[ap.g];
+                a_piece<W>(G.fmt, st + kXB, ap.nrows, G.vpad, reinterpret_cast<const W*>(st), cw, lane, aacc);
 #ifdef HODLR_TRACE
                 split[0] += clock64() - ts0;
                 ts0 = clock64();
@@ -771,7 +783,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 if (ap.last_of_group) {
                     // combine the warps' column sums in warp order, write the partials
                     W* red = reinterpret_cast<W*>(st);
-                    const int vp = P.vpad[ap.g];
+                    const int vp = G.vpad;
                     consumer_sync();
 #pragma unroll
                     for (int i = 0; i < 2; ++i) {
@@ -781,11 +793,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                             for (int e = 0; e < 4; ++e) red[cw * vp + 4 * qq + e] = aacc[i][e];
                     }
                     consumer_sync();
-                    for (int c = ctid; c < P.gcols[ap.g]; c += kConsumers * 32) {
+                    for (int c = ctid; c < G.ncols; c += kConsumers * 32) {
                         W s = red[c];
 #pragma unroll
                         for (int w = 1; w < kConsumers; ++w) s += red[w * vp + c];
-                        const int flat = P.gstart[ap.g] + c;
+                        const int flat = P.gstart[G.fmt] + G.c0 + c;
                         const int sh = C.psh_c[flat];
                         const int jn = h.leaf >> sh;
                         a.partial[(int64_t)C.pbase_c[flat] + (int64_t)jn * C.pstride_c[flat] +
@@ -990,14 +1002,15 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     for (int k = 1; k <= depth; ++k) {
         const int base = (1 << k) - 2;
         const NodeDesc& n0 = nodes[base];
-        for (int j = 0; j < (1 << k); ++j) {
+        int rmax = 0;
+        for (int j = 0; j < (1 << k); ++j) {  // ranks may differ per block: padded to the level max
             const NodeDesc& nd = nodes[base + j];
-            if (nd.level != k || nd.ext_slot >= 0 || nd.rv != n0.rv || nd.ru != n0.rv || nd.u_fmt != n0.u_fmt ||
-                nd.v_fmt != n0.u_fmt || nd.nchunk != (1 << (depth - k)) || nd.row0 != j * (kM << (depth - k)) ||
-                nd.part_off != n0.part_off + (int64_t)j * n0.rv * n0.nchunk)
+            if (nd.level != k || nd.ext_slot >= 0 || nd.u_fmt != n0.u_fmt || nd.v_fmt != n0.u_fmt ||
+                nd.nchunk != (1 << (depth - k)) || nd.row0 != j * (kM << (depth - k)))
                 return HODLR_OK;
+            rmax = std::max(rmax, std::max(nd.rv, nd.ru));
         }
-        P.lev[k - 1].r = n0.rv;
+        P.lev[k - 1].r = rmax;
         P.lev[k - 1].fmt = n0.u_fmt;
     }
     // column lists per format group (level-major inside a group)
@@ -1016,9 +1029,28 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
             }
         }
         P.gcols[g] = cnt;
-        P.vpad[g] = (cnt + 3) / 4 * 4;
-        if (P.vpad[g] > 256) return HODLR_OK;  // phase-A lanes own <= 2 x 32 column quads
     }
+    // phase-A column groups: whole levels of one format, <= 256 columns each
+    P.nag = 0;
+    int lev_ag[kMaxLev];
+    for (int k = 0; k < depth; ++k) lev_ag[k] = -1;
+    for (int g = 0; g < 5; ++g) {
+        int c0 = 0, cur = -1;
+        for (int k = 0; k < depth; ++k) {
+            if (P.lev[k].fmt != g || P.lev[k].r == 0) continue;
+            const int r = P.lev[k].r;
+            if (r > 256) return HODLR_OK;
+            if (cur < 0 || P.ag[cur].ncols + r > 256) {
+                if (P.nag == kMaxAG) return HODLR_OK;
+                cur = P.nag++;
+                P.ag[cur] = AGroup{g, c0, 0, 0, 0};
+            }
+            P.ag[cur].ncols += r;
+            lev_ag[k] = cur;
+            c0 += r;
+        }
+    }
+    for (int i = 0; i < P.nag; ++i) P.ag[i].vpad = (P.ag[i].ncols + 3) / 4 * 4;
     P.gstart[5] = (int16_t)flat;
     if (flat == 0) return HODLR_OK;  // all ranks zero: generic path
     // coefficient slots and partial / coefficient buffers
@@ -1036,9 +1068,9 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     // slab geometry
     const int dsz = fmt_bytes(lf);
     int64_t vs = 0;
-    for (int g = 0; g < 5; ++g) {
-        P.vgoff[g] = vs;
-        vs += (int64_t)kM * P.vpad[g] * fmt_bytes(g);
+    for (int i = 0; i < P.nag; ++i) {
+        P.ag[i].voff = vs;
+        vs += (int64_t)kM * P.ag[i].vpad * fmt_bytes(P.ag[i].fmt);
     }
     P.dblock_bytes = (int64_t)kM * kRB * dsz;
     int64_t ub = 0;
@@ -1055,9 +1087,8 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     const int64_t slab_total = P.u_region + (int64_t)nleaves * P.us_bytes;
     // phase-A pieces: row blocks of each format's V' sub-slab (multiples of 8 rows)
     P.napieces = 0;
-    for (int g = 0; g < 5; ++g) {
-        if (P.gcols[g] == 0) continue;
-        int rows = (kStage - kXB) / (P.vpad[g] * fmt_bytes(g));
+    for (int g = 0; g < P.nag; ++g) {
+        int rows = (kStage - kXB) / (P.ag[g].vpad * fmt_bytes(P.ag[g].fmt));
         rows = std::min(kM, rows / 8 * 8);
         if (rows < 8) return HODLR_OK;
         for (int r0 = 0; r0 < kM; r0 += rows) {
@@ -1087,7 +1118,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         Level& L = P.lev[k];
         L.npc = 0;
         for (int i = 0; i < P.napieces; ++i)
-            if (P.ap[i].g == L.fmt) L.npc = P.ap[i].npc;
+            if (P.ap[i].g == lev_ag[k]) L.npc = P.ap[i].npc;
         if (L.r > 0 && L.npc == 0) return HODLR_OK;
         L.cst = (int)(((int64_t)(nleaves >> (k + 1)) * std::max(L.npc, 1) + 3) / 4 * 4);
         L.pbase = pb;
@@ -1095,8 +1126,8 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     }
     if (pb >= (int64_t(1) << 31)) return HODLR_OK;  // int32 partial indices in shared tables
     // reduction scratch in an A piece's stage: kConsumers x vpad values
-    for (int g = 0; g < 5; ++g)
-        if ((size_t)kConsumers * P.vpad[g] * 8 > (size_t)kStage) return HODLR_OK;
+    for (int g = 0; g < P.nag; ++g)
+        if ((size_t)kConsumers * P.ag[g].vpad * 8 > (size_t)kStage) return HODLR_OK;
     // phase-B pieces: column blocks of a 64-row block
     // [x segment: dcols working values][dcols D columns]; balanced pieces
     for (int wi = 0; wi < 2; ++wi) {
@@ -1173,20 +1204,26 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
         uint8_t* out_u = slab.data() + P.u_region + (size_t)leaf * P.us_bytes;
         for (int g = 0; g < 5; ++g) {
             const int w = fmt_bytes(g);
-            int col = 0;
+            int col = 0;  // flat column inside format g (levels padded to their max rank)
             for (int k = 0; k < depth; ++k) {
-                if (P.lev[k].fmt != g) continue;
+                if (P.lev[k].fmt != g || P.lev[k].r == 0) continue;
                 const int lvl = k + 1;
                 const NodeDesc& nd = nodes[(1 << lvl) - 2 + (leaf >> (depth - lvl))];
                 const int64_t roff = (int64_t)leaf * kM - nd.row0;
-                for (int c = 0; c < nd.rv; ++c, ++col) {
-                    const uint8_t* vsrc = arena.data() + nd.v_off + ((int64_t)c * nd.v_ld + roff) * w;
-                    const uint8_t* usrc = arena.data() + nd.u_off + ((int64_t)c * nd.u_ld + roff) * w;
-                    for (int r = 0; r < kM; ++r)  // V' row-major
-                        memcpy(out_v + P.vgoff[g] + ((int64_t)r * P.vpad[g] + col) * w, vsrc + (int64_t)r * w, (size_t)w);
-                    for (int rb = 0; rb < kM / kRB; ++rb)  // U column-major per 64-row block
-                        memcpy(out_u + rb * P.ublock_bytes + P.ugoff[g] + (int64_t)col * kRB * w,
-                               usrc + (int64_t)rb * kRB * w, (size_t)kRB * w);
+                const AGroup& G = P.ag[lev_ag[k]];
+                for (int c = 0; c < P.lev[k].r; ++c, ++col) {
+                    if (c < nd.rv) {  // V' row-major inside the level's A group
+                        const uint8_t* vsrc = arena.data() + nd.v_off + ((int64_t)c * nd.v_ld + roff) * w;
+                        for (int r = 0; r < kM; ++r)
+                            memcpy(out_v + G.voff + ((int64_t)r * G.vpad + (col - G.c0)) * w, vsrc + (int64_t)r * w,
+                                   (size_t)w);
+                    }
+                    if (c < nd.ru) {  // U column-major per 64-row block
+                        const uint8_t* usrc = arena.data() + nd.u_off + ((int64_t)c * nd.u_ld + roff) * w;
+                        for (int rb = 0; rb < kM / kRB; ++rb)
+                            memcpy(out_u + rb * P.ublock_bytes + P.ugoff[g] + (int64_t)col * kRB * w,
+                                   usrc + (int64_t)rb * kRB * w, (size_t)kRB * w);
+                    }
                 }
             }
         }

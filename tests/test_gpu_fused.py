@@ -120,16 +120,35 @@ def test_cfg1_built_by_harness_matches_reference_golden(cuda):
     assert beta <= 10 * matvec_bound(4, 1e-8)
 
 
-def test_variable_ranks_take_generic_path(cuda):
-    """Per-block ranks that differ inside a level (the cfg3 situation) are served
-    by the generic kernels; results still match the oracle."""
+@pytest.mark.parametrize("working", ["fp64", "fp32"])
+def test_variable_ranks_fused(cuda, working):
+    """Per-block ranks that differ inside a level (the cfg3 situation): the
+    leaf slabs pad each level to its largest rank with zero columns; the fused
+    kernel serves it and matches the oracle and the generic kernels."""
     torch = cuda
-    H = random_hodlr(2048, 3, ["fp32", "bf16", "q52"], [(1, 24), (0, 17), (3, 9)], "fp64", seed=11)
+    H = random_hodlr(2048, 3, ["fp32", "bf16", "q52"], [(1, 24), (0, 17), (3, 9)], working, seed=11)
     op = make_op(H)
-    assert op.launches_per_matvec == 3
+    assert op.launches_per_matvec == 1
+    gen = make_op(H, fused=False)
     x = np.random.default_rng(5).standard_normal(H.n)
-    b = op.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
-    assert rel(b, matvec_oracle(H, x)) <= 1e-12
+    dt = torch.float64 if working == "fp64" else torch.float32
+    xd = torch.from_numpy(x).cuda().to(dt)
+    b = op.matvec(xd).double().cpu().numpy()
+    xw = x.astype(np.float32).astype(np.float64) if working == "fp32" else x
+    assert rel(b, matvec_oracle(H, xw)) <= (1e-12 if working == "fp64" else 1e-5)
+    assert rel(b, gen.matvec(xd).double().cpu().numpy()) <= (1e-13 if working == "fp64" else 1e-6)
+
+
+def test_wide_levels_split_into_column_groups(cuda):
+    """More than 256 columns of one format per leaf (cfg3 has ~340 fp32
+    columns): phase A runs over several column groups."""
+    torch = cuda
+    H = random_hodlr(4096, 4, ["fp32"] * 4, [120, 100, 80, 60], "fp32", seed=12)
+    op = make_op(H)
+    assert op.launches_per_matvec == 1
+    x = np.random.default_rng(6).standard_normal(H.n).astype(np.float32).astype(np.float64)
+    b = op.matvec(torch.from_numpy(x).cuda().float()).double().cpu().numpy()
+    assert rel(b, matvec_oracle(H, x)) <= 1e-5
 
 
 @pytest.mark.parametrize("depth", [1, 2, 5])
