@@ -13,6 +13,7 @@
 #include "../../include/hodlr_b200.h"
 #include "formats.cuh"
 #include "kernels.h"
+#include "mrhs.h"
 #include "plan.h"
 #include "sv.h"
 
@@ -81,6 +82,7 @@ struct hodlr_handle {
     PlanView view{};
     bool sv_ok = false;  // single-vector fast path usable
     SvPlan sv{};
+    MrPlan mr{};  // multi-RHS tensor-core path
     std::mutex mu;
 };
 
@@ -339,7 +341,9 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
         seg_byte_off[f] = (int64_t)off;
         off += round_up(seg_elems[f] * fmt_bytes(f), kAlign);
     }
-    h->arena_bytes = std::max<size_t>(off, kAlign);
+    // + slack: 4-element vector loads at a column's ragged end may touch up to
+    // 15 elements past it (the values are masked, the addresses must be valid)
+    h->arena_bytes = std::max<size_t>(off, kAlign) + kAlign;
     for (LeafDesc& l : h->leaves) l.off *= fmt_bytes(d->leaf_fmt);
     for (NodeDesc& nd : h->nodes) {
         nd.u_off = seg_byte_off[nd.u_fmt] + nd.u_off * fmt_bytes(nd.u_fmt);
@@ -446,6 +450,12 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
     v.t_count = h->t_count;
     v.ext_count = h->ext_count;
 
+    {
+        MrInput mi{&h->nodes, &h->chunks, &h->leaves, &h->chunk_nodes, nlev, d->leaf_fmt, device};
+        if (mr_prepare(mi, h->mr) != HODLR_OK) return cleanup(fail(HODLR_ERR_CUDA, "multi-RHS plan upload failed"));
+        const char* no_mr = getenv("HODLR_B200_DISABLE_MRHS");
+        if (no_mr && no_mr[0] == '1') mr_release(h->mr);
+    }
     const char* no_sv = getenv("HODLR_B200_DISABLE_FUSED");
     if (!(no_sv && no_sv[0] == '1')) {
         // sharded handles: the fused kernel runs the rank's subtree (levels
@@ -477,6 +487,10 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
 // Workspace: [fused-path sync state (fixed offset 0, must start zeroed)]
 //            [partials: part_count*s][coefficients: t_count*s]
 //            [sharded only: k_ext_v per-block partials | discarded send | ticket]
+// partial sums: the generic layout or the multi-RHS slot layout, whichever is larger
+int64_t part_elems(const hodlr_handle* h, int64_t s) {
+    return std::max<int64_t>(h->part_count * s, h->mr.ok ? mr_part_elems(h->mr, s) : 0);
+}
 template <typename W>
 size_t ext_ws_bytes(const hodlr_handle* h, int64_t s) {
     if (h->nranks == 1 || h->ext_count == 0) return 0;
@@ -486,7 +500,7 @@ size_t ext_ws_bytes(const hodlr_handle* h, int64_t s) {
 template <typename W>
 size_t ws_bytes_for(const hodlr_handle* h, int64_t s) {
     return (size_t)round_up((int64_t)sv_extra_ws(h->sv, s), kAlign) +
-           (size_t)round_up((h->part_count * s) * sizeof(W), kAlign) +
+           (size_t)round_up(part_elems(h, s) * sizeof(W), kAlign) +
            (size_t)round_up((h->t_count * s) * sizeof(W), kAlign) + ext_ws_bytes<W>(h, s);
 }
 
@@ -498,7 +512,7 @@ void carve(const hodlr_handle* h, int64_t s, void* ws, W** partial, W** tbuf, vo
     *extra = p;
     p += round_up((int64_t)sv_extra_ws(h->sv, s), kAlign);
     *partial = (W*)p;
-    p += round_up((h->part_count * s) * sizeof(W), kAlign);
+    p += round_up(part_elems(h, s) * sizeof(W), kAlign);
     *tbuf = (W*)p;
 }
 
@@ -552,6 +566,8 @@ hodlr_status run_local(hodlr_handle* h, const W* x, int64_t ldx, W* b, int64_t l
     cudaError_t e;
     if (h->sv_ok && s == 1 && ldx == 1 && ldb == 1 && h->nranks == 1) {
         e = sv_matvec<W>(h->view, h->sv, x, b, partial, tbuf, extra, st);
+    } else if (h->nranks == 1 && mr_usable(h->mr, sizeof(W) == 8 ? HODLR_FMT_FP64 : HODLR_FMT_FP32)) {
+        e = mr_matvec<W>(h->view, h->mr, 0, x, ldx, b, ldb, s, partial, tbuf, st);
     } else {
         e = gen_begin<W>(h->view, x, ldx, s, partial, tbuf, nullptr, st);
         if (e == cudaSuccess) e = gen_end<W>(h->view, x, ldx, tbuf, b, ldb, s, h->max_chunk_rows, st);
@@ -567,6 +583,10 @@ cudaError_t shard_local_impl(hodlr_handle* h, const W* x, int64_t ldx, W* b, int
     void* extra;
     carve<W>(h, s, ws, &partial, &tbuf, &extra);
     if (h->sv_ok && s == 1 && ldx == 1 && ldb == 1) return sv_matvec<W>(h->view, h->sv, x, b, partial, tbuf, extra, st);
+    // multi-RHS kernels over the subtree levels (L+1..l) and the leaves; the
+    // external levels are added by shard_end
+    if (mr_usable(h->mr, sizeof(W) == 8 ? HODLR_FMT_FP64 : HODLR_FMT_FP32))
+        return mr_matvec<W>(h->view, h->mr, h->L, x, ldx, b, ldb, s, partial, tbuf, st);
     // generic: the whole local plan with the external coefficients set to 0
     // (their products add exact zeros); the external partials go to a
     // discarded buffer, shard_begin owns the real ones.
@@ -602,7 +622,26 @@ hodlr_status hodlr_destroy(hodlr_handle* h) {
     h->ws.release();
     h->e2e.release();
     sv_release(h->sv);
+    mr_release(h->mr);
     delete h;
+    return HODLR_OK;
+}
+
+hodlr_status hodlr_matvec_path(const hodlr_handle* h, int32_t working, int64_t s, int32_t* path,
+                               int32_t* launches) {
+    if (!h || !path || !launches || s < 1) return fail(HODLR_ERR_INVALID, "bad arguments");
+    hodlr_status st = check_working(working);
+    if (st != HODLR_OK) return st;
+    if (h->sv_ok && s == 1) {
+        *path = HODLR_PATH_FUSED_SV;
+        *launches = sv_launches(h->sv);
+    } else if (mr_usable(h->mr, working)) {
+        *path = HODLR_PATH_MRHS;
+        *launches = mr_launches();
+    } else {
+        *path = HODLR_PATH_GENERIC;
+        *launches = 3;
+    }
     return HODLR_OK;
 }
 

@@ -1,0 +1,88 @@
+// Multi-right-hand-side (s > 1) path: the batched U/V application and the
+// leaf products as dense contractions on the tensor cores (SURVEY.md §7.1
+// step 5; north star "tensor cores only in the multi-RHS mode").
+//
+// Three stream-ordered launches per matvec over the level-batched arena of
+// plan.h (no separate layout):
+//   MA  persistent-range phase A: CTA b owns a contiguous run of chunks (row
+//       tiles) and accumulates V'_k[rows]^T X[rows] for every level k in
+//       shared memory while consecutive chunks stay inside one level-k node;
+//       a node boundary (or the end of the run) flushes the tile to a partial
+//       slot (level k, slot = b + index of the node in its level).
+//   MR  fixed-order reduction of a node's slots (CTA order) -> T_k
+//       (deterministic; no atomics anywhere).
+//   MB  one CTA per chunk: b[rows] = [D | U_1 .. U_l] [X_leaf ; T_1 .. T_l],
+//       i.e. the leaf product and every level's U T as ONE contraction with
+//       K = m + sum_k r_k, written once (disjoint rows).
+// Tensor-core kinds: fp64 working -> DMMA (mma.sync m8n8k4 f64, the B200's
+// FP64 tensor path); fp32 working -> TF32 with a hi/lo split of both operands
+// (3 products, "3xTF32"), which keeps fp32-level accuracy.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "../../include/hodlr_b200.h"
+#include "plan.h"
+
+namespace hodlr {
+
+constexpr int kMrMaxLevels = 31;
+
+struct MrLevel {
+    int32_t node0, nnodes;   // node ids of the level: [node0, node0 + nnodes)
+    int32_t rv_max, ru_max;  // max ranks over the level's nodes
+    int32_t rv_pad;          // rv_max rounded up to 8: rows of one partial slot
+    int32_t pad_;
+    int64_t part_rows;       // first partial row of the level (a row holds spad values)
+};
+
+// Per node id: the phase-A CTAs whose chunk runs intersect the node, its index
+// within its level, and its level (0-based).
+struct MrSlot {
+    int32_t b0, b1, jrel, lv;
+};
+
+struct MrView {
+    int32_t nlev;            // levels 0..nlev-1 = tree levels 1..nlev
+    int32_t nb;              // phase-A CTAs; slots per level = nb + nnodes
+    int64_t part_rows;       // total partial rows (x spad values)
+    const MrSlot* slots;     // device, indexed by node id
+    MrLevel lev[kMrMaxLevels];
+};
+
+struct MrPlan {
+    bool ok = false;
+    bool has_fp64_operand = false;  // an fp64 factor or leaf: the TF32 kind cannot take it
+    int leaf_fmt = HODLR_FMT_FP64;
+    MrView view{};
+    void* dev = nullptr;
+    int max_leaf_m = 0;
+};
+
+struct MrInput {
+    const std::vector<NodeDesc>* nodes;
+    const std::vector<ChunkDesc>* chunks;
+    const std::vector<LeafDesc>* leaves;
+    const std::vector<int32_t>* chunk_nodes;
+    int nlev;
+    int leaf_fmt;
+    int device;
+};
+
+hodlr_status mr_prepare(const MrInput& in, MrPlan& mr);
+void mr_release(MrPlan& mr);
+inline int64_t mr_spad(int64_t s) { return (s + 7) / 8 * 8; }
+// partial elements needed for s right-hand sides
+inline int64_t mr_part_elems(const MrPlan& mr, int64_t s) { return mr.view.part_rows * mr_spad(s); }
+// true if the multi-RHS kernels take this call
+bool mr_usable(const MrPlan& mr, int working_fmt);
+int mr_launches();
+// Levels lev_lo..nlev-1 only (lev_lo = L on a sharded handle: the external
+// levels run in kernels_shard.cu).  `send` receives external-level sums when
+// lev_lo = 0 on a sharded handle (unused otherwise).
+template <typename W>
+cudaError_t mr_matvec(const PlanView& p, const MrPlan& mr, int lev_lo, const W* x, int64_t ldx, W* b,
+                      int64_t ldb, int64_t s, W* partial, W* tbuf, cudaStream_t st);
+
+}  // namespace hodlr

@@ -137,6 +137,15 @@ class HodlrOperator:
         self.launches_per_matvec = int(info.launches_per_matvec)
         self._finalizer = weakref.finalize(self, L.hodlr_destroy, h)
 
+    def path(self, s: int = 1, working=None) -> tuple[str, int]:
+        """(kernel path, launches per matvec) for s right-hand sides:
+        "fused_sv" (one persistent kernel), "mrhs" (tensor-core multi-RHS
+        kernels) or "generic"."""
+        p, n = _lib.c_i32(), _lib.c_i32()
+        _lib.check(_lib.lib().hodlr_matvec_path(self._h, _working_code(self, working), int(s),
+                                                ctypes.byref(p), ctypes.byref(n)), "hodlr_matvec_path")
+        return _lib.PATH_NAMES[p.value], int(n.value)
+
     # ---------------------------------------------------------------- device
     def matvec(self, x, working=None, out=None, stream=None):
         """b = H x for a CUDA tensor x ((n,) or (n, s)), returns a CUDA tensor of

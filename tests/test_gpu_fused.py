@@ -29,15 +29,19 @@ def rel(a, b):
 def make_op(H, fused=True):
     from paper_2407_21637_b200 import linops
 
-    old = os.environ.get("HODLR_B200_DISABLE_FUSED")
-    os.environ["HODLR_B200_DISABLE_FUSED"] = "0" if fused else "1"
+    # fused=False: the generic three-launch kernels (multi-RHS kernels off too)
+    keys = ("HODLR_B200_DISABLE_FUSED", "HODLR_B200_DISABLE_MRHS")
+    old = {k: os.environ.get(k) for k in keys}
+    for k in keys:
+        os.environ[k] = "0" if fused else "1"
     try:
         return linops.HodlrOperator(H)
     finally:
-        if old is None:
-            del os.environ["HODLR_B200_DISABLE_FUSED"]
-        else:
-            os.environ["HODLR_B200_DISABLE_FUSED"] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
 
 
 @pytest.mark.parametrize("working,fmts", FMT_SETS)

@@ -1,0 +1,134 @@
+"""Multi-right-hand-side tensor-core path (kernels_mrhs.cu): DMMA for fp64
+working, 3xTF32 for fp32 working, against the CPU oracle and against the
+generic three-launch kernels, over every storage format, ragged chunk ends,
+variable per-node ranks, several s (including s not a multiple of 8 and
+column-group splits), and the sharded subtree path.
+
+Tolerances (relative, Frobenius over X): fp64 working 1e-12; fp32 working
+1e-5 (the split-TF32 products keep fp32-level accuracy; single-pass TF32 would
+sit near 1e-3 and fail)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import load_case, random_hodlr
+from oracle.matvec import matvec_oracle
+
+pytestmark = pytest.mark.gpu
+
+FMT_SETS = [
+    ("fp64", ["fp32", "fp64", "fp64"]),
+    ("fp64", ["q52", "bf16", "fp16"]),
+    ("fp32", ["bf16", "fp16", "fp32"]),
+    ("fp32", ["q52", "q52", "bf16"]),
+]
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def make_op(H, mrhs=True, **kw):
+    from paper_2407_21637_b200 import linops
+
+    old = os.environ.get("HODLR_B200_DISABLE_MRHS")
+    os.environ["HODLR_B200_DISABLE_MRHS"] = "0" if mrhs else "1"
+    try:
+        return linops.HodlrOperator(H, **kw)
+    finally:
+        if old is None:
+            del os.environ["HODLR_B200_DISABLE_MRHS"]
+        else:
+            os.environ["HODLR_B200_DISABLE_MRHS"] = old
+
+
+def run(torch, op, X, working):
+    dt = torch.float64 if working == "fp64" else torch.float32
+    return op.matvec(torch.from_numpy(np.ascontiguousarray(X)).cuda().to(dt)).double().cpu().numpy()
+
+
+def xin(X, working):
+    return X.astype(np.float32).astype(np.float64) if working == "fp32" else X
+
+
+@pytest.mark.parametrize("working,fmts", FMT_SETS)
+@pytest.mark.parametrize("s", [2, 8, 16, 33, 64])
+def test_mrhs_matches_oracle_and_generic(cuda, working, fmts, s):
+    H = random_hodlr(4096, 3, fmts, [24, 17, 9], working, seed=s + len(fmts[0]))
+    op = make_op(H)
+    assert op.path(s) == ("mrhs", 3)
+    X = np.random.default_rng(s).standard_normal((H.n, s))
+    B = run(cuda, op, X, working)
+    tol = 1e-12 if working == "fp64" else 1e-5
+    assert rel(B, matvec_oracle(H, xin(X, working))) <= tol
+    gen = make_op(H, mrhs=False)
+    assert gen.path(s)[0] == "generic"
+    assert rel(B, run(cuda, gen, X, working)) <= tol
+
+
+@pytest.mark.parametrize("working", ["fp64", "fp32"])
+def test_mrhs_variable_ranks_and_rank_zero(cuda, working):
+    """Per-node ranks differ inside a level (cfg3-like), some are 0."""
+    fmts = ["fp32", "fp16", "bf16", "fp32"] if working == "fp32" else ["fp64", "fp32", "q52", "fp16"]
+    H = random_hodlr(4096, 4, fmts, [(30, 45), (0, 20), (5, 12), (0, 3)], working, seed=3)
+    op = make_op(H)
+    assert op.path(16)[0] == "mrhs"
+    X = np.random.default_rng(2).standard_normal((H.n, 16))
+    tol = 1e-12 if working == "fp64" else 1e-5
+    assert rel(run(cuda, op, X, working), matvec_oracle(H, xin(X, working))) <= tol
+
+
+@pytest.mark.parametrize("working", ["fp64", "fp32"])
+def test_mrhs_ragged_chunks_depth0_and_wide_leaves(cuda, working):
+    """Leaves wider than one 256-row chunk (K loop over column blocks) and a
+    ragged last chunk (rows masked inside a 16-row step)."""
+    for n, depth in ((1000, 0), (3968, 2)):
+        H = random_hodlr(n, depth, ["fp32"] * depth, [7] * depth, working, seed=n)
+        op = make_op(H)
+        assert op.path(5)[0] == "mrhs"
+        X = np.random.default_rng(n).standard_normal((n, 5))
+        tol = 1e-12 if working == "fp64" else 1e-5
+        assert rel(run(cuda, op, X, working), matvec_oracle(H, xin(X, working))) <= tol
+
+
+def test_mrhs_fp64_operand_under_fp32_working_uses_generic(cuda):
+    H = random_hodlr(2048, 3, ["fp64", "fp32", "fp16"], [8, 6, 4], "fp32", seed=1)
+    op = make_op(H)
+    assert op.path(8)[0] == "generic"
+    assert op.path(8, "fp64")[0] == "mrhs"
+
+
+def test_mrhs_golden_cases(cuda):
+    for name in ("g2000_fp32", "toep1024_e4_fp64", "g512_fp64", "toep512_e3_fp64"):
+        H, vec, summ = load_case(name)
+        X = np.random.default_rng(1).standard_normal((H.n, 12))
+        op = make_op(H)
+        w = summ["working"]
+        B = run(cuda, op, X, w)
+        tol = 1e-12 if w == "fp64" else 1e-5
+        assert rel(B, matvec_oracle(H, xin(X, w))) <= tol, (name, op.path(12))
+
+
+def test_mrhs_deterministic(cuda):
+    H = random_hodlr(8192, 5, ["fp32"] * 5, [12, 10, 9, 7, 6], "fp64", seed=4)
+    op = make_op(H)
+    X = np.random.default_rng(0).standard_normal((H.n, 16))
+    a = run(cuda, op, X, "fp64")
+    b = run(cuda, op, X, "fp64")
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+@pytest.mark.parametrize("working", ["fp64", "fp32"])
+def test_mrhs_sharded_subtree(cuda, nranks, working):
+    from test_gpu_shard import run_emulated
+
+    H = random_hodlr(8192, 5, ["fp32", "bf16", "fp16", "q52", "fp32"], [12, 10, 9, 7, 6], working, seed=5)
+    X = np.random.default_rng(3).standard_normal((H.n, 16))
+    out, ops = run_emulated(cuda, H, X, nranks)
+    assert all(op.path(16)[0] == "mrhs" for op in ops)
+    tol = 1e-12 if working == "fp64" else 1e-5
+    assert rel(out, matvec_oracle(H, xin(X, working))) <= tol
