@@ -182,8 +182,15 @@ hodlr_status hodlr_info(const hodlr_handle* h, hodlr_info_t* info);
 /* Which kernels a matvec with `s` right-hand sides in `working` precision
  * runs on this handle (for a sharded handle: shard_local), and how many
  * kernel launches that is.  *path: 0 generic (three launches, any layout),
- * 1 fused single-vector kernel, 2 multi-RHS tensor-core kernels. */
-typedef enum { HODLR_PATH_GENERIC = 0, HODLR_PATH_FUSED_SV = 1, HODLR_PATH_MRHS = 2 } hodlr_path;
+ * 1 fused single-vector kernel, 2 multi-RHS tensor-core kernels over the
+ * level-batched arena, 3 multi-RHS tensor-core kernels over the fragment
+ * slabs (uniform 256-row leaves, bulk-copy streamed). */
+typedef enum {
+    HODLR_PATH_GENERIC = 0,
+    HODLR_PATH_FUSED_SV = 1,
+    HODLR_PATH_MRHS = 2,
+    HODLR_PATH_MRHS_SLAB = 3
+} hodlr_path;
 hodlr_status hodlr_matvec_path(const hodlr_handle* h, int32_t working, int64_t s, int32_t* path,
                                int32_t* launches);
 

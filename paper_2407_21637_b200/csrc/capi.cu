@@ -451,7 +451,8 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
     v.ext_count = h->ext_count;
 
     {
-        MrInput mi{&h->nodes, &h->chunks, &h->leaves, &h->chunk_nodes, nlev, d->leaf_fmt, device};
+        MrInput mi{&h->view, (const uint8_t*)h->arena.p, L, &h->nodes, &h->chunks, &h->leaves, &h->chunk_nodes, nlev,
+                   d->leaf_fmt, device};
         if (mr_prepare(mi, h->mr) != HODLR_OK) return cleanup(fail(HODLR_ERR_CUDA, "multi-RHS plan upload failed"));
         const char* no_mr = getenv("HODLR_B200_DISABLE_MRHS");
         if (no_mr && no_mr[0] == '1') mr_release(h->mr);
@@ -636,7 +637,7 @@ hodlr_status hodlr_matvec_path(const hodlr_handle* h, int32_t working, int64_t s
         *path = HODLR_PATH_FUSED_SV;
         *launches = sv_launches(h->sv);
     } else if (mr_usable(h->mr, working)) {
-        *path = HODLR_PATH_MRHS;
+        *path = mr_slab_used(h->mr, working, h->L) ? HODLR_PATH_MRHS_SLAB : HODLR_PATH_MRHS;
         *launches = mr_launches();
     } else {
         *path = HODLR_PATH_GENERIC;

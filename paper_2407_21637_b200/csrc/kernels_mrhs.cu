@@ -19,11 +19,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "async.cuh"
 #include "mrhs.h"
 
 namespace hodlr {
@@ -112,56 +114,111 @@ __device__ __forceinline__ void tmma(float (&c)[4], uint32_t a0, uint32_t a1, ui
 struct PolF64 {
     using W = double;
     static constexpr int MR = 8, AR = 1, CR = 2, KU = 4, UV = 1;
-    // 16-wide k step, lane k positions = rows 4*tig + j
-    __device__ static __forceinline__ void mma16(W (&c)[CR], const W (&a)[AR][4], const W (&b)[4]) {
+    // operand fragments as the MMA consumes them (fp64: as loaded)
+    struct AF { W v[AR][4]; };
+    struct BF { W v[4]; };
+    struct AUF { W v[AR][UV]; };
+    struct BUF { W v[UV]; };
+    __device__ static __forceinline__ void prep_a(AF& f, const W (&a)[AR][4]) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(c, a[0][j], b[j]);
+        for (int j = 0; j < 4; ++j) f.v[0][j] = a[0][j];
+    }
+    __device__ static __forceinline__ void prep_b(BF& f, const W (&b)[4]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f.v[j] = b[j];
+    }
+    __device__ static __forceinline__ void prep_au(AUF& f, const W (&a)[AR][UV]) { f.v[0][0] = a[0][0]; }
+    __device__ static __forceinline__ void prep_bu(BUF& f, const W (&b)[UV]) { f.v[0] = b[0]; }
+    // 16-wide k step, lane k positions = rows 4*tig + j
+    __device__ static __forceinline__ void mma16(W (&c)[CR], const AF& a, const BF& b) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(c, a.v[0][j], b.v[j]);
     }
     // U step: lane k position tig = column 4*step + tig
-    __device__ static __forceinline__ void mmau(W (&c)[CR], const W (&a)[AR][UV], const W (&b)[UV]) {
-        dmma884(c, a[0][0], b[0]);
+    __device__ static __forceinline__ void mmau(W (&c)[CR], const AUF& a, const BUF& b) {
+        dmma884(c, a.v[0][0], b.v[0]);
     }
 };
 
 struct PolTF32 {
     using W = float;
     static constexpr int MR = 16, AR = 2, CR = 4, KU = 8, UV = 2;
+    // operands split once into tf32 hi/lo pairs, reused across tiles
+    struct AF { uint32_t h[AR][4], l[AR][4]; };
+    struct BF { uint32_t h[4], l[4]; };
+    struct AUF { uint32_t h[AR][UV], l[AR][UV]; };
+    struct BUF { uint32_t h[UV], l[UV]; };
+    __device__ static __forceinline__ void prep_a(AF& f, const W (&a)[AR][4]) {
+#pragma unroll
+        for (int r = 0; r < AR; ++r)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) split_tf32(a[r][j], f.h[r][j], f.l[r][j]);
+    }
+    __device__ static __forceinline__ void prep_b(BF& f, const W (&b)[4]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) split_tf32(b[j], f.h[j], f.l[j]);
+    }
+    __device__ static __forceinline__ void prep_au(AUF& f, const W (&a)[AR][UV]) {
+#pragma unroll
+        for (int r = 0; r < AR; ++r)
+#pragma unroll
+            for (int u = 0; u < UV; ++u) split_tf32(a[r][u], f.h[r][u], f.l[r][u]);
+    }
+    __device__ static __forceinline__ void prep_bu(BUF& f, const W (&b)[UV]) {
+#pragma unroll
+        for (int u = 0; u < UV; ++u) split_tf32(b[u], f.h[u], f.l[u]);
+    }
     // two m16n8k8 per 16-wide step: MMA p, k position tig -> row 4*tig+2p,
-    // k position tig+4 -> row 4*tig+2p+1
-    __device__ static __forceinline__ void mma16(W (&c)[CR], const W (&a)[AR][4], const W (&b)[4]) {
+    // k position tig+4 -> row 4*tig+2p+1; acc += hi*lo' + lo*hi' + hi*hi'
+    __device__ static __forceinline__ void mma16(W (&c)[CR], const AF& a, const BF& b) {
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-            uint32_t ah[4], al[4], bh[2], bl[2];
-            split_tf32(a[0][2 * p], ah[0], al[0]);
-            split_tf32(a[1][2 * p], ah[1], al[1]);
-            split_tf32(a[0][2 * p + 1], ah[2], al[2]);
-            split_tf32(a[1][2 * p + 1], ah[3], al[3]);
-            split_tf32(b[2 * p], bh[0], bl[0]);
-            split_tf32(b[2 * p + 1], bh[1], bl[1]);
-            tmma(c, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
-            tmma(c, al[0], al[1], al[2], al[3], bh[0], bh[1]);
-            tmma(c, ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
+            const int j0 = 2 * p, j1 = 2 * p + 1;
+            tmma(c, a.h[0][j0], a.h[1][j0], a.h[0][j1], a.h[1][j1], b.l[j0], b.l[j1]);
+            tmma(c, a.l[0][j0], a.l[1][j0], a.l[0][j1], a.l[1][j1], b.h[j0], b.h[j1]);
+            tmma(c, a.h[0][j0], a.h[1][j0], a.h[0][j1], a.h[1][j1], b.h[j0], b.h[j1]);
         }
     }
     // U step (k = 8): k position tig -> column 8*step + 2*tig, tig+4 -> 2*tig+1
-    __device__ static __forceinline__ void mmau(W (&c)[CR], const W (&a)[AR][UV], const W (&b)[UV]) {
-        uint32_t ah[4], al[4], bh[2], bl[2];
-        split_tf32(a[0][0], ah[0], al[0]);
-        split_tf32(a[1][0], ah[1], al[1]);
-        split_tf32(a[0][1], ah[2], al[2]);
-        split_tf32(a[1][1], ah[3], al[3]);
-        split_tf32(b[0], bh[0], bl[0]);
-        split_tf32(b[1], bh[1], bl[1]);
-        tmma(c, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
-        tmma(c, al[0], al[1], al[2], al[3], bh[0], bh[1]);
-        tmma(c, ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
+    __device__ static __forceinline__ void mmau(W (&c)[CR], const AUF& a, const BUF& b) {
+        tmma(c, a.h[0][0], a.h[1][0], a.h[0][1], a.h[1][1], b.l[0], b.l[1]);
+        tmma(c, a.l[0][0], a.l[1][0], a.l[0][1], a.l[1][1], b.h[0], b.h[1]);
+        tmma(c, a.h[0][0], a.h[1][0], a.h[0][1], a.h[1][1], b.h[0], b.h[1]);
     }
 };
 
-// Fragment-order index of X element (row r < 256, column q < ncol) for a
-// CTA holding nct n-tiles: [r/16][q/8][lane = 4*(q%8) + (r/4)%4][r%4].
+// Byte offset of element e (of n per lane, fb bytes each) of `lane` inside a
+// 32-lane fragment block.  A lane holding <= 16 B keeps them contiguous (lanes
+// consecutive); wider lanes are split into 16-byte units stored unit-major
+// ([unit][lane][16 B]).  Either way every warp-wide vector load of a block is
+// one contiguous, bank-conflict-free sweep.
+__host__ __device__ __forceinline__ int frag_byte(int lane, int e, int fb, int n) {
+    const int lb = n * fb;
+    if (lb <= 16) return lane * lb + e * fb;
+    const int byte = e * fb;
+    return (byte >> 4) * 512 + lane * 16 + (byte & 15);
+}
+
+// Fragment-order index (elements) of X element (row r < 256, column q < ncol)
+// for a CTA holding nct n-tiles: block [r/16][q/8] of 32 lanes x 4 values,
+// lane = 4*(q%8) + (r/4)%4, value r%4.
+template <typename W>
 __device__ __forceinline__ int xfrag(int r, int q, int nct) {
-    return ((((r >> 4) * nct + (q >> 3)) * 32 + (((q & 7) << 2) | ((r >> 2) & 3))) << 2) | (r & 3);
+    const int lane = ((q & 7) << 2) | ((r >> 2) & 3);
+    return ((r >> 4) * nct + (q >> 3)) * 128 + frag_byte(lane, r & 3, (int)sizeof(W), 4) / (int)sizeof(W);
+}
+
+// A lane's B fragment (4 values) of block `blk` (128 elements).
+template <typename W>
+__device__ __forceinline__ void load_bfrag(const W* blk, int lane, W (&bv)[4]) {
+    if constexpr (sizeof(W) == 8) {
+        const double2 d0 = reinterpret_cast<const double2*>(blk)[lane];
+        const double2 d1 = reinterpret_cast<const double2*>(blk)[32 + lane];
+        bv[0] = d0.x; bv[1] = d0.y; bv[2] = d1.x; bv[3] = d1.y;
+    } else {
+        const float4 u0 = reinterpret_cast<const float4*>(blk)[lane];
+        bv[0] = u0.x; bv[1] = u0.y; bv[2] = u0.z; bv[3] = u0.w;
+    }
 }
 
 // Stage rows [r0, r0 + nrows) (zero beyond) and columns [q0, q0 + ncol) (zero
@@ -174,7 +231,7 @@ __device__ __forceinline__ void stage_x(W* xs, const W* __restrict__ x, int64_t 
         const int r = i / ncol, q = i - r * ncol;
         W v = W(0);
         if (r < nrows && q0 + q < s) v = x[(r0 + r) * ldx + q0 + q];
-        xs[xfrag(r, q, nct)] = v;
+        xs[xfrag<W>(r, q, nct)] = v;
     }
 }
 
@@ -265,18 +322,13 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_a(PlanView p, const __grid_co
                         for (int j = 0; j < 4; ++j) av[a][j] = W(0);
                     }
                 }
-                const float4* bp = reinterpret_cast<const float4*>(xs + ((kb * nct + nt) * 32 + lane) * 4);
                 W bv[4];
-                if constexpr (sizeof(W) == 8) {
-                    const float4 u0 = bp[0], u1 = bp[1];
-                    const double2 d0 = *reinterpret_cast<const double2*>(&u0);
-                    const double2 d1 = *reinterpret_cast<const double2*>(&u1);
-                    bv[0] = d0.x; bv[1] = d0.y; bv[2] = d1.x; bv[3] = d1.y;
-                } else {
-                    const float4 u0 = bp[0];
-                    bv[0] = u0.x; bv[1] = u0.y; bv[2] = u0.z; bv[3] = u0.w;
-                }
-                Pol::mma16(acc, av, bv);
+                load_bfrag<W>(xs + (kb * nct + nt) * 128, lane, bv);
+                typename Pol::AF af;
+                typename Pol::BF bf;
+                Pol::prep_a(af, av);
+                Pol::prep_b(bf, bv);
+                Pol::mma16(acc, af, bf);
             }
             W* my = accs + ((size_t)t * 32 + lane) * Pol::CR;
 #pragma unroll
@@ -300,7 +352,8 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_a(PlanView p, const __grid_co
 }
 
 // ------------------------------------------------------------------ MR
-// One CTA per node: T[c][q] = sum over the node's slots in CTA order.
+// grid.x = nodes, grid.y = tiles of 256 (c, q) coefficients: T[c][q] = sum
+// over the node's slots in CTA order (fixed order: deterministic).
 template <typename W>
 __global__ void __launch_bounds__(256) k_mr_reduce(PlanView p, const __grid_constant__ MrView m, int node_lo,
                                                    int64_t s, int spad, const W* __restrict__ partial,
@@ -311,14 +364,31 @@ __global__ void __launch_bounds__(256) k_mr_reduce(PlanView p, const __grid_cons
     const MrLevel L = m.lev[sl.lv];
     const int64_t cnt = (int64_t)nd.rv * s;
     W* dst = tbuf + nd.t_off * s;
-    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const int64_t stride = (int64_t)L.rv_pad * spad;
+    for (int64_t i = blockIdx.y * 256 + threadIdx.x; i < cnt; i += (int64_t)gridDim.y * 256) {
         const int64_t c = i / s, q = i - c * s;
         const W* src = partial + (L.part_rows + (int64_t)(sl.b0 + sl.jrel) * L.rv_pad + c) * spad + q;
-        const int64_t stride = (int64_t)L.rv_pad * spad;
         W acc = src[0];
-        for (int b = sl.b0 + 1; b <= sl.b1; ++b) acc += src[(int64_t)(b - sl.b0) * stride];
+        const int nb = sl.b1 - sl.b0;
+        int b = 1;
+        for (; b + 3 <= nb; b += 4) {  // four loads in flight, additions in slot order
+            const W v1 = src[(int64_t)b * stride], v2 = src[(int64_t)(b + 1) * stride];
+            const W v3 = src[(int64_t)(b + 2) * stride], v4 = src[(int64_t)(b + 3) * stride];
+            acc += v1;
+            acc += v2;
+            acc += v3;
+            acc += v4;
+        }
+        for (; b <= nb; ++b) acc += src[(int64_t)b * stride];
         dst[i] = acc;
     }
+}
+
+inline dim3 reduce_grid(const MrView& m, int node_lo, int nnodes_total, int64_t s) {
+    int rmax = 0;
+    for (int lv = 0; lv < m.nlev; ++lv) rmax = rmax > m.lev[lv].rv_max ? rmax : m.lev[lv].rv_max;
+    const int64_t tiles = ((int64_t)rmax * s + 255) / 256;
+    return dim3(nnodes_total - node_lo, (unsigned)(tiles < 1 ? 1 : tiles > 64 ? 64 : tiles));
 }
 
 // ------------------------------------------------------------------ MB
@@ -410,21 +480,17 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_b(PlanView p, const __grid_co
                         for (int j = 0; j < 4; ++j) av[mt][a][j] = W(0);
                     }
                 }
+            typename Pol::AF af[MT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) Pol::prep_a(af[mt], av[mt]);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-                const float4* bp = reinterpret_cast<const float4*>(xs + ((kb * NT + nt) * 32 + lane) * 4);
                 W bv[4];
-                if constexpr (sizeof(W) == 8) {
-                    const float4 u0 = bp[0], u1 = bp[1];
-                    const double2 d0 = *reinterpret_cast<const double2*>(&u0);
-                    const double2 d1 = *reinterpret_cast<const double2*>(&u1);
-                    bv[0] = d0.x; bv[1] = d0.y; bv[2] = d1.x; bv[3] = d1.y;
-                } else {
-                    const float4 u0 = bp[0];
-                    bv[0] = u0.x; bv[1] = u0.y; bv[2] = u0.z; bv[3] = u0.w;
-                }
+                load_bfrag<W>(xs + (kb * NT + nt) * 128, lane, bv);
+                typename Pol::BF bf;
+                Pol::prep_b(bf, bv);
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) Pol::mma16(acc[mt][nt], av[mt], bv);
+                for (int mt = 0; mt < MT; ++mt) Pol::mma16(acc[mt][nt], af[mt], bf);
             }
         }
     }
@@ -454,14 +520,19 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_b(PlanView p, const __grid_co
                                            : W(0);
                     }
                 }
+            typename Pol::AUF af[MT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) Pol::prep_au(af[mt], av[mt]);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 W bv[Pol::UV];
 #pragma unroll
                 for (int u = 0; u < Pol::UV; ++u)
                     bv[u] = ts[base + ((step * NT + nt) * 32 + lane) * Pol::UV + u];
+                typename Pol::BUF bf;
+                Pol::prep_bu(bf, bv);
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) Pol::mmau(acc[mt][nt], av[mt], bv);
+                for (int mt = 0; mt < MT; ++mt) Pol::mmau(acc[mt][nt], af[mt], bf);
             }
         }
         base += steps * NT * 32 * Pol::UV;
@@ -477,6 +548,521 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_b(PlanView p, const __grid_co
                 const int row = warp * 32 + mt * Pol::MR + g + 8 * (i >> 1);
                 const int64_t q = q0 + nt * 8 + 2 * tig + (i & 1);
                 if (row < ch.nrows && q < s) b[(int64_t)(ch.row0 + row) * ldb + q] = acc[mt][nt][i];
+            }
+}
+
+// ================================================================== slab path
+// Relayout kernels (create time): arena -> fragment slabs.  Pure byte moves of
+// already-quantised values (no rounding), zero fill for padding.
+template <class Pol>
+__global__ void k_slab_a(PlanView p, const __grid_constant__ Mr2View v, uint8_t* __restrict__ slab) {
+    // one thread per (chunk, level, m-tile, k-block, lane, a): 4 consecutive rows of one V' column
+    int64_t per_chunk = 0;
+    for (int lv = v.lev_lo; lv < v.nlev; ++lv) per_chunk += (int64_t)v.lev[lv].nmt * 16 * 32 * Pol::AR;
+    const int64_t total = per_chunk * p.nchunks;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int chunk = (int)(i / per_chunk);
+        int64_t r = i - (int64_t)chunk * per_chunk;
+        int lv = v.lev_lo;
+        for (;; ++lv) {
+            const int64_t c = (int64_t)v.lev[lv].nmt * 16 * 32 * Pol::AR;
+            if (r < c) break;
+            r -= c;
+        }
+        const int a = (int)(r % Pol::AR);
+        r /= Pol::AR;
+        const int lane = (int)(r % 32);
+        r /= 32;
+        const int kb = (int)(r % 16);
+        const int mt = (int)(r / 16);
+        const Mr2Level L = v.lev[lv];
+        const int fb = fmt_bytes(L.vfmt);
+        uint8_t* blk = slab + (int64_t)chunk * v.a_chunk_bytes + L.aoff + ((int64_t)mt * 16 + kb) * L.ablk;
+        const ChunkDesc ch = p.chunks[chunk];
+        const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
+        const int c = mt * Pol::MR + (lane >> 2) + 8 * a;
+        const int row = kb * 16 + 4 * (lane & 3);
+        for (int j = 0; j < 4; ++j) {
+            uint8_t* dst = blk + frag_byte(lane, a * 4 + j, fb, Pol::AR * 4);
+            if (c < nd.rv) {
+                const uint8_t* src = p.arena + nd.v_off + ((int64_t)c * nd.v_ld + (ch.row0 - nd.row0) + row + j) * fb;
+                for (int b = 0; b < fb; ++b) dst[b] = src[b];
+            } else {
+                for (int b = 0; b < fb; ++b) dst[b] = 0;
+            }
+        }
+    }
+}
+
+template <class Pol>
+__global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t* __restrict__ slab) {
+    constexpr int MT = 32 / Pol::MR;
+    // D part: one thread per (chunk, warp, kb, mt, lane, a): 4 consecutive leaf columns
+    const int64_t dper = 8LL * 16 * MT * 32 * Pol::AR;
+    const int64_t dtotal = dper * p.nchunks;
+    const int lfb = fmt_bytes(v.leaf_fmt);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dtotal; i += (int64_t)gridDim.x * blockDim.x) {
+        const int chunk = (int)(i / dper);
+        int64_t r = i - (int64_t)chunk * dper;
+        const int a = (int)(r % Pol::AR); r /= Pol::AR;
+        const int lane = (int)(r % 32); r /= 32;
+        const int mt = (int)(r % MT); r /= MT;
+        const int kb = (int)(r % 16);
+        const int w = (int)(r / 16);
+        const ChunkDesc ch = p.chunks[chunk];
+        const LeafDesc lf = p.leaves[ch.leaf];
+        const int row = (ch.row0 - lf.row0) + 32 * w + mt * Pol::MR + (lane >> 2) + 8 * a;
+        const int col = kb * 16 + 4 * (lane & 3);
+        const uint8_t* src = p.arena + lf.off + ((int64_t)row * lf.ld + col) * lfb;
+        uint8_t* blk = slab + (int64_t)chunk * v.b_chunk_bytes + (int64_t)w * v.warp_bytes + (int64_t)kb * v.d_item +
+                       (int64_t)mt * 32 * Pol::AR * 4 * lfb;
+        for (int j = 0; j < 4; ++j) {
+            uint8_t* dst = blk + frag_byte(lane, a * 4 + j, lfb, Pol::AR * 4);
+            for (int b = 0; b < lfb; ++b) dst[b] = src[j * lfb + b];
+        }
+    }
+    // U part: one thread per (chunk, warp, level, step, mt, lane, a, u): one element
+    int64_t uper = 0;
+    for (int lv = v.lev_lo; lv < v.nlev; ++lv) uper += (int64_t)v.lev[lv].steps * MT * 32 * Pol::AR * Pol::UV;
+    const int64_t utotal = uper * 8 * p.nchunks;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < utotal; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cw = i / uper;
+        int64_t r = i - cw * uper;
+        const int chunk = (int)(cw / 8), w = (int)(cw % 8);
+        int lv = v.lev_lo;
+        for (;; ++lv) {
+            const int64_t c = (int64_t)v.lev[lv].steps * MT * 32 * Pol::AR * Pol::UV;
+            if (r < c) break;
+            r -= c;
+        }
+        const int u = (int)(r % Pol::UV); r /= Pol::UV;
+        const int a = (int)(r % Pol::AR); r /= Pol::AR;
+        const int lane = (int)(r % 32); r /= 32;
+        const int mt = (int)(r % MT);
+        const int step = (int)(r / MT);
+        const Mr2Level L = v.lev[lv];
+        const int fb = fmt_bytes(L.ufmt);
+        const ChunkDesc ch = p.chunks[chunk];
+        const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
+        const int row = (ch.row0 - nd.row0) + 32 * w + mt * Pol::MR + (lane >> 2) + 8 * a;
+        const int c = step * Pol::KU + Pol::UV * (lane & 3) + u;
+        uint8_t* dst = slab + (int64_t)chunk * v.b_chunk_bytes + (int64_t)w * v.warp_bytes + L.uoff +
+                       (int64_t)step * L.usz + (int64_t)mt * 32 * Pol::AR * Pol::UV * fb +
+                       frag_byte(lane, a * Pol::UV + u, fb, Pol::AR * Pol::UV);
+        if (c < nd.ru) {
+            const uint8_t* src = p.arena + nd.u_off + ((int64_t)c * nd.u_ld + row) * fb;
+            for (int b = 0; b < fb; ++b) dst[b] = src[b];
+        } else {
+            for (int b = 0; b < fb; ++b) dst[b] = 0;
+        }
+    }
+}
+
+// A lane's N values of a fragment block (layout of frag_byte), decoded to W.
+template <typename W, int N>
+__device__ __forceinline__ void frag_load(int fmt, const uint8_t* blk, int lane, W (&v)[N]) {
+    switch (fmt) {
+        case HODLR_FMT_FP64:
+            if constexpr (N == 1) {
+                v[0] = (W) reinterpret_cast<const double*>(blk)[lane];
+            } else {
+#pragma unroll
+                for (int u = 0; u < N / 2; ++u) {
+                    const double2 d = reinterpret_cast<const double2*>(blk + u * 512)[lane];
+                    v[2 * u] = (W)d.x;
+                    v[2 * u + 1] = (W)d.y;
+                }
+            }
+            break;
+        case HODLR_FMT_FP32:
+            if constexpr (N == 1) {
+                v[0] = (W) reinterpret_cast<const float*>(blk)[lane];
+            } else if constexpr (N == 2) {
+                const float2 f = reinterpret_cast<const float2*>(blk)[lane];
+                v[0] = (W)f.x; v[1] = (W)f.y;
+            } else {
+#pragma unroll
+                for (int u = 0; u < N / 4; ++u) {
+                    const float4 f = reinterpret_cast<const float4*>(blk + u * 512)[lane];
+                    v[4 * u] = (W)f.x; v[4 * u + 1] = (W)f.y; v[4 * u + 2] = (W)f.z; v[4 * u + 3] = (W)f.w;
+                }
+            }
+            break;
+        case HODLR_FMT_FP16:
+        case HODLR_FMT_BF16: {
+            uint32_t w[(N + 1) / 2];
+            if constexpr (N == 1) {
+                w[0] = reinterpret_cast<const uint16_t*>(blk)[lane];
+            } else if constexpr (N == 2) {
+                w[0] = reinterpret_cast<const uint32_t*>(blk)[lane];
+            } else if constexpr (N == 4) {
+                const uint2 t = reinterpret_cast<const uint2*>(blk)[lane];
+                w[0] = t.x; w[1] = t.y;
+            } else {
+#pragma unroll
+                for (int u = 0; u < N / 8; ++u) {
+                    const uint4 t = reinterpret_cast<const uint4*>(blk + u * 512)[lane];
+                    w[4 * u] = t.x; w[4 * u + 1] = t.y; w[4 * u + 2] = t.z; w[4 * u + 3] = t.w;
+                }
+            }
+            const bool bf = fmt == HODLR_FMT_BF16;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const uint16_t h = (uint16_t)(w[i / 2] >> (16 * (i & 1)));
+                v[i] = bf ? (W)__uint_as_float((uint32_t)h << 16) : (W)dec_fp16(h);
+            }
+            break;
+        }
+        default: {  // q52
+            uint32_t w[(N + 3) / 4];
+            if constexpr (N == 1) {
+                w[0] = blk[lane];
+            } else if constexpr (N == 2) {
+                w[0] = reinterpret_cast<const uint16_t*>(blk)[lane];
+            } else if constexpr (N == 4) {
+                w[0] = reinterpret_cast<const uint32_t*>(blk)[lane];
+            } else if constexpr (N == 8) {
+                const uint2 t = reinterpret_cast<const uint2*>(blk)[lane];
+                w[0] = t.x; w[1] = t.y;
+            } else {
+#pragma unroll
+                for (int u = 0; u < N / 16; ++u) {
+                    const uint4 t = reinterpret_cast<const uint4*>(blk + u * 512)[lane];
+                    w[4 * u] = t.x; w[4 * u + 1] = t.y; w[4 * u + 2] = t.z; w[4 * u + 3] = t.w;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < N; ++i) v[i] = (W)dec_q52((uint8_t)(w[i / 4] >> (8 * (i & 3))));
+            break;
+        }
+    }
+}
+
+constexpr int kRingMax = 4;  // max slots per warp ring (runtime depth ns <= kRingMax)
+
+// ------------------------------------------------------------------ per-warp ring
+// A warp-private ring of `ns` slots of `slot` bytes, filled by lane 0 with
+// cp.async.bulk (complete_tx on the slot's mbarrier).  Item i lives in slot
+// i % ns; its (i / ns)-th fill completes phase parity (i / ns) & 1.  An item is
+// released (refilled with item i + ns) right after the warp has READ its last
+// sub-block into registers, before the math on it, so ns items stay in flight.
+struct WarpRing {
+    uint64_t* bar;
+    uint8_t* buf;
+    int ns, slot;
+    __device__ __forceinline__ const uint8_t* wait(int64_t i) const {
+        const int k = (int)(i % ns);
+        tma::mbar_wait(&bar[k], (unsigned)((i / ns) & 1));
+        return buf + (size_t)k * slot;
+    }
+    __device__ __forceinline__ void fill(int64_t i, const void* src, unsigned bytes, uint64_t pol) const {
+        const int k = (int)(i % ns);
+        tma::mbar_arrive_tx(&bar[k], bytes);
+        tma::bulk_g2s(buf + (size_t)k * slot, src, bytes, &bar[k], pol);
+    }
+};
+
+// ------------------------------------------------------------------ MA2
+// Persistent-range phase A over the A slab.  Warp w's stream: for every chunk
+// of the CTA's run, for its tasks t = w, w+8, ... (m-tiles of all levels), the
+// task's 16 k-blocks in items of kbi blocks (<= 4 KB).
+template <class Pol, int NCT>
+__global__ void __launch_bounds__(kMrThreads) k_mr2_a(PlanView p, const __grid_constant__ MrView m,
+                                                      const __grid_constant__ Mr2View v,
+                                                      const typename Pol::W* __restrict__ x, int64_t ldx,
+                                                      int64_t s, int spad, int kbi, int slot_bytes, int ns,
+                                                      typename Pol::W* __restrict__ partial) {
+    using W = typename Pol::W;
+    constexpr int ncol = NCT * 8;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                 // [8][kRingMax]
+    W* xs = reinterpret_cast<W*>(smem_raw + 8 * kRingMax * 8);              // [256 x ncol]
+    W* accs = xs + kChunk * ncol;                                           // [task][NCT][32][CR]
+    uint8_t* ring = reinterpret_cast<uint8_t*>(accs + (size_t)v.ntasks * NCT * 32 * Pol::CR);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tig = lane & 3;
+    const int64_t q0 = (int64_t)blockIdx.y * ncol;
+    const int c_beg = (int)((int64_t)blockIdx.x * p.nchunks / gridDim.x);
+    const int c_end = (int)((int64_t)(blockIdx.x + 1) * p.nchunks / gridDim.x);
+    const WarpRing R{bars + warp * kRingMax, ring + (size_t)warp * ns * slot_bytes, ns, slot_bytes};
+    const int ipt = 16 / kbi;                                   // items per task
+    const int my_tasks = warp < v.ntasks ? (v.ntasks - 1 - warp) / kMrWarps + 1 : 0;
+    const int64_t per_chunk = (int64_t)my_tasks * ipt;
+    const int64_t nitems = (int64_t)(c_end - c_beg) * per_chunk;
+    const uint64_t pol = tma::policy_evict_first();
+
+    auto issue = [&](int64_t it) {
+        const int ci = c_beg + (int)(it / per_chunk);
+        const int64_t r = it - (int64_t)(ci - c_beg) * per_chunk;
+        const int tt = (int)(r / ipt);
+        const int kb0 = (int)(r - (int64_t)tt * ipt) * kbi;
+        int mt = warp + tt * kMrWarps, lv = v.lev_lo;
+        while (mt >= v.lev[lv].nmt) { mt -= v.lev[lv].nmt; ++lv; }
+        const Mr2Level L = v.lev[lv];
+        R.fill(it, v.slab_a + (int64_t)ci * v.a_chunk_bytes + L.aoff + ((int64_t)mt * 16 + kb0) * L.ablk,
+               (unsigned)(kbi * L.ablk), pol);
+    };
+
+    if (lane == 0) {
+        for (int i = 0; i < ns; ++i) tma::mbar_init(&R.bar[i], 1);
+        tma::fence_mbar_init();
+        for (int64_t i = 0; i < ns && i < nitems; ++i) issue(i);
+    }
+    for (int t = warp; t < v.ntasks; t += kMrWarps)
+#pragma unroll
+        for (int nt = 0; nt < NCT; ++nt)
+#pragma unroll
+            for (int i = 0; i < Pol::CR; ++i) accs[(((size_t)t * NCT + nt) * 32 + lane) * Pol::CR + i] = W(0);
+
+    int64_t it = 0;
+    for (int ci = c_beg; ci < c_end; ++ci) {
+        const ChunkDesc ch = p.chunks[ci];
+        __syncthreads();  // previous chunk's X consumed (and, first time, barrier inits visible)
+        stage_x<W>(xs, x, ldx, ch.row0, ch.nrows, q0, ncol, s);
+        __syncthreads();
+        for (int tt = 0; tt < my_tasks; ++tt) {
+            const int t = warp + tt * kMrWarps;
+            int lv = v.lev_lo, mt = t;
+            while (mt >= v.lev[lv].nmt) { mt -= v.lev[lv].nmt; ++lv; }
+            const int vfmt = v.lev[lv].vfmt;
+            const int ablk = v.lev[lv].ablk;
+            W acc[NCT][Pol::CR];
+#pragma unroll
+            for (int nt = 0; nt < NCT; ++nt)
+#pragma unroll
+                for (int i = 0; i < Pol::CR; ++i) acc[nt][i] = W(0);
+            for (int q = 0; q < ipt; ++q, ++it) {
+                const uint8_t* base = R.wait(it);
+                for (int k = 0; k < kbi; ++k) {
+                    W tmp[Pol::AR * 4];
+                    frag_load<W, Pol::AR * 4>(vfmt, base + (size_t)k * ablk, lane, tmp);
+                    if (k == kbi - 1) {  // item fully read: refill its slot
+                        __syncwarp();
+                        if (lane == 0 && it + ns < nitems) {
+                            tma::fence_proxy_async_smem();
+                            issue(it + ns);
+                        }
+                    }
+                    W av[Pol::AR][4];
+#pragma unroll
+                    for (int a = 0; a < Pol::AR; ++a)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) av[a][j] = tmp[a * 4 + j];
+                    typename Pol::AF af;
+                    Pol::prep_a(af, av);
+                    const int kb = q * kbi + k;
+#pragma unroll
+                    for (int nt = 0; nt < NCT; ++nt) {
+                        W bv[4];
+                        load_bfrag<W>(xs + (kb * NCT + nt) * 128, lane, bv);
+                        typename Pol::BF bf;
+                        Pol::prep_b(bf, bv);
+                        Pol::mma16(acc[nt], af, bf);
+                    }
+                }
+            }
+            // accumulate into the task tile; flush at the node's last chunk of this run
+            const int node = p.chunk_nodes[ci * p.nlev + lv];
+            const bool more = ci + 1 < c_end && p.chunk_nodes[(ci + 1) * p.nlev + lv] == node;
+            const MrLevel L = m.lev[lv];
+            const int64_t slot = (int64_t)blockIdx.x + m.slots[node].jrel;
+#pragma unroll
+            for (int nt = 0; nt < NCT; ++nt) {
+                W* my = accs + (((size_t)t * NCT + nt) * 32 + lane) * Pol::CR;
+#pragma unroll
+                for (int i = 0; i < Pol::CR; ++i) {
+                    W val = my[i] + acc[nt][i];
+                    if (more) {
+                        my[i] = val;
+                    } else {
+                        const int c = mt * Pol::MR + g + 8 * (i >> 1);
+                        const int q = nt * 8 + 2 * tig + (i & 1);
+                        if (c < L.rv_max && q0 + q < spad)
+                            partial[(L.part_rows + slot * L.rv_pad + c) * spad + q0 + q] = val;
+                        my[i] = W(0);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ MB2
+// One CTA per (chunk, column group); warp w owns chunk rows 32w..32w+31 and
+// streams its B-region bytes (16 D items, then the U steps of every level
+// packed into items of the same size) through a private ring.
+template <class Pol, int NT>
+__global__ void __launch_bounds__(kMrThreads) k_mr2_b(PlanView p, const __grid_constant__ MrView m,
+                                                      const __grid_constant__ Mr2View v,
+                                                      const typename Pol::W* __restrict__ x, int64_t ldx,
+                                                      const typename Pol::W* __restrict__ tbuf,
+                                                      typename Pol::W* __restrict__ b, int64_t ldb, int64_t s,
+                                                      int ngrp, int ns) {
+    using W = typename Pol::W;
+    constexpr int MT = 32 / Pol::MR;
+    constexpr int ncol = NT * 8;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+    uint8_t* ring = smem_raw + 8 * kRingMax * 8;
+    const int slot_bytes = v.d_item;
+    W* xs = reinterpret_cast<W*>(ring + (size_t)8 * ns * slot_bytes);
+    W* ts = xs + kChunk * ncol;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tig = lane & 3;
+    const int chunk = blockIdx.x / ngrp;
+    const int64_t q0 = (int64_t)(blockIdx.x - chunk * ngrp) * ncol;
+    const ChunkDesc ch = p.chunks[chunk];
+    const WarpRing R{bars + warp * kRingMax, ring + (size_t)warp * ns * slot_bytes, ns, slot_bytes};
+    const uint8_t* wsrc = v.slab_b + (int64_t)chunk * v.b_chunk_bytes + (int64_t)warp * v.warp_bytes;
+    const int nitems = (v.warp_bytes + slot_bytes - 1) / slot_bytes;
+    const uint64_t pol = tma::policy_evict_first();
+    auto issue = [&](int it) {
+        const int64_t off = (int64_t)it * slot_bytes;
+        const int64_t rem = v.warp_bytes - off;
+        R.fill(it, wsrc + off, (unsigned)(rem < slot_bytes ? rem : slot_bytes), pol);
+    };
+    auto release = [&](int it) {
+        __syncwarp();
+        if (lane == 0 && it + ns < nitems) {
+            tma::fence_proxy_async_smem();
+            issue(it + ns);
+        }
+    };
+    if (lane == 0) {
+        for (int i = 0; i < ns; ++i) tma::mbar_init(&R.bar[i], 1);
+        tma::fence_mbar_init();
+        for (int i = 0; i < ns && i < nitems; ++i) issue(i);
+    }
+
+    // stage X (leaf rows) and the coefficients of every level (fragment order)
+    stage_x<W>(xs, x, ldx, ch.row0, ch.nrows, q0, ncol, s);
+    {
+        int base = 0;
+        for (int lv = v.lev_lo; lv < v.nlev; ++lv) {
+            const int steps = v.lev[lv].steps;
+            const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
+            const W* t = tbuf + nd.tsrc_off * s;
+            for (int i = threadIdx.x; i < steps * Pol::KU * ncol; i += blockDim.x) {
+                const int c = i / ncol, q = i - c * ncol;
+                W val = W(0);
+                if (c < nd.ru && q0 + q < s) val = t[(int64_t)c * s + q0 + q];
+                const int step = c / Pol::KU, w = c - step * Pol::KU;
+                const int tg = w / Pol::UV, u = w - tg * Pol::UV;
+                ts[base + ((step * NT + (q >> 3)) * 32 + (q & 7) * 4 + tg) * Pol::UV + u] = val;
+            }
+            base += steps * NT * 32 * Pol::UV;
+        }
+    }
+    __syncthreads();
+
+    W acc[MT][NT][Pol::CR];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < Pol::CR; ++i) acc[mt][nt][i] = W(0);
+
+    const int lfmt = v.leaf_fmt;
+    const int lfb = fmt_bytes(lfmt);
+    // D items: k-step kb (exactly one item each)
+    for (int kb = 0; kb < 16; ++kb) {
+        const uint8_t* base = R.wait(kb);
+        W tmp[MT][Pol::AR * 4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+            frag_load<W, Pol::AR * 4>(lfmt, base + (size_t)mt * 32 * Pol::AR * 4 * lfb, lane, tmp[mt]);
+        release(kb);
+        typename Pol::AF af[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            W av[Pol::AR][4];
+#pragma unroll
+            for (int a = 0; a < Pol::AR; ++a)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) av[a][j] = tmp[mt][a * 4 + j];
+            Pol::prep_a(af[mt], av);
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            W bv[4];
+            load_bfrag<W>(xs + (kb * NT + nt) * 128, lane, bv);
+            typename Pol::BF bf;
+            Pol::prep_b(bf, bv);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) Pol::mma16(acc[mt][nt], af[mt], bf);
+        }
+    }
+    // U steps, level by level; several steps per item
+    int tbase = 0;
+    int held = -1;
+    const uint8_t* hbase = nullptr;
+    for (int lv = v.lev_lo; lv < v.nlev; ++lv) {
+        const Mr2Level L = v.lev[lv];
+        const int ufb = fmt_bytes(L.ufmt);
+        for (int step = 0; step < L.steps; ++step) {
+            const int64_t off = L.uoff + (int64_t)step * L.usz;
+            const int item = (int)(off / slot_bytes);
+            if (item != held) {
+                hbase = R.wait(item);
+                held = item;
+            }
+            const uint8_t* base = hbase + (off - (int64_t)item * slot_bytes);
+            W tmp[MT][Pol::AR * Pol::UV];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+                frag_load<W, Pol::AR * Pol::UV>(L.ufmt, base + (size_t)mt * 32 * Pol::AR * Pol::UV * ufb, lane,
+                                                tmp[mt]);
+            // next step's item (or none): release this one once it is fully read
+            int64_t noff = -1;
+            if (step + 1 < L.steps) {
+                noff = off + L.usz;
+            } else {
+                for (int l2 = lv + 1; l2 < v.nlev; ++l2)
+                    if (v.lev[l2].steps > 0) {
+                        noff = v.lev[l2].uoff;
+                        break;
+                    }
+            }
+            if (noff < 0 || (int)(noff / slot_bytes) != item) release(item);
+            typename Pol::AUF af[MT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                W av[Pol::AR][Pol::UV];
+#pragma unroll
+                for (int a = 0; a < Pol::AR; ++a)
+#pragma unroll
+                    for (int u = 0; u < Pol::UV; ++u) av[a][u] = tmp[mt][a * Pol::UV + u];
+                Pol::prep_au(af[mt], av);
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                W bv[Pol::UV];
+#pragma unroll
+                for (int u = 0; u < Pol::UV; ++u) bv[u] = ts[tbase + ((step * NT + nt) * 32 + lane) * Pol::UV + u];
+                typename Pol::BUF bf;
+                Pol::prep_bu(bf, bv);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) Pol::mmau(acc[mt][nt], af[mt], bf);
+            }
+        }
+        tbase += L.steps * NT * 32 * Pol::UV;
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < Pol::CR; i += 2) {
+                const int row = warp * 32 + mt * Pol::MR + g + 8 * (i >> 1);
+                const int64_t q = q0 + nt * 8 + 2 * tig;
+                W* dst = b + (int64_t)(ch.row0 + row) * ldb + q;
+                if (q + 1 < s) {
+                    dst[0] = acc[mt][nt][i];
+                    dst[1] = acc[mt][nt][i + 1];
+                } else if (q < s) {
+                    dst[0] = acc[mt][nt][i];
+                }
             }
 }
 
@@ -518,6 +1104,86 @@ cudaError_t launch_mb(int nt, dim3 grid, size_t smem, cudaStream_t st, const Pla
 #undef HODLR_MB_CASE
 }
 
+
+// ---- slab path launchers
+inline int pick_nt(int spad) { return spad >= 32 ? 4 : spad >= 16 ? 2 : 1; }
+
+template <class Pol>
+size_t ma2_smem(const Mr2View& v, int nct, int slot_bytes, int ns) {
+    using W = typename Pol::W;
+    return 8 * kRingMax * 8 + (size_t)kChunk * nct * 8 * sizeof(W) +
+           (size_t)v.ntasks * nct * 32 * Pol::CR * sizeof(W) + (size_t)8 * ns * slot_bytes;
+}
+template <class Pol>
+size_t mb2_smem(const Mr2View& v, int nt, int ns) {
+    using W = typename Pol::W;
+    size_t trows = 0;
+    for (int lv = v.lev_lo; lv < v.nlev; ++lv) trows += (size_t)v.lev[lv].steps * Pol::KU;
+    return 8 * kRingMax * 8 + (size_t)8 * ns * v.d_item + ((size_t)kChunk + trows) * nt * 8 * sizeof(W);
+}
+
+template <class Pol, int NCT>
+cudaError_t launch_ma2_t(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
+                         int64_t ldx, int64_t s, int spad, typename Pol::W* partial, cudaStream_t st) {
+    int kbi = 16;
+    while (kbi > 1 && kbi * v.max_ablk > 4096) kbi /= 2;
+    const int slot = kbi * v.max_ablk;
+    // deepest ring that keeps two CTAs per SM, else the deepest that fits one
+    int ns = kRingMax;
+    while (ns > 2 && ma2_smem<Pol>(v, NCT, slot, ns) > 113 * 1024) --ns;
+    if (ma2_smem<Pol>(v, NCT, slot, ns) > 113 * 1024) {
+        ns = kRingMax;
+        while (ns > 2 && ma2_smem<Pol>(v, NCT, slot, ns) > 227 * 1024) --ns;
+    }
+    const size_t sm = ma2_smem<Pol>(v, NCT, slot, ns);
+    if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
+    auto k = k_mr2_a<Pol, NCT>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    dim3 grid(m.nb, (spad + NCT * 8 - 1) / (NCT * 8));
+    k<<<grid, kMrThreads, sm, st>>>(p, m, v, x, ldx, s, spad, kbi, slot, ns, partial);
+    return cudaGetLastError();
+}
+template <class Pol>
+cudaError_t launch_ma2(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
+                       int64_t ldx, int64_t s, int spad, typename Pol::W* partial, cudaStream_t st) {
+    int nct = pick_nt(spad);
+    while (nct > 1 && ma2_smem<Pol>(v, nct, 4096, 2) > 227 * 1024) nct /= 2;
+    if (nct == 4) return launch_ma2_t<Pol, 4>(p, m, v, x, ldx, s, spad, partial, st);
+    if (nct == 2) return launch_ma2_t<Pol, 2>(p, m, v, x, ldx, s, spad, partial, st);
+    return launch_ma2_t<Pol, 1>(p, m, v, x, ldx, s, spad, partial, st);
+}
+
+template <class Pol, int NT>
+cudaError_t launch_mb2_t(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
+                         int64_t ldx, const typename Pol::W* tbuf, typename Pol::W* b, int64_t ldb, int64_t s,
+                         int spad, cudaStream_t st) {
+    int ns = kRingMax;
+    while (ns > 2 && mb2_smem<Pol>(v, NT, ns) > 113 * 1024) --ns;
+    if (mb2_smem<Pol>(v, NT, ns) > 113 * 1024) {
+        ns = kRingMax;
+        while (ns > 2 && mb2_smem<Pol>(v, NT, ns) > 227 * 1024) --ns;
+    }
+    const size_t sm = mb2_smem<Pol>(v, NT, ns);
+    if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
+    auto k = k_mr2_b<Pol, NT>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    const int ngrp = (spad + NT * 8 - 1) / (NT * 8);
+    k<<<p.nchunks * ngrp, kMrThreads, sm, st>>>(p, m, v, x, ldx, tbuf, b, ldb, s, ngrp, ns);
+    return cudaGetLastError();
+}
+template <class Pol>
+cudaError_t launch_mb2(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
+                       int64_t ldx, const typename Pol::W* tbuf, typename Pol::W* b, int64_t ldb, int64_t s,
+                       int spad, cudaStream_t st) {
+    int nt = pick_nt(spad);
+    while (nt > 1 && mb2_smem<Pol>(v, nt, 2) > 227 * 1024) nt /= 2;
+    if (nt == 4) return launch_mb2_t<Pol, 4>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st);
+    if (nt == 2) return launch_mb2_t<Pol, 2>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st);
+    return launch_mb2_t<Pol, 1>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st);
+}
+
 template <class Pol>
 cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typename Pol::W* x, int64_t ldx,
                    typename Pol::W* b, int64_t ldb, int64_t s, typename Pol::W* partial,
@@ -527,6 +1193,21 @@ cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typena
     const int spad = (int)mr_spad(s);
     if (p.nchunks == 0) return cudaSuccess;
     const bool any_level = lev_lo < m.nlev;
+    const int wfmt = sizeof(W) == 8 ? HODLR_FMT_FP64 : HODLR_FMT_FP32;
+    if (mr_slab_used(mr, wfmt, lev_lo)) {
+        cudaError_t e = cudaSuccess;
+        if (any_level) {
+            e = launch_ma2<Pol>(p, m, mr.v2, x, ldx, s, spad, partial, st);
+            const int node_lo = m.lev[lev_lo].node0;
+            const int nred = p.nnodes - node_lo;
+            if (e == cudaSuccess && nred > 0) {
+                k_mr_reduce<W><<<reduce_grid(m, node_lo, p.nnodes, s), 256, 0, st>>>(p, m, node_lo, s, spad, partial, tbuf);
+                e = cudaGetLastError();
+            }
+        }
+        if (e == cudaSuccess) e = launch_mb2<Pol>(p, m, mr.v2, x, ldx, tbuf, b, ldb, s, spad, st);
+        return e;
+    }
     if (any_level) {
         // MA: widest column group whose shared memory keeps two CTAs per SM
         int ncol = spad;
@@ -543,7 +1224,7 @@ cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typena
         const int node_lo = m.lev[lev_lo].node0;
         const int nred = p.nnodes - node_lo;
         if (nred > 0) {
-            k_mr_reduce<W><<<nred, 256, 0, st>>>(p, m, node_lo, s, spad, partial, tbuf);
+            k_mr_reduce<W><<<reduce_grid(m, node_lo, p.nnodes, s), 256, 0, st>>>(p, m, node_lo, s, spad, partial, tbuf);
             e = cudaGetLastError();
             if (e != cudaSuccess) return e;
         }
@@ -560,6 +1241,91 @@ cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typena
 }  // namespace
 
 // ------------------------------------------------------------------ plan
+
+// Fragment slabs for the policy of the handle's leaf (= working) format.
+template <class Pol>
+hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
+    constexpr int MT = 32 / Pol::MR;
+    const auto& nodes = *in.nodes;
+    const auto& chunks = *in.chunks;
+    const auto& leaves = *in.leaves;
+    const int nlev = in.nlev, lev_lo = in.lev_lo;
+    for (const ChunkDesc& c : chunks) {
+        const LeafDesc& l = leaves[c.leaf];
+        if (c.nrows != kChunk || l.m != kChunk || l.row0 != c.row0 || l.fmt != in.leaf_fmt) return HODLR_OK;
+    }
+    Mr2View& v = mr.v2;
+    v = Mr2View{};
+    v.nlev = nlev;
+    v.lev_lo = lev_lo;
+    v.leaf_fmt = in.leaf_fmt;
+    const int lfb = fmt_bytes(in.leaf_fmt);
+    v.d_item = MT * 32 * Pol::AR * 4 * lfb;
+    int64_t aoff = 0, uoff = 16LL * v.d_item;
+    for (int lv = lev_lo; lv < nlev; ++lv) {
+        const MrLevel& L = mr.view.lev[lv];
+        Mr2Level& M = v.lev[lv];
+        M.vfmt = M.ufmt = -1;
+        for (int id = L.node0; id < L.node0 + L.nnodes; ++id) {
+            const NodeDesc& nd = nodes[id];
+            if (nd.rv > 0) {
+                if (M.vfmt >= 0 && M.vfmt != nd.v_fmt) return HODLR_OK;  // one format per level
+                M.vfmt = nd.v_fmt;
+            }
+            if (nd.ru > 0) {
+                if (M.ufmt >= 0 && M.ufmt != nd.u_fmt) return HODLR_OK;
+                M.ufmt = nd.u_fmt;
+            }
+        }
+        if (M.vfmt < 0) M.vfmt = HODLR_FMT_FP32;
+        if (M.ufmt < 0) M.ufmt = HODLR_FMT_FP32;
+        if (sizeof(typename Pol::W) == 4 && (M.vfmt == HODLR_FMT_FP64 || M.ufmt == HODLR_FMT_FP64)) return HODLR_OK;
+        M.nmt = (L.rv_max + Pol::MR - 1) / Pol::MR;
+        M.ablk = 32 * Pol::AR * 4 * fmt_bytes(M.vfmt);
+        M.aoff = aoff;
+        aoff += (int64_t)M.nmt * 16 * M.ablk;
+        M.steps = (L.ru_max + Pol::KU - 1) / Pol::KU;
+        M.usz = MT * 32 * Pol::AR * Pol::UV * fmt_bytes(M.ufmt);
+        uoff = (uoff + M.usz - 1) / M.usz * M.usz;  // a step never straddles a ring item
+        M.uoff = uoff;
+        uoff += (int64_t)M.steps * M.usz;
+        v.ntasks += M.nmt;
+        v.nu_items += M.steps;
+        v.max_ablk = std::max(v.max_ablk, M.ablk);
+    }
+    if (v.max_ablk == 0) v.max_ablk = 128;
+    v.a_chunk_bytes = (aoff + 127) / 128 * 128;
+    v.warp_bytes = (int32_t)((uoff + 127) / 128 * 128);
+    v.b_chunk_bytes = 8LL * v.warp_bytes;
+    const size_t a_bytes = (size_t)v.a_chunk_bytes * chunks.size();
+    const size_t b_bytes = (size_t)v.b_chunk_bytes * chunks.size();
+    void* d = nullptr;
+    if (cudaMalloc(&d, a_bytes + b_bytes + 256) != cudaSuccess) {
+        cudaGetLastError();
+        return HODLR_OK;  // no room for a second copy: the arena kernels serve
+    }
+    v.slab_a = (const uint8_t*)d;
+    v.slab_b = (const uint8_t*)d + (a_bytes + 255) / 256 * 256;
+    cudaError_t e = cudaSuccess;
+    if (a_bytes) {
+        k_slab_a<Pol><<<148 * 8, 256>>>(*in.view, v, (uint8_t*)v.slab_a);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+        k_slab_b<Pol><<<148 * 8, 256>>>(*in.view, v, (uint8_t*)v.slab_b);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return HODLR_ERR_CUDA;
+    }
+    mr.slab_dev = d;
+    mr.slab_ok = true;
+    mr.slab_fmt = sizeof(typename Pol::W) == 8 ? HODLR_FMT_FP64 : HODLR_FMT_FP32;
+    return HODLR_OK;
+}
+
 hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
     mr = MrPlan{};
     const auto& nodes = *in.nodes;
@@ -634,13 +1400,27 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
     }
     v.slots = (const MrSlot*)mr.dev;
     mr.ok = true;
+    if (in.view && in.d_arena && !getenv("HODLR_B200_NO_SLAB")) {
+        hodlr_status st = HODLR_OK;
+        if (in.leaf_fmt == HODLR_FMT_FP64)
+            st = build_slab<PolF64>(in, mr);
+        else if (in.leaf_fmt == HODLR_FMT_FP32)
+            st = build_slab<PolTF32>(in, mr);
+        if (st != HODLR_OK) {
+            mr_release(mr);
+            return st;
+        }
+    }
     return HODLR_OK;
 }
 
 void mr_release(MrPlan& mr) {
     if (mr.dev) cudaFree(mr.dev);
+    if (mr.slab_dev) cudaFree(mr.slab_dev);
     mr.dev = nullptr;
+    mr.slab_dev = nullptr;
     mr.ok = false;
+    mr.slab_ok = false;
 }
 
 bool mr_usable(const MrPlan& mr, int working_fmt) {
@@ -652,6 +1432,10 @@ bool mr_usable(const MrPlan& mr, int working_fmt) {
 }
 
 int mr_launches() { return 3; }
+
+bool mr_slab_used(const MrPlan& mr, int working_fmt, int lev_lo) {
+    return mr.slab_ok && mr.slab_fmt == working_fmt && mr.v2.lev_lo == lev_lo && !getenv("HODLR_B200_NO_SLAB");
+}
 
 template <>
 cudaError_t mr_matvec<double>(const PlanView& p, const MrPlan& mr, int lev_lo, const double* x, int64_t ldx,

@@ -51,8 +51,45 @@ struct MrView {
     MrLevel lev[kMrMaxLevels];
 };
 
+// Fragment slabs (uniform trees: every leaf one 256-row chunk, one storage
+// format per level): the quantised factors and leaves re-ordered, per chunk,
+// into exactly the sequence of MMA operand fragments the kernels consume, so
+// each warp streams contiguous bytes with cp.async.bulk into a private ring.
+//   A region (phase A), per chunk: level-major, m-tile-major, 16 k-blocks
+//     (one k-block = 32 lanes x AR rows x 4 consecutive rows of V').
+//   B region (phase B), per chunk and warp (rows 32w..32w+31): 16 D items
+//     (one per 16-column k step: MT m-tiles x 32 lanes x AR x 4 values), then
+//     the U items of every level (one per KU-column step).
+struct Mr2Level {
+    int32_t nmt;      // phase-A m-tiles (ceil(rv_max / MR))
+    int32_t vfmt;     // V' storage format of the level
+    int32_t ablk;     // bytes of one A k-block
+    int32_t steps;    // U steps (ceil(ru_max / KU))
+    int32_t ufmt;     // U storage format of the level
+    int32_t usz;      // bytes of one U item
+    int64_t aoff;     // offset of the level's A blocks in a chunk's A region
+    int64_t uoff;     // offset of the level's first U item in a warp's B region
+};
+struct Mr2View {
+    int32_t nlev, lev_lo;      // levels lev_lo..nlev-1 are in the slab
+    int32_t ntasks;            // phase-A tasks (m-tiles) per chunk
+    int32_t nu_items;          // U items per warp per chunk
+    int64_t a_chunk_bytes, b_chunk_bytes;
+    int32_t warp_bytes;        // B bytes per warp per chunk
+    int32_t d_item;            // bytes of one D item
+    int32_t leaf_fmt;
+    int32_t max_ablk;
+    const uint8_t* slab_a;
+    const uint8_t* slab_b;
+    Mr2Level lev[kMrMaxLevels];
+};
+
 struct MrPlan {
     bool ok = false;
+    bool slab_ok = false;      // fragment slabs built (for the working precision slab_fmt)
+    int slab_fmt = -1;
+    Mr2View v2{};
+    void* slab_dev = nullptr;
     bool has_fp64_operand = false;  // an fp64 factor or leaf: the TF32 kind cannot take it
     int leaf_fmt = HODLR_FMT_FP64;
     MrView view{};
@@ -61,6 +98,9 @@ struct MrPlan {
 };
 
 struct MrInput {
+    const PlanView* view;      // device tables of the handle (for the relayout kernels)
+    const uint8_t* d_arena;    // quantised level-batched arena (device)
+    int lev_lo;                // first level handled by the multi-RHS kernels
     const std::vector<NodeDesc>* nodes;
     const std::vector<ChunkDesc>* chunks;
     const std::vector<LeafDesc>* leaves;
@@ -77,6 +117,8 @@ inline int64_t mr_spad(int64_t s) { return (s + 7) / 8 * 8; }
 inline int64_t mr_part_elems(const MrPlan& mr, int64_t s) { return mr.view.part_rows * mr_spad(s); }
 // true if the multi-RHS kernels take this call
 bool mr_usable(const MrPlan& mr, int working_fmt);
+// true if such a call runs the fragment-slab kernels
+bool mr_slab_used(const MrPlan& mr, int working_fmt, int lev_lo);
 int mr_launches();
 // Levels lev_lo..nlev-1 only (lev_lo = L on a sharded handle: the external
 // levels run in kernels_shard.cu).  `send` receives external-level sums when

@@ -56,10 +56,13 @@ def xin(X, working):
 
 @pytest.mark.parametrize("working,fmts", FMT_SETS)
 @pytest.mark.parametrize("s", [2, 8, 16, 33, 64])
-def test_mrhs_matches_oracle_and_generic(cuda, working, fmts, s):
-    H = random_hodlr(4096, 3, fmts, [24, 17, 9], working, seed=s + len(fmts[0]))
+@pytest.mark.parametrize("n,path", [(4096, "mrhs"), (2048, "mrhs_slab")])
+def test_mrhs_matches_oracle_and_generic(cuda, working, fmts, s, n, path):
+    """n=4096, depth 3: 512-row leaves (two chunks each) -> arena kernels;
+    n=2048: 256-row leaves -> fragment-slab kernels."""
+    H = random_hodlr(n, 3, fmts, [24, 17, 9], working, seed=s + len(fmts[0]))
     op = make_op(H)
-    assert op.path(s) == ("mrhs", 3)
+    assert op.path(s) == (path, 3)
     X = np.random.default_rng(s).standard_normal((H.n, s))
     B = run(cuda, op, X, working)
     tol = 1e-12 if working == "fp64" else 1e-5
@@ -73,12 +76,13 @@ def test_mrhs_matches_oracle_and_generic(cuda, working, fmts, s):
 def test_mrhs_variable_ranks_and_rank_zero(cuda, working):
     """Per-node ranks differ inside a level (cfg3-like), some are 0."""
     fmts = ["fp32", "fp16", "bf16", "fp32"] if working == "fp32" else ["fp64", "fp32", "q52", "fp16"]
-    H = random_hodlr(4096, 4, fmts, [(30, 45), (0, 20), (5, 12), (0, 3)], working, seed=3)
-    op = make_op(H)
-    assert op.path(16)[0] == "mrhs"
-    X = np.random.default_rng(2).standard_normal((H.n, 16))
-    tol = 1e-12 if working == "fp64" else 1e-5
-    assert rel(run(cuda, op, X, working), matvec_oracle(H, xin(X, working))) <= tol
+    for n in (8192, 4096):  # 512-row leaves (arena kernels), 256-row leaves (slabs)
+        H = random_hodlr(n, 4, fmts, [(30, 45), (0, 20), (5, 12), (0, 3)], working, seed=3)
+        op = make_op(H)
+        assert op.path(16)[0] == ("mrhs" if n == 8192 else "mrhs_slab")
+        X = np.random.default_rng(2).standard_normal((H.n, 16))
+        tol = 1e-12 if working == "fp64" else 1e-5
+        assert rel(run(cuda, op, X, working), matvec_oracle(H, xin(X, working))) <= tol
 
 
 @pytest.mark.parametrize("working", ["fp64", "fp32"])
@@ -98,7 +102,7 @@ def test_mrhs_fp64_operand_under_fp32_working_uses_generic(cuda):
     H = random_hodlr(2048, 3, ["fp64", "fp32", "fp16"], [8, 6, 4], "fp32", seed=1)
     op = make_op(H)
     assert op.path(8)[0] == "generic"
-    assert op.path(8, "fp64")[0] == "mrhs"
+    assert op.path(8, "fp64")[0] == "mrhs"  # fp32 leaves: no fp64 slab, arena kernels
 
 
 def test_mrhs_golden_cases(cuda):
@@ -115,6 +119,7 @@ def test_mrhs_golden_cases(cuda):
 def test_mrhs_deterministic(cuda):
     H = random_hodlr(8192, 5, ["fp32"] * 5, [12, 10, 9, 7, 6], "fp64", seed=4)
     op = make_op(H)
+    assert op.path(16)[0] == "mrhs_slab"
     X = np.random.default_rng(0).standard_normal((H.n, 16))
     a = run(cuda, op, X, "fp64")
     b = run(cuda, op, X, "fp64")
@@ -129,6 +134,28 @@ def test_mrhs_sharded_subtree(cuda, nranks, working):
     H = random_hodlr(8192, 5, ["fp32", "bf16", "fp16", "q52", "fp32"], [12, 10, 9, 7, 6], working, seed=5)
     X = np.random.default_rng(3).standard_normal((H.n, 16))
     out, ops = run_emulated(cuda, H, X, nranks)
-    assert all(op.path(16)[0] == "mrhs" for op in ops)
+    assert all(op.path(16)[0] == "mrhs_slab" for op in ops)
     tol = 1e-12 if working == "fp64" else 1e-5
     assert rel(out, matvec_oracle(H, xin(X, working))) <= tol
+
+
+@pytest.mark.parametrize("working", ["fp64", "fp32"])
+def test_mrhs_slab_matches_arena_kernels(cuda, working):
+    """The fragment-slab kernels and the arena kernels on one matrix."""
+    fmts = ["fp32", "fp16", "bf16", "q52", "fp32"]
+    H = random_hodlr(8192, 5, fmts, [(20, 40), 16, (0, 9), 7, 5], working, seed=8)
+    X = np.random.default_rng(4).standard_normal((H.n, 24))
+    a = run(cuda, make_op(H), X, working)
+    old = os.environ.get("HODLR_B200_NO_SLAB")
+    os.environ["HODLR_B200_NO_SLAB"] = "1"
+    try:
+        op2 = make_op(H)
+        assert op2.path(24)[0] == "mrhs"
+        b = run(cuda, op2, X, working)
+    finally:
+        if old is None:
+            del os.environ["HODLR_B200_NO_SLAB"]
+        else:
+            os.environ["HODLR_B200_NO_SLAB"] = old
+    tol = 1e-13 if working == "fp64" else 1e-6
+    assert rel(a, b) <= tol

@@ -1,0 +1,37 @@
+"""Summarise an ncu report: duration, DRAM traffic/throughput, issue activity, pipes, stall reasons."""
+import csv
+import io
+import subprocess
+import sys
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size",
+        "launch__registers_per_thread", "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers",
+        "sm__warps_active.avg.per_cycle_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "sm__cycles_elapsed.avg.per_second"]
+
+
+def main(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")][:80] if "Kernel Name" in hdr else "?"
+        print("==", name)
+        for i, h in enumerate(hdr):
+            if h in WANT or ("pipe_tensor" in h and "avg.pct_of_peak_sustained_active" in h and "sm__" in h):
+                print(f"   {h:70s} {r[i]} {units[i]}")
+        stalls = [(float(r[i]) if r[i] not in ("", "n/a") else 0.0, h) for i, h in enumerate(hdr)
+                  if h.startswith("smsp__average_warp_latency_issue_stalled_") and h.endswith(".ratio")]
+        stalls = sorted(stalls, reverse=True)[:8]
+        if stalls:
+            print("   stalls (cycles per issued instr):", ", ".join(f"{h.split('stalled_')[1].split('.')[0]}={v:.1f}" for v, h in stalls))
+
+
+if __name__ == "__main__":
+    for p in sys.argv[1:]:
+        main(p)
