@@ -36,6 +36,8 @@ constexpr int kMrThreads = 256;
 constexpr int kMrWarps = kMrThreads / 32;
 constexpr int kChunk = 256;            // rows per chunk (plan.h chunks are <= 256 rows)
 constexpr size_t kMrSmemTarget = 110 * 1024;  // keep two CTAs per SM
+constexpr int kBWarps = 16;                  // slab phase-B CTA: 16 warps ...
+constexpr int kBRows = kChunk / kBWarps;     // ... of 16 chunk rows each
 
 // ------------------------------------------------------------------ operand loads
 template <typename W>
@@ -138,6 +140,23 @@ struct PolF64 {
     __device__ static __forceinline__ void mmau(W (&c)[CR], const AUF& a, const BUF& b) {
         dmma884(c, a.v[0][0], b.v[0]);
     }
+    // whole warp tile, independent accumulators interleaved between dependent MMAs
+    template <int MT, int NT>
+    __device__ static __forceinline__ void mma16_tile(W (&c)[MT][NT][CR], const AF (&a)[MT], const BF (&b)[NT]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt], a[mt].v[0][j], b[nt].v[j]);
+    }
+    template <int MT, int NT>
+    __device__ static __forceinline__ void mmau_tile(W (&c)[MT][NT][CR], const AUF (&a)[MT], const BUF (&b)[NT]) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt], a[mt].v[0][0], b[nt].v[0]);
+    }
 };
 
 struct PolTF32 {
@@ -184,6 +203,47 @@ struct PolTF32 {
         tmma(c, a.h[0][0], a.h[1][0], a.h[0][1], a.h[1][1], b.l[0], b.l[1]);
         tmma(c, a.l[0][0], a.l[1][0], a.l[0][1], a.l[1][1], b.h[0], b.h[1]);
         tmma(c, a.h[0][0], a.h[1][0], a.h[0][1], a.h[1][1], b.h[0], b.h[1]);
+    }
+    // whole warp tile, independent accumulators interleaved between dependent MMAs
+    template <int MT, int NT>
+    __device__ static __forceinline__ void mma16_tile(W (&c)[MT][NT][CR], const AF (&a)[MT], const BF (&b)[NT]) {
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int j0 = 2 * p, j1 = 2 * p + 1;
+#pragma unroll
+            for (int pass = 0; pass < 3; ++pass)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const auto& A = a[mt];
+                        const auto& B = b[nt];
+                        if (pass == 0)
+                            tmma(c[mt][nt], A.h[0][j0], A.h[1][j0], A.h[0][j1], A.h[1][j1], B.l[j0], B.l[j1]);
+                        else if (pass == 1)
+                            tmma(c[mt][nt], A.l[0][j0], A.l[1][j0], A.l[0][j1], A.l[1][j1], B.h[j0], B.h[j1]);
+                        else
+                            tmma(c[mt][nt], A.h[0][j0], A.h[1][j0], A.h[0][j1], A.h[1][j1], B.h[j0], B.h[j1]);
+                    }
+        }
+    }
+    template <int MT, int NT>
+    __device__ static __forceinline__ void mmau_tile(W (&c)[MT][NT][CR], const AUF (&a)[MT], const BUF (&b)[NT]) {
+#pragma unroll
+        for (int pass = 0; pass < 3; ++pass)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const auto& A = a[mt];
+                    const auto& B = b[nt];
+                    if (pass == 0)
+                        tmma(c[mt][nt], A.h[0][0], A.h[1][0], A.h[0][1], A.h[1][1], B.l[0], B.l[1]);
+                    else if (pass == 1)
+                        tmma(c[mt][nt], A.l[0][0], A.l[1][0], A.l[0][1], A.l[1][1], B.h[0], B.h[1]);
+                    else
+                        tmma(c[mt][nt], A.h[0][0], A.h[1][0], A.h[0][1], A.h[1][1], B.h[0], B.h[1]);
+                }
     }
 };
 
@@ -596,9 +656,9 @@ __global__ void k_slab_a(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
 
 template <class Pol>
 __global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t* __restrict__ slab) {
-    constexpr int MT = 32 / Pol::MR;
+    constexpr int MT = kBRows / Pol::MR;
     // D part: one thread per (chunk, warp, kb, mt, lane, a): 4 consecutive leaf columns
-    const int64_t dper = 8LL * 16 * MT * 32 * Pol::AR;
+    const int64_t dper = (int64_t)kBWarps * 16 * MT * 32 * Pol::AR;
     const int64_t dtotal = dper * p.nchunks;
     const int lfb = fmt_bytes(v.leaf_fmt);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dtotal; i += (int64_t)gridDim.x * blockDim.x) {
@@ -611,7 +671,7 @@ __global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
         const int w = (int)(r / 16);
         const ChunkDesc ch = p.chunks[chunk];
         const LeafDesc lf = p.leaves[ch.leaf];
-        const int row = (ch.row0 - lf.row0) + 32 * w + mt * Pol::MR + (lane >> 2) + 8 * a;
+        const int row = (ch.row0 - lf.row0) + kBRows * w + mt * Pol::MR + (lane >> 2) + 8 * a;
         const int col = kb * 16 + 4 * (lane & 3);
         const uint8_t* src = p.arena + lf.off + ((int64_t)row * lf.ld + col) * lfb;
         uint8_t* blk = slab + (int64_t)chunk * v.b_chunk_bytes + (int64_t)w * v.warp_bytes + (int64_t)kb * v.d_item +
@@ -624,11 +684,11 @@ __global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
     // U part: one thread per (chunk, warp, level, step, mt, lane, a, u): one element
     int64_t uper = 0;
     for (int lv = v.lev_lo; lv < v.nlev; ++lv) uper += (int64_t)v.lev[lv].steps * MT * 32 * Pol::AR * Pol::UV;
-    const int64_t utotal = uper * 8 * p.nchunks;
+    const int64_t utotal = uper * kBWarps * p.nchunks;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < utotal; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t cw = i / uper;
         int64_t r = i - cw * uper;
-        const int chunk = (int)(cw / 8), w = (int)(cw % 8);
+        const int chunk = (int)(cw / kBWarps), w = (int)(cw % kBWarps);
         int lv = v.lev_lo;
         for (;; ++lv) {
             const int64_t c = (int64_t)v.lev[lv].steps * MT * 32 * Pol::AR * Pol::UV;
@@ -644,7 +704,7 @@ __global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
         const int fb = fmt_bytes(L.ufmt);
         const ChunkDesc ch = p.chunks[chunk];
         const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
-        const int row = (ch.row0 - nd.row0) + 32 * w + mt * Pol::MR + (lane >> 2) + 8 * a;
+        const int row = (ch.row0 - nd.row0) + kBRows * w + mt * Pol::MR + (lane >> 2) + 8 * a;
         const int c = step * Pol::KU + Pol::UV * (lane & 3) + u;
         uint8_t* dst = slab + (int64_t)chunk * v.b_chunk_bytes + (int64_t)w * v.warp_bytes + L.uoff +
                        (int64_t)step * L.usz + (int64_t)mt * 32 * Pol::AR * Pol::UV * fb +
@@ -742,30 +802,64 @@ constexpr int kRingMax = 4;  // max slots per warp ring (runtime depth ns <= kRi
 
 // ------------------------------------------------------------------ per-warp ring
 // A warp-private ring of `ns` slots of `slot` bytes, filled by lane 0 with
-// cp.async.bulk (complete_tx on the slot's mbarrier).  Item i lives in slot
-// i % ns; its (i / ns)-th fill completes phase parity (i / ns) & 1.  An item is
-// released (refilled with item i + ns) right after the warp has READ its last
-// sub-block into registers, before the math on it, so ns items stay in flight.
+// cp.async.bulk (complete_tx on the slot's mbarrier).  Items are consumed in
+// order; the consumer state (slot, phase parity) advances by one per item.  An
+// item is released -- its slot refilled with the producer's next item -- right
+// after the warp has READ its last sub-block into registers, before the math,
+// so ns items stay in flight.
 struct WarpRing {
     uint64_t* bar;
     uint8_t* buf;
     int ns, slot;
-    __device__ __forceinline__ const uint8_t* wait(int64_t i) const {
-        const int k = (int)(i % ns);
-        tma::mbar_wait(&bar[k], (unsigned)((i / ns) & 1));
-        return buf + (size_t)k * slot;
+    int cs = 0;
+    unsigned cph = 0;
+    __device__ __forceinline__ const uint8_t* wait() const {
+        tma::mbar_wait(&bar[cs], cph);
+        return buf + cs * slot;
     }
-    __device__ __forceinline__ void fill(int64_t i, const void* src, unsigned bytes, uint64_t pol) const {
-        const int k = (int)(i % ns);
+    __device__ __forceinline__ int advance() {
+        const int k = cs;
+        if (++cs == ns) {
+            cs = 0;
+            cph ^= 1u;
+        }
+        return k;
+    }
+    __device__ __forceinline__ void fill(int k, const void* src, unsigned bytes, uint64_t pol) const {
         tma::mbar_arrive_tx(&bar[k], bytes);
-        tma::bulk_g2s(buf + (size_t)k * slot, src, bytes, &bar[k], pol);
+        tma::bulk_g2s(buf + k * slot, src, bytes, &bar[k], pol);
     }
 };
+
+__device__ __forceinline__ void cp_async(void* dst, const void* src, int bytes) {
+    if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(tma::smem_u32(dst)), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tma::smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Asynchronous stage_x (cp.async, element copies into fragment order); zero
+// padding is stored directly.  Complete after cp_async_wait_all + a barrier.
+template <typename W>
+__device__ __forceinline__ void stage_x_async(W* xs, const W* __restrict__ x, int64_t ldx, int64_t r0, int nrows,
+                                              int64_t q0, int ncol, int64_t s) {
+    const int nct = ncol >> 3;
+    for (int i = threadIdx.x; i < kChunk * ncol; i += blockDim.x) {
+        const int r = i / ncol, q = i - r * ncol;
+        W* dst = xs + xfrag<W>(r, q, nct);
+        if (r < nrows && q0 + q < s)
+            cp_async(dst, x + (r0 + r) * ldx + q0 + q, (int)sizeof(W));
+        else
+            *dst = W(0);
+    }
+}
 
 // ------------------------------------------------------------------ MA2
 // Persistent-range phase A over the A slab.  Warp w's stream: for every chunk
 // of the CTA's run, for its tasks t = w, w+8, ... (m-tiles of all levels), the
-// task's 16 k-blocks in items of kbi blocks (<= 4 KB).
+// task's 16 k-blocks in items of kbi blocks (<= 4 KB).  X of the next chunk is
+// staged (cp.async) into the other buffer while the current one is consumed.
 template <class Pol, int NCT>
 __global__ void __launch_bounds__(kMrThreads) k_mr2_a(PlanView p, const __grid_constant__ MrView m,
                                                       const __grid_constant__ Mr2View v,
@@ -776,71 +870,86 @@ __global__ void __launch_bounds__(kMrThreads) k_mr2_a(PlanView p, const __grid_c
     constexpr int ncol = NCT * 8;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                 // [8][kRingMax]
-    W* xs = reinterpret_cast<W*>(smem_raw + 8 * kRingMax * 8);              // [256 x ncol]
-    W* accs = xs + kChunk * ncol;                                           // [task][NCT][32][CR]
+    W* xsb = reinterpret_cast<W*>(smem_raw + 8 * kRingMax * 8);             // [2][256 x ncol]
+    W* accs = xsb + 2 * kChunk * ncol;                                      // [task][NCT][32][CR]
     uint8_t* ring = reinterpret_cast<uint8_t*>(accs + (size_t)v.ntasks * NCT * 32 * Pol::CR);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, tig = lane & 3;
     const int64_t q0 = (int64_t)blockIdx.y * ncol;
     const int c_beg = (int)((int64_t)blockIdx.x * p.nchunks / gridDim.x);
     const int c_end = (int)((int64_t)(blockIdx.x + 1) * p.nchunks / gridDim.x);
-    const WarpRing R{bars + warp * kRingMax, ring + (size_t)warp * ns * slot_bytes, ns, slot_bytes};
+    WarpRing R{bars + warp * kRingMax, ring + (size_t)warp * ns * slot_bytes, ns, slot_bytes};
     const int ipt = 16 / kbi;                                   // items per task
     const int my_tasks = warp < v.ntasks ? (v.ntasks - 1 - warp) / kMrWarps + 1 : 0;
-    const int64_t per_chunk = (int64_t)my_tasks * ipt;
-    const int64_t nitems = (int64_t)(c_end - c_beg) * per_chunk;
     const uint64_t pol = tma::policy_evict_first();
 
-    auto issue = [&](int64_t it) {
-        const int ci = c_beg + (int)(it / per_chunk);
-        const int64_t r = it - (int64_t)(ci - c_beg) * per_chunk;
-        const int tt = (int)(r / ipt);
-        const int kb0 = (int)(r - (int64_t)tt * ipt) * kbi;
-        int mt = warp + tt * kMrWarps, lv = v.lev_lo;
-        while (mt >= v.lev[lv].nmt) { mt -= v.lev[lv].nmt; ++lv; }
-        const Mr2Level L = v.lev[lv];
-        R.fill(it, v.slab_a + (int64_t)ci * v.a_chunk_bytes + L.aoff + ((int64_t)mt * 16 + kb0) * L.ablk,
-               (unsigned)(kbi * L.ablk), pol);
+    // producer cursor (lane 0): chunk, task of this warp, item within the task
+    int pc = c_beg, ptt = 0, pq = 0;
+    const uint8_t* ptask = nullptr;  // A blocks of (chunk pc, task ptt)
+    int pablk = 0;
+    auto produce = [&](int k) {  // fill slot k with the next item, if any
+        if (pc >= c_end || my_tasks == 0) return;
+        if (pq == 0) {
+            int mt = warp + ptt * kMrWarps, lv = v.lev_lo;
+            while (mt >= v.lev[lv].nmt) { mt -= v.lev[lv].nmt; ++lv; }
+            pablk = v.lev[lv].ablk;
+            ptask = v.slab_a + (int64_t)pc * v.a_chunk_bytes + v.lev[lv].aoff + (int64_t)mt * 16 * pablk;
+        }
+        R.fill(k, ptask + (int64_t)pq * kbi * pablk, (unsigned)(kbi * pablk), pol);
+        if (++pq == ipt) {
+            pq = 0;
+            if (++ptt == my_tasks) {
+                ptt = 0;
+                ++pc;
+            }
+        }
     };
 
     if (lane == 0) {
         for (int i = 0; i < ns; ++i) tma::mbar_init(&R.bar[i], 1);
         tma::fence_mbar_init();
-        for (int64_t i = 0; i < ns && i < nitems; ++i) issue(i);
+        for (int i = 0; i < ns; ++i) produce(i);
     }
     for (int t = warp; t < v.ntasks; t += kMrWarps)
 #pragma unroll
         for (int nt = 0; nt < NCT; ++nt)
 #pragma unroll
             for (int i = 0; i < Pol::CR; ++i) accs[(((size_t)t * NCT + nt) * 32 + lane) * Pol::CR + i] = W(0);
+    if (c_beg < c_end) {
+        const ChunkDesc ch = p.chunks[c_beg];
+        stage_x_async<W>(xsb, x, ldx, ch.row0, ch.nrows, q0, ncol, s);
+    }
 
-    int64_t it = 0;
     for (int ci = c_beg; ci < c_end; ++ci) {
-        const ChunkDesc ch = p.chunks[ci];
-        __syncthreads();  // previous chunk's X consumed (and, first time, barrier inits visible)
-        stage_x<W>(xs, x, ldx, ch.row0, ch.nrows, q0, ncol, s);
-        __syncthreads();
+        W* xs = xsb + ((ci - c_beg) & 1) * kChunk * ncol;
+        cp_async_wait_all();
+        __syncthreads();  // X(ci) staged; every warp is done with X(ci - 1)
+        if (ci + 1 < c_end) {
+            const ChunkDesc nx = p.chunks[ci + 1];
+            stage_x_async<W>(xsb + ((ci + 1 - c_beg) & 1) * kChunk * ncol, x, ldx, nx.row0, nx.nrows, q0, ncol, s);
+        }
         for (int tt = 0; tt < my_tasks; ++tt) {
             const int t = warp + tt * kMrWarps;
             int lv = v.lev_lo, mt = t;
             while (mt >= v.lev[lv].nmt) { mt -= v.lev[lv].nmt; ++lv; }
             const int vfmt = v.lev[lv].vfmt;
             const int ablk = v.lev[lv].ablk;
-            W acc[NCT][Pol::CR];
+            W acc[1][NCT][Pol::CR];
 #pragma unroll
             for (int nt = 0; nt < NCT; ++nt)
 #pragma unroll
-                for (int i = 0; i < Pol::CR; ++i) acc[nt][i] = W(0);
-            for (int q = 0; q < ipt; ++q, ++it) {
-                const uint8_t* base = R.wait(it);
+                for (int i = 0; i < Pol::CR; ++i) acc[0][nt][i] = W(0);
+            for (int q = 0; q < ipt; ++q) {
+                const uint8_t* base = R.wait();
                 for (int k = 0; k < kbi; ++k) {
                     W tmp[Pol::AR * 4];
-                    frag_load<W, Pol::AR * 4>(vfmt, base + (size_t)k * ablk, lane, tmp);
+                    frag_load<W, Pol::AR * 4>(vfmt, base + k * ablk, lane, tmp);
                     if (k == kbi - 1) {  // item fully read: refill its slot
+                        const int ks = R.advance();
                         __syncwarp();
-                        if (lane == 0 && it + ns < nitems) {
+                        if (lane == 0) {
                             tma::fence_proxy_async_smem();
-                            issue(it + ns);
+                            produce(ks);
                         }
                     }
                     W av[Pol::AR][4];
@@ -848,17 +957,17 @@ __global__ void __launch_bounds__(kMrThreads) k_mr2_a(PlanView p, const __grid_c
                     for (int a = 0; a < Pol::AR; ++a)
 #pragma unroll
                         for (int j = 0; j < 4; ++j) av[a][j] = tmp[a * 4 + j];
-                    typename Pol::AF af;
-                    Pol::prep_a(af, av);
+                    typename Pol::AF af[1];
+                    Pol::prep_a(af[0], av);
                     const int kb = q * kbi + k;
+                    typename Pol::BF bf[NCT];
 #pragma unroll
                     for (int nt = 0; nt < NCT; ++nt) {
                         W bv[4];
                         load_bfrag<W>(xs + (kb * NCT + nt) * 128, lane, bv);
-                        typename Pol::BF bf;
-                        Pol::prep_b(bf, bv);
-                        Pol::mma16(acc[nt], af, bf);
+                        Pol::prep_b(bf[nt], bv);
                     }
+                    Pol::template mma16_tile<1, NCT>(acc, af, bf);
                 }
             }
             // accumulate into the task tile; flush at the node's last chunk of this run
@@ -871,7 +980,7 @@ __global__ void __launch_bounds__(kMrThreads) k_mr2_a(PlanView p, const __grid_c
                 W* my = accs + (((size_t)t * NCT + nt) * 32 + lane) * Pol::CR;
 #pragma unroll
                 for (int i = 0; i < Pol::CR; ++i) {
-                    W val = my[i] + acc[nt][i];
+                    W val = my[i] + acc[0][nt][i];
                     if (more) {
                         my[i] = val;
                     } else {
@@ -888,182 +997,234 @@ __global__ void __launch_bounds__(kMrThreads) k_mr2_a(PlanView p, const __grid_c
 }
 
 // ------------------------------------------------------------------ MB2
-// One CTA per (chunk, column group); warp w owns chunk rows 32w..32w+31 and
-// streams its B-region bytes (16 D items, then the U steps of every level
-// packed into items of the same size) through a private ring.
+// Persistent: CTA b takes works (chunk, column group) b, b + grid, ...
+//   warps 0..15  compute: warp w owns chunk rows 16w..16w+15 and streams its
+//                B-region bytes (16 D items, then the U steps of every level,
+//                packed into items of the same size) through a private ring
+//                that runs ahead across works;
+//   warp 16      stager: X and the coefficients of work k+1 into buffer
+//                (k+1)&1 with cp.async while work k is computed
+//                (mbarriers full[2] / empty[2], no block-wide barrier).
 template <class Pol, int NT>
-__global__ void __launch_bounds__(kMrThreads) k_mr2_b(PlanView p, const __grid_constant__ MrView m,
-                                                      const __grid_constant__ Mr2View v,
-                                                      const typename Pol::W* __restrict__ x, int64_t ldx,
-                                                      const typename Pol::W* __restrict__ tbuf,
-                                                      typename Pol::W* __restrict__ b, int64_t ldb, int64_t s,
-                                                      int ngrp, int ns) {
+__global__ void __launch_bounds__((kBWarps + 1) * 32) k_mr2_b(PlanView p, const __grid_constant__ MrView m,
+                                                            const __grid_constant__ Mr2View v,
+                                                            const typename Pol::W* __restrict__ x, int64_t ldx,
+                                                            const typename Pol::W* __restrict__ tbuf,
+                                                            typename Pol::W* __restrict__ b, int64_t ldb, int64_t s,
+                                                            int ngrp, int ns, int trows) {
     using W = typename Pol::W;
-    constexpr int MT = 32 / Pol::MR;
+    constexpr int MT = kBRows / Pol::MR;
     constexpr int ncol = NT * 8;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
-    uint8_t* ring = smem_raw + 8 * kRingMax * 8;
-    const int slot_bytes = v.d_item;
-    W* xs = reinterpret_cast<W*>(ring + (size_t)8 * ns * slot_bytes);
-    W* ts = xs + kChunk * ncol;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);          // [16][kRingMax] rings, then full[2], empty[2]
+    uint64_t* full = bars + kBWarps * kRingMax;
+    uint64_t* empty = full + 2;
+    uint8_t* ring = smem_raw + (kBWarps * kRingMax + 4) * 8;
+    const int slot_bytes = v.d_item, lslot = v.lslot;
+    W* xsb = reinterpret_cast<W*>(ring + (size_t)kBWarps * ns * slot_bytes);  // [2][256 x ncol]
+    W* tsb = xsb + 2 * kChunk * ncol;                                         // [2][trows x ncol]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, tig = lane & 3;
-    const int chunk = blockIdx.x / ngrp;
-    const int64_t q0 = (int64_t)(blockIdx.x - chunk * ngrp) * ncol;
-    const ChunkDesc ch = p.chunks[chunk];
-    const WarpRing R{bars + warp * kRingMax, ring + (size_t)warp * ns * slot_bytes, ns, slot_bytes};
-    const uint8_t* wsrc = v.slab_b + (int64_t)chunk * v.b_chunk_bytes + (int64_t)warp * v.warp_bytes;
-    const int nitems = (v.warp_bytes + slot_bytes - 1) / slot_bytes;
-    const uint64_t pol = tma::policy_evict_first();
-    auto issue = [&](int it) {
-        const int64_t off = (int64_t)it * slot_bytes;
-        const int64_t rem = v.warp_bytes - off;
-        R.fill(it, wsrc + off, (unsigned)(rem < slot_bytes ? rem : slot_bytes), pol);
-    };
-    auto release = [&](int it) {
+    const int nwork = p.nchunks * ngrp;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            tma::mbar_init(&full[i], 32);
+            tma::mbar_init(&empty[i], kBWarps);
+        }
+    }
+    if (warp == kBWarps) {
+        // ---------------- stager
         __syncwarp();
-        if (lane == 0 && it + ns < nitems) {
+        if (lane == 0) tma::fence_mbar_init();
+        asm volatile("bar.sync 1, %0;" ::"n"((kBWarps + 1) * 32));
+        int k = 0;
+        for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++k) {
+            const int buf = k & 1, use = k >> 1;
+            if (use > 0) tma::mbar_wait(&empty[buf], (unsigned)((use - 1) & 1));
+            const int chunk = ngrp == 1 ? work : work / ngrp;
+            const int64_t q0 = (int64_t)(work - chunk * ngrp) * ncol;
+            const ChunkDesc ch = p.chunks[chunk];
+            W* xs = xsb + buf * kChunk * ncol;
+            for (int i = lane; i < kChunk * ncol; i += 32) {
+                const int r = i / ncol, q = i - r * ncol;
+                W* dst = xs + xfrag<W>(r, q, NT);
+                if (r < ch.nrows && q0 + q < s)
+                    cp_async(dst, x + (ch.row0 + r) * ldx + q0 + q, (int)sizeof(W));
+                else
+                    *dst = W(0);
+            }
+            W* ts = tsb + buf * trows * ncol;
+            int base = 0;
+            for (int lv = v.lev_lo; lv < v.nlev; ++lv) {
+                const int steps = v.lev[lv].steps;
+                if (steps == 0) continue;
+                const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
+                const W* t = tbuf + nd.tsrc_off * s;
+                for (int i = lane; i < steps * Pol::KU * ncol; i += 32) {
+                    const int c = i / ncol, q = i - c * ncol;
+                    const int step = c / Pol::KU, w = c - step * Pol::KU;
+                    const int tg = w / Pol::UV, u = w - tg * Pol::UV;
+                    W* dst = ts + base + ((step * NT + (q >> 3)) * 32 + (q & 7) * 4 + tg) * Pol::UV + u;
+                    if (c < nd.ru && q0 + q < s)
+                        cp_async(dst, t + (int64_t)c * s + q0 + q, (int)sizeof(W));
+                    else
+                        *dst = W(0);
+                }
+                base += steps * NT * 32 * Pol::UV;
+            }
+            cp_async_wait_all();
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tma::smem_u32(&full[buf]))
+                         : "memory");
+        }
+        return;
+    }
+
+    // ---------------- compute warps
+    const int g = lane >> 2, tig = lane & 3;
+    WarpRing R{bars + warp * kRingMax, ring + (size_t)warp * ns * slot_bytes, ns, slot_bytes};
+    const int nitems = (v.warp_bytes + slot_bytes - 1) >> lslot;
+    const int last_bytes = v.warp_bytes - ((nitems - 1) << lslot);
+    const uint64_t pol = tma::policy_evict_first();
+    int pw = blockIdx.x, pi = 0;  // producer cursor (lane 0): work, item
+    auto produce = [&](int k) {
+        if (pw >= nwork) return;
+        const int chunk = ngrp == 1 ? pw : pw / ngrp;
+        const uint8_t* src = v.slab_b + (int64_t)chunk * v.b_chunk_bytes + (int64_t)warp * v.warp_bytes +
+                             ((int64_t)pi << lslot);
+        R.fill(k, src, (unsigned)(pi == nitems - 1 ? last_bytes : slot_bytes), pol);
+        if (++pi == nitems) {
+            pi = 0;
+            pw += gridDim.x;
+        }
+    };
+    auto release = [&]() {
+        const int k = R.advance();
+        __syncwarp();
+        if (lane == 0) {
             tma::fence_proxy_async_smem();
-            issue(it + ns);
+            produce(k);
         }
     };
     if (lane == 0) {
         for (int i = 0; i < ns; ++i) tma::mbar_init(&R.bar[i], 1);
         tma::fence_mbar_init();
-        for (int i = 0; i < ns && i < nitems; ++i) issue(i);
     }
-
-    // stage X (leaf rows) and the coefficients of every level (fragment order)
-    stage_x<W>(xs, x, ldx, ch.row0, ch.nrows, q0, ncol, s);
-    {
-        int base = 0;
-        for (int lv = v.lev_lo; lv < v.nlev; ++lv) {
-            const int steps = v.lev[lv].steps;
-            const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
-            const W* t = tbuf + nd.tsrc_off * s;
-            for (int i = threadIdx.x; i < steps * Pol::KU * ncol; i += blockDim.x) {
-                const int c = i / ncol, q = i - c * ncol;
-                W val = W(0);
-                if (c < nd.ru && q0 + q < s) val = t[(int64_t)c * s + q0 + q];
-                const int step = c / Pol::KU, w = c - step * Pol::KU;
-                const int tg = w / Pol::UV, u = w - tg * Pol::UV;
-                ts[base + ((step * NT + (q >> 3)) * 32 + (q & 7) * 4 + tg) * Pol::UV + u] = val;
-            }
-            base += steps * NT * 32 * Pol::UV;
-        }
-    }
-    __syncthreads();
-
-    W acc[MT][NT][Pol::CR];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-            for (int i = 0; i < Pol::CR; ++i) acc[mt][nt][i] = W(0);
+    asm volatile("bar.sync 1, %0;" ::"n"((kBWarps + 1) * 32));  // all barrier inits visible
+    if (lane == 0)
+        for (int i = 0; i < ns; ++i) produce(i);
 
     const int lfmt = v.leaf_fmt;
     const int lfb = fmt_bytes(lfmt);
-    // D items: k-step kb (exactly one item each)
-    for (int kb = 0; kb < 16; ++kb) {
-        const uint8_t* base = R.wait(kb);
-        W tmp[MT][Pol::AR * 4];
+    int k = 0;
+    for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++k) {
+        const int buf = k & 1;
+        const int chunk = ngrp == 1 ? work : work / ngrp;
+        const int64_t q0 = (int64_t)(work - chunk * ngrp) * ncol;
+        tma::mbar_wait(&full[buf], (unsigned)((k >> 1) & 1));
+        const W* xs = xsb + buf * kChunk * ncol;
+        const W* ts = tsb + buf * trows * ncol;
+
+        W acc[MT][NT][Pol::CR];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
-            frag_load<W, Pol::AR * 4>(lfmt, base + (size_t)mt * 32 * Pol::AR * 4 * lfb, lane, tmp[mt]);
-        release(kb);
-        typename Pol::AF af[MT];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            W av[Pol::AR][4];
+            for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-            for (int a = 0; a < Pol::AR; ++a)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) av[a][j] = tmp[mt][a * 4 + j];
-            Pol::prep_a(af[mt], av);
-        }
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            W bv[4];
-            load_bfrag<W>(xs + (kb * NT + nt) * 128, lane, bv);
-            typename Pol::BF bf;
-            Pol::prep_b(bf, bv);
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) Pol::mma16(acc[mt][nt], af[mt], bf);
-        }
-    }
-    // U steps, level by level; several steps per item
-    int tbase = 0;
-    int held = -1;
-    const uint8_t* hbase = nullptr;
-    for (int lv = v.lev_lo; lv < v.nlev; ++lv) {
-        const Mr2Level L = v.lev[lv];
-        const int ufb = fmt_bytes(L.ufmt);
-        for (int step = 0; step < L.steps; ++step) {
-            const int64_t off = L.uoff + (int64_t)step * L.usz;
-            const int item = (int)(off / slot_bytes);
-            if (item != held) {
-                hbase = R.wait(item);
-                held = item;
-            }
-            const uint8_t* base = hbase + (off - (int64_t)item * slot_bytes);
-            W tmp[MT][Pol::AR * Pol::UV];
+                for (int i = 0; i < Pol::CR; ++i) acc[mt][nt][i] = W(0);
+
+        // D items: k-step kb (exactly one item each)
+        for (int kb = 0; kb < 16; ++kb) {
+            const uint8_t* base = R.wait();
+            W tmp[MT][Pol::AR * 4];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
-                frag_load<W, Pol::AR * Pol::UV>(L.ufmt, base + (size_t)mt * 32 * Pol::AR * Pol::UV * ufb, lane,
-                                                tmp[mt]);
-            // next step's item (or none): release this one once it is fully read
-            int64_t noff = -1;
-            if (step + 1 < L.steps) {
-                noff = off + L.usz;
-            } else {
-                for (int l2 = lv + 1; l2 < v.nlev; ++l2)
-                    if (v.lev[l2].steps > 0) {
-                        noff = v.lev[l2].uoff;
-                        break;
-                    }
-            }
-            if (noff < 0 || (int)(noff / slot_bytes) != item) release(item);
-            typename Pol::AUF af[MT];
+                frag_load<W, Pol::AR * 4>(lfmt, base + mt * 32 * Pol::AR * 4 * lfb, lane, tmp[mt]);
+            release();
+            typename Pol::AF af[MT];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-                W av[Pol::AR][Pol::UV];
+                W av[Pol::AR][4];
 #pragma unroll
                 for (int a = 0; a < Pol::AR; ++a)
 #pragma unroll
-                    for (int u = 0; u < Pol::UV; ++u) av[a][u] = tmp[mt][a * Pol::UV + u];
-                Pol::prep_au(af[mt], av);
+                    for (int j = 0; j < 4; ++j) av[a][j] = tmp[mt][a * 4 + j];
+                Pol::prep_a(af[mt], av);
             }
+            typename Pol::BF bf[NT];
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-                W bv[Pol::UV];
-#pragma unroll
-                for (int u = 0; u < Pol::UV; ++u) bv[u] = ts[tbase + ((step * NT + nt) * 32 + lane) * Pol::UV + u];
-                typename Pol::BUF bf;
-                Pol::prep_bu(bf, bv);
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) Pol::mmau(acc[mt][nt], af[mt], bf);
+                W bv[4];
+                load_bfrag<W>(xs + (kb * NT + nt) * 128, lane, bv);
+                Pol::prep_b(bf[nt], bv);
             }
+            Pol::template mma16_tile<MT, NT>(acc, af, bf);
         }
-        tbase += L.steps * NT * 32 * Pol::UV;
-    }
+        // U steps, level by level; several steps per item, a step never straddles items
+        int tbase = 0;
+        const uint8_t* hbase = nullptr;
+        for (int lv = v.lev_lo; lv < v.nlev; ++lv) {
+            const Mr2Level& L = v.lev[lv];
+            const int steps = L.steps;
+            if (steps == 0) continue;
+            const int ufmt = L.ufmt, usz = L.usz;
+            const int ufb = fmt_bytes(ufmt);
+            int lo = L.ulo;
+            for (int step = 0; step < steps; ++step, lo += usz) {
+                const int ioff = lo & (slot_bytes - 1);
+                if (hbase == nullptr) hbase = R.wait();
+                const uint8_t* base = hbase + ioff;
+                W tmp[MT][Pol::AR * Pol::UV];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-            for (int i = 0; i < Pol::CR; i += 2) {
-                const int row = warp * 32 + mt * Pol::MR + g + 8 * (i >> 1);
-                const int64_t q = q0 + nt * 8 + 2 * tig;
-                W* dst = b + (int64_t)(ch.row0 + row) * ldb + q;
-                if (q + 1 < s) {
-                    dst[0] = acc[mt][nt][i];
-                    dst[1] = acc[mt][nt][i + 1];
-                } else if (q < s) {
-                    dst[0] = acc[mt][nt][i];
+                for (int mt = 0; mt < MT; ++mt)
+                    frag_load<W, Pol::AR * Pol::UV>(ufmt, base + mt * 32 * Pol::AR * Pol::UV * ufb, lane, tmp[mt]);
+                const int nlo = step + 1 < steps ? lo + usz : L.unext;
+                if (nlo < 0 || (nlo >> lslot) != (lo >> lslot)) {  // item fully read
+                    release();
+                    hbase = nullptr;
                 }
+                typename Pol::AUF af[MT];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    W av[Pol::AR][Pol::UV];
+#pragma unroll
+                    for (int a = 0; a < Pol::AR; ++a)
+#pragma unroll
+                        for (int u = 0; u < Pol::UV; ++u) av[a][u] = tmp[mt][a * Pol::UV + u];
+                    Pol::prep_au(af[mt], av);
+                }
+                typename Pol::BUF bf[NT];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    W bv[Pol::UV];
+#pragma unroll
+                    for (int u = 0; u < Pol::UV; ++u) bv[u] = ts[tbase + ((step * NT + nt) * 32 + lane) * Pol::UV + u];
+                    Pol::prep_bu(bf[nt], bv);
+                }
+                Pol::template mmau_tile<MT, NT>(acc, af, bf);
             }
+            tbase += steps * NT * 32 * Pol::UV;
+        }
+        // buffer consumed
+        __syncwarp();
+        if (lane == 0) tma::mbar_arrive(&empty[buf]);
+        const int row0 = p.chunks[chunk].row0;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int i = 0; i < Pol::CR; i += 2) {
+                    const int row = warp * kBRows + mt * Pol::MR + g + 8 * (i >> 1);
+                    const int64_t q = q0 + nt * 8 + 2 * tig;
+                    W* dst = b + (int64_t)(row0 + row) * ldb + q;
+                    if (q + 1 < s) {
+                        dst[0] = acc[mt][nt][i];
+                        dst[1] = acc[mt][nt][i + 1];
+                    } else if (q < s) {
+                        dst[0] = acc[mt][nt][i];
+                    }
+                }
+    }
 }
 
 // ------------------------------------------------------------------ host helpers
@@ -1111,30 +1272,44 @@ inline int pick_nt(int spad) { return spad >= 32 ? 4 : spad >= 16 ? 2 : 1; }
 template <class Pol>
 size_t ma2_smem(const Mr2View& v, int nct, int slot_bytes, int ns) {
     using W = typename Pol::W;
-    return 8 * kRingMax * 8 + (size_t)kChunk * nct * 8 * sizeof(W) +
+    return 8 * kRingMax * 8 + (size_t)2 * kChunk * nct * 8 * sizeof(W) +
            (size_t)v.ntasks * nct * 32 * Pol::CR * sizeof(W) + (size_t)8 * ns * slot_bytes;
+}
+template <class Pol>
+int mb2_trows(const Mr2View& v) {
+    int trows = 0;
+    for (int lv = v.lev_lo; lv < v.nlev; ++lv) trows += v.lev[lv].steps * Pol::KU;
+    return trows;
 }
 template <class Pol>
 size_t mb2_smem(const Mr2View& v, int nt, int ns) {
     using W = typename Pol::W;
-    size_t trows = 0;
-    for (int lv = v.lev_lo; lv < v.nlev; ++lv) trows += (size_t)v.lev[lv].steps * Pol::KU;
-    return 8 * kRingMax * 8 + (size_t)8 * ns * v.d_item + ((size_t)kChunk + trows) * nt * 8 * sizeof(W);
+    return (kBWarps * kRingMax + 4) * 8 + (size_t)kBWarps * ns * v.d_item +
+           2 * ((size_t)kChunk + mb2_trows<Pol>(v)) * nt * 8 * sizeof(W);
 }
 
 template <class Pol, int NCT>
 cudaError_t launch_ma2_t(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
                          int64_t ldx, int64_t s, int spad, typename Pol::W* partial, cudaStream_t st) {
-    int kbi = 16;
-    while (kbi > 1 && kbi * v.max_ablk > 4096) kbi /= 2;
-    const int slot = kbi * v.max_ablk;
-    // deepest ring that keeps two CTAs per SM, else the deepest that fits one
-    int ns = kRingMax;
-    while (ns > 2 && ma2_smem<Pol>(v, NCT, slot, ns) > 113 * 1024) --ns;
-    if (ma2_smem<Pol>(v, NCT, slot, ns) > 113 * 1024) {
+    // prefer two CTAs per SM (items >= 1 KB, ring >= 2 deep), else one CTA with the deepest ring
+    int kbi0 = 16;
+    while (kbi0 > 1 && kbi0 * v.max_ablk > 4096) kbi0 /= 2;
+    int kbi = kbi0, ns = 2;
+    bool two = false;
+    for (int kb = kbi0; kb >= 1 && kb * v.max_ablk >= 1024 && !two; kb /= 2)
+        for (int n = kRingMax; n >= 2; --n)
+            if (ma2_smem<Pol>(v, NCT, kb * v.max_ablk, n) <= 113 * 1024) {
+                kbi = kb;
+                ns = n;
+                two = true;
+                break;
+            }
+    if (!two) {
+        kbi = kbi0;
         ns = kRingMax;
-        while (ns > 2 && ma2_smem<Pol>(v, NCT, slot, ns) > 227 * 1024) --ns;
+        while (ns > 2 && ma2_smem<Pol>(v, NCT, kbi * v.max_ablk, ns) > 227 * 1024) --ns;
     }
+    const int slot = kbi * v.max_ablk;
     const size_t sm = ma2_smem<Pol>(v, NCT, slot, ns);
     if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
     auto k = k_mr2_a<Pol, NCT>;
@@ -1170,7 +1345,13 @@ cudaError_t launch_mb2_t(const PlanView& p, const MrView& m, const Mr2View& v, c
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int ngrp = (spad + NT * 8 - 1) / (NT * 8);
-    k<<<p.nchunks * ngrp, kMrThreads, sm, st>>>(p, m, v, x, ldx, tbuf, b, ldb, s, ngrp, ns);
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, (kBWarps + 1) * 32, sm);
+    const int nwork = p.nchunks * ngrp;
+    const int grid = std::max(1, std::min(nwork, sms * std::max(occ, 1)));
+    k<<<grid, (kBWarps + 1) * 32, sm, st>>>(p, m, v, x, ldx, tbuf, b, ldb, s, ngrp, ns, mb2_trows<Pol>(v));
     return cudaGetLastError();
 }
 template <class Pol>
@@ -1245,7 +1426,7 @@ cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typena
 // Fragment slabs for the policy of the handle's leaf (= working) format.
 template <class Pol>
 hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
-    constexpr int MT = 32 / Pol::MR;
+    constexpr int MT = kBRows / Pol::MR;
     const auto& nodes = *in.nodes;
     const auto& chunks = *in.chunks;
     const auto& leaves = *in.leaves;
@@ -1294,9 +1475,20 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
         v.max_ablk = std::max(v.max_ablk, M.ablk);
     }
     if (v.max_ablk == 0) v.max_ablk = 128;
+    if (v.d_item & (v.d_item - 1)) return HODLR_OK;
+    while ((1 << v.lslot) < v.d_item) ++v.lslot;
+    {
+        int next = -1;
+        for (int lv = nlev - 1; lv >= lev_lo; --lv) {
+            Mr2Level& M = v.lev[lv];
+            M.ulo = (int32_t)(M.uoff - 16LL * v.d_item);
+            M.unext = next;
+            if (M.steps > 0) next = M.ulo;
+        }
+    }
     v.a_chunk_bytes = (aoff + 127) / 128 * 128;
     v.warp_bytes = (int32_t)((uoff + 127) / 128 * 128);
-    v.b_chunk_bytes = 8LL * v.warp_bytes;
+    v.b_chunk_bytes = (int64_t)kBWarps * v.warp_bytes;
     const size_t a_bytes = (size_t)v.a_chunk_bytes * chunks.size();
     const size_t b_bytes = (size_t)v.b_chunk_bytes * chunks.size();
     void* d = nullptr;

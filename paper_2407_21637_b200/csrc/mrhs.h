@@ -69,6 +69,8 @@ struct Mr2Level {
     int32_t usz;      // bytes of one U item
     int64_t aoff;     // offset of the level's A blocks in a chunk's A region
     int64_t uoff;     // offset of the level's first U item in a warp's B region
+    int32_t ulo;      // the same, relative to the start of the U area (after the 16 D items)
+    int32_t unext;    // U-area offset of the next level with steps, -1 if none
 };
 struct Mr2View {
     int32_t nlev, lev_lo;      // levels lev_lo..nlev-1 are in the slab
@@ -76,7 +78,8 @@ struct Mr2View {
     int32_t nu_items;          // U items per warp per chunk
     int64_t a_chunk_bytes, b_chunk_bytes;
     int32_t warp_bytes;        // B bytes per warp per chunk
-    int32_t d_item;            // bytes of one D item
+    int32_t d_item;            // bytes of one D item (a power of two: the ring slot)
+    int32_t lslot;             // log2(d_item)
     int32_t leaf_fmt;
     int32_t max_ablk;
     const uint8_t* slab_a;

@@ -25,11 +25,16 @@ def main(path):
         for i, h in enumerate(hdr):
             if h in WANT or ("pipe_tensor" in h and "avg.pct_of_peak_sustained_active" in h and "sm__" in h):
                 print(f"   {h:70s} {r[i]} {units[i]}")
-        stalls = [(float(r[i]) if r[i] not in ("", "n/a") else 0.0, h) for i, h in enumerate(hdr)
-                  if h.startswith("smsp__average_warp_latency_issue_stalled_") and h.endswith(".ratio")]
+        stalls = []
+        for i, h in enumerate(hdr):
+            if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
+                try:
+                    stalls.append((float(r[i]), h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
         stalls = sorted(stalls, reverse=True)[:8]
         if stalls:
-            print("   stalls (cycles per issued instr):", ", ".join(f"{h.split('stalled_')[1].split('.')[0]}={v:.1f}" for v, h in stalls))
+            print("   stalls (warps per issue):", ", ".join(f"{n}={v:.2f}" for v, n in stalls))
 
 
 if __name__ == "__main__":
