@@ -674,7 +674,7 @@ __global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
         const int row = (ch.row0 - lf.row0) + kBRows * w + mt * Pol::MR + (lane >> 2) + 8 * a;
         const int col = kb * 16 + 4 * (lane & 3);
         const uint8_t* src = p.arena + lf.off + ((int64_t)row * lf.ld + col) * lfb;
-        uint8_t* blk = slab + (int64_t)chunk * v.b_chunk_bytes + (int64_t)w * v.warp_bytes + (int64_t)kb * v.d_item +
+        uint8_t* blk = slab + (int64_t)chunk * v.b_chunk_bytes + ((int64_t)kb * kBWarps + w) * v.d_item +
                        (int64_t)mt * 32 * Pol::AR * 4 * lfb;
         for (int j = 0; j < 4; ++j) {
             uint8_t* dst = blk + frag_byte(lane, a * 4 + j, lfb, Pol::AR * 4);
@@ -706,8 +706,8 @@ __global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
         const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
         const int row = (ch.row0 - nd.row0) + kBRows * w + mt * Pol::MR + (lane >> 2) + 8 * a;
         const int c = step * Pol::KU + Pol::UV * (lane & 3) + u;
-        uint8_t* dst = slab + (int64_t)chunk * v.b_chunk_bytes + (int64_t)w * v.warp_bytes + L.uoff +
-                       (int64_t)step * L.usz + (int64_t)mt * 32 * Pol::AR * Pol::UV * fb +
+        uint8_t* dst = slab + (int64_t)chunk * v.b_chunk_bytes + 16LL * kBWarps * v.d_item + L.uoff +
+                       ((int64_t)step * kBWarps + w) * L.usz + (int64_t)mt * 32 * Pol::AR * Pol::UV * fb +
                        frag_byte(lane, a * Pol::UV + u, fb, Pol::AR * Pol::UV);
         if (c < nd.ru) {
             const uint8_t* src = p.arena + nd.u_off + ((int64_t)c * nd.u_ld + row) * fb;
@@ -798,7 +798,7 @@ __device__ __forceinline__ void frag_load(int fmt, const uint8_t* blk, int lane,
     }
 }
 
-constexpr int kRingMax = 4;  // max slots per warp ring (runtime depth ns <= kRingMax)
+constexpr int kRingMax = 8;  // max slots per warp ring (runtime depth ns <= kRingMax)
 
 // ------------------------------------------------------------------ per-warp ring
 // A warp-private ring of `ns` slots of `slot` bytes, filled by lane 0 with
@@ -998,49 +998,90 @@ __global__ void __launch_bounds__(kMrThreads) k_mr2_a(PlanView p, const __grid_c
 
 // ------------------------------------------------------------------ MB2
 // Persistent: CTA b takes works (chunk, column group) b, b + grid, ...
-//   warps 0..15  compute: warp w owns chunk rows 16w..16w+15 and streams its
-//                B-region bytes (16 D items, then the U steps of every level,
-//                packed into items of the same size) through a private ring
-//                that runs ahead across works;
-//   warp 16      stager: X and the coefficients of work k+1 into buffer
-//                (k+1)&1 with cp.async while work k is computed
-//                (mbarriers full[2] / empty[2], no block-wide barrier).
+//   warps 0..15  compute: warp w owns chunk rows 16w..16w+15;
+//   warp 16      producer: streams each work's B region through a CTA-wide
+//                ring of ns stages (16 warps' D items of one k-step per stage,
+//                then the U steps of every level), one cp.async.bulk per stage;
+//   warp 17      stager: X and the coefficients of work k+1 into buffer
+//                (k+1)&1 with cp.async while work k is computed.
+// All hand-offs are mbarriers (full/empty per stage and per X buffer).
+constexpr int kBThreads = (kBWarps + 2) * 32;
+
 template <class Pol, int NT>
-__global__ void __launch_bounds__((kBWarps + 1) * 32) k_mr2_b(PlanView p, const __grid_constant__ MrView m,
-                                                            const __grid_constant__ Mr2View v,
-                                                            const typename Pol::W* __restrict__ x, int64_t ldx,
-                                                            const typename Pol::W* __restrict__ tbuf,
-                                                            typename Pol::W* __restrict__ b, int64_t ldb, int64_t s,
-                                                            int ngrp, int ns, int trows) {
+__global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_constant__ MrView m,
+                                                    const __grid_constant__ Mr2View v,
+                                                    const typename Pol::W* __restrict__ x, int64_t ldx,
+                                                    const typename Pol::W* __restrict__ tbuf,
+                                                    typename Pol::W* __restrict__ b, int64_t ldb, int64_t s,
+                                                    int ngrp, int ns, int trows, int nbuf) {
     using W = typename Pol::W;
     constexpr int MT = kBRows / Pol::MR;
     constexpr int ncol = NT * 8;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);          // [16][kRingMax] rings, then full[2], empty[2]
-    uint64_t* full = bars + kBWarps * kRingMax;
-    uint64_t* empty = full + 2;
-    uint8_t* ring = smem_raw + (kBWarps * kRingMax + 4) * 8;
-    const int slot_bytes = v.d_item, lslot = v.lslot;
-    W* xsb = reinterpret_cast<W*>(ring + (size_t)kBWarps * ns * slot_bytes);  // [2][256 x ncol]
-    W* tsb = xsb + 2 * kChunk * ncol;                                         // [2][trows x ncol]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [kRingMax]
+    uint64_t* empty = full + kRingMax;                       // [kRingMax]
+    uint64_t* xfull = empty + kRingMax;                      // [2]
+    uint64_t* xempty = xfull + 2;                            // [2]
+    uint8_t* ring = smem_raw + (2 * kRingMax + 4) * 8 + 96;  // 128-aligned
+    const int lslot = v.lslot, lstage = v.lslot + 4;         // stage = 16 D items
+    const int stage_bytes = 1 << lstage;
+    W* xsb = reinterpret_cast<W*>(ring + (size_t)ns * stage_bytes);  // [nbuf][256 x ncol]
+    W* tsb = xsb + nbuf * kChunk * ncol;                            // [nbuf][trows x ncol]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwork = p.nchunks * ngrp;
+    const int64_t dbytes = 16LL << lstage;                           // D region of a chunk
+    const int nstage = 16 + (v.warp_bytes + stage_bytes - 1) / stage_bytes;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
-            tma::mbar_init(&full[i], 32);
+        for (int i = 0; i < ns; ++i) {
+            tma::mbar_init(&full[i], 1);
             tma::mbar_init(&empty[i], kBWarps);
         }
+        for (int i = 0; i < 2; ++i) {
+            tma::mbar_init(&xfull[i], 32);
+            tma::mbar_init(&xempty[i], kBWarps);
+        }
+        tma::fence_mbar_init();
     }
+    __syncthreads();
+
     if (warp == kBWarps) {
+        // ---------------- producer (one lane)
+        if (lane == 0) {
+            const uint64_t pol = tma::policy_evict_first();
+            int slot = 0;
+            unsigned ph = 0;
+            int64_t n = 0;  // stages issued
+            for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
+                const int chunk = ngrp == 1 ? work : work / ngrp;
+                const uint8_t* src = v.slab_b + (int64_t)chunk * v.b_chunk_bytes;
+                for (int st = 0; st < nstage; ++st, ++n) {
+                    if (n >= ns) tma::mbar_wait(&empty[slot], ph ^ 1u);
+                    int64_t off, bytes;
+                    if (st < 16) {
+                        off = (int64_t)st << lstage;
+                        bytes = stage_bytes;
+                    } else {
+                        off = dbytes + ((int64_t)(st - 16) << lstage);
+                        bytes = min((int64_t)stage_bytes, dbytes + v.warp_bytes - off);
+                    }
+                    tma::mbar_arrive_tx(&full[slot], (unsigned)bytes);
+                    tma::bulk_g2s(ring + (size_t)slot * stage_bytes, src + off, (unsigned)bytes, &full[slot], pol);
+                    if (++slot == ns) {
+                        slot = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+    if (warp == kBWarps + 1) {
         // ---------------- stager
-        __syncwarp();
-        if (lane == 0) tma::fence_mbar_init();
-        asm volatile("bar.sync 1, %0;" ::"n"((kBWarps + 1) * 32));
         int k = 0;
         for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++k) {
-            const int buf = k & 1, use = k >> 1;
-            if (use > 0) tma::mbar_wait(&empty[buf], (unsigned)((use - 1) & 1));
+            const int buf = nbuf == 2 ? (k & 1) : 0, use = nbuf == 2 ? (k >> 1) : k;
+            if (use > 0) tma::mbar_wait(&xempty[buf], (unsigned)((use - 1) & 1));
             const int chunk = ngrp == 1 ? work : work / ngrp;
             const int64_t q0 = (int64_t)(work - chunk * ngrp) * ncol;
             const ChunkDesc ch = p.chunks[chunk];
@@ -1073,7 +1114,7 @@ __global__ void __launch_bounds__((kBWarps + 1) * 32) k_mr2_b(PlanView p, const 
                 base += steps * NT * 32 * Pol::UV;
             }
             cp_async_wait_all();
-            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tma::smem_u32(&full[buf]))
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tma::smem_u32(&xfull[buf]))
                          : "memory");
         }
         return;
@@ -1081,46 +1122,28 @@ __global__ void __launch_bounds__((kBWarps + 1) * 32) k_mr2_b(PlanView p, const 
 
     // ---------------- compute warps
     const int g = lane >> 2, tig = lane & 3;
-    WarpRing R{bars + warp * kRingMax, ring + (size_t)warp * ns * slot_bytes, ns, slot_bytes};
-    const int nitems = (v.warp_bytes + slot_bytes - 1) >> lslot;
-    const int last_bytes = v.warp_bytes - ((nitems - 1) << lslot);
-    const uint64_t pol = tma::policy_evict_first();
-    int pw = blockIdx.x, pi = 0;  // producer cursor (lane 0): work, item
-    auto produce = [&](int k) {
-        if (pw >= nwork) return;
-        const int chunk = ngrp == 1 ? pw : pw / ngrp;
-        const uint8_t* src = v.slab_b + (int64_t)chunk * v.b_chunk_bytes + (int64_t)warp * v.warp_bytes +
-                             ((int64_t)pi << lslot);
-        R.fill(k, src, (unsigned)(pi == nitems - 1 ? last_bytes : slot_bytes), pol);
-        if (++pi == nitems) {
-            pi = 0;
-            pw += gridDim.x;
-        }
+    int slot = 0;
+    unsigned ph = 0;
+    auto next_stage = [&]() -> const uint8_t* {
+        tma::mbar_wait(&full[slot], ph);
+        return ring + (size_t)slot * stage_bytes;
     };
-    auto release = [&]() {
-        const int k = R.advance();
+    auto release_stage = [&]() {
         __syncwarp();
-        if (lane == 0) {
-            tma::fence_proxy_async_smem();
-            produce(k);
+        if (lane == 0) tma::mbar_arrive(&empty[slot]);
+        if (++slot == ns) {
+            slot = 0;
+            ph ^= 1u;
         }
     };
-    if (lane == 0) {
-        for (int i = 0; i < ns; ++i) tma::mbar_init(&R.bar[i], 1);
-        tma::fence_mbar_init();
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"((kBWarps + 1) * 32));  // all barrier inits visible
-    if (lane == 0)
-        for (int i = 0; i < ns; ++i) produce(i);
-
     const int lfmt = v.leaf_fmt;
     const int lfb = fmt_bytes(lfmt);
     int k = 0;
     for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++k) {
-        const int buf = k & 1;
+        const int buf = nbuf == 2 ? (k & 1) : 0, use = nbuf == 2 ? (k >> 1) : k;
         const int chunk = ngrp == 1 ? work : work / ngrp;
         const int64_t q0 = (int64_t)(work - chunk * ngrp) * ncol;
-        tma::mbar_wait(&full[buf], (unsigned)((k >> 1) & 1));
+        tma::mbar_wait(&xfull[buf], (unsigned)(use & 1));
         const W* xs = xsb + buf * kChunk * ncol;
         const W* ts = tsb + buf * trows * ncol;
 
@@ -1132,14 +1155,14 @@ __global__ void __launch_bounds__((kBWarps + 1) * 32) k_mr2_b(PlanView p, const 
 #pragma unroll
                 for (int i = 0; i < Pol::CR; ++i) acc[mt][nt][i] = W(0);
 
-        // D items: k-step kb (exactly one item each)
+        // D: stage kb holds every warp's item of k-step kb
         for (int kb = 0; kb < 16; ++kb) {
-            const uint8_t* base = R.wait();
+            const uint8_t* base = next_stage() + (warp << lslot);
             W tmp[MT][Pol::AR * 4];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
                 frag_load<W, Pol::AR * 4>(lfmt, base + mt * 32 * Pol::AR * 4 * lfb, lane, tmp[mt]);
-            release();
+            release_stage();
             typename Pol::AF af[MT];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
@@ -1159,28 +1182,28 @@ __global__ void __launch_bounds__((kBWarps + 1) * 32) k_mr2_b(PlanView p, const 
             }
             Pol::template mma16_tile<MT, NT>(acc, af, bf);
         }
-        // U steps, level by level; several steps per item, a step never straddles items
+        // U: per step, the 16 warps' blocks are adjacent; several steps per stage
         int tbase = 0;
-        const uint8_t* hbase = nullptr;
+        const uint8_t* sbase = nullptr;
         for (int lv = v.lev_lo; lv < v.nlev; ++lv) {
             const Mr2Level& L = v.lev[lv];
             const int steps = L.steps;
             if (steps == 0) continue;
             const int ufmt = L.ufmt, usz = L.usz;
             const int ufb = fmt_bytes(ufmt);
+            const int sstep = usz * kBWarps;
             int lo = L.ulo;
-            for (int step = 0; step < steps; ++step, lo += usz) {
-                const int ioff = lo & (slot_bytes - 1);
-                if (hbase == nullptr) hbase = R.wait();
-                const uint8_t* base = hbase + ioff;
+            for (int step = 0; step < steps; ++step, lo += sstep) {
+                if (sbase == nullptr) sbase = next_stage();
+                const uint8_t* base = sbase + (lo & (stage_bytes - 1)) + warp * usz;
                 W tmp[MT][Pol::AR * Pol::UV];
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt)
                     frag_load<W, Pol::AR * Pol::UV>(ufmt, base + mt * 32 * Pol::AR * Pol::UV * ufb, lane, tmp[mt]);
-                const int nlo = step + 1 < steps ? lo + usz : L.unext;
-                if (nlo < 0 || (nlo >> lslot) != (lo >> lslot)) {  // item fully read
-                    release();
-                    hbase = nullptr;
+                const int nlo = step + 1 < steps ? lo + sstep : L.unext;
+                if (nlo < 0 || (nlo >> lstage) != (lo >> lstage)) {  // stage fully read
+                    release_stage();
+                    sbase = nullptr;
                 }
                 typename Pol::AUF af[MT];
 #pragma unroll
@@ -1204,9 +1227,8 @@ __global__ void __launch_bounds__((kBWarps + 1) * 32) k_mr2_b(PlanView p, const 
             }
             tbase += steps * NT * 32 * Pol::UV;
         }
-        // buffer consumed
         __syncwarp();
-        if (lane == 0) tma::mbar_arrive(&empty[buf]);
+        if (lane == 0) tma::mbar_arrive(&xempty[buf]);
         const int row0 = p.chunks[chunk].row0;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
@@ -1282,10 +1304,10 @@ int mb2_trows(const Mr2View& v) {
     return trows;
 }
 template <class Pol>
-size_t mb2_smem(const Mr2View& v, int nt, int ns) {
+size_t mb2_smem(const Mr2View& v, int nt, int ns, int nbuf = 2) {
     using W = typename Pol::W;
-    return (kBWarps * kRingMax + 4) * 8 + (size_t)kBWarps * ns * v.d_item +
-           2 * ((size_t)kChunk + mb2_trows<Pol>(v)) * nt * 8 * sizeof(W);
+    return (2 * kRingMax + 4) * 8 + 96 + (size_t)ns * kBWarps * v.d_item +
+           nbuf * ((size_t)kChunk + mb2_trows<Pol>(v)) * nt * 8 * sizeof(W);
 }
 
 template <class Pol, int NCT>
@@ -1333,13 +1355,15 @@ template <class Pol, int NT>
 cudaError_t launch_mb2_t(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
                          int64_t ldx, const typename Pol::W* tbuf, typename Pol::W* b, int64_t ldb, int64_t s,
                          int spad, cudaStream_t st) {
+    // one CTA per SM; X / coefficients double-buffered when it leaves >= 3 ring
+    // stages, else single-buffered; the ring takes the rest of shared memory
+    int nbuf = 2;
+    if (mb2_smem<Pol>(v, NT, 3, 2) > 225 * 1024) nbuf = 1;
+    if (const char* e = getenv("HODLR_B200_MB_NBUF")) nbuf = atoi(e) == 1 ? 1 : 2;
     int ns = kRingMax;
-    while (ns > 2 && mb2_smem<Pol>(v, NT, ns) > 113 * 1024) --ns;
-    if (mb2_smem<Pol>(v, NT, ns) > 113 * 1024) {
-        ns = kRingMax;
-        while (ns > 2 && mb2_smem<Pol>(v, NT, ns) > 227 * 1024) --ns;
-    }
-    const size_t sm = mb2_smem<Pol>(v, NT, ns);
+    while (ns > 2 && mb2_smem<Pol>(v, NT, ns, nbuf) > 225 * 1024) --ns;
+    if (const char* e = getenv("HODLR_B200_MB_NS")) ns = std::max(2, std::min(ns, atoi(e)));
+    const size_t sm = mb2_smem<Pol>(v, NT, ns, nbuf);
     if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
     auto k = k_mr2_b<Pol, NT>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1348,10 +1372,10 @@ cudaError_t launch_mb2_t(const PlanView& p, const MrView& m, const Mr2View& v, c
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, (kBWarps + 1) * 32, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBThreads, sm);
     const int nwork = p.nchunks * ngrp;
     const int grid = std::max(1, std::min(nwork, sms * std::max(occ, 1)));
-    k<<<grid, (kBWarps + 1) * 32, sm, st>>>(p, m, v, x, ldx, tbuf, b, ldb, s, ngrp, ns, mb2_trows<Pol>(v));
+    k<<<grid, kBThreads, sm, st>>>(p, m, v, x, ldx, tbuf, b, ldb, s, ngrp, ns, mb2_trows<Pol>(v), nbuf);
     return cudaGetLastError();
 }
 template <class Pol>
@@ -1359,7 +1383,7 @@ cudaError_t launch_mb2(const PlanView& p, const MrView& m, const Mr2View& v, con
                        int64_t ldx, const typename Pol::W* tbuf, typename Pol::W* b, int64_t ldb, int64_t s,
                        int spad, cudaStream_t st) {
     int nt = pick_nt(spad);
-    while (nt > 1 && mb2_smem<Pol>(v, nt, 2) > 227 * 1024) nt /= 2;
+    while (nt > 1 && mb2_smem<Pol>(v, nt, 2, 1) > 225 * 1024) nt /= 2;
     if (nt == 4) return launch_mb2_t<Pol, 4>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st);
     if (nt == 2) return launch_mb2_t<Pol, 2>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st);
     return launch_mb2_t<Pol, 1>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st);
@@ -1442,7 +1466,7 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
     v.leaf_fmt = in.leaf_fmt;
     const int lfb = fmt_bytes(in.leaf_fmt);
     v.d_item = MT * 32 * Pol::AR * 4 * lfb;
-    int64_t aoff = 0, uoff = 16LL * v.d_item;
+    int64_t aoff = 0, uoff = 0;  // uoff: offset inside the chunk's U area
     for (int lv = lev_lo; lv < nlev; ++lv) {
         const MrLevel& L = mr.view.lev[lv];
         Mr2Level& M = v.lev[lv];
@@ -1467,9 +1491,12 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
         aoff += (int64_t)M.nmt * 16 * M.ablk;
         M.steps = (L.ru_max + Pol::KU - 1) / Pol::KU;
         M.usz = MT * 32 * Pol::AR * Pol::UV * fmt_bytes(M.ufmt);
-        uoff = (uoff + M.usz - 1) / M.usz * M.usz;  // a step never straddles a ring item
+        // all 16 warps' blocks of one step are adjacent; a level starts at a
+        // multiple of its step size so a step never straddles a ring stage
+        const int64_t sstep = (int64_t)kBWarps * M.usz;
+        uoff = (uoff + sstep - 1) / sstep * sstep;
         M.uoff = uoff;
-        uoff += (int64_t)M.steps * M.usz;
+        uoff += (int64_t)M.steps * sstep;
         v.ntasks += M.nmt;
         v.nu_items += M.steps;
         v.max_ablk = std::max(v.max_ablk, M.ablk);
@@ -1481,14 +1508,14 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
         int next = -1;
         for (int lv = nlev - 1; lv >= lev_lo; --lv) {
             Mr2Level& M = v.lev[lv];
-            M.ulo = (int32_t)(M.uoff - 16LL * v.d_item);
+            M.ulo = (int32_t)M.uoff;
             M.unext = next;
             if (M.steps > 0) next = M.ulo;
         }
     }
     v.a_chunk_bytes = (aoff + 127) / 128 * 128;
-    v.warp_bytes = (int32_t)((uoff + 127) / 128 * 128);
-    v.b_chunk_bytes = (int64_t)kBWarps * v.warp_bytes;
+    v.warp_bytes = (int32_t)((uoff + 127) / 128 * 128);  // U area bytes per chunk (all warps)
+    v.b_chunk_bytes = 16LL * kBWarps * v.d_item + v.warp_bytes;
     const size_t a_bytes = (size_t)v.a_chunk_bytes * chunks.size();
     const size_t b_bytes = (size_t)v.b_chunk_bytes * chunks.size();
     void* d = nullptr;
