@@ -38,6 +38,7 @@ constexpr int kChunk = 256;            // rows per chunk (plan.h chunks are <= 2
 constexpr size_t kMrSmemTarget = 110 * 1024;  // keep two CTAs per SM
 constexpr int kBWarps = 16;                  // slab phase-B CTA: 16 warps ...
 constexpr int kBRows = kChunk / kBWarps;     // ... of 16 chunk rows each
+constexpr int kAWarps = 16;                  // slab phase-A CTA warps (one task list each)
 
 // ------------------------------------------------------------------ operand loads
 template <typename W>
@@ -637,7 +638,7 @@ __global__ void k_slab_a(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
         const int mt = (int)(r / 16);
         const Mr2Level L = v.lev[lv];
         const int fb = fmt_bytes(L.vfmt);
-        uint8_t* blk = slab + (int64_t)chunk * v.a_chunk_bytes + L.aoff + ((int64_t)mt * 16 + kb) * L.ablk;
+        uint8_t* blk = slab + (int64_t)chunk * v.a_chunk_bytes + (int64_t)kb * v.arow + L.aoff + (int64_t)mt * L.ablk;
         const ChunkDesc ch = p.chunks[chunk];
         const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
         const int c = mt * Pol::MR + (lane >> 2) + 8 * a;
@@ -856,139 +857,200 @@ __device__ __forceinline__ void stage_x_async(W* xs, const W* __restrict__ x, in
 }
 
 // ------------------------------------------------------------------ MA2
-// Persistent-range phase A over the A slab.  Warp w's stream: for every chunk
-// of the CTA's run, for its tasks t = w, w+8, ... (m-tiles of all levels), the
-// task's 16 k-blocks in items of kbi blocks (<= 4 KB).  X of the next chunk is
-// staged (cp.async) into the other buffer while the current one is consumed.
-template <class Pol, int NCT>
-__global__ void __launch_bounds__(kMrThreads) k_mr2_a(PlanView p, const __grid_constant__ MrView m,
-                                                      const __grid_constant__ Mr2View v,
-                                                      const typename Pol::W* __restrict__ x, int64_t ldx,
-                                                      int64_t s, int spad, int kbi, int slot_bytes, int ns,
-                                                      typename Pol::W* __restrict__ partial) {
+// Persistent-range phase A over the A slab (CTA b: chunks [c_beg, c_end)).
+//   warps 0..15  compute: warp w owns tasks t = w, w+16, ... (m-tiles of all
+//                levels, <= MAXTW each), accumulators in registers per chunk,
+//                then in a shared-memory tile per task across the chunks of one
+//                node, flushed to the node's partial slot at its last chunk;
+//   warp 16      producer: the run's A bytes are ONE contiguous range, streamed
+//                in stages of G k-steps (all tasks) through a CTA-wide ring;
+//   warp 17      stager: X of the next chunk (cp.async, fragment order).
+constexpr int kAThreads = (kAWarps + 2) * 32;
+
+template <class Pol, int NCT, int MAXTW>
+__global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_constant__ MrView m,
+                                                    const __grid_constant__ Mr2View v,
+                                                    const typename Pol::W* __restrict__ x, int64_t ldx,
+                                                    int64_t s, int spad, int G, int ns,
+                                                    typename Pol::W* __restrict__ partial) {
     using W = typename Pol::W;
     constexpr int ncol = NCT * 8;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                 // [8][kRingMax]
-    W* xsb = reinterpret_cast<W*>(smem_raw + 8 * kRingMax * 8);             // [2][256 x ncol]
-    W* accs = xsb + 2 * kChunk * ncol;                                      // [task][NCT][32][CR]
-    uint8_t* ring = reinterpret_cast<uint8_t*>(accs + (size_t)v.ntasks * NCT * 32 * Pol::CR);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [kRingMax]
+    uint64_t* empty = full + kRingMax;
+    uint64_t* xfull = empty + kRingMax;                      // [2]
+    uint64_t* xempty = xfull + 2;
+    const int stage_bytes = G * v.arow;
+    uint8_t* ring = smem_raw + 256;
+    W* xsb = reinterpret_cast<W*>(ring + (size_t)ns * stage_bytes);  // [2][256 x ncol]
+    W* accs = xsb + 2 * kChunk * ncol;                              // [task][NCT][32][CR]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, tig = lane & 3;
     const int64_t q0 = (int64_t)blockIdx.y * ncol;
     const int c_beg = (int)((int64_t)blockIdx.x * p.nchunks / gridDim.x);
     const int c_end = (int)((int64_t)(blockIdx.x + 1) * p.nchunks / gridDim.x);
-    WarpRing R{bars + warp * kRingMax, ring + (size_t)warp * ns * slot_bytes, ns, slot_bytes};
-    const int ipt = 16 / kbi;                                   // items per task
-    const int my_tasks = warp < v.ntasks ? (v.ntasks - 1 - warp) / kMrWarps + 1 : 0;
-    const uint64_t pol = tma::policy_evict_first();
+    const int nst = 16 / G;  // stages per chunk
 
-    // producer cursor (lane 0): chunk, task of this warp, item within the task
-    int pc = c_beg, ptt = 0, pq = 0;
-    const uint8_t* ptask = nullptr;  // A blocks of (chunk pc, task ptt)
-    int pablk = 0;
-    auto produce = [&](int k) {  // fill slot k with the next item, if any
-        if (pc >= c_end || my_tasks == 0) return;
-        if (pq == 0) {
-            int mt = warp + ptt * kMrWarps, lv = v.lev_lo;
-            while (mt >= v.lev[lv].nmt) { mt -= v.lev[lv].nmt; ++lv; }
-            pablk = v.lev[lv].ablk;
-            ptask = v.slab_a + (int64_t)pc * v.a_chunk_bytes + v.lev[lv].aoff + (int64_t)mt * 16 * pablk;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < ns; ++i) {
+            tma::mbar_init(&full[i], 1);
+            tma::mbar_init(&empty[i], kAWarps);
         }
-        R.fill(k, ptask + (int64_t)pq * kbi * pablk, (unsigned)(kbi * pablk), pol);
-        if (++pq == ipt) {
-            pq = 0;
-            if (++ptt == my_tasks) {
-                ptt = 0;
-                ++pc;
+        for (int i = 0; i < 2; ++i) {
+            tma::mbar_init(&xfull[i], 32);
+            tma::mbar_init(&xempty[i], kAWarps);
+        }
+        tma::fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kAWarps) {
+        // ---------------- producer
+        if (lane == 0) {
+            const uint64_t pol = tma::policy_evict_first();
+            int slot = 0;
+            unsigned ph = 0;
+            int64_t n = 0;
+            const uint8_t* src = v.slab_a + (int64_t)c_beg * v.a_chunk_bytes;
+            const int64_t total = (int64_t)(c_end - c_beg) * nst;
+            for (int64_t i = 0; i < total; ++i, ++n, src += stage_bytes) {
+                if (n >= ns) tma::mbar_wait(&empty[slot], ph ^ 1u);
+                tma::mbar_arrive_tx(&full[slot], (unsigned)stage_bytes);
+                tma::bulk_g2s(ring + (size_t)slot * stage_bytes, src, (unsigned)stage_bytes, &full[slot], pol);
+                if (++slot == ns) {
+                    slot = 0;
+                    ph ^= 1u;
+                }
             }
         }
-    };
-
-    if (lane == 0) {
-        for (int i = 0; i < ns; ++i) tma::mbar_init(&R.bar[i], 1);
-        tma::fence_mbar_init();
-        for (int i = 0; i < ns; ++i) produce(i);
+        return;
     }
-    for (int t = warp; t < v.ntasks; t += kMrWarps)
-#pragma unroll
-        for (int nt = 0; nt < NCT; ++nt)
-#pragma unroll
-            for (int i = 0; i < Pol::CR; ++i) accs[(((size_t)t * NCT + nt) * 32 + lane) * Pol::CR + i] = W(0);
-    if (c_beg < c_end) {
-        const ChunkDesc ch = p.chunks[c_beg];
-        stage_x_async<W>(xsb, x, ldx, ch.row0, ch.nrows, q0, ncol, s);
-    }
-
-    for (int ci = c_beg; ci < c_end; ++ci) {
-        W* xs = xsb + ((ci - c_beg) & 1) * kChunk * ncol;
-        cp_async_wait_all();
-        __syncthreads();  // X(ci) staged; every warp is done with X(ci - 1)
-        if (ci + 1 < c_end) {
-            const ChunkDesc nx = p.chunks[ci + 1];
-            stage_x_async<W>(xsb + ((ci + 1 - c_beg) & 1) * kChunk * ncol, x, ldx, nx.row0, nx.nrows, q0, ncol, s);
+    if (warp == kAWarps + 1) {
+        // ---------------- stager
+        for (int ci = c_beg; ci < c_end; ++ci) {
+            const int k = ci - c_beg, buf = k & 1, use = k >> 1;
+            if (use > 0) tma::mbar_wait(&xempty[buf], (unsigned)((use - 1) & 1));
+            const ChunkDesc ch = p.chunks[ci];
+            W* xs = xsb + buf * kChunk * ncol;
+            for (int i = lane; i < kChunk * ncol; i += 32) {
+                const int r = i / ncol, q = i - r * ncol;
+                W* dst = xs + xfrag<W>(r, q, NCT);
+                if (r < ch.nrows && q0 + q < s)
+                    cp_async(dst, x + (ch.row0 + r) * ldx + q0 + q, (int)sizeof(W));
+                else
+                    *dst = W(0);
+            }
+            cp_async_wait_all();
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tma::smem_u32(&xfull[buf]))
+                         : "memory");
         }
-        for (int tt = 0; tt < my_tasks; ++tt) {
-            const int t = warp + tt * kMrWarps;
-            int lv = v.lev_lo, mt = t;
+        return;
+    }
+
+    // ---------------- compute warps
+    const int g = lane >> 2, tig = lane & 3;
+    int tlv[MAXTW], tmt[MAXTW], toff[MAXTW], tfmt[MAXTW];
+    int ntw = 0;
+#pragma unroll
+    for (int i = 0; i < MAXTW; ++i) {
+        const int t = warp + i * kAWarps;
+        tlv[i] = v.lev_lo;
+        tmt[i] = 0;
+        toff[i] = 0;
+        tfmt[i] = HODLR_FMT_FP32;
+        if (t < v.ntasks) {
+            int mt = t, lv = v.lev_lo;
             while (mt >= v.lev[lv].nmt) { mt -= v.lev[lv].nmt; ++lv; }
-            const int vfmt = v.lev[lv].vfmt;
-            const int ablk = v.lev[lv].ablk;
-            W acc[1][NCT][Pol::CR];
+            tlv[i] = lv;
+            tmt[i] = mt;
+            toff[i] = (int)v.lev[lv].aoff + mt * v.lev[lv].ablk;
+            tfmt[i] = v.lev[lv].vfmt;
+            ntw = i + 1;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < MAXTW; ++i)
+        if (i < ntw)
 #pragma unroll
             for (int nt = 0; nt < NCT; ++nt)
 #pragma unroll
-                for (int i = 0; i < Pol::CR; ++i) acc[0][nt][i] = W(0);
-            for (int q = 0; q < ipt; ++q) {
-                const uint8_t* base = R.wait();
-                for (int k = 0; k < kbi; ++k) {
-                    W tmp[Pol::AR * 4];
-                    frag_load<W, Pol::AR * 4>(vfmt, base + k * ablk, lane, tmp);
-                    if (k == kbi - 1) {  // item fully read: refill its slot
-                        const int ks = R.advance();
-                        __syncwarp();
-                        if (lane == 0) {
-                            tma::fence_proxy_async_smem();
-                            produce(ks);
-                        }
+                for (int e = 0; e < Pol::CR; ++e)
+                    accs[((((size_t)(warp + i * kAWarps)) * NCT + nt) * 32 + lane) * Pol::CR + e] = W(0);
+    int slot = 0;
+    unsigned ph = 0;
+    for (int ci = c_beg; ci < c_end; ++ci) {
+        const int k = ci - c_beg, buf = k & 1;
+        tma::mbar_wait(&xfull[buf], (unsigned)((k >> 1) & 1));
+        const W* xs = xsb + buf * kChunk * ncol;
+        W acc[MAXTW][1][NCT][Pol::CR];
+#pragma unroll
+        for (int i = 0; i < MAXTW; ++i)
+#pragma unroll
+            for (int nt = 0; nt < NCT; ++nt)
+#pragma unroll
+                for (int e = 0; e < Pol::CR; ++e) acc[i][0][nt][e] = W(0);
+        for (int gi = 0; gi < nst; ++gi) {
+            tma::mbar_wait(&full[slot], ph);
+            const uint8_t* base = ring + (size_t)slot * stage_bytes;
+            for (int kk = 0; kk < G; ++kk) {
+                W tmp[MAXTW][Pol::AR * 4];
+#pragma unroll
+                for (int i = 0; i < MAXTW; ++i)
+                    if (i < ntw) frag_load<W, Pol::AR * 4>(tfmt[i], base + kk * v.arow + toff[i], lane, tmp[i]);
+                if (kk == G - 1) {  // stage fully read
+                    __syncwarp();
+                    if (lane == 0) tma::mbar_arrive(&empty[slot]);
+                    if (++slot == ns) {
+                        slot = 0;
+                        ph ^= 1u;
                     }
-                    W av[Pol::AR][4];
-#pragma unroll
-                    for (int a = 0; a < Pol::AR; ++a)
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) av[a][j] = tmp[a * 4 + j];
-                    typename Pol::AF af[1];
-                    Pol::prep_a(af[0], av);
-                    const int kb = q * kbi + k;
-                    typename Pol::BF bf[NCT];
-#pragma unroll
-                    for (int nt = 0; nt < NCT; ++nt) {
-                        W bv[4];
-                        load_bfrag<W>(xs + (kb * NCT + nt) * 128, lane, bv);
-                        Pol::prep_b(bf[nt], bv);
-                    }
-                    Pol::template mma16_tile<1, NCT>(acc, af, bf);
                 }
+                const int kb = gi * G + kk;
+                typename Pol::BF bf[NCT];
+#pragma unroll
+                for (int nt = 0; nt < NCT; ++nt) {
+                    W bv[4];
+                    load_bfrag<W>(xs + (kb * NCT + nt) * 128, lane, bv);
+                    Pol::prep_b(bf[nt], bv);
+                }
+#pragma unroll
+                for (int i = 0; i < MAXTW; ++i)
+                    if (i < ntw) {
+                        W av[Pol::AR][4];
+#pragma unroll
+                        for (int a = 0; a < Pol::AR; ++a)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) av[a][j] = tmp[i][a * 4 + j];
+                        typename Pol::AF af[1];
+                        Pol::prep_a(af[0], av);
+                        Pol::template mma16_tile<1, NCT>(acc[i], af, bf);
+                    }
             }
-            // accumulate into the task tile; flush at the node's last chunk of this run
+        }
+        __syncwarp();
+        if (lane == 0) tma::mbar_arrive(&xempty[buf]);
+        // accumulate into the task tiles; flush at a node's last chunk of this run
+#pragma unroll
+        for (int i = 0; i < MAXTW; ++i) {
+            if (i >= ntw) continue;
+            const int t = warp + i * kAWarps, lv = tlv[i], mt = tmt[i];
             const int node = p.chunk_nodes[ci * p.nlev + lv];
             const bool more = ci + 1 < c_end && p.chunk_nodes[(ci + 1) * p.nlev + lv] == node;
             const MrLevel L = m.lev[lv];
-            const int64_t slot = (int64_t)blockIdx.x + m.slots[node].jrel;
+            const int64_t pslot = (int64_t)blockIdx.x + m.slots[node].jrel;
 #pragma unroll
             for (int nt = 0; nt < NCT; ++nt) {
                 W* my = accs + (((size_t)t * NCT + nt) * 32 + lane) * Pol::CR;
 #pragma unroll
-                for (int i = 0; i < Pol::CR; ++i) {
-                    W val = my[i] + acc[0][nt][i];
+                for (int e = 0; e < Pol::CR; ++e) {
+                    const W val = my[e] + acc[i][0][nt][e];
                     if (more) {
-                        my[i] = val;
+                        my[e] = val;
                     } else {
-                        const int c = mt * Pol::MR + g + 8 * (i >> 1);
-                        const int q = nt * 8 + 2 * tig + (i & 1);
+                        const int c = mt * Pol::MR + g + 8 * (e >> 1);
+                        const int q = nt * 8 + 2 * tig + (e & 1);
                         if (c < L.rv_max && q0 + q < spad)
-                            partial[(L.part_rows + slot * L.rv_pad + c) * spad + q0 + q] = val;
-                        my[i] = W(0);
+                            partial[(L.part_rows + pslot * L.rv_pad + c) * spad + q0 + q] = val;
+                        my[e] = W(0);
                     }
                 }
             }
@@ -1294,8 +1356,8 @@ inline int pick_nt(int spad) { return spad >= 32 ? 4 : spad >= 16 ? 2 : 1; }
 template <class Pol>
 size_t ma2_smem(const Mr2View& v, int nct, int slot_bytes, int ns) {
     using W = typename Pol::W;
-    return 8 * kRingMax * 8 + (size_t)2 * kChunk * nct * 8 * sizeof(W) +
-           (size_t)v.ntasks * nct * 32 * Pol::CR * sizeof(W) + (size_t)8 * ns * slot_bytes;
+    return 256 + (size_t)2 * kChunk * nct * 8 * sizeof(W) + (size_t)v.ntasks * nct * 32 * Pol::CR * sizeof(W) +
+           (size_t)ns * slot_bytes;
 }
 template <class Pol>
 int mb2_trows(const Mr2View& v) {
@@ -1310,45 +1372,40 @@ size_t mb2_smem(const Mr2View& v, int nt, int ns, int nbuf = 2) {
            nbuf * ((size_t)kChunk + mb2_trows<Pol>(v)) * nt * 8 * sizeof(W);
 }
 
-template <class Pol, int NCT>
+template <class Pol, int NCT, int MAXTW>
 cudaError_t launch_ma2_t(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
                          int64_t ldx, int64_t s, int spad, typename Pol::W* partial, cudaStream_t st) {
-    // prefer two CTAs per SM (items >= 1 KB, ring >= 2 deep), else one CTA with the deepest ring
-    int kbi0 = 16;
-    while (kbi0 > 1 && kbi0 * v.max_ablk > 4096) kbi0 /= 2;
-    int kbi = kbi0, ns = 2;
-    bool two = false;
-    for (int kb = kbi0; kb >= 1 && kb * v.max_ablk >= 1024 && !two; kb /= 2)
-        for (int n = kRingMax; n >= 2; --n)
-            if (ma2_smem<Pol>(v, NCT, kb * v.max_ablk, n) <= 113 * 1024) {
-                kbi = kb;
-                ns = n;
-                two = true;
-                break;
-            }
-    if (!two) {
-        kbi = kbi0;
-        ns = kRingMax;
-        while (ns > 2 && ma2_smem<Pol>(v, NCT, kbi * v.max_ablk, ns) > 227 * 1024) --ns;
-    }
-    const int slot = kbi * v.max_ablk;
-    const size_t sm = ma2_smem<Pol>(v, NCT, slot, ns);
+    // stage = G k-steps of every task, G * MAXTW * AR * 4 <= 16 values per lane
+    int G = 16 / (MAXTW * Pol::AR);
+    if (G < 1) G = 1;
+    while (G > 1 && (size_t)G * v.arow > 32 * 1024) G /= 2;
+    int ns = kRingMax;
+    while (ns > 2 && ma2_smem<Pol>(v, NCT, G * v.arow, ns) > 225 * 1024) --ns;
+    const size_t sm = ma2_smem<Pol>(v, NCT, G * v.arow, ns);
     if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
-    auto k = k_mr2_a<Pol, NCT>;
+    auto k = k_mr2_a<Pol, NCT, MAXTW>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     dim3 grid(m.nb, (spad + NCT * 8 - 1) / (NCT * 8));
-    k<<<grid, kMrThreads, sm, st>>>(p, m, v, x, ldx, s, spad, kbi, slot, ns, partial);
+    k<<<grid, kAThreads, sm, st>>>(p, m, v, x, ldx, s, spad, G, ns, partial);
     return cudaGetLastError();
+}
+template <class Pol, int NCT>
+cudaError_t launch_ma2_n(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
+                         int64_t ldx, int64_t s, int spad, typename Pol::W* partial, cudaStream_t st) {
+    const int maxtw = (v.ntasks + kAWarps - 1) / kAWarps;
+    if (maxtw <= 1) return launch_ma2_t<Pol, NCT, 1>(p, m, v, x, ldx, s, spad, partial, st);
+    if (maxtw <= 2) return launch_ma2_t<Pol, NCT, 2>(p, m, v, x, ldx, s, spad, partial, st);
+    return launch_ma2_t<Pol, NCT, 4>(p, m, v, x, ldx, s, spad, partial, st);
 }
 template <class Pol>
 cudaError_t launch_ma2(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
                        int64_t ldx, int64_t s, int spad, typename Pol::W* partial, cudaStream_t st) {
     int nct = pick_nt(spad);
-    while (nct > 1 && ma2_smem<Pol>(v, nct, 4096, 2) > 227 * 1024) nct /= 2;
-    if (nct == 4) return launch_ma2_t<Pol, 4>(p, m, v, x, ldx, s, spad, partial, st);
-    if (nct == 2) return launch_ma2_t<Pol, 2>(p, m, v, x, ldx, s, spad, partial, st);
-    return launch_ma2_t<Pol, 1>(p, m, v, x, ldx, s, spad, partial, st);
+    while (nct > 1 && ma2_smem<Pol>(v, nct, 16 * 1024, 2) > 225 * 1024) nct /= 2;
+    if (nct == 4) return launch_ma2_n<Pol, 4>(p, m, v, x, ldx, s, spad, partial, st);
+    if (nct == 2) return launch_ma2_n<Pol, 2>(p, m, v, x, ldx, s, spad, partial, st);
+    return launch_ma2_n<Pol, 1>(p, m, v, x, ldx, s, spad, partial, st);
 }
 
 template <class Pol, int NT>
@@ -1488,7 +1545,7 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
         M.nmt = (L.rv_max + Pol::MR - 1) / Pol::MR;
         M.ablk = 32 * Pol::AR * 4 * fmt_bytes(M.vfmt);
         M.aoff = aoff;
-        aoff += (int64_t)M.nmt * 16 * M.ablk;
+        aoff += (int64_t)M.nmt * M.ablk;
         M.steps = (L.ru_max + Pol::KU - 1) / Pol::KU;
         M.usz = MT * 32 * Pol::AR * Pol::UV * fmt_bytes(M.ufmt);
         // all 16 warps' blocks of one step are adjacent; a level starts at a
@@ -1513,7 +1570,9 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
             if (M.steps > 0) next = M.ulo;
         }
     }
-    v.a_chunk_bytes = (aoff + 127) / 128 * 128;
+    if (v.ntasks > 4 * kAWarps) return HODLR_OK;  // phase-A tasks per warp are register-resident (<= 4)
+    v.arow = (int32_t)aoff;
+    v.a_chunk_bytes = 16 * aoff;  // ablk is a multiple of 128
     v.warp_bytes = (int32_t)((uoff + 127) / 128 * 128);  // U area bytes per chunk (all warps)
     v.b_chunk_bytes = 16LL * kBWarps * v.d_item + v.warp_bytes;
     const size_t a_bytes = (size_t)v.a_chunk_bytes * chunks.size();

@@ -55,8 +55,9 @@ struct MrView {
 // format per level): the quantised factors and leaves re-ordered, per chunk,
 // into exactly the sequence of MMA operand fragments the kernels consume, so
 // each warp streams contiguous bytes with cp.async.bulk into a private ring.
-//   A region (phase A), per chunk: level-major, m-tile-major, 16 k-blocks
-//     (one k-block = 32 lanes x AR rows x 4 consecutive rows of V').
+//   A region (phase A), per chunk: 16 k-steps, each holding one k-block of
+//     every task (level-major, m-tile-major; one k-block = 32 lanes x AR rows
+//     x 4 consecutive rows of V'), so any run of k-steps is one contiguous stage.
 //   B region (phase B), per chunk and warp (rows 32w..32w+31): 16 D items
 //     (one per 16-column k step: MT m-tiles x 32 lanes x AR x 4 values), then
 //     the U items of every level (one per KU-column step).
@@ -67,7 +68,7 @@ struct Mr2Level {
     int32_t steps;    // U steps (ceil(ru_max / KU))
     int32_t ufmt;     // U storage format of the level
     int32_t usz;      // bytes of one U item
-    int64_t aoff;     // offset of the level's A blocks in a chunk's A region
+    int64_t aoff;     // offset of the level's first task block inside one k-step of the A region
     int64_t uoff;     // offset of the level's first U item in a warp's B region
     int32_t ulo;      // the same, relative to the start of the U area (after the 16 D items)
     int32_t unext;    // U-area offset of the next level with steps, -1 if none
@@ -82,6 +83,7 @@ struct Mr2View {
     int32_t lslot;             // log2(d_item)
     int32_t leaf_fmt;
     int32_t max_ablk;
+    int32_t arow;              // A bytes of one k-step, all tasks ([kb][task] layout)
     const uint8_t* slab_a;
     const uint8_t* slab_b;
     Mr2Level lev[kMrMaxLevels];
