@@ -865,7 +865,8 @@ __device__ __forceinline__ void stage_x_async(W* xs, const W* __restrict__ x, in
 //   warp 16      producer: the run's A bytes are ONE contiguous range, streamed
 //                in stages of G k-steps (all tasks) through a CTA-wide ring;
 //   warp 17      stager: X of the next chunk (cp.async, fragment order).
-constexpr int kAThreads = (kAWarps + 2) * 32;
+constexpr int kAStagers = 4;  // X staging warps of the phase-A CTA
+constexpr int kAThreads = (kAWarps + 1 + kAStagers) * 32;
 
 template <class Pol, int NCT, int MAXTW>
 __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_constant__ MrView m,
@@ -896,7 +897,7 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
             tma::mbar_init(&empty[i], kAWarps);
         }
         for (int i = 0; i < 2; ++i) {
-            tma::mbar_init(&xfull[i], 32);
+            tma::mbar_init(&xfull[i], 32 * kAStagers);
             tma::mbar_init(&xempty[i], kAWarps);
         }
         tma::fence_mbar_init();
@@ -924,14 +925,15 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
         }
         return;
     }
-    if (warp == kAWarps + 1) {
-        // ---------------- stager
+    if (warp > kAWarps) {
+        // ---------------- stagers
+        const int sl = threadIdx.x - (kAWarps + 1) * 32;
         for (int ci = c_beg; ci < c_end; ++ci) {
             const int k = ci - c_beg, buf = k & 1, use = k >> 1;
             if (use > 0) tma::mbar_wait(&xempty[buf], (unsigned)((use - 1) & 1));
             const ChunkDesc ch = p.chunks[ci];
             W* xs = xsb + buf * kChunk * ncol;
-            for (int i = lane; i < kChunk * ncol; i += 32) {
+            for (int i = sl; i < kChunk * ncol; i += 32 * kAStagers) {
                 const int r = i / ncol, q = i - r * ncol;
                 W* dst = xs + xfrag<W>(r, q, NCT);
                 if (r < ch.nrows && q0 + q < s)
@@ -1067,7 +1069,8 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
 //   warp 17      stager: X and the coefficients of work k+1 into buffer
 //                (k+1)&1 with cp.async while work k is computed.
 // All hand-offs are mbarriers (full/empty per stage and per X buffer).
-constexpr int kBThreads = (kBWarps + 2) * 32;
+constexpr int kBStagers = 2;  // X / coefficient staging warps of the phase-B CTA
+constexpr int kBThreads = (kBWarps + 1 + kBStagers) * 32;
 
 template <class Pol, int NT>
 __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_constant__ MrView m,
@@ -1100,7 +1103,7 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
             tma::mbar_init(&empty[i], kBWarps);
         }
         for (int i = 0; i < 2; ++i) {
-            tma::mbar_init(&xfull[i], 32);
+            tma::mbar_init(&xfull[i], 32 * kBStagers);
             tma::mbar_init(&xempty[i], kBWarps);
         }
         tma::fence_mbar_init();
@@ -1138,8 +1141,9 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
         }
         return;
     }
-    if (warp == kBWarps + 1) {
-        // ---------------- stager
+    if (warp > kBWarps) {
+        // ---------------- stagers
+        const int sl = threadIdx.x - (kBWarps + 1) * 32;
         int k = 0;
         for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++k) {
             const int buf = nbuf == 2 ? (k & 1) : 0, use = nbuf == 2 ? (k >> 1) : k;
@@ -1148,7 +1152,7 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
             const int64_t q0 = (int64_t)(work - chunk * ngrp) * ncol;
             const ChunkDesc ch = p.chunks[chunk];
             W* xs = xsb + buf * kChunk * ncol;
-            for (int i = lane; i < kChunk * ncol; i += 32) {
+            for (int i = sl; i < kChunk * ncol; i += 32 * kBStagers) {
                 const int r = i / ncol, q = i - r * ncol;
                 W* dst = xs + xfrag<W>(r, q, NT);
                 if (r < ch.nrows && q0 + q < s)
@@ -1163,7 +1167,7 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
                 if (steps == 0) continue;
                 const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
                 const W* t = tbuf + nd.tsrc_off * s;
-                for (int i = lane; i < steps * Pol::KU * ncol; i += 32) {
+                for (int i = sl; i < steps * Pol::KU * ncol; i += 32 * kBStagers) {
                     const int c = i / ncol, q = i - c * ncol;
                     const int step = c / Pol::KU, w = c - step * Pol::KU;
                     const int tg = w / Pol::UV, u = w - tg * Pol::UV;
