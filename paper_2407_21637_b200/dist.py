@@ -187,6 +187,8 @@ def _bench_sharded(args, build_workload, alg_bytes, peaks, ClockSampler, rank, w
         H, x, desc, Kx, normA = build_workload(args.config)
         desc += f"; tree sharded at level {_levels(world)} (strong scaling)"
     t_build = time.perf_counter() - t_build
+    x = np.asarray(x).reshape(H.n, -1)
+    s = x.shape[1]
     wb = 8 if H.working_format.name == "fp64" else 4
     dt = torch.float64 if wb == 8 else torch.float32
     sop = ShardedOperator(H, rank, world, device=local)
@@ -198,7 +200,7 @@ def _bench_sharded(args, build_workload, alg_bytes, peaks, ClockSampler, rank, w
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        sop.matvec(xd, out=bd.view(-1, 1))
+        sop.matvec(xd, out=bd)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -214,9 +216,10 @@ def _bench_sharded(args, build_workload, alg_bytes, peaks, ClockSampler, rank, w
         from .metrics import matvec_backward_error, matvec_bound
 
         b = torch.cat(parts).double().cpu().numpy()
-        b_or = matvec_oracle(H, x)
         xw = x.astype(np.float32).astype(np.float64) if wb == 4 else x
-        beta = matvec_backward_error(Kx(xw), xw, b, normA)
+        b_or = matvec_oracle(H, xw, "fp64")
+        kx = np.asarray(Kx(xw if s > 1 else xw[:, 0])).reshape(H.n, s)
+        beta = matvec_backward_error(kx, xw, b, normA)
         bound = matvec_bound(H.depth, H.eps)
         parity = {"rel_err_vs_oracle": float(np.linalg.norm(b - b_or) / np.linalg.norm(b_or)),
                   "backward_error": beta, "bound_thm35": bound, "within_10x_bound": beta <= 10 * bound}
@@ -237,12 +240,12 @@ def _bench_sharded(args, build_workload, alg_bytes, peaks, ClockSampler, rank, w
         Ke = max(10, K // 4)
         xh = torch.from_numpy(np.ascontiguousarray(x[r0:r0 + nl])).pin_memory()
         bh = torch.empty_like(xh).pin_memory()
-        xe = torch.empty(nl, dtype=torch.float64, device=dev)
+        xe = torch.empty((nl, s), dtype=torch.float64, device=dev)
 
         def e2e_step():
             xe.copy_(xh, non_blocking=True)
             step_in = xe if dt == torch.float64 else xe.to(dt)
-            sop.matvec(step_in, out=bd.view(-1, 1))
+            sop.matvec(step_in, out=bd)
             bh.copy_(bd.double() if dt != torch.float64 else bd, non_blocking=True)
 
         for _ in range(3):
@@ -260,8 +263,8 @@ def _bench_sharded(args, build_workload, alg_bytes, peaks, ClockSampler, rank, w
     t = torch.tensor([ms_local, ms_e2e_local], dtype=torch.float64, device=dev)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms, ms_e2e = float(t[0]), float(t[1])
-    B_all = alg_bytes(H, 1, wb)
-    mb = torch.tensor([op.matrix_bytes + 2 * nl * wb], dtype=torch.float64, device=dev)
+    B_all = alg_bytes(H, s, wb)
+    mb = torch.tensor([op.matrix_bytes + 2 * nl * s * wb], dtype=torch.float64, device=dev)
     tdist.all_reduce(mb, op=tdist.ReduceOp.MAX)
     if rank != 0:
         return 0
@@ -277,11 +280,11 @@ def _bench_sharded(args, build_workload, alg_bytes, peaks, ClockSampler, rank, w
         "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64" if wb == 8 else "f32",
         "data": "synthetic (seeded, BASELINE shapes)",
         "config": {
-            "workload": desc, "n": H.n, "depth": H.depth, "s": 1, "eps": H.eps,
+            "workload": desc, "n": H.n, "depth": H.depth, "s": s, "eps": H.eps,
             "level_formats": [f.name for f in H.plan.chosen],
             "global_matvecs_per_s": 1000.0 / ms, "alg_bytes_per_matvec": int(B_all),
             "alg_bytes_largest_shard": int(per_gpu), "effective_GBps_total": B_all / (ms * 1e-3) / 1e9,
-            "exchange_bytes_per_rank": sop.exchange_bytes(1, wb),
+            "exchange_bytes_per_rank": sop.exchange_bytes(s, wb),
             "l2": "flushed before every timed step (256 MiB read, untimed)",
             "build_seconds": t_build, "parallelism": f"tree sharded at level {_levels(world)} over {world} GPUs, "
                                                      "NCCL all-gather of V^T x coefficients",
@@ -291,9 +294,9 @@ def _bench_sharded(args, build_workload, alg_bytes, peaks, ClockSampler, rank, w
                      "traffic": None, "peak_source": peak_src,
                      "kernel": "whole sharded step per GPU (k_ext_v + k_stream subtree + k_ext_u, "
                                "all-gather overlapped)"},
-        "e2e": {"value": units * 1000.0 / ms_e2e, "unit": _unit(weak), "h2d_bytes_per_step": int(H.n * 8),
-                "d2h_bytes_per_step": int(H.n * 8), "ms_per_step": ms_e2e},
-        "gpu_launches": K * op.launches_per_matvec * world,
+        "e2e": {"value": units * 1000.0 / ms_e2e, "unit": _unit(weak), "h2d_bytes_per_step": int(H.n * s * 8),
+                "d2h_bytes_per_step": int(H.n * s * 8), "ms_per_step": ms_e2e},
+        "gpu_launches": K * (op.path(s)[1] + 3 * (world > 1)) * world,
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
