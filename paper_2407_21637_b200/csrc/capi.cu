@@ -452,7 +452,7 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
 
     {
         MrInput mi{&h->view, (const uint8_t*)h->arena.p, L, &h->nodes, &h->chunks, &h->leaves, &h->chunk_nodes, nlev,
-                   d->leaf_fmt, device};
+                   d->leaf_fmt, device, h->ext_count};
         if (mr_prepare(mi, h->mr) != HODLR_OK) return cleanup(fail(HODLR_ERR_CUDA, "multi-RHS plan upload failed"));
         const char* no_mr = getenv("HODLR_B200_DISABLE_MRHS");
         if (no_mr && no_mr[0] == '1') mr_release(h->mr);
@@ -577,6 +577,9 @@ hodlr_status run_local(hodlr_handle* h, const W* x, int64_t ldx, W* b, int64_t l
     return HODLR_OK;
 }
 
+// the single-vector fused kernel runs a rank's subtree (its own phase A)
+bool shard_sv_local(const hodlr_handle* h, int64_t s, int64_t ldx) { return h->sv_ok && s == 1 && ldx == 1; }
+
 template <typename W>
 cudaError_t shard_local_impl(hodlr_handle* h, const W* x, int64_t ldx, W* b, int64_t ldb, int64_t s, void* ws,
                              cudaStream_t st) {
@@ -585,9 +588,12 @@ cudaError_t shard_local_impl(hodlr_handle* h, const W* x, int64_t ldx, W* b, int
     carve<W>(h, s, ws, &partial, &tbuf, &extra);
     if (h->sv_ok && s == 1 && ldx == 1 && ldb == 1) return sv_matvec<W>(h->view, h->sv, x, b, partial, tbuf, extra, st);
     // multi-RHS kernels over the subtree levels (L+1..l) and the leaves; the
-    // external levels are added by shard_end
-    if (mr_usable(h->mr, sizeof(W) == 8 ? HODLR_FMT_FP64 : HODLR_FMT_FP32))
-        return mr_matvec<W>(h->view, h->mr, h->L, x, ldx, b, ldb, s, partial, tbuf, st);
+    // external levels are added by shard_end.  With fragment slabs, shard_begin
+    // already ran phase A (all levels): only phase B is left.
+    const int wf = sizeof(W) == 8 ? HODLR_FMT_FP64 : HODLR_FMT_FP32;
+    if (!shard_sv_local(h, s, ldx) && mr_slab_begin_usable(h->mr, wf))
+        return cudaSuccess;  // slab path: phase B (every level) runs in shard_end, after the exchange
+    if (mr_usable(h->mr, wf)) return mr_matvec<W>(h->view, h->mr, h->L, x, ldx, b, ldb, s, partial, tbuf, st);
     // generic: the whole local plan with the external coefficients set to 0
     // (their products add exact zeros); the external partials go to a
     // discarded buffer, shard_begin owns the real ones.
@@ -637,7 +643,8 @@ hodlr_status hodlr_matvec_path(const hodlr_handle* h, int32_t working, int64_t s
         *path = HODLR_PATH_FUSED_SV;
         *launches = sv_launches(h->sv);
     } else if (mr_usable(h->mr, working)) {
-        *path = mr_slab_used(h->mr, working, h->L) ? HODLR_PATH_MRHS_SLAB : HODLR_PATH_MRHS;
+        const bool slab = h->nranks > 1 ? mr_slab_begin_usable(h->mr, working) : mr_slab_used(h->mr, working, h->L);
+        *path = slab ? HODLR_PATH_MRHS_SLAB : HODLR_PATH_MRHS;
         *launches = mr_launches();
     } else {
         *path = HODLR_PATH_GENERIC;
@@ -724,7 +731,20 @@ hodlr_status hodlr_matvec_shard_begin(hodlr_handle* h, int32_t working, const vo
     if (r != HODLR_OK) return r;
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
-    if (working == HODLR_FMT_FP64) {
+    if (!shard_sv_local(h, s, ldx) && mr_slab_begin_usable(h->mr, working)) {
+        // phase A over every level on the tensor cores: external partials -> send
+        if (working == HODLR_FMT_FP64) {
+            double *partial, *tbuf;
+            void* extra;
+            carve<double>(h, s, ws, &partial, &tbuf, &extra);
+            e = mr_shard_begin<double>(h->view, h->mr, (const double*)x_local, ldx, s, partial, tbuf, (double*)send, st);
+        } else {
+            float *partial, *tbuf;
+            void* extra;
+            carve<float>(h, s, ws, &partial, &tbuf, &extra);
+            e = mr_shard_begin<float>(h->view, h->mr, (const float*)x_local, ldx, s, partial, tbuf, (float*)send, st);
+        }
+    } else if (working == HODLR_FMT_FP64) {
         ExtWs<double> x = carve_ext<double>(h, s, ws);
         e = ext_begin<double>(h->view, (const double*)x_local, ldx, s, x.scratch, x.ticket, (double*)send, st);
     } else {
@@ -764,16 +784,31 @@ hodlr_status hodlr_matvec_shard_end(hodlr_handle* h, int32_t working, const void
     if (r != HODLR_OK) return r;
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
+    const bool slab = !shard_sv_local(h, s, ldx) && mr_slab_begin_usable(h->mr, working);
     if (working == HODLR_FMT_FP64) {
         double *partial, *tbuf;
         void* extra;
         carve<double>(h, s, ws, &partial, &tbuf, &extra);
-        e = ext_finish<double>(h->view, s, (const double*)recv, tbuf, (double*)b_local, ldb, st);
+        if (slab) {
+            e = gen_ext<double>(h->view, s, (const double*)recv, tbuf, st);
+            if (e == cudaSuccess)
+                e = mr_slab_phase_b<double>(h->view, h->mr, (const double*)x_local, ldx, (double*)b_local, ldb, s,
+                                            tbuf, st);
+        } else {
+            e = ext_finish<double>(h->view, s, (const double*)recv, tbuf, (double*)b_local, ldb, st);
+        }
     } else {
         float *partial, *tbuf;
         void* extra;
         carve<float>(h, s, ws, &partial, &tbuf, &extra);
-        e = ext_finish<float>(h->view, s, (const float*)recv, tbuf, (float*)b_local, ldb, st);
+        if (slab) {
+            e = gen_ext<float>(h->view, s, (const float*)recv, tbuf, st);
+            if (e == cudaSuccess)
+                e = mr_slab_phase_b<float>(h->view, h->mr, (const float*)x_local, ldx, (float*)b_local, ldb, s,
+                                           tbuf, st);
+        } else {
+            e = ext_finish<float>(h->view, s, (const float*)recv, tbuf, (float*)b_local, ldb, st);
+        }
     }
     if (e != cudaSuccess) return fail(HODLR_ERR_CUDA, std::string("shard_end: ") + cudaGetErrorString(e));
     return HODLR_OK;

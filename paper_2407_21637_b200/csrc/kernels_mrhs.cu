@@ -99,9 +99,12 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return r;
 }
+// x = hi + lo (+ O(2^-22 |x|)).  Non-finite x: lo = 0, so inf propagates as
+// inf instead of turning into inf - inf = NaN.
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
     hi = tf32_rna(x);
-    lo = tf32_rna(x - __uint_as_float(hi));
+    const float r = x - __uint_as_float(hi);
+    lo = tf32_rna(fabsf(x) <= 3.402823466e38f ? r : 0.0f);
 }
 __device__ __forceinline__ void tmma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                      uint32_t b0, uint32_t b1) {
@@ -418,38 +421,84 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_a(PlanView p, const __grid_co
 template <typename W>
 __global__ void __launch_bounds__(256) k_mr_reduce(PlanView p, const __grid_constant__ MrView m, int node_lo,
                                                    int64_t s, int spad, const W* __restrict__ partial,
-                                                   W* __restrict__ tbuf) {
-    const int node = node_lo + blockIdx.x;
+                                                   W* __restrict__ tbuf, W* __restrict__ send,
+                                                   const int32_t* __restrict__ list) {
+    // one warp per output coefficient: lane l sums slots b0+l, b0+l+32, ... in
+    // order, then a fixed xor tree combines the lanes (deterministic)
+    const int node = list ? list[blockIdx.x] : node_lo + blockIdx.x;
     const NodeDesc nd = p.nodes[node];
     const MrSlot sl = m.slots[node];
     const MrLevel L = m.lev[sl.lv];
     const int64_t cnt = (int64_t)nd.rv * s;
-    W* dst = tbuf + nd.t_off * s;
+    // external level of a sharded handle: this rank's partial goes to the send
+    // buffer, zero-padded to the level's slot width
+    const bool ext = nd.ext_slot >= 0;
+    W* dst = ext ? send + (int64_t)nd.ext_slot * s : tbuf + nd.t_off * s;
+    const int64_t cnt_out = ext ? (int64_t)L.ext_w * s : cnt;
     const int64_t stride = (int64_t)L.rv_pad * spad;
-    for (int64_t i = blockIdx.y * 256 + threadIdx.x; i < cnt; i += (int64_t)gridDim.y * 256) {
-        const int64_t c = i / s, q = i - c * s;
-        const W* src = partial + (L.part_rows + (int64_t)(sl.b0 + sl.jrel) * L.rv_pad + c) * spad + q;
-        W acc = src[0];
-        const int nb = sl.b1 - sl.b0;
-        int b = 1;
-        for (; b + 3 <= nb; b += 4) {  // four loads in flight, additions in slot order
-            const W v1 = src[(int64_t)b * stride], v2 = src[(int64_t)(b + 1) * stride];
-            const W v3 = src[(int64_t)(b + 2) * stride], v4 = src[(int64_t)(b + 3) * stride];
-            acc += v1;
-            acc += v2;
-            acc += v3;
-            acc += v4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nb = sl.b1 - sl.b0 + 1;
+    const int64_t i0 = (int64_t)blockIdx.y * 256;
+    if (nb <= 32) {
+        if (i0 >= cnt_out) return;
+        // few slots: one thread per coefficient, slots in order
+        for (int64_t i = i0 + threadIdx.x; i < cnt_out; i += (int64_t)gridDim.y * 256) {
+            W acc = W(0);
+            if (i < cnt) {
+                const int64_t c = i / s, q = i - c * s;
+                const W* src = partial + (L.part_rows + (int64_t)(sl.b0 + sl.jrel) * L.rv_pad + c) * spad + q;
+                int b = 0;
+                for (; b + 8 <= nb; b += 8) {  // 8 loads in flight, additions in slot order
+                    W v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = src[(int64_t)(b + u) * stride];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc += v[u];
+                }
+                for (; b < nb; ++b) acc += src[(int64_t)b * stride];
+            }
+            dst[i] = acc;
         }
-        for (; b <= nb; ++b) acc += src[(int64_t)b * stride];
-        dst[i] = acc;
+        return;
+    }
+    // many slots (upper levels): one warp per coefficient, lane l sums slots
+    // l, l+32, ... in order, then a fixed xor tree (deterministic)
+    for (int64_t base = (int64_t)blockIdx.y * 8; base < cnt_out; base += (int64_t)gridDim.y * 8) {
+        {
+            const int64_t i = base + warp;
+            if (i >= cnt_out) break;
+            W acc = W(0);
+            if (i < cnt) {
+                const int64_t c = i / s, q = i - c * s;
+                const W* src = partial + (L.part_rows + (int64_t)(sl.b0 + sl.jrel) * L.rv_pad + c) * spad + q;
+                int b = lane;
+                for (; b + 96 < nb; b += 128) {
+                    const W v0 = src[(int64_t)b * stride], v1 = src[(int64_t)(b + 32) * stride];
+                    const W v2 = src[(int64_t)(b + 64) * stride], v3 = src[(int64_t)(b + 96) * stride];
+                    acc += v0;
+                    acc += v1;
+                    acc += v2;
+                    acc += v3;
+                }
+                for (; b < nb; b += 32) acc += src[(int64_t)b * stride];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            }
+            if (lane == 0) dst[i] = acc;
+        }
     }
 }
 
 inline dim3 reduce_grid(const MrView& m, int node_lo, int nnodes_total, int64_t s) {
     int rmax = 0;
-    for (int lv = 0; lv < m.nlev; ++lv) rmax = rmax > m.lev[lv].rv_max ? rmax : m.lev[lv].rv_max;
-    const int64_t tiles = ((int64_t)rmax * s + 255) / 256;
-    return dim3(nnodes_total - node_lo, (unsigned)(tiles < 1 ? 1 : tiles > 64 ? 64 : tiles));
+    for (int lv = 0; lv < m.nlev; ++lv) {
+        rmax = rmax > m.lev[lv].rv_max ? rmax : m.lev[lv].rv_max;
+        rmax = rmax > m.lev[lv].ext_w ? rmax : m.lev[lv].ext_w;
+    }
+    // y tiles of 8 coefficients (one per warp) for many-slot nodes; the
+    // one-thread-per-coefficient nodes use tiles of 256 (extra CTAs exit)
+    const int64_t tiles = ((int64_t)rmax * s + 7) / 8;
+    return dim3(nnodes_total - node_lo, (unsigned)(tiles < 1 ? 1 : tiles > 2048 ? 2048 : tiles));
 }
 
 // ------------------------------------------------------------------ MB
@@ -619,12 +668,12 @@ template <class Pol>
 __global__ void k_slab_a(PlanView p, const __grid_constant__ Mr2View v, uint8_t* __restrict__ slab) {
     // one thread per (chunk, level, m-tile, k-block, lane, a): 4 consecutive rows of one V' column
     int64_t per_chunk = 0;
-    for (int lv = v.lev_lo; lv < v.nlev; ++lv) per_chunk += (int64_t)v.lev[lv].nmt * 16 * 32 * Pol::AR;
+    for (int lv = v.alev_lo; lv < v.nlev; ++lv) per_chunk += (int64_t)v.lev[lv].nmt * 16 * 32 * Pol::AR;
     const int64_t total = per_chunk * p.nchunks;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int chunk = (int)(i / per_chunk);
         int64_t r = i - (int64_t)chunk * per_chunk;
-        int lv = v.lev_lo;
+        int lv = v.alev_lo;
         for (;; ++lv) {
             const int64_t c = (int64_t)v.lev[lv].nmt * 16 * 32 * Pol::AR;
             if (r < c) break;
@@ -873,7 +922,8 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
                                                     const __grid_constant__ Mr2View v,
                                                     const typename Pol::W* __restrict__ x, int64_t ldx,
                                                     int64_t s, int spad, int G, int ns,
-                                                    typename Pol::W* __restrict__ partial) {
+                                                    typename Pol::W* __restrict__ partial,
+                                                    typename Pol::W* __restrict__ tbuf) {
     using W = typename Pol::W;
     constexpr int ncol = NCT * 8;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -960,7 +1010,7 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
         toff[i] = 0;
         tfmt[i] = HODLR_FMT_FP32;
         if (t < v.ntasks) {
-            int mt = t, lv = v.lev_lo;
+            int mt = t, lv = v.alev_lo;
             while (mt >= v.lev[lv].nmt) { mt -= v.lev[lv].nmt; ++lv; }
             tlv[i] = lv;
             tmt[i] = mt;
@@ -1038,7 +1088,18 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
             const int node = p.chunk_nodes[ci * p.nlev + lv];
             const bool more = ci + 1 < c_end && p.chunk_nodes[(ci + 1) * p.nlev + lv] == node;
             const MrLevel L = m.lev[lv];
-            const int64_t pslot = (int64_t)blockIdx.x + m.slots[node].jrel;
+            const MrSlot sl = m.slots[node];
+            const int64_t pslot = (int64_t)blockIdx.x + sl.jrel;
+            // a node inside this CTA's run has one slot: its sum IS the coefficient
+            int direct_rv = -1;
+            int64_t toff = 0;
+            if (!more && sl.b0 == sl.b1) {
+                const NodeDesc nd = p.nodes[node];
+                if (nd.ext_slot < 0) {
+                    direct_rv = nd.rv;
+                    toff = nd.t_off * s;
+                }
+            }
 #pragma unroll
             for (int nt = 0; nt < NCT; ++nt) {
                 W* my = accs + (((size_t)t * NCT + nt) * 32 + lane) * Pol::CR;
@@ -1050,8 +1111,11 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
                     } else {
                         const int c = mt * Pol::MR + g + 8 * (e >> 1);
                         const int q = nt * 8 + 2 * tig + (e & 1);
-                        if (c < L.rv_max && q0 + q < spad)
+                        if (direct_rv >= 0) {
+                            if (c < direct_rv && q0 + q < s) tbuf[toff + (int64_t)c * s + q0 + q] = val;
+                        } else if (c < L.rv_max && q0 + q < spad) {
                             partial[(L.part_rows + pslot * L.rv_pad + c) * spad + q0 + q] = val;
+                        }
                         my[e] = W(0);
                     }
                 }
@@ -1378,7 +1442,8 @@ size_t mb2_smem(const Mr2View& v, int nt, int ns, int nbuf = 2) {
 
 template <class Pol, int NCT, int MAXTW>
 cudaError_t launch_ma2_t(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
-                         int64_t ldx, int64_t s, int spad, typename Pol::W* partial, cudaStream_t st) {
+                         int64_t ldx, int64_t s, int spad, typename Pol::W* partial, typename Pol::W* tbuf,
+                         cudaStream_t st) {
     // stage = G k-steps of every task, G * MAXTW * AR * 4 <= 16 values per lane
     int G = 16 / (MAXTW * Pol::AR);
     if (G < 1) G = 1;
@@ -1391,25 +1456,27 @@ cudaError_t launch_ma2_t(const PlanView& p, const MrView& m, const Mr2View& v, c
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     dim3 grid(m.nb, (spad + NCT * 8 - 1) / (NCT * 8));
-    k<<<grid, kAThreads, sm, st>>>(p, m, v, x, ldx, s, spad, G, ns, partial);
+    k<<<grid, kAThreads, sm, st>>>(p, m, v, x, ldx, s, spad, G, ns, partial, tbuf);
     return cudaGetLastError();
 }
 template <class Pol, int NCT>
 cudaError_t launch_ma2_n(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
-                         int64_t ldx, int64_t s, int spad, typename Pol::W* partial, cudaStream_t st) {
+                         int64_t ldx, int64_t s, int spad, typename Pol::W* partial, typename Pol::W* tbuf,
+                         cudaStream_t st) {
     const int maxtw = (v.ntasks + kAWarps - 1) / kAWarps;
-    if (maxtw <= 1) return launch_ma2_t<Pol, NCT, 1>(p, m, v, x, ldx, s, spad, partial, st);
-    if (maxtw <= 2) return launch_ma2_t<Pol, NCT, 2>(p, m, v, x, ldx, s, spad, partial, st);
-    return launch_ma2_t<Pol, NCT, 4>(p, m, v, x, ldx, s, spad, partial, st);
+    if (maxtw <= 1) return launch_ma2_t<Pol, NCT, 1>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
+    if (maxtw <= 2) return launch_ma2_t<Pol, NCT, 2>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
+    return launch_ma2_t<Pol, NCT, 4>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
 }
 template <class Pol>
 cudaError_t launch_ma2(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
-                       int64_t ldx, int64_t s, int spad, typename Pol::W* partial, cudaStream_t st) {
+                       int64_t ldx, int64_t s, int spad, typename Pol::W* partial, typename Pol::W* tbuf,
+                       cudaStream_t st) {
     int nct = pick_nt(spad);
     while (nct > 1 && ma2_smem<Pol>(v, nct, 16 * 1024, 2) > 225 * 1024) nct /= 2;
-    if (nct == 4) return launch_ma2_n<Pol, 4>(p, m, v, x, ldx, s, spad, partial, st);
-    if (nct == 2) return launch_ma2_n<Pol, 2>(p, m, v, x, ldx, s, spad, partial, st);
-    return launch_ma2_n<Pol, 1>(p, m, v, x, ldx, s, spad, partial, st);
+    if (nct == 4) return launch_ma2_n<Pol, 4>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
+    if (nct == 2) return launch_ma2_n<Pol, 2>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
+    return launch_ma2_n<Pol, 1>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
 }
 
 template <class Pol, int NT>
@@ -1463,11 +1530,13 @@ cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typena
     if (mr_slab_used(mr, wfmt, lev_lo)) {
         cudaError_t e = cudaSuccess;
         if (any_level) {
-            e = launch_ma2<Pol>(p, m, mr.v2, x, ldx, s, spad, partial, st);
+            e = launch_ma2<Pol>(p, m, mr.v2, x, ldx, s, spad, partial, tbuf, st);
             const int node_lo = m.lev[lev_lo].node0;
             const int nred = p.nnodes - node_lo;
-            if (e == cudaSuccess && nred > 0) {
-                k_mr_reduce<W><<<reduce_grid(m, node_lo, p.nnodes, s), 256, 0, st>>>(p, m, node_lo, s, spad, partial, tbuf);
+            if (e == cudaSuccess && nred > 0 && mr.nmulti > 0) {  // single-slot nodes were written by phase A
+                dim3 gr = reduce_grid(m, node_lo, p.nnodes, s);
+                gr.x = mr.nmulti;
+                k_mr_reduce<W><<<gr, 256, 0, st>>>(p, m, node_lo, s, spad, partial, tbuf, nullptr, mr.multi);
                 e = cudaGetLastError();
             }
         }
@@ -1490,7 +1559,7 @@ cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typena
         const int node_lo = m.lev[lev_lo].node0;
         const int nred = p.nnodes - node_lo;
         if (nred > 0) {
-            k_mr_reduce<W><<<reduce_grid(m, node_lo, p.nnodes, s), 256, 0, st>>>(p, m, node_lo, s, spad, partial, tbuf);
+            k_mr_reduce<W><<<reduce_grid(m, node_lo, p.nnodes, s), 256, 0, st>>>(p, m, node_lo, s, spad, partial, tbuf, nullptr, nullptr);
             e = cudaGetLastError();
             if (e != cudaSuccess) return e;
         }
@@ -1523,14 +1592,19 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
     Mr2View& v = mr.v2;
     v = Mr2View{};
     v.nlev = nlev;
-    v.lev_lo = lev_lo;
+    // sharded handles: both regions cover every level, external ones included --
+    // phase A sends their partials, phase B (after the exchange) applies their U
+    v.lev_lo = 0;
+    v.alev_lo = 0;
+    (void)lev_lo;
     v.leaf_fmt = in.leaf_fmt;
     const int lfb = fmt_bytes(in.leaf_fmt);
     v.d_item = MT * 32 * Pol::AR * 4 * lfb;
     int64_t aoff = 0, uoff = 0;  // uoff: offset inside the chunk's U area
-    for (int lv = lev_lo; lv < nlev; ++lv) {
+    for (int lv = 0; lv < nlev; ++lv) {
         const MrLevel& L = mr.view.lev[lv];
         Mr2Level& M = v.lev[lv];
+        const bool bpart = true;
         M.vfmt = M.ufmt = -1;
         for (int id = L.node0; id < L.node0 + L.nnodes; ++id) {
             const NodeDesc& nd = nodes[id];
@@ -1538,7 +1612,7 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
                 if (M.vfmt >= 0 && M.vfmt != nd.v_fmt) return HODLR_OK;  // one format per level
                 M.vfmt = nd.v_fmt;
             }
-            if (nd.ru > 0) {
+            if (nd.ru > 0 && bpart) {
                 if (M.ufmt >= 0 && M.ufmt != nd.u_fmt) return HODLR_OK;
                 M.ufmt = nd.u_fmt;
             }
@@ -1550,6 +1624,9 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
         M.ablk = 32 * Pol::AR * 4 * fmt_bytes(M.vfmt);
         M.aoff = aoff;
         aoff += (int64_t)M.nmt * M.ablk;
+        v.ntasks += M.nmt;
+        v.max_ablk = std::max(v.max_ablk, M.ablk);
+        if (!bpart) continue;
         M.steps = (L.ru_max + Pol::KU - 1) / Pol::KU;
         M.usz = MT * 32 * Pol::AR * Pol::UV * fmt_bytes(M.ufmt);
         // all 16 warps' blocks of one step are adjacent; a level starts at a
@@ -1558,16 +1635,14 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
         uoff = (uoff + sstep - 1) / sstep * sstep;
         M.uoff = uoff;
         uoff += (int64_t)M.steps * sstep;
-        v.ntasks += M.nmt;
         v.nu_items += M.steps;
-        v.max_ablk = std::max(v.max_ablk, M.ablk);
     }
     if (v.max_ablk == 0) v.max_ablk = 128;
     if (v.d_item & (v.d_item - 1)) return HODLR_OK;
     while ((1 << v.lslot) < v.d_item) ++v.lslot;
     {
         int next = -1;
-        for (int lv = nlev - 1; lv >= lev_lo; --lv) {
+        for (int lv = nlev - 1; lv >= 0; --lv) {
             Mr2Level& M = v.lev[lv];
             M.ulo = (int32_t)M.uoff;
             M.unext = next;
@@ -1610,6 +1685,7 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
 
 hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
     mr = MrPlan{};
+    mr.sharded = in.lev_lo > 0;
     const auto& nodes = *in.nodes;
     const auto& chunks = *in.chunks;
     const auto& cn = *in.chunk_nodes;
@@ -1656,6 +1732,15 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
         rows += (int64_t)(v.nb + L.nnodes) * L.rv_pad;
     }
     v.part_rows = rows;
+    // send-slot width of each external level (sharded handles; node ids 0..L-1)
+    for (size_t id = 0; id < nodes.size(); ++id) {
+        const NodeDesc& nd = nodes[id];
+        if (nd.ext_slot < 0) continue;
+        int64_t next = in.ext_count;
+        for (size_t j = 0; j < nodes.size(); ++j)
+            if (nodes[j].ext_slot > nd.ext_slot && nodes[j].ext_slot < next) next = nodes[j].ext_slot;
+        v.lev[nd.level - 1].ext_w = (int32_t)(next - nd.ext_slot);
+    }
     // node -> CTA range of the phase-A grid
     std::vector<MrSlot> slots(nodes.size(), MrSlot{-1, -1, 0, 0});
     for (int b = 0; b < v.nb; ++b) {
@@ -1673,9 +1758,18 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
         slots[id].jrel = (int)id - v.lev[lv].node0;
         if (slots[id].b0 < 0) return HODLR_OK;  // node without rows: generic path
     }
-    cudaError_t e = cudaMalloc(&mr.dev, slots.size() * sizeof(MrSlot));
+    // nodes whose sum spans several phase-A CTAs (or goes to the send buffer)
+    std::vector<int32_t> multi;
+    for (size_t id = 0; id < nodes.size(); ++id)
+        if (slots[id].b1 > slots[id].b0 || nodes[id].ext_slot >= 0) multi.push_back((int32_t)id);
+    mr.nmulti = (int)multi.size();
+    const size_t sbytes = (slots.size() * sizeof(MrSlot) + 255) / 256 * 256;
+    cudaError_t e = cudaMalloc(&mr.dev, sbytes + multi.size() * sizeof(int32_t) + 4);
     if (e == cudaSuccess)
         e = cudaMemcpy(mr.dev, slots.data(), slots.size() * sizeof(MrSlot), cudaMemcpyHostToDevice);
+    mr.multi = (int32_t*)((uint8_t*)mr.dev + sbytes);
+    if (e == cudaSuccess && !multi.empty())
+        e = cudaMemcpy(mr.multi, multi.data(), multi.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         mr_release(mr);
         return HODLR_ERR_CUDA;
@@ -1715,8 +1809,47 @@ bool mr_usable(const MrPlan& mr, int working_fmt) {
 
 int mr_launches() { return 3; }
 
+bool mr_slab_begin_usable(const MrPlan& mr, int working_fmt) {
+    return mr.slab_ok && mr.slab_fmt == working_fmt && mr.sharded && !getenv("HODLR_B200_NO_SLAB");
+}
+
+template <class Pol>
+static cudaError_t shard_begin_t(const PlanView& p, const MrPlan& mr, const typename Pol::W* x, int64_t ldx,
+                                 int64_t s, typename Pol::W* partial, typename Pol::W* tbuf,
+                                 typename Pol::W* send, cudaStream_t st) {
+    using W = typename Pol::W;
+    const int spad = (int)mr_spad(s);
+    cudaError_t e = launch_ma2<Pol>(p, mr.view, mr.v2, x, ldx, s, spad, partial, tbuf, st);
+    if (e != cudaSuccess) return e;
+    if (mr.nmulti == 0) return cudaSuccess;
+    dim3 gr = reduce_grid(mr.view, 0, p.nnodes, s);
+    gr.x = mr.nmulti;
+    k_mr_reduce<W><<<gr, 256, 0, st>>>(p, mr.view, 0, s, spad, partial, tbuf, send, mr.multi);
+    return cudaGetLastError();
+}
+template <>
+cudaError_t mr_shard_begin<double>(const PlanView& p, const MrPlan& mr, const double* x, int64_t ldx, int64_t s,
+                                   double* partial, double* tbuf, double* send, cudaStream_t st) {
+    return shard_begin_t<PolF64>(p, mr, x, ldx, s, partial, tbuf, send, st);
+}
+template <>
+cudaError_t mr_shard_begin<float>(const PlanView& p, const MrPlan& mr, const float* x, int64_t ldx, int64_t s,
+                                  float* partial, float* tbuf, float* send, cudaStream_t st) {
+    return shard_begin_t<PolTF32>(p, mr, x, ldx, s, partial, tbuf, send, st);
+}
+template <>
+cudaError_t mr_slab_phase_b<double>(const PlanView& p, const MrPlan& mr, const double* x, int64_t ldx, double* b,
+                                    int64_t ldb, int64_t s, const double* tbuf, cudaStream_t st) {
+    return launch_mb2<PolF64>(p, mr.view, mr.v2, x, ldx, tbuf, b, ldb, s, (int)mr_spad(s), st);
+}
+template <>
+cudaError_t mr_slab_phase_b<float>(const PlanView& p, const MrPlan& mr, const float* x, int64_t ldx, float* b,
+                                   int64_t ldb, int64_t s, const float* tbuf, cudaStream_t st) {
+    return launch_mb2<PolTF32>(p, mr.view, mr.v2, x, ldx, tbuf, b, ldb, s, (int)mr_spad(s), st);
+}
+
 bool mr_slab_used(const MrPlan& mr, int working_fmt, int lev_lo) {
-    return mr.slab_ok && mr.slab_fmt == working_fmt && mr.v2.lev_lo == lev_lo && !getenv("HODLR_B200_NO_SLAB");
+    return mr.slab_ok && mr.slab_fmt == working_fmt && !mr.sharded && lev_lo == 0 && !getenv("HODLR_B200_NO_SLAB");
 }
 
 template <>

@@ -33,7 +33,7 @@ struct MrLevel {
     int32_t node0, nnodes;   // node ids of the level: [node0, node0 + nnodes)
     int32_t rv_max, ru_max;  // max ranks over the level's nodes
     int32_t rv_pad;          // rv_max rounded up to 8: rows of one partial slot
-    int32_t pad_;
+    int32_t ext_w;           // external level of a sharded handle: its send-slot width (else 0)
     int64_t part_rows;       // first partial row of the level (a row holds spad values)
 };
 
@@ -74,7 +74,8 @@ struct Mr2Level {
     int32_t unext;    // U-area offset of the next level with steps, -1 if none
 };
 struct Mr2View {
-    int32_t nlev, lev_lo;      // levels lev_lo..nlev-1 are in the slab
+    int32_t nlev, lev_lo;      // levels lev_lo..nlev-1 are in the B region (phase B)
+    int32_t alev_lo;           // levels alev_lo..nlev-1 are in the A region (0: incl. external levels)
     int32_t ntasks;            // phase-A tasks (m-tiles) per chunk
     int32_t nu_items;          // U items per warp per chunk
     int64_t a_chunk_bytes, b_chunk_bytes;
@@ -92,6 +93,7 @@ struct Mr2View {
 struct MrPlan {
     bool ok = false;
     bool slab_ok = false;      // fragment slabs built (for the working precision slab_fmt)
+    bool sharded = false;      // handle of a sharded tree (external levels 1..L)
     int slab_fmt = -1;
     Mr2View v2{};
     void* slab_dev = nullptr;
@@ -99,6 +101,8 @@ struct MrPlan {
     int leaf_fmt = HODLR_FMT_FP64;
     MrView view{};
     void* dev = nullptr;
+    int32_t* multi = nullptr;  // device: ids of nodes summed over several phase-A CTAs (or external)
+    int nmulti = 0;
     int max_leaf_m = 0;
 };
 
@@ -113,6 +117,7 @@ struct MrInput {
     int nlev;
     int leaf_fmt;
     int device;
+    int64_t ext_count;         // sharded: send slots per unit s (external levels)
 };
 
 hodlr_status mr_prepare(const MrInput& in, MrPlan& mr);
@@ -131,5 +136,16 @@ int mr_launches();
 template <typename W>
 cudaError_t mr_matvec(const PlanView& p, const MrPlan& mr, int lev_lo, const W* x, int64_t ldx, W* b,
                       int64_t ldb, int64_t s, W* partial, W* tbuf, cudaStream_t st);
+// Sharded handles with fragment slabs: shard_begin runs phase A over ALL levels
+// (external partials -> send, subtree coefficients -> tbuf); shard_local does
+// nothing; shard_end reduces the gathered external coefficients and runs phase
+// B over ALL levels (mr_slab_phase_b): b is written once, no read-modify-write.
+bool mr_slab_begin_usable(const MrPlan& mr, int working_fmt);
+template <typename W>
+cudaError_t mr_shard_begin(const PlanView& p, const MrPlan& mr, const W* x, int64_t ldx, int64_t s, W* partial,
+                           W* tbuf, W* send, cudaStream_t st);
+template <typename W>
+cudaError_t mr_slab_phase_b(const PlanView& p, const MrPlan& mr, const W* x, int64_t ldx, W* b, int64_t ldb,
+                            int64_t s, const W* tbuf, cudaStream_t st);
 
 }  // namespace hodlr

@@ -48,7 +48,10 @@ def run_emulated(torch, H, X, nranks, check_send=True):
             emu.shard_begin(torch.from_numpy(xl.double().cpu().numpy()), ref)
             got = send.double().cpu().numpy()
             assert np.isfinite(got).all(), "send slots left unwritten"
-            assert rel(got, ref.numpy()) <= (1e-13 if wdt == torch.float64 else 1e-6)
+            # fp32: 1e-6 for the SIMT external-level kernels; the tensor-core
+            # phase A (3xTF32, fragment slabs) sums hi/lo products: 1e-5
+            slab = op.path(s)[0] == "mrhs_slab"
+            assert rel(got, ref.numpy()) <= (1e-13 if wdt == torch.float64 else (1e-5 if slab else 1e-6))
         sends.append(send)
         xs.append(xl)
     recv = torch.cat(sends)
