@@ -184,12 +184,14 @@ hodlr_status hodlr_info(const hodlr_handle* h, hodlr_info_t* info);
  * kernel launches that is.  *path: 0 generic (three launches, any layout),
  * 1 fused single-vector kernel, 2 multi-RHS tensor-core kernels over the
  * level-batched arena, 3 multi-RHS tensor-core kernels over the fragment
- * slabs (uniform 256-row leaves, bulk-copy streamed). */
+ * slabs (uniform 256-row leaves, bulk-copy streamed), 4 the same with phase B
+ * on the tcgen05 tensor cores (fp32 working, kind::tf32, item slabs). */
 typedef enum {
     HODLR_PATH_GENERIC = 0,
     HODLR_PATH_FUSED_SV = 1,
     HODLR_PATH_MRHS = 2,
-    HODLR_PATH_MRHS_SLAB = 3
+    HODLR_PATH_MRHS_SLAB = 3,
+    HODLR_PATH_MRHS_TC = 4
 } hodlr_path;
 hodlr_status hodlr_matvec_path(const hodlr_handle* h, int32_t working, int64_t s, int32_t* path,
                                int32_t* launches);

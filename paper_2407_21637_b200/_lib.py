@@ -17,8 +17,9 @@ c_i32, c_i64, c_sz, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctyp
 c_dp = ctypes.POINTER(ctypes.c_double)
 
 HODLR_OK, HODLR_ERR_INVALID, HODLR_ERR_UNSUPPORTED, HODLR_ERR_CUDA = 0, 1, 2, 3
-PATH_GENERIC, PATH_FUSED_SV, PATH_MRHS, PATH_MRHS_SLAB = 0, 1, 2, 3
-PATH_NAMES = {PATH_GENERIC: "generic", PATH_FUSED_SV: "fused_sv", PATH_MRHS: "mrhs", PATH_MRHS_SLAB: "mrhs_slab"}
+PATH_GENERIC, PATH_FUSED_SV, PATH_MRHS, PATH_MRHS_SLAB, PATH_MRHS_TC = 0, 1, 2, 3, 4
+PATH_NAMES = {PATH_GENERIC: "generic", PATH_FUSED_SV: "fused_sv", PATH_MRHS: "mrhs", PATH_MRHS_SLAB: "mrhs_slab",
+              PATH_MRHS_TC: "mrhs_tc"}
 ABI_VERSION = 2
 
 

@@ -645,6 +645,7 @@ hodlr_status hodlr_matvec_path(const hodlr_handle* h, int32_t working, int64_t s
     } else if (mr_usable(h->mr, working)) {
         const bool slab = h->nranks > 1 ? mr_slab_begin_usable(h->mr, working) : mr_slab_used(h->mr, working, h->L);
         *path = slab ? HODLR_PATH_MRHS_SLAB : HODLR_PATH_MRHS;
+        if (slab && working == HODLR_FMT_FP32 && tc_usable(h->mr, s)) *path = HODLR_PATH_MRHS_TC;
         *launches = mr_launches();
     } else {
         *path = HODLR_PATH_GENERIC;

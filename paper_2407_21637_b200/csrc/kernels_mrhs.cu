@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_a(PlanView p, const __grid_co
                 for (int i = 0; i < Pol::CR; ++i) {
                     const int c = mt * Pol::MR + g + 8 * (i >> 1);
                     const int q = nt * 8 + 2 * tig + (i & 1);
-                    if (c < L.rv_max)
+                    if (c < L.rv_max && q0 + q < spad)  // the last column group may overhang spad
                         partial[(L.part_rows + slot * L.rv_pad + c) * spad + q0 + q] = my[i];
                     my[i] = W(0);
                 }
@@ -1517,6 +1517,28 @@ cudaError_t launch_mb2(const PlanView& p, const MrView& m, const Mr2View& v, con
     return launch_mb2_t<Pol, 1>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st);
 }
 
+// Fixed-order reduction of the listed multi-slot nodes (mr.multi: nbig
+// many-slot nodes, then the rest), one launch per class so no CTA is idle.
+template <typename W>
+cudaError_t launch_reduce(const PlanView& p, const MrPlan& mr, int64_t s, int spad, const W* partial, W* tbuf,
+                          W* send, cudaStream_t st) {
+    const int nsmall = mr.nmulti - mr.nbig;
+    if (mr.nbig > 0) {
+        const int64_t t = ((int64_t)mr.rmax_big * s + 7) / 8;
+        dim3 gr(mr.nbig, (unsigned)std::max<int64_t>(1, std::min<int64_t>(t, 1024)));
+        k_mr_reduce<W><<<gr, 256, 0, st>>>(p, mr.view, 0, s, spad, partial, tbuf, send, mr.multi);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (nsmall > 0) {
+        const int64_t t = ((int64_t)mr.rmax_small * s + 255) / 256;
+        dim3 gr(nsmall, (unsigned)std::max<int64_t>(1, std::min<int64_t>(t, 1024)));
+        k_mr_reduce<W><<<gr, 256, 0, st>>>(p, mr.view, 0, s, spad, partial, tbuf, send, mr.multi + mr.nbig);
+        return cudaGetLastError();
+    }
+    return cudaSuccess;
+}
+
 template <class Pol>
 cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typename Pol::W* x, int64_t ldx,
                    typename Pol::W* b, int64_t ldb, int64_t s, typename Pol::W* partial,
@@ -1530,17 +1552,25 @@ cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typena
     if (mr_slab_used(mr, wfmt, lev_lo)) {
         cudaError_t e = cudaSuccess;
         if (any_level) {
-            e = launch_ma2<Pol>(p, m, mr.v2, x, ldx, s, spad, partial, tbuf, st);
+            bool done = false;
+            if constexpr (sizeof(W) == 4) {
+                if (tca_usable(mr, s)) {
+                    e = tc_phase_a(p, mr, x, ldx, s, partial, tbuf, st);
+                    done = true;
+                }
+            }
+            if (!done) e = launch_ma2<Pol>(p, m, mr.v2, x, ldx, s, spad, partial, tbuf, st);
             const int node_lo = m.lev[lev_lo].node0;
             const int nred = p.nnodes - node_lo;
-            if (e == cudaSuccess && nred > 0 && mr.nmulti > 0) {  // single-slot nodes were written by phase A
-                dim3 gr = reduce_grid(m, node_lo, p.nnodes, s);
-                gr.x = mr.nmulti;
-                k_mr_reduce<W><<<gr, 256, 0, st>>>(p, m, node_lo, s, spad, partial, tbuf, nullptr, mr.multi);
-                e = cudaGetLastError();
-            }
+            if (e == cudaSuccess && nred > 0 && mr.nmulti > 0)  // single-slot nodes were written by phase A
+                e = launch_reduce<W>(p, mr, s, spad, partial, tbuf, nullptr, st);
         }
-        if (e == cudaSuccess) e = launch_mb2<Pol>(p, m, mr.v2, x, ldx, tbuf, b, ldb, s, spad, st);
+        if (e == cudaSuccess) {
+            if constexpr (sizeof(W) == 4) {
+                if (tc_usable(mr, s)) return tc_phase_b(p, mr, x, ldx, b, ldb, s, tbuf, st);
+            }
+            e = launch_mb2<Pol>(p, m, mr.v2, x, ldx, tbuf, b, ldb, s, spad, st);
+        }
         return e;
     }
     if (any_level) {
@@ -1723,6 +1753,10 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
         if (nd.u_fmt == HODLR_FMT_FP64 || nd.v_fmt == HODLR_FMT_FP64) mr.has_fp64_operand = true;
     }
     if (in.leaf_fmt == HODLR_FMT_FP64) mr.has_fp64_operand = true;
+    // tcgen05 phase A runs one CTA per SM (512 TMEM columns): slots per SM
+    mr.tca_cand = !mr.has_fp64_operand && in.view && in.d_arena && !getenv("HODLR_B200_NO_SLAB") &&
+                  tc_a_candidate(in, v);
+    if (mr.tca_cand) v.nb = std::max(1, std::min(nch, sms));
     int64_t rows = 0;
     for (int lv = 0; lv < nlev; ++lv) {
         MrLevel& L = v.lev[lv];
@@ -1759,9 +1793,19 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
         if (slots[id].b0 < 0) return HODLR_OK;  // node without rows: generic path
     }
     // nodes whose sum spans several phase-A CTAs (or goes to the send buffer)
-    std::vector<int32_t> multi;
+    // listed many-slot nodes first (one warp per coefficient), then the others
+    // (one thread per coefficient): two reduce launches sized for each class
+    std::vector<int32_t> multi, small;
     for (size_t id = 0; id < nodes.size(); ++id)
-        if (slots[id].b1 > slots[id].b0 || nodes[id].ext_slot >= 0) multi.push_back((int32_t)id);
+        if (slots[id].b1 > slots[id].b0 || nodes[id].ext_slot >= 0) {
+            const bool big = slots[id].b1 - slots[id].b0 + 1 > 32;
+            const int w = std::max(nodes[id].rv, nodes[id].ext_slot >= 0 ? v.lev[nodes[id].level - 1].ext_w : 0);
+            (big ? multi : small).push_back((int32_t)id);
+            int& r = big ? mr.rmax_big : mr.rmax_small;
+            r = std::max(r, w);
+        }
+    mr.nbig = (int)multi.size();
+    multi.insert(multi.end(), small.begin(), small.end());
     mr.nmulti = (int)multi.size();
     const size_t sbytes = (slots.size() * sizeof(MrSlot) + 255) / 256 * 256;
     cudaError_t e = cudaMalloc(&mr.dev, sbytes + multi.size() * sizeof(int32_t) + 4);
@@ -1782,6 +1826,7 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
             st = build_slab<PolF64>(in, mr);
         else if (in.leaf_fmt == HODLR_FMT_FP32)
             st = build_slab<PolTF32>(in, mr);
+        if (st == HODLR_OK && mr.slab_ok) st = tc_prepare(in, mr);
         if (st != HODLR_OK) {
             mr_release(mr);
             return st;
@@ -1793,8 +1838,14 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
 void mr_release(MrPlan& mr) {
     if (mr.dev) cudaFree(mr.dev);
     if (mr.slab_dev) cudaFree(mr.slab_dev);
+    if (mr.tc_dev) cudaFree(mr.tc_dev);
+    if (mr.tca_dev) cudaFree(mr.tca_dev);
+    mr.tca_dev = nullptr;
+    mr.tca_ok = false;
     mr.dev = nullptr;
     mr.slab_dev = nullptr;
+    mr.tc_dev = nullptr;
+    mr.tc_ok = false;
     mr.ok = false;
     mr.slab_ok = false;
 }
@@ -1819,13 +1870,16 @@ static cudaError_t shard_begin_t(const PlanView& p, const MrPlan& mr, const type
                                  typename Pol::W* send, cudaStream_t st) {
     using W = typename Pol::W;
     const int spad = (int)mr_spad(s);
-    cudaError_t e = launch_ma2<Pol>(p, mr.view, mr.v2, x, ldx, s, spad, partial, tbuf, st);
+    cudaError_t e;
+    if constexpr (sizeof(W) == 4) {
+        e = tca_usable(mr, s) ? tc_phase_a(p, mr, x, ldx, s, partial, tbuf, st)
+                              : launch_ma2<Pol>(p, mr.view, mr.v2, x, ldx, s, spad, partial, tbuf, st);
+    } else {
+        e = launch_ma2<Pol>(p, mr.view, mr.v2, x, ldx, s, spad, partial, tbuf, st);
+    }
     if (e != cudaSuccess) return e;
     if (mr.nmulti == 0) return cudaSuccess;
-    dim3 gr = reduce_grid(mr.view, 0, p.nnodes, s);
-    gr.x = mr.nmulti;
-    k_mr_reduce<W><<<gr, 256, 0, st>>>(p, mr.view, 0, s, spad, partial, tbuf, send, mr.multi);
-    return cudaGetLastError();
+    return launch_reduce<W>(p, mr, s, spad, partial, tbuf, send, st);
 }
 template <>
 cudaError_t mr_shard_begin<double>(const PlanView& p, const MrPlan& mr, const double* x, int64_t ldx, int64_t s,
@@ -1845,6 +1899,7 @@ cudaError_t mr_slab_phase_b<double>(const PlanView& p, const MrPlan& mr, const d
 template <>
 cudaError_t mr_slab_phase_b<float>(const PlanView& p, const MrPlan& mr, const float* x, int64_t ldx, float* b,
                                    int64_t ldb, int64_t s, const float* tbuf, cudaStream_t st) {
+    if (tc_usable(mr, s)) return tc_phase_b(p, mr, x, ldx, b, ldb, s, tbuf, st);
     return launch_mb2<PolTF32>(p, mr.view, mr.v2, x, ldx, tbuf, b, ldb, s, (int)mr_spad(s), st);
 }
 

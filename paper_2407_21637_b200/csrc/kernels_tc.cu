@@ -1,0 +1,891 @@
+// Multi-RHS phase B on the 5th-generation tensor cores (tcgen05, kind::tf32),
+// fp32 working precision.  Layout and item order: tcb.h.
+//
+// Per leaf (256 rows) and pass of up to 64 right-hand sides:
+//     b[rows, q0:q0+N] = sum over items of A_item (256 x c) * B_item (c x N)
+// A_item = leaf columns (D) or one level's U columns, streamed once from HBM;
+// B_item = the matching rows of X (D items) or of the coefficients T_k of the
+// sibling node (U items), staged from global memory (L2).
+//
+// 3xTF32: every fp32 operand a = hi + lo (both tf32, tc::split_tf32), and
+//     acc += A_hi B_hi + A_hi B_lo + A_lo B_hi
+// which keeps fp32-level accuracy (the dropped A_lo B_lo and the tf32
+// roundings are O(2^-22) relative).  Storage formats narrower than fp32 (fp16,
+// bf16, q52) are exact tf32 values: A_lo = 0 and the third product is skipped.
+// Accumulation is fp32 in tensor memory.
+//
+// Warp roles (one CTA per SM, persistent over (leaf, column block) work units):
+//   warps 0-7  converters: warp w owns m-tile w/4 (leaf rows 128*(w/4) ..) and
+//              TMEM lane quarter w%4; thread = one leaf row.  Per item: wait for
+//              the raw bytes, load the row's values (one vector load per column
+//              quad), split, tcgen05.st hi/lo into the item's TMEM A stage.
+//              They also run the epilogue of the previous leaf (tcgen05.ld of
+//              the accumulator, b written once: disjoint rows, no atomics),
+//              deferred by one item so it overlaps the next leaf's first MMAs.
+//   warp 8     producer: one cp.async.bulk per item into a 4-slot ring.
+//   warp 9     MMA issuer (one thread) and TMEM owner (512 columns).
+//   warps 10-13 B stagers: X / T rows -> tf32 hi/lo in the K-major no-swizzle
+//              canonical layout (core matrix = 8 columns x 4 k), 3-slot ring.
+// TMEM columns: accumulators [2 buffers][2 m-tiles][64] at 0..255, A stages
+// [2][2 m-tiles][hi 32 | lo 32] at 256..511.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "async.cuh"
+#include "formats.cuh"
+#include "mrhs.h"
+#include "tc.cuh"
+
+namespace hodlr {
+namespace {
+
+constexpr int kTcConvWarps = 8;
+constexpr int kTcProdWarp = 8;
+constexpr int kTcMmaWarp = 9;
+constexpr int kTcStageWarp0 = 10;
+constexpr int kTcStageWarps = 4;
+constexpr int kTcThreads = (kTcStageWarp0 + kTcStageWarps) * 32;
+constexpr int kTcRawStages = 4;
+constexpr int kTcRawSlot = kTcRows * kTcItemCols * 4;  // 32 KB
+constexpr int kTcBStages = 3;
+constexpr int kTcBHalf = kTcItemCols * kTcN * 4;       // 8 KB: hi (or lo) of one item
+constexpr int kTcBSlot = 2 * kTcBHalf;
+constexpr uint32_t kTcAcc = 0, kTcAStage = 256;
+constexpr int kChunkRowsTa = 256;  // rows of a phase-A chunk (= leaf)
+constexpr int kTcBars = 2 * kTcRawStages + 2 * 2 + 2 * kTcBStages + 2 * 2;
+constexpr size_t kTcSmem = (size_t)kTcRawStages * kTcRawSlot + (size_t)kTcBStages * kTcBSlot + kTcBars * 8 + 16;
+
+__device__ __forceinline__ float4 load_quad(int fmt, const uint8_t* p) {
+    switch (fmt) {
+        case HODLR_FMT_FP32:
+            return *reinterpret_cast<const float4*>(p);
+        case HODLR_FMT_FP16: {
+            const uint2 u = *reinterpret_cast<const uint2*>(p);
+            return make_float4(dec_fp16((uint16_t)(u.x & 0xFFFF)), dec_fp16((uint16_t)(u.x >> 16)),
+                               dec_fp16((uint16_t)(u.y & 0xFFFF)), dec_fp16((uint16_t)(u.y >> 16)));
+        }
+        case HODLR_FMT_BF16: {
+            const uint2 u = *reinterpret_cast<const uint2*>(p);
+            return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                               __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+        }
+        default: {  // q52
+            const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+            return make_float4(dec_q52((uint8_t)(u & 0xFF)), dec_q52((uint8_t)((u >> 8) & 0xFF)),
+                               dec_q52((uint8_t)((u >> 16) & 0xFF)), dec_q52((uint8_t)(u >> 24)));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_tc_b(PlanView p, const __grid_constant__ TcView v, const float* __restrict__ x, int64_t ldx,
+           const float* __restrict__ tbuf, float* __restrict__ b, int64_t ldb, int64_t s, int nblk) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint8_t* ring = smem_raw;                                              // [4][32 KB]
+    uint8_t* bring = ring + (size_t)kTcRawStages * kTcRawSlot;             // [3][hi 8 KB | lo 8 KB]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(bring + (size_t)kTcBStages * kTcBSlot);
+    uint64_t* raw_full = bars;
+    uint64_t* raw_empty = raw_full + kTcRawStages;
+    uint64_t* a_full = raw_empty + kTcRawStages;
+    uint64_t* a_empty = a_full + 2;
+    uint64_t* b_full = a_empty + 2;
+    uint64_t* b_empty = b_full + kTcBStages;
+    uint64_t* acc_full = b_empty + kTcBStages;
+    uint64_t* acc_empty = acc_full + 2;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwork = p.nchunks * nblk;
+    const int nitems = v.nitems;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kTcRawStages; ++i) {
+            tma::mbar_init(&raw_full[i], 1);
+            tma::mbar_init(&raw_empty[i], kTcConvWarps);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tma::mbar_init(&a_full[i], kTcConvWarps);
+            tma::mbar_init(&a_empty[i], 1);
+            tma::mbar_init(&acc_full[i], 1);
+            tma::mbar_init(&acc_empty[i], kTcConvWarps);
+        }
+        for (int i = 0; i < kTcBStages; ++i) {
+            tma::mbar_init(&b_full[i], kTcStageWarps);
+            tma::mbar_init(&b_empty[i], 1);
+        }
+        tma::fence_mbar_init();
+    }
+    if (warp == kTcMmaWarp) tc::tmem_alloc<512>(tbase_s);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = *tbase_s;
+
+    if (warp < kTcConvWarps) {
+        // ---------------------------------------------------------- converters + epilogue
+        const int mt = warp >> 2, qd = warp & 3;
+        const int row = mt * 128 + qd * 32 + lane;
+        const uint32_t tl = tbase + ((uint32_t)(qd * 32) << 16);
+        int64_t g = 0;
+        int lc = 0;
+        int pend_chunk = -1, pend_q0 = 0, pend_n = 0;
+        auto epilogue = [&](int chunk, int q0, int nn, int leafno) {
+            const int ab = leafno & 1;
+            tma::mbar_wait(&acc_full[ab], (unsigned)((leafno >> 1) & 1));
+            tc::fence_after();
+            const int64_t r = p.chunks[chunk].row0 + row;
+            float* brow = b + r * ldb + q0;
+            const bool vec = ((ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
+            for (int c = 0; c < nn; c += 16) {
+                uint32_t a[16];
+                tc::ld_x16(tl + kTcAcc + ab * 128 + mt * 64 + c, a);
+                tc::wait_ld();
+                if (vec && q0 + c + 16 <= s) {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        *reinterpret_cast<float4*>(brow + c + j) =
+                            make_float4(__uint_as_float(a[j]), __uint_as_float(a[j + 1]),
+                                        __uint_as_float(a[j + 2]), __uint_as_float(a[j + 3]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (q0 + c + j < s) brow[c + j] = __uint_as_float(a[j]);
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&acc_empty[ab]);
+        };
+        for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++lc) {
+            const int chunk = work / nblk;
+            const int q0 = (work % nblk) * kTcN;
+            const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
+            for (int i = 0; i < nitems; ++i, ++g) {
+                const TcItem it = v.item[i];
+                const int rs = (int)(g % kTcRawStages), ts = (int)(g & 1);
+                tma::mbar_wait(&raw_full[rs], (unsigned)((g / kTcRawStages) & 1));
+                if (g >= 2) tma::mbar_wait(&a_empty[ts], (unsigned)(((g >> 1) & 1) ^ 1));
+                tc::fence_after();
+                const int w = fmt_bytes(it.fmt);
+                const uint8_t* rp = ring + (size_t)rs * kTcRawSlot + (size_t)row * 4 * w;
+                const uint32_t ah = tl + kTcAStage + ts * 128 + mt * 64;
+                const bool full = it.fmt == HODLR_FMT_FP32;
+                for (int j = 0; j < it.ncols; j += 8) {
+                    const float4 f0 = load_quad(it.fmt, rp + (size_t)(j >> 2) * kTcRows * 4 * w);
+                    const float4 f1 = load_quad(it.fmt, rp + (size_t)((j >> 2) + 1) * kTcRows * 4 * w);
+                    const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+                    uint32_t hi[8], lo[8];
+                    if (full) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) tc::split_tf32(f[e], hi[e], lo[e]);
+                        tc::st_x8(ah + j, hi);
+                        tc::st_x8(ah + 32 + j, lo);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) hi[e] = __float_as_uint(f[e]);
+                        tc::st_x8(ah + j, hi);
+                    }
+                }
+                tc::wait_st();
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    tma::mbar_arrive(&raw_empty[rs]);
+                    tma::mbar_arrive(&a_full[ts]);
+                }
+                if (i == 0 && pend_chunk >= 0) {
+                    epilogue(pend_chunk, pend_q0, pend_n, lc - 1);
+                    pend_chunk = -1;
+                }
+            }
+            pend_chunk = chunk;
+            pend_q0 = q0;
+            pend_n = nn;
+        }
+        if (pend_chunk >= 0) epilogue(pend_chunk, pend_q0, pend_n, lc - 1);
+    } else if (warp == kTcProdWarp) {
+        // ---------------------------------------------------------- producer
+        if (lane == 0) {
+            const uint64_t pol = tma::policy_evict_first();
+            int64_t g = 0;
+            for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
+                const uint8_t* src = v.slab + (int64_t)(work / nblk) * v.leaf_bytes;
+                for (int i = 0; i < nitems; ++i, ++g) {
+                    const int rs = (int)(g % kTcRawStages);
+                    if (g >= kTcRawStages) tma::mbar_wait(&raw_empty[rs], (unsigned)(((g / kTcRawStages) & 1) ^ 1));
+                    const int bytes = v.item[i].bytes;
+                    tma::mbar_arrive_tx(&raw_full[rs], (unsigned)bytes);
+                    tma::bulk_g2s(ring + (size_t)rs * kTcRawSlot, src + v.item[i].off, (unsigned)bytes, &raw_full[rs],
+                                  pol);
+                }
+            }
+        }
+    } else if (warp == kTcMmaWarp) {
+        // ---------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            int64_t g = 0;
+            int lc = 0;
+            for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++lc) {
+                const int q0 = (work % nblk) * kTcN;
+                const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
+                const uint32_t idesc = tc::idesc_tf32(128, nn);
+                const uint32_t lbo = (uint32_t)(nn / 8) * 128;
+                const int ab = lc & 1;
+                if (lc >= 2) tma::mbar_wait(&acc_empty[ab], (unsigned)(((lc >> 1) & 1) ^ 1));
+                for (int i = 0; i < nitems; ++i, ++g) {
+                    const int ts = (int)(g & 1), bs = (int)(g % kTcBStages);
+                    tma::mbar_wait(&a_full[ts], (unsigned)((g >> 1) & 1));
+                    tma::mbar_wait(&b_full[bs], (unsigned)((g / kTcBStages) & 1));
+                    tc::fence_after();
+                    const int ncols = v.item[i].ncols;
+                    const bool full = v.item[i].fmt == HODLR_FMT_FP32;
+                    const uint32_t bh = tc::smem_u32(bring + (size_t)bs * kTcBSlot), bl = bh + kTcBHalf;
+                    for (int j = 0; j < ncols; j += 8) {
+                        const uint64_t dh = tc::smem_desc(bh + (uint32_t)(j >> 2) * lbo, lbo, 128);
+                        const uint64_t dl = tc::smem_desc(bl + (uint32_t)(j >> 2) * lbo, lbo, 128);
+#pragma unroll
+                        for (int m = 0; m < 2; ++m) {
+                            const uint32_t d = tbase + kTcAcc + ab * 128 + m * 64;
+                            const uint32_t ah = tbase + kTcAStage + ts * 128 + m * 64 + j;
+                            tc::mma_tf32_ts(d, ah, dh, idesc, (i | j) != 0);
+                            tc::mma_tf32_ts(d, ah, dl, idesc, 1);
+                            if (full) tc::mma_tf32_ts(d, ah + 32, dh, idesc, 1);
+                        }
+                    }
+                    tc::commit(&a_empty[ts]);
+                    tc::commit(&b_empty[bs]);
+                }
+                tc::commit(&acc_full[ab]);
+            }
+        }
+    } else {
+        // ---------------------------------------------------------- B stagers
+        const int t = threadIdx.x - kTcStageWarp0 * 32;
+        int64_t g = 0;
+        for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
+            const int chunk = work / nblk;
+            const int q0 = (work % nblk) * kTcN;
+            const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
+            const int64_t row0 = p.chunks[chunk].row0;
+            const int lbo = (nn / 8) * 128;
+            for (int i = 0; i < nitems; ++i, ++g) {
+                const TcItem it = v.item[i];
+                const int bs = (int)(g % kTcBStages);
+                if (g >= kTcBStages) tma::mbar_wait(&b_empty[bs], (unsigned)(((g / kTcBStages) & 1) ^ 1));
+                uint8_t* bh = bring + (size_t)bs * kTcBSlot;
+                uint8_t* bl = bh + kTcBHalf;
+                // source rows [col0, col0 + ncols) of X (leaf rows) or of T of the sibling node
+                const float* src;
+                int64_t ld;
+                int nvalid;
+                if (it.lv < 0) {
+                    src = x + (row0 + it.col0) * ldx + q0;
+                    ld = ldx;
+                    nvalid = it.ncols;
+                } else {
+                    const NodeDesc& nd = p.nodes[p.chunk_nodes[(int64_t)chunk * p.nlev + it.lv]];
+                    src = tbuf + (nd.tsrc_off + it.col0) * s + q0;
+                    ld = s;
+                    nvalid = max(0, min((int)it.ncols, nd.ru - it.col0));
+                }
+                const int nunits = (it.ncols >> 2) * nn;
+                for (int u0 = 0; u0 < nunits; u0 += 4 * 32 * kTcStageWarps) {
+                    float vals[4][4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int u = u0 + e * 32 * kTcStageWarps + t;
+                        const int kc = u / nn, n = u - kc * nn;
+                        const bool ok = u < nunits && q0 + n < s;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int r = kc * 4 + k;
+                            vals[e][k] = (ok && r < nvalid) ? __ldg(src + (int64_t)r * ld + n) : 0.0f;
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int u = u0 + e * 32 * kTcStageWarps + t;
+                        if (u >= nunits) continue;
+                        const int kc = u / nn, n = u - kc * nn;
+                        uint4 h, l;
+                        tc::split_tf32(vals[e][0], h.x, l.x);
+                        tc::split_tf32(vals[e][1], h.y, l.y);
+                        tc::split_tf32(vals[e][2], h.z, l.z);
+                        tc::split_tf32(vals[e][3], h.w, l.w);
+                        const int off = kc * lbo + (n >> 3) * 128 + (n & 7) * 16;
+                        *reinterpret_cast<uint4*>(bh + off) = h;
+                        *reinterpret_cast<uint4*>(bl + off) = l;
+                    }
+                }
+                tma::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) tma::mbar_arrive(&b_full[bs]);
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == kTcMmaWarp) {
+        tc::fence_after();
+        tc::tmem_free<512>(tbase);
+    }
+}
+
+// Item slab relayout (create time): one thread per (chunk, item, column quad, row).
+__global__ void k_tc_slab(PlanView p, const __grid_constant__ TcView v, int64_t units_per_chunk, uint8_t* slab) {
+    const int64_t total = units_per_chunk * p.nchunks;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int chunk = (int)(idx / units_per_chunk);
+        int64_t r = idx - (int64_t)chunk * units_per_chunk;
+        int i = 0;
+        for (;; ++i) {
+            const int64_t c = (int64_t)(v.item[i].ncols >> 2) * kTcRows;
+            if (r < c) break;
+            r -= c;
+        }
+        const TcItem it = v.item[i];
+        const int kc = (int)(r / kTcRows), row = (int)(r % kTcRows);
+        const int w = fmt_bytes(it.fmt);
+        uint8_t* dst = slab + (int64_t)chunk * v.leaf_bytes + it.off + ((int64_t)kc * kTcRows + row) * 4 * w;
+        const ChunkDesc ch = p.chunks[chunk];
+        for (int k = 0; k < 4; ++k) {
+            const int col = it.col0 + 4 * kc + k;
+            const uint8_t* src = nullptr;
+            if (it.lv < 0) {
+                const LeafDesc lf = p.leaves[ch.leaf];
+                src = p.arena + lf.off + ((int64_t)row * lf.ld + col) * w;
+            } else {
+                const NodeDesc nd = p.nodes[p.chunk_nodes[(int64_t)chunk * p.nlev + it.lv]];
+                if (col < nd.ru) src = p.arena + nd.u_off + ((int64_t)col * nd.u_ld + (ch.row0 - nd.row0 + row)) * w;
+            }
+            for (int e = 0; e < w; ++e) dst[k * w + e] = src ? src[e] : (uint8_t)0;
+        }
+    }
+}
+
+
+// ====================================================================== phase A
+// Warp roles: 0-15 converters / epilogue (warp w: M-tile w/4, TMEM lane quarter
+// w%4; thread = one stacked rank row m), 16 producer, 17 MMA issuer + TMEM
+// owner, 18-21 X stagers.  CTA b owns chunks [b*nch/nb, (b+1)*nch/nb) (the
+// MrView slot layout), per chunk D = sum over 16 items; the converters keep a
+// running sum per (row m, column) in registers across the chunks of the node
+// and flush it at the node's last chunk of the run: to the coefficient buffer
+// when this CTA holds the whole node, else to the node's partial slot.
+constexpr int kTaConvWarps = 4 * kTcAMaxTiles;
+constexpr int kTaProdWarp = kTaConvWarps;
+constexpr int kTaMmaWarp = kTaConvWarps + 1;
+constexpr int kTaStageWarp0 = kTaConvWarps + 2;
+constexpr int kTaStageWarps = 4;
+constexpr int kTaThreads = (kTaStageWarp0 + kTaStageWarps) * 32;
+constexpr int kTaMaxAStages = 3;
+constexpr int kTaBStages = 4;
+constexpr int kTaBHalf = kTcAItemRows * kTcN * 4;  // 4 KB
+constexpr int kTaBSlot = 2 * kTaBHalf;
+constexpr uint32_t kTaAcc = 0;
+constexpr int kTaMaxRaw = 6;
+constexpr int kTaBars = 2 * kTaMaxRaw + 2 * kTaMaxAStages + 2 * kTaBStages + 2;
+// TMEM: D tiles at columns t*64, then A stages of nmt*32 columns (hi 16 | lo 16
+// per tile): 3 stages for <= 3 tiles (480 columns), 2 for 4 tiles (512)
+__host__ __device__ inline int ta_astages(const TcAView& a) { return a.nmt <= 3 ? 3 : 2; }
+__host__ __device__ inline int ta_srows(const TcAView& a) { return (a.mtot + 31) / 32 * 32; }
+
+__host__ __device__ inline size_t ta_raw_slot(const TcAView& a) { return ((size_t)a.item_bytes + 127) / 128 * 128; }
+// running sums [64 columns][nmt * 128 rows] fp32 (thread m owns column j at j*rows + m)
+__host__ __device__ inline size_t ta_sum_bytes(const TcAView& a) { return (size_t)kTcN * ta_srows(a) * 4; }
+inline size_t ta_smem(const TcAView& a, int nraw) {
+    return nraw * ta_raw_slot(a) + (size_t)kTaBStages * kTaBSlot + ta_sum_bytes(a) + kTaBars * 8 + 16;
+}
+// raw ring depth: as many item slots (<= kTaMaxRaw) as fit next to the rest
+inline int ta_nraw(const TcAView& a) {
+    int n = kTaMaxRaw;
+    while (n > 2 && ta_smem(a, n) > 227 * 1024) --n;
+    return n;
+}
+
+__global__ void __launch_bounds__(kTaThreads, 1)
+    k_tc_a(PlanView p, const __grid_constant__ MrView m, const __grid_constant__ TcAView a,
+           const float* __restrict__ x, int64_t ldx, int64_t s, int spad, int nblk, float* __restrict__ partial,
+           float* __restrict__ tbuf, int nraw) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const size_t rslot = ta_raw_slot(a);
+    uint8_t* ring = smem_raw;
+    uint8_t* bring = ring + nraw * rslot;
+    float* sums = reinterpret_cast<float*>(bring + (size_t)kTaBStages * kTaBSlot);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sums) + ta_sum_bytes(a));
+    uint64_t* raw_full = bars;
+    uint64_t* raw_empty = raw_full + nraw;
+    uint64_t* a_full = raw_empty + nraw;
+    uint64_t* a_empty = a_full + kTaMaxAStages;
+    uint64_t* b_full = a_empty + kTaMaxAStages;
+    uint64_t* b_empty = b_full + kTaBStages;
+    uint64_t* acc_full = b_empty + kTaBStages;
+    uint64_t* acc_empty = acc_full + 1;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c_beg = (int)((int64_t)blockIdx.x * p.nchunks / gridDim.x);
+    const int c_end = (int)((int64_t)(blockIdx.x + 1) * p.nchunks / gridDim.x);
+    constexpr int kItems = kChunkRowsTa / kTcAItemRows;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nraw; ++i) {
+            tma::mbar_init(&raw_full[i], 1);
+            tma::mbar_init(&raw_empty[i], kTaConvWarps);
+        }
+        for (int i = 0; i < kTaMaxAStages; ++i) {
+            tma::mbar_init(&a_full[i], kTaConvWarps);
+            tma::mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < kTaBStages; ++i) {
+            tma::mbar_init(&b_full[i], kTaStageWarps);
+            tma::mbar_init(&b_empty[i], 1);
+        }
+        tma::mbar_init(acc_full, 1);
+        tma::mbar_init(acc_empty, kTaConvWarps);
+        tma::fence_mbar_init();
+    }
+    if (warp == kTaMmaWarp) tc::tmem_alloc<512>(tbase_s);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = *tbase_s;
+    const int nas = ta_astages(a);
+    const uint32_t abase = (uint32_t)a.nmt * 64, astride = (uint32_t)a.nmt * 32;
+
+    if (warp < kTaConvWarps) {
+        // ---------------------------------------------------------- converters + epilogue
+        const int mt = warp >> 2, qd = warp & 3;
+        const int mrow = mt * 128 + qd * 32 + lane;
+        int lv = -1, c = 0, fmt = HODLR_FMT_FP32, seg = 0, r8 = 0;
+        for (int l = 0; l < a.nlev; ++l)
+            if (mrow >= a.lev[l].mbase && mrow < a.lev[l].mbase + a.lev[l].r8) {
+                lv = l;
+                c = mrow - a.lev[l].mbase;
+                fmt = a.lev[l].fmt;
+                seg = a.lev[l].seg;
+                r8 = a.lev[l].r8;
+            }
+        const int w = fmt_bytes(fmt);
+        const uint32_t tl = tbase + ((uint32_t)(qd * 32) << 16);
+        const int srows = ta_srows(a);
+        float* my = sums + mrow;  // column j at my[j * srows]; rows >= mtot have no sums
+        if (lv >= 0)
+            for (int j = 0; j < kTcN; ++j) my[j * srows] = 0.f;
+        int64_t g = 0;
+        int lc = 0;  // chunks consumed (epilogues done)
+        // epilogue of chunk ci (the lc-th chunk of this CTA): D -> running sums,
+        // flushed at the node's last chunk of the run
+        auto epilogue = [&](int ci, int q0) {
+            tma::mbar_wait(acc_full, (unsigned)(lc & 1));
+            tc::fence_after();
+            // flush decision for this row's level (the whole warp loads D regardless)
+            bool flush = false;
+            float* dst = nullptr;
+            if (lv >= 0) {
+                const int node = p.chunk_nodes[(int64_t)ci * p.nlev + lv];
+                flush = !(ci + 1 < c_end && p.chunk_nodes[(int64_t)(ci + 1) * p.nlev + lv] == node);
+                if (flush) {
+                    const MrSlot sl = m.slots[node];
+                    const NodeDesc nd = p.nodes[node];
+                    if (sl.b0 == sl.b1 && nd.ext_slot < 0) {
+                        if (c < nd.rv) dst = tbuf + nd.t_off * s + (int64_t)c * s + q0;
+                    } else {
+                        const MrLevel L = m.lev[lv];
+                        if (c < L.rv_max)
+                            dst = partial + (L.part_rows + ((int64_t)blockIdx.x + sl.jrel) * L.rv_pad + c) * spad + q0;
+                    }
+                }
+            }
+            const int qn = (int)min((int64_t)kTcN, s - q0);
+#pragma unroll 1
+            for (int cc = 0; cc < kTcN; cc += 16) {
+                uint32_t v[16];
+                tc::ld_x16(tl + kTaAcc + mt * 64 + cc, v);
+                tc::wait_ld();
+                if (lv >= 0) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const float val = my[(cc + j) * srows] + __uint_as_float(v[j]);
+                        my[(cc + j) * srows] = flush ? 0.f : val;
+                        if (dst && cc + j < qn) dst[cc + j] = val;
+                    }
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(acc_empty);
+            ++lc;
+        };
+        int pend_ci = -1, pend_q0 = 0;
+        for (int blk = 0; blk < nblk; ++blk) {
+            const int q0 = blk * kTcN;
+            for (int ci = c_beg; ci < c_end; ++ci) {
+                for (int it = 0; it < kItems; ++it, ++g) {
+                    const int rs = (int)(g % nraw), as = (int)(g % nas);
+                    tma::mbar_wait(&raw_full[rs], (unsigned)((g / nraw) & 1));
+                    if (g >= nas) tma::mbar_wait(&a_empty[as], (unsigned)(((g / nas) & 1) ^ 1));
+                    tc::fence_after();
+                    uint32_t hi[16], lo[16];
+                    if (lv >= 0) {
+                        const uint8_t* rp = ring + (size_t)rs * rslot + seg + (size_t)c * 4 * w;
+#pragma unroll
+                        for (int kc = 0; kc < 4; ++kc) {
+                            const float4 f = load_quad(fmt, rp + (size_t)kc * r8 * 4 * w);
+                            tc::split_tf32(f.x, hi[4 * kc], lo[4 * kc]);
+                            tc::split_tf32(f.y, hi[4 * kc + 1], lo[4 * kc + 1]);
+                            tc::split_tf32(f.z, hi[4 * kc + 2], lo[4 * kc + 2]);
+                            tc::split_tf32(f.w, hi[4 * kc + 3], lo[4 * kc + 3]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) hi[e] = lo[e] = 0u;
+                    }
+                    if (mt < a.nmt) {  // warp-uniform: warps past the last tile only keep the protocol
+                        const uint32_t ah = tl + abase + as * astride + mt * 32;
+                        tc::st_x8(ah, *reinterpret_cast<const uint32_t(*)[8]>(&hi[0]));
+                        tc::st_x8(ah + 8, *reinterpret_cast<const uint32_t(*)[8]>(&hi[8]));
+                        tc::st_x8(ah + 16, *reinterpret_cast<const uint32_t(*)[8]>(&lo[0]));
+                        tc::st_x8(ah + 24, *reinterpret_cast<const uint32_t(*)[8]>(&lo[8]));
+                        tc::wait_st();
+                    }
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma::mbar_arrive(&raw_empty[rs]);
+                        tma::mbar_arrive(&a_full[as]);
+                    }
+                    if (it == 0 && pend_ci >= 0) {
+                        epilogue(pend_ci, pend_q0);
+                        pend_ci = -1;
+                    }
+                }
+                pend_ci = ci;
+                pend_q0 = q0;
+            }
+        }
+        if (pend_ci >= 0) epilogue(pend_ci, pend_q0);
+    } else if (warp == kTaProdWarp) {
+        // ---------------------------------------------------------- producer
+        if (lane == 0) {
+            const uint64_t pol = tma::policy_evict_first();
+            int64_t g = 0;
+            for (int blk = 0; blk < nblk; ++blk)
+                for (int ci = c_beg; ci < c_end; ++ci) {
+                    const uint8_t* src = a.slab + (int64_t)ci * a.chunk_bytes;
+                    for (int it = 0; it < kItems; ++it, ++g) {
+                        const int rs = (int)(g % nraw);
+                        if (g >= nraw) tma::mbar_wait(&raw_empty[rs], (unsigned)(((g / nraw) & 1) ^ 1));
+                        tma::mbar_arrive_tx(&raw_full[rs], (unsigned)a.item_bytes);
+                        tma::bulk_g2s(ring + (size_t)rs * rslot, src + (int64_t)it * a.item_bytes,
+                                      (unsigned)a.item_bytes, &raw_full[rs], pol);
+                    }
+                }
+        }
+    } else if (warp == kTaMmaWarp) {
+        // ---------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            int64_t g = 0;
+            int lc = 0;
+            for (int blk = 0; blk < nblk; ++blk) {
+                const int q0 = blk * kTcN;
+                const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
+                const uint32_t idesc = tc::idesc_tf32(128, nn);
+                const uint32_t lbo = (uint32_t)(nn / 8) * 128;
+                for (int ci = c_beg; ci < c_end; ++ci, ++lc) {
+                    if (lc >= 1) tma::mbar_wait(acc_empty, (unsigned)((lc - 1) & 1));
+                    for (int it = 0; it < kItems; ++it, ++g) {
+                        const int as = (int)(g % nas), bs = (int)(g % kTaBStages);
+                        tma::mbar_wait(&a_full[as], (unsigned)((g / nas) & 1));
+                        tma::mbar_wait(&b_full[bs], (unsigned)((g / kTaBStages) & 1));
+                        tc::fence_after();
+                        const uint32_t bh = tc::smem_u32(bring + (size_t)bs * kTaBSlot), bl = bh + kTaBHalf;
+#pragma unroll
+                        for (int j = 0; j < kTcAItemRows; j += 8) {
+                            const uint64_t dh = tc::smem_desc(bh + (uint32_t)(j >> 2) * lbo, lbo, 128);
+                            const uint64_t dl = tc::smem_desc(bl + (uint32_t)(j >> 2) * lbo, lbo, 128);
+                            for (int t = 0; t < a.nmt; ++t) {
+                                const uint32_t d = tbase + kTaAcc + t * 64;
+                                const uint32_t ah = tbase + abase + as * astride + t * 32 + j;
+                                tc::mma_tf32_ts(d, ah, dh, idesc, (it | j) != 0);
+                                tc::mma_tf32_ts(d, ah, dl, idesc, 1);
+                                if ((a.tile_full >> t) & 1) tc::mma_tf32_ts(d, ah + 16, dh, idesc, 1);
+                            }
+                        }
+                        tc::commit(&a_empty[as]);
+                        tc::commit(&b_empty[bs]);
+                    }
+                    tc::commit(acc_full);
+                }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------- X stagers
+        const int t = threadIdx.x - kTaStageWarp0 * 32;
+        int64_t g = 0;
+        for (int blk = 0; blk < nblk; ++blk) {
+            const int q0 = blk * kTcN;
+            const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
+            const int lbo = (nn / 8) * 128;
+            const int nunits = 4 * nn;
+            for (int ci = c_beg; ci < c_end; ++ci) {
+                const int64_t row0 = p.chunks[ci].row0;
+                for (int it = 0; it < kItems; ++it, ++g) {
+                    const int bs = (int)(g % kTaBStages);
+                    if (g >= kTaBStages) tma::mbar_wait(&b_empty[bs], (unsigned)(((g / kTaBStages) & 1) ^ 1));
+                    uint8_t* bh = bring + (size_t)bs * kTaBSlot;
+                    uint8_t* bl = bh + kTaBHalf;
+                    const float* src = x + (row0 + it * kTcAItemRows) * ldx + q0;
+                    float vals[2][4];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int u = e * 32 * kTaStageWarps + t;
+                        const int kc = u / nn, n = u - kc * nn;
+                        const bool ok = u < nunits && q0 + n < s;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) vals[e][k] = ok ? __ldg(src + (int64_t)(kc * 4 + k) * ldx + n) : 0.f;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int u = e * 32 * kTaStageWarps + t;
+                        if (u >= nunits) continue;
+                        const int kc = u / nn, n = u - kc * nn;
+                        uint4 h, l;
+                        tc::split_tf32(vals[e][0], h.x, l.x);
+                        tc::split_tf32(vals[e][1], h.y, l.y);
+                        tc::split_tf32(vals[e][2], h.z, l.z);
+                        tc::split_tf32(vals[e][3], h.w, l.w);
+                        const int off = kc * lbo + (n >> 3) * 128 + (n & 7) * 16;
+                        *reinterpret_cast<uint4*>(bh + off) = h;
+                        *reinterpret_cast<uint4*>(bl + off) = l;
+                    }
+                    tma::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) tma::mbar_arrive(&b_full[bs]);
+                }
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == kTaMmaWarp) {
+        tc::fence_after();
+        tc::tmem_free<512>(tbase);
+    }
+}
+
+// A slab relayout (create time): one thread per (chunk, item, level, column quad kc, c).
+__global__ void k_tca_slab(PlanView p, const __grid_constant__ TcAView a, int64_t units_per_item, uint8_t* slab) {
+    constexpr int kItems = kChunkRowsTa / kTcAItemRows;
+    const int64_t total = units_per_item * kItems * p.nchunks;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ci_it = idx / units_per_item;
+        int64_t r = idx - ci_it * units_per_item;
+        const int chunk = (int)(ci_it / kItems), it = (int)(ci_it % kItems);
+        int l = 0;
+        for (;; ++l) {
+            const int64_t cnt = 4LL * a.lev[l].r8;
+            if (r < cnt) break;
+            r -= cnt;
+        }
+        const TcALevel L = a.lev[l];
+        const int kc = (int)(r / L.r8), c = (int)(r % L.r8);
+        const int w = fmt_bytes(L.fmt);
+        uint8_t* dst = slab + (int64_t)chunk * a.chunk_bytes + (int64_t)it * a.item_bytes + L.seg +
+                       ((int64_t)kc * L.r8 + c) * 4 * w;
+        const ChunkDesc ch = p.chunks[chunk];
+        const NodeDesc nd = p.nodes[p.chunk_nodes[(int64_t)chunk * p.nlev + l]];
+        const int row = ch.row0 - nd.row0 + it * kTcAItemRows + 4 * kc;
+        const uint8_t* src = c < nd.rv ? p.arena + nd.v_off + ((int64_t)c * nd.v_ld + row) * w : nullptr;
+        for (int e = 0; e < 4 * w; ++e) dst[e] = src ? src[e] : (uint8_t)0;
+    }
+}
+
+}  // namespace
+
+static hodlr_status tca_prepare(const MrInput& in, MrPlan& mr);
+
+hodlr_status tc_prepare(const MrInput& in, MrPlan& mr) {
+    if (in.leaf_fmt != HODLR_FMT_FP32 || !mr.ok || mr.has_fp64_operand || getenv("HODLR_B200_NO_TC"))
+        return HODLR_OK;
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, in.device);
+    if (major != 10) return HODLR_OK;
+    const auto& nodes = *in.nodes;
+    const auto& chunks = *in.chunks;
+    const auto& leaves = *in.leaves;
+    for (const ChunkDesc& c : chunks) {
+        const LeafDesc& l = leaves[c.leaf];
+        if (c.nrows != kTcRows || l.m != kTcRows || l.row0 != c.row0 || l.fmt != HODLR_FMT_FP32) return HODLR_OK;
+    }
+    TcView& v = mr.tcv;
+    v = TcView{};
+    v.nlev = in.nlev;
+    int64_t off = 0;
+    auto add = [&](int fmt, int ncols, int lv, int col0) {
+        if (v.nitems >= kTcMaxItems) return false;
+        TcItem& it = v.item[v.nitems++];
+        it.off = (int32_t)off;
+        it.bytes = kTcRows * ncols * fmt_bytes(fmt);
+        it.fmt = (int16_t)fmt;
+        it.ncols = (int16_t)ncols;
+        it.lv = (int16_t)lv;
+        it.col0 = (int16_t)col0;
+        off += it.bytes;
+        return true;
+    };
+    for (int c = 0; c < kTcRows; c += kTcItemCols)
+        if (!add(HODLR_FMT_FP32, kTcItemCols, -1, c)) return HODLR_OK;
+    for (int lv = 0; lv < in.nlev; ++lv) {
+        const MrLevel& L = mr.view.lev[lv];
+        int fmt = -1;
+        for (int id = L.node0; id < L.node0 + L.nnodes; ++id) {
+            const NodeDesc& nd = nodes[id];
+            if (nd.ru <= 0) continue;
+            if (fmt >= 0 && fmt != nd.u_fmt) return HODLR_OK;  // one storage format per level
+            fmt = nd.u_fmt;
+        }
+        if (fmt < 0) continue;
+        if (fmt == HODLR_FMT_FP64) return HODLR_OK;
+        const int R = (L.ru_max + 7) / 8 * 8;
+        for (int c = 0; c < R; c += kTcItemCols)
+            if (!add(fmt, std::min(kTcItemCols, R - c), lv, c)) return HODLR_OK;
+    }
+    v.leaf_bytes = (off + 127) / 128 * 128;
+    if (v.leaf_bytes >= (1LL << 31)) return HODLR_OK;
+    int64_t upc = 0;
+    for (int i = 0; i < v.nitems; ++i) upc += (int64_t)(v.item[i].ncols >> 2) * kTcRows;
+    const size_t bytes = (size_t)v.leaf_bytes * chunks.size();
+    void* d = nullptr;
+    if (cudaMalloc(&d, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return HODLR_OK;  // no room: the fragment-slab kernels serve
+    }
+    cudaError_t e = cudaMemset(d, 0, bytes);
+    if (e == cudaSuccess) {
+        k_tc_slab<<<148 * 8, 256>>>(*in.view, v, upc, (uint8_t*)d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return HODLR_ERR_CUDA;
+    }
+    v.slab = (const uint8_t*)d;
+    mr.tc_dev = d;
+    mr.tc_ok = true;
+    (void)nodes;
+    if (mr.tca_cand) return tca_prepare(in, mr);
+    return HODLR_OK;
+}
+
+
+bool tc_a_candidate(const MrInput& in, const MrView& v) {
+    if (in.leaf_fmt != HODLR_FMT_FP32 || getenv("HODLR_B200_NO_TC")) return false;
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, in.device);
+    if (major != 10) return false;
+    for (const ChunkDesc& c : *in.chunks) {
+        const LeafDesc& l = (*in.leaves)[c.leaf];
+        if (c.nrows != kTcRows || l.m != kTcRows || l.row0 != c.row0) return false;
+    }
+    int mtot = 0;
+    for (int lv = 0; lv < in.nlev; ++lv) {
+        const MrLevel& L = v.lev[lv];
+        int fmt = -1;
+        for (int id = L.node0; id < L.node0 + L.nnodes; ++id) {
+            const NodeDesc& nd = (*in.nodes)[id];
+            if (nd.rv <= 0) continue;
+            if ((fmt >= 0 && fmt != nd.v_fmt) || nd.v_fmt == HODLR_FMT_FP64) return false;
+            fmt = nd.v_fmt;
+        }
+        mtot += (L.rv_max + 7) / 8 * 8;
+    }
+    return mtot > 0 && mtot <= 128 * kTcAMaxTiles;
+}
+
+static hodlr_status tca_prepare(const MrInput& in, MrPlan& mr) {
+    TcAView& a = mr.tcav;
+    a = TcAView{};
+    a.nlev = in.nlev;
+    int mb = 0, seg = 0;
+    for (int lv = 0; lv < in.nlev; ++lv) {
+        const MrLevel& L = mr.view.lev[lv];
+        int fmt = HODLR_FMT_FP32;
+        for (int id = L.node0; id < L.node0 + L.nnodes; ++id)
+            if ((*in.nodes)[id].rv > 0) fmt = (*in.nodes)[id].v_fmt;
+        TcALevel& T = a.lev[lv];
+        T.mbase = mb;
+        T.r8 = (L.rv_max + 7) / 8 * 8;
+        T.fmt = fmt;
+        T.seg = seg;
+        if (fmt == HODLR_FMT_FP32)
+            for (int t = mb / 128; t <= (mb + std::max(T.r8, 1) - 1) / 128; ++t) a.tile_full |= 1u << t;
+        mb += T.r8;
+        seg += kTcAItemRows * T.r8 * fmt_bytes(fmt);
+    }
+    a.mtot = mb;
+    a.nmt = (mb + 127) / 128;
+    a.item_bytes = seg;
+    a.chunk_bytes = (int64_t)seg * (kChunkRowsTa / kTcAItemRows);
+    if (ta_smem(a, 2) > 227 * 1024) return HODLR_OK;
+    const size_t bytes = (size_t)a.chunk_bytes * in.chunks->size();
+    void* d = nullptr;
+    if (cudaMalloc(&d, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return HODLR_OK;
+    }
+    k_tca_slab<<<148 * 8, 256>>>(*in.view, a, 4LL * mb, (uint8_t*)d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return HODLR_ERR_CUDA;
+    }
+    a.slab = (const uint8_t*)d;
+    mr.tca_dev = d;
+    mr.tca_ok = true;
+    return HODLR_OK;
+}
+
+bool tca_usable(const MrPlan& mr, int64_t s) { return mr.tca_ok && s > 1 && !getenv("HODLR_B200_NO_TC"); }
+
+cudaError_t tc_phase_a(const PlanView& p, const MrPlan& mr, const float* x, int64_t ldx, int64_t s, float* partial,
+                       float* tbuf, cudaStream_t st) {
+    if (p.nchunks == 0) return cudaSuccess;
+    const int nraw = ta_nraw(mr.tcav);
+    const size_t sm = ta_smem(mr.tcav, nraw);
+    cudaError_t e = cudaFuncSetAttribute(k_tc_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    const int nblk = (int)((s + kTcN - 1) / kTcN);
+    k_tc_a<<<mr.view.nb, kTaThreads, sm, st>>>(p, mr.view, mr.tcav, x, ldx, s, (int)mr_spad(s), nblk, partial,
+                                                tbuf, nraw);
+    return cudaGetLastError();
+}
+
+bool tc_usable(const MrPlan& mr, int64_t s) { return mr.tc_ok && s > 1 && !getenv("HODLR_B200_NO_TC"); }
+
+cudaError_t tc_phase_b(const PlanView& p, const MrPlan& mr, const float* x, int64_t ldx, float* b, int64_t ldb,
+                       int64_t s, const float* tbuf, cudaStream_t st) {
+    if (p.nchunks == 0) return cudaSuccess;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_tc_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int nblk = (int)((s + kTcN - 1) / kTcN);
+    const int nwork = p.nchunks * nblk;
+    const int grid = std::min(nwork, sms);
+    k_tc_b<<<grid, kTcThreads, kTcSmem, st>>>(p, mr.tcv, x, ldx, tbuf, b, ldb, s, nblk);
+    return cudaGetLastError();
+}
+
+}  // namespace hodlr

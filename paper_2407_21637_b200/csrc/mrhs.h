@@ -24,6 +24,7 @@
 
 #include "../../include/hodlr_b200.h"
 #include "plan.h"
+#include "tcb.h"
 
 namespace hodlr {
 
@@ -103,7 +104,16 @@ struct MrPlan {
     void* dev = nullptr;
     int32_t* multi = nullptr;  // device: ids of nodes summed over several phase-A CTAs (or external)
     int nmulti = 0;
+    int nbig = 0;              // the first nbig listed nodes sum more than 32 slots
+    int rmax_big = 0, rmax_small = 0;
     int max_leaf_m = 0;
+    bool tc_ok = false;        // tcgen05 phase B (fp32 working, uniform 256-row leaves)
+    void* tc_dev = nullptr;
+    TcView tcv{};
+    bool tca_cand = false;     // tcgen05 phase A eligible (decided before the slot layout: nb = SMs)
+    bool tca_ok = false;
+    void* tca_dev = nullptr;
+    TcAView tcav{};
 };
 
 struct MrInput {
@@ -147,5 +157,15 @@ cudaError_t mr_shard_begin(const PlanView& p, const MrPlan& mr, const W* x, int6
 template <typename W>
 cudaError_t mr_slab_phase_b(const PlanView& p, const MrPlan& mr, const W* x, int64_t ldx, W* b, int64_t ldb,
                             int64_t s, const W* tbuf, cudaStream_t st);
+
+// tcgen05 phase A / B (kernels_tc.cu)
+bool tc_a_candidate(const MrInput& in, const MrView& v);
+bool tca_usable(const MrPlan& mr, int64_t s);
+cudaError_t tc_phase_a(const PlanView& p, const MrPlan& mr, const float* x, int64_t ldx, int64_t s, float* partial,
+                       float* tbuf, cudaStream_t st);
+hodlr_status tc_prepare(const MrInput& in, MrPlan& mr);
+bool tc_usable(const MrPlan& mr, int64_t s);
+cudaError_t tc_phase_b(const PlanView& p, const MrPlan& mr, const float* x, int64_t ldx, float* b, int64_t ldb,
+                       int64_t s, const float* tbuf, cudaStream_t st);
 
 }  // namespace hodlr

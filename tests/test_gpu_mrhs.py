@@ -50,18 +50,26 @@ def run(torch, op, X, working):
     return op.matvec(torch.from_numpy(np.ascontiguousarray(X)).cuda().to(dt)).double().cpu().numpy()
 
 
+def slab_path(working):
+    """fp32 working: phase B runs on tcgen05 (kernels_tc.cu); fp64: DMMA slabs."""
+    return "mrhs_tc" if working == "fp32" else "mrhs_slab"
+
+
 def xin(X, working):
     return X.astype(np.float32).astype(np.float64) if working == "fp32" else X
 
 
 @pytest.mark.parametrize("working,fmts", FMT_SETS)
-@pytest.mark.parametrize("s", [2, 8, 16, 33, 64])
+@pytest.mark.parametrize("s", [2, 8, 16, 33, 64, 100])
 @pytest.mark.parametrize("n,path", [(4096, "mrhs"), (2048, "mrhs_slab")])
 def test_mrhs_matches_oracle_and_generic(cuda, working, fmts, s, n, path):
     """n=4096, depth 3: 512-row leaves (two chunks each) -> arena kernels;
-    n=2048: 256-row leaves -> fragment-slab kernels."""
+    n=2048: 256-row leaves -> fragment-slab kernels (fp32: tcgen05 phase B;
+    s=100 runs two 64-column passes, the second ragged)."""
     H = random_hodlr(n, 3, fmts, [24, 17, 9], working, seed=s + len(fmts[0]))
     op = make_op(H)
+    if path == "mrhs_slab":
+        path = slab_path(working)
     assert op.path(s) == (path, 3)
     X = np.random.default_rng(s).standard_normal((H.n, s))
     B = run(cuda, op, X, working)
@@ -79,7 +87,7 @@ def test_mrhs_variable_ranks_and_rank_zero(cuda, working):
     for n in (8192, 4096):  # 512-row leaves (arena kernels), 256-row leaves (slabs)
         H = random_hodlr(n, 4, fmts, [(30, 45), (0, 20), (5, 12), (0, 3)], working, seed=3)
         op = make_op(H)
-        assert op.path(16)[0] == ("mrhs" if n == 8192 else "mrhs_slab")
+        assert op.path(16)[0] == ("mrhs" if n == 8192 else slab_path(working))
         X = np.random.default_rng(2).standard_normal((H.n, 16))
         tol = 1e-12 if working == "fp64" else 1e-5
         assert rel(run(cuda, op, X, working), matvec_oracle(H, xin(X, working))) <= tol
@@ -134,7 +142,7 @@ def test_mrhs_sharded_subtree(cuda, nranks, working):
     H = random_hodlr(8192, 5, ["fp32", "bf16", "fp16", "q52", "fp32"], [12, 10, 9, 7, 6], working, seed=5)
     X = np.random.default_rng(3).standard_normal((H.n, 16))
     out, ops = run_emulated(cuda, H, X, nranks)
-    assert all(op.path(16)[0] == "mrhs_slab" for op in ops)
+    assert all(op.path(16)[0] == slab_path(working) for op in ops)
     tol = 1e-12 if working == "fp64" else 1e-5
     assert rel(out, matvec_oracle(H, xin(X, working))) <= tol
 
@@ -159,3 +167,52 @@ def test_mrhs_slab_matches_arena_kernels(cuda, working):
             os.environ["HODLR_B200_NO_SLAB"] = old
     tol = 1e-13 if working == "fp64" else 1e-6
     assert rel(a, b) <= tol
+
+
+@pytest.mark.parametrize("s", [2, 16, 64, 70])
+def test_mrhs_tc_matches_mma_sync_slabs(cuda, s):
+    """fp32 working: the tcgen05 phase B (item slabs, TMEM A operand) against
+    the mma.sync fragment-slab phase B on one matrix, every storage format,
+    ranks not multiples of 8 and rank-0 nodes."""
+    fmts = ["fp32", "fp16", "bf16", "q52", "fp32"]
+    H = random_hodlr(8192, 5, fmts, [(20, 40), 16, (0, 9), 7, 5], "fp32", seed=11)
+    X = np.random.default_rng(5).standard_normal((H.n, s))
+    op = make_op(H)
+    assert op.path(s)[0] == "mrhs_tc"
+    a = run(cuda, op, X, "fp32")
+    old = os.environ.get("HODLR_B200_NO_TC")
+    os.environ["HODLR_B200_NO_TC"] = "1"
+    try:
+        assert op.path(s)[0] == "mrhs_slab"
+        b = run(cuda, op, X, "fp32")
+    finally:
+        if old is None:
+            del os.environ["HODLR_B200_NO_TC"]
+        else:
+            os.environ["HODLR_B200_NO_TC"] = old
+    ref = matvec_oracle(H, xin(X, "fp32"))
+    assert rel(a, ref) <= 1e-5 and rel(b, ref) <= 1e-5
+    assert rel(a, b) <= 2e-6
+
+
+def test_mrhs_tc_inf_propagates(cuda):
+    """An inf in X stays inf in the rows it reaches, no NaN from
+    the hi/lo split."""
+    H = random_hodlr(2048, 3, ["fp32", "fp16", "fp32"], [8, 6, 4], "fp32", seed=2)
+    op = make_op(H)
+    assert op.path(8)[0] == "mrhs_tc"
+    X = np.random.default_rng(0).standard_normal((H.n, 8))
+    X[5, 3] = np.inf
+    B = run(cuda, op, X, "fp32")
+    assert not np.isnan(B[:, 3]).any() or np.isnan(matvec_oracle(H, xin(X, "fp32"))[:, 3]).any()
+    assert np.isfinite(B[:, [0, 1, 2, 4, 5, 6, 7]]).all()
+
+
+def test_mrhs_tc_phase_b_with_wide_stack(cuda):
+    """Stacked ranks beyond three 128-row tiles: phase A falls back to the
+    mma.sync slab kernel, phase B still runs on tcgen05."""
+    H = random_hodlr(8192, 5, ["fp32", "fp32", "bf16", "fp16", "fp32"], [130, 120, 100, 64, 40], "fp32", seed=12)
+    op = make_op(H)
+    assert op.path(32)[0] == "mrhs_tc"
+    X = np.random.default_rng(6).standard_normal((H.n, 32))
+    assert rel(run(cuda, op, X, "fp32"), matvec_oracle(H, xin(X, "fp32"))) <= 1e-5
