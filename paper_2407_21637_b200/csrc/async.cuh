@@ -30,6 +30,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+// Same wait, but a thread whose phase is not complete may be suspended for up
+// to `ns` nanoseconds per try (instead of spinning): for role warps that wait
+// most of the time, so their polling does not take issue slots from the warps
+// doing the work.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity, unsigned ns = 20000) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(ns)
+        : "memory");
+}
 // Streaming (read-once) bytes: L2 evict-first.
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;

@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <vector>
 
 #include "async.cuh"
@@ -41,21 +42,37 @@
 namespace hodlr {
 namespace {
 
-constexpr int kTcConvWarps = 8;
-constexpr int kTcProdWarp = 8;
-constexpr int kTcMmaWarp = 9;
-constexpr int kTcStageWarp0 = 10;
+// Build with -DHODLR_TC_TRACE for per-item clock traces of CTA 0 (printf at exit).
+#ifdef HODLR_TC_TRACE
+#define TC_TRACE_DECL long long tra[48] = {}, trb[48] = {}, trc[48] = {}, trw[48] = {};
+#define TC_TR(arr, cond) if ((cond) && blockIdx.x == 0 && g < 48) arr[g] = clock64();
+#define TC_TRACE_DUMP(role, lead) \
+    if (blockIdx.x == 0 && (lead)) \
+        for (int i_ = 0; i_ < 48; ++i_) \
+            printf("TRACE role %d item %d a %lld b %lld c %lld w %lld\n", role, i_, tra[i_], trb[i_], trc[i_], trw[i_]);
+#else
+#define TC_TRACE_DECL
+#define TC_TR(arr, cond)
+#define TC_TRACE_DUMP(role, lead)
+#endif
+
+constexpr int kTcConvWarps = 16;   // warp w: m-tile (w>>2)&1, lane quarter w&3, column half w>>3
+constexpr int kTcProdWarp = 16;
+constexpr int kTcMmaWarp = 17;
+constexpr int kTcStageWarp0 = 18;
 constexpr int kTcStageWarps = 4;
 constexpr int kTcThreads = (kTcStageWarp0 + kTcStageWarps) * 32;
 constexpr int kTcRawStages = 4;
 constexpr int kTcRawSlot = kTcRows * kTcItemCols * 4;  // 32 KB
+constexpr int kTcAStages = 3;
 constexpr int kTcBStages = 3;
 constexpr int kTcBHalf = kTcItemCols * kTcN * 4;       // 8 KB: hi (or lo) of one item
 constexpr int kTcBSlot = 2 * kTcBHalf;
-constexpr uint32_t kTcAcc = 0, kTcAStage = 256;
+constexpr uint32_t kTcAcc = 0, kTcAStage = 128;        // accumulator [2 m-tiles][64]; A stages [3][2][hi 32 | lo 32]
 constexpr int kChunkRowsTa = 256;  // rows of a phase-A chunk (= leaf)
-constexpr int kTcBars = 2 * kTcRawStages + 2 * 2 + 2 * kTcBStages + 2 * 2;
-constexpr size_t kTcSmem = (size_t)kTcRawStages * kTcRawSlot + (size_t)kTcBStages * kTcBSlot + kTcBars * 8 + 16;
+constexpr int kTcBars = 2 * kTcRawStages + 2 * kTcAStages + 2 * kTcBStages + 2;
+constexpr size_t kTcSmem = (size_t)kTcRawStages * kTcRawSlot + (size_t)kTcBStages * kTcBSlot + kTcBars * 8 +
+                           2 * 2 * kMrMaxLevels * 8 + 16;
 
 __device__ __forceinline__ float4 load_quad(int fmt, const uint8_t* p) {
     switch (fmt) {
@@ -81,7 +98,7 @@ __device__ __forceinline__ float4 load_quad(int fmt, const uint8_t* p) {
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_tc_b(PlanView p, const __grid_constant__ TcView v, const float* __restrict__ x, int64_t ldx,
-           const float* __restrict__ tbuf, float* __restrict__ b, int64_t ldb, int64_t s, int nblk) {
+           const float* __restrict__ tbuf, float* __restrict__ b, int64_t ldb, int64_t s, int nblk, int dbg) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     uint8_t* ring = smem_raw;                                              // [4][32 KB]
     uint8_t* bring = ring + (size_t)kTcRawStages * kTcRawSlot;             // [3][hi 8 KB | lo 8 KB]
@@ -89,12 +106,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t* raw_full = bars;
     uint64_t* raw_empty = raw_full + kTcRawStages;
     uint64_t* a_full = raw_empty + kTcRawStages;
-    uint64_t* a_empty = a_full + 2;
-    uint64_t* b_full = a_empty + 2;
+    uint64_t* a_empty = a_full + kTcAStages;
+    uint64_t* b_full = a_empty + kTcAStages;
     uint64_t* b_empty = b_full + kTcBStages;
     uint64_t* acc_full = b_empty + kTcBStages;
-    uint64_t* acc_empty = acc_full + 2;
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint64_t* acc_empty = acc_full + 1;
+    // stagers' per-leaf node table, double-buffered by leaf parity: [2][level] (tsrc_off, ru)
+    int64_t* ntab_off = reinterpret_cast<int64_t*>(acc_empty + 1);
+    int32_t* ntab_ru = reinterpret_cast<int32_t*>(ntab_off + 2 * kMrMaxLevels);
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(ntab_ru + 2 * kMrMaxLevels);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwork = p.nchunks * nblk;
@@ -105,16 +125,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tma::mbar_init(&raw_full[i], 1);
             tma::mbar_init(&raw_empty[i], kTcConvWarps);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kTcAStages; ++i) {
             tma::mbar_init(&a_full[i], kTcConvWarps);
             tma::mbar_init(&a_empty[i], 1);
-            tma::mbar_init(&acc_full[i], 1);
-            tma::mbar_init(&acc_empty[i], kTcConvWarps);
         }
         for (int i = 0; i < kTcBStages; ++i) {
             tma::mbar_init(&b_full[i], kTcStageWarps);
             tma::mbar_init(&b_empty[i], 1);
         }
+        tma::mbar_init(acc_full, 1);
+        tma::mbar_init(acc_empty, kTcConvWarps);
         tma::fence_mbar_init();
     }
     if (warp == kTcMmaWarp) tc::tmem_alloc<512>(tbase_s);
@@ -122,25 +142,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = *tbase_s;
+    TC_TRACE_DECL
 
     if (warp < kTcConvWarps) {
         // ---------------------------------------------------------- converters + epilogue
-        const int mt = warp >> 2, qd = warp & 3;
+        const int mt = (warp >> 2) & 1, qd = warp & 3, half = warp >> 3;
         const int row = mt * 128 + qd * 32 + lane;
         const uint32_t tl = tbase + ((uint32_t)(qd * 32) << 16);
         int64_t g = 0;
         int lc = 0;
-        int pend_chunk = -1, pend_q0 = 0, pend_n = 0;
-        auto epilogue = [&](int chunk, int q0, int nn, int leafno) {
-            const int ab = leafno & 1;
-            tma::mbar_wait(&acc_full[ab], (unsigned)((leafno >> 1) & 1));
+        int pend_chunk = -1, pend_q0 = 0;
+        // epilogue of the lc-th leaf: this warp's 32 accumulator columns -> b
+        auto epilogue = [&](int chunk, int q0) {
+            tma::mbar_wait_sleep(acc_full, (unsigned)(lc & 1));
             tc::fence_after();
             const int64_t r = p.chunks[chunk].row0 + row;
             float* brow = b + r * ldb + q0;
             const bool vec = ((ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
-            for (int c = 0; c < nn; c += 16) {
+#pragma unroll
+            for (int c = half * 32; c < half * 32 + 32; c += 16) {
+                if (q0 + c >= s) break;  // warp-uniform
                 uint32_t a[16];
-                tc::ld_x16(tl + kTcAcc + ab * 128 + mt * 64 + c, a);
+                tc::ld_x16(tl + kTcAcc + mt * 64 + c, a);
                 tc::wait_ld();
                 if (vec && q0 + c + 16 <= s) {
 #pragma unroll
@@ -156,30 +179,42 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) tma::mbar_arrive(&acc_empty[ab]);
+            if (lane == 0) tma::mbar_arrive(acc_empty);
+            ++lc;
         };
-        for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++lc) {
+        for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
             const int chunk = work / nblk;
             const int q0 = (work % nblk) * kTcN;
-            const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
             for (int i = 0; i < nitems; ++i, ++g) {
                 const TcItem it = v.item[i];
-                const int rs = (int)(g % kTcRawStages), ts = (int)(g & 1);
-                tma::mbar_wait(&raw_full[rs], (unsigned)((g / kTcRawStages) & 1));
-                if (g >= 2) tma::mbar_wait(&a_empty[ts], (unsigned)(((g >> 1) & 1) ^ 1));
+                const int rs = (int)(g % kTcRawStages), ts = (int)(g % kTcAStages);
+                tma::mbar_wait_sleep(&raw_full[rs], (unsigned)((g / kTcRawStages) & 1));
+                TC_TR(tra, warp == 0 && lane == 0)
+                if (g >= kTcAStages) tma::mbar_wait_sleep(&a_empty[ts], (unsigned)(((g / kTcAStages) & 1) ^ 1));
+                TC_TR(trb, warp == 0 && lane == 0)
                 tc::fence_after();
+                TC_TR(trc, warp == 0 && lane == 0)
                 const int w = fmt_bytes(it.fmt);
                 const uint8_t* rp = ring + (size_t)rs * kTcRawSlot + (size_t)row * 4 * w;
                 const uint32_t ah = tl + kTcAStage + ts * 128 + mt * 64;
                 const bool full = it.fmt == HODLR_FMT_FP32;
-                for (int j = 0; j < it.ncols; j += 8) {
-                    const float4 f0 = load_quad(it.fmt, rp + (size_t)(j >> 2) * kTcRows * 4 * w);
-                    const float4 f1 = load_quad(it.fmt, rp + (size_t)((j >> 2) + 1) * kTcRows * 4 * w);
+                const int j0 = half * 16, j1 = min((int)it.ncols, j0 + 16);
+                for (int j = j0; j < j1; j += 8) {
+                    float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f), f1 = f0;
+                    if (!(dbg & 4)) {
+                        f0 = load_quad(it.fmt, rp + (size_t)(j >> 2) * kTcRows * 4 * w);
+                        f1 = load_quad(it.fmt, rp + (size_t)((j >> 2) + 1) * kTcRows * 4 * w);
+                    }
                     const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
                     uint32_t hi[8], lo[8];
                     if (full) {
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) tc::split_tf32(f[e], hi[e], lo[e]);
+                        for (int e = 0; e < 8; ++e) {
+                            if (v.finite)
+                                tc::split_tf32_fast(f[e], hi[e], lo[e]);
+                            else
+                                tc::split_tf32(f[e], hi[e], lo[e]);
+                        }
                         tc::st_x8(ah + j, hi);
                         tc::st_x8(ah + 32 + j, lo);
                     } else {
@@ -188,6 +223,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         tc::st_x8(ah + j, hi);
                     }
                 }
+                TC_TR(trw, warp == 0 && lane == 0)
                 tc::wait_st();
                 tc::fence_before();
                 __syncwarp();
@@ -196,15 +232,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     tma::mbar_arrive(&a_full[ts]);
                 }
                 if (i == 0 && pend_chunk >= 0) {
-                    epilogue(pend_chunk, pend_q0, pend_n, lc - 1);
+                    epilogue(pend_chunk, pend_q0);
                     pend_chunk = -1;
                 }
             }
             pend_chunk = chunk;
             pend_q0 = q0;
-            pend_n = nn;
         }
-        if (pend_chunk >= 0) epilogue(pend_chunk, pend_q0, pend_n, lc - 1);
+        if (pend_chunk >= 0) epilogue(pend_chunk, pend_q0);
     } else if (warp == kTcProdWarp) {
         // ---------------------------------------------------------- producer
         if (lane == 0) {
@@ -214,7 +249,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint8_t* src = v.slab + (int64_t)(work / nblk) * v.leaf_bytes;
                 for (int i = 0; i < nitems; ++i, ++g) {
                     const int rs = (int)(g % kTcRawStages);
-                    if (g >= kTcRawStages) tma::mbar_wait(&raw_empty[rs], (unsigned)(((g / kTcRawStages) & 1) ^ 1));
+                    if (g >= kTcRawStages) tma::mbar_wait_sleep(&raw_empty[rs], (unsigned)(((g / kTcRawStages) & 1) ^ 1));
+                    TC_TR(trw, true)
                     const int bytes = v.item[i].bytes;
                     tma::mbar_arrive_tx(&raw_full[rs], (unsigned)bytes);
                     tma::bulk_g2s(ring + (size_t)rs * kTcRawSlot, src + v.item[i].off, (unsigned)bytes, &raw_full[rs],
@@ -232,12 +268,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
                 const uint32_t idesc = tc::idesc_tf32(128, nn);
                 const uint32_t lbo = (uint32_t)(nn / 8) * 128;
-                const int ab = lc & 1;
-                if (lc >= 2) tma::mbar_wait(&acc_empty[ab], (unsigned)(((lc >> 1) & 1) ^ 1));
+                if (lc >= 1) tma::mbar_wait_sleep(acc_empty, (unsigned)((lc - 1) & 1));
                 for (int i = 0; i < nitems; ++i, ++g) {
-                    const int ts = (int)(g & 1), bs = (int)(g % kTcBStages);
-                    tma::mbar_wait(&a_full[ts], (unsigned)((g >> 1) & 1));
-                    tma::mbar_wait(&b_full[bs], (unsigned)((g / kTcBStages) & 1));
+                    const int ts = (int)(g % kTcAStages), bs = (int)(g % kTcBStages);
+                    tma::mbar_wait_sleep(&a_full[ts], (unsigned)((g / kTcAStages) & 1));
+                    TC_TR(tra, true)
+                    tma::mbar_wait_sleep(&b_full[bs], (unsigned)((g / kTcBStages) & 1));
+                    TC_TR(trb, true)
                     tc::fence_after();
                     const int ncols = v.item[i].ncols;
                     const bool full = v.item[i].fmt == HODLR_FMT_FP32;
@@ -247,35 +284,44 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         const uint64_t dl = tc::smem_desc(bl + (uint32_t)(j >> 2) * lbo, lbo, 128);
 #pragma unroll
                         for (int m = 0; m < 2; ++m) {
-                            const uint32_t d = tbase + kTcAcc + ab * 128 + m * 64;
+                            if (dbg & 2) continue;
+                            const uint32_t d = tbase + kTcAcc + m * 64;
                             const uint32_t ah = tbase + kTcAStage + ts * 128 + m * 64 + j;
                             tc::mma_tf32_ts(d, ah, dh, idesc, (i | j) != 0);
                             tc::mma_tf32_ts(d, ah, dl, idesc, 1);
-                            if (full) tc::mma_tf32_ts(d, ah + 32, dh, idesc, 1);
+                            if (full && !(dbg & 1)) tc::mma_tf32_ts(d, ah + 32, dh, idesc, 1);
                         }
                     }
                     tc::commit(&a_empty[ts]);
                     tc::commit(&b_empty[bs]);
+                    TC_TR(trc, true)
                 }
-                tc::commit(&acc_full[ab]);
+                tc::commit(acc_full);
             }
         }
     } else {
         // ---------------------------------------------------------- B stagers
         const int t = threadIdx.x - kTcStageWarp0 * 32;
         int64_t g = 0;
-        for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
+        int lc = 0;
+        for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++lc) {
             const int chunk = work / nblk;
             const int q0 = (work % nblk) * kTcN;
             const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
             const int64_t row0 = p.chunks[chunk].row0;
             const int lbo = (nn / 8) * 128;
+            // node table of this leaf (one dependent lookup per level, not per item)
+            int64_t* toff = ntab_off + (lc & 1) * kMrMaxLevels;
+            int32_t* tru = ntab_ru + (lc & 1) * kMrMaxLevels;
+            if (t < v.nlev) {
+                const NodeDesc& nd = p.nodes[p.chunk_nodes[(int64_t)chunk * p.nlev + t]];
+                toff[t] = nd.tsrc_off;
+                tru[t] = nd.ru;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcStageWarps) : "memory");
             for (int i = 0; i < nitems; ++i, ++g) {
                 const TcItem it = v.item[i];
                 const int bs = (int)(g % kTcBStages);
-                if (g >= kTcBStages) tma::mbar_wait(&b_empty[bs], (unsigned)(((g / kTcBStages) & 1) ^ 1));
-                uint8_t* bh = bring + (size_t)bs * kTcBSlot;
-                uint8_t* bl = bh + kTcBHalf;
                 // source rows [col0, col0 + ncols) of X (leaf rows) or of T of the sibling node
                 const float* src;
                 int64_t ld;
@@ -285,30 +331,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     ld = ldx;
                     nvalid = it.ncols;
                 } else {
-                    const NodeDesc& nd = p.nodes[p.chunk_nodes[(int64_t)chunk * p.nlev + it.lv]];
-                    src = tbuf + (nd.tsrc_off + it.col0) * s + q0;
+                    src = tbuf + (toff[it.lv] + it.col0) * s + q0;
                     ld = s;
-                    nvalid = max(0, min((int)it.ncols, nd.ru - it.col0));
+                    nvalid = max(0, min((int)it.ncols, tru[it.lv] - it.col0));
                 }
-                const int nunits = (it.ncols >> 2) * nn;
-                for (int u0 = 0; u0 < nunits; u0 += 4 * 32 * kTcStageWarps) {
-                    float vals[4][4];
+                // thread t: column n = t % 64, column quads kc = t / 64 + 2e (no division)
+                const int n = t & 63, kq = t >> 6, nkc = it.ncols >> 2;
+                const bool colok = n < nn && q0 + n < s && !(dbg & 8);
+                float vals[4][4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int u = u0 + e * 32 * kTcStageWarps + t;
-                        const int kc = u / nn, n = u - kc * nn;
-                        const bool ok = u < nunits && q0 + n < s;
+                for (int e = 0; e < 4; ++e) {
+                    const int kc = kq + 2 * e;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const int r = kc * 4 + k;
-                            vals[e][k] = (ok && r < nvalid) ? __ldg(src + (int64_t)r * ld + n) : 0.0f;
-                        }
+                    for (int k = 0; k < 4; ++k) {
+                        const int r = kc * 4 + k;
+                        vals[e][k] = (colok && kc < nkc && r < nvalid) ? __ldg(src + (int64_t)r * ld + n) : 0.0f;
                     }
+                }
+                if (g >= kTcBStages) tma::mbar_wait_sleep(&b_empty[bs], (unsigned)(((g / kTcBStages) & 1) ^ 1));
+                TC_TR(trw, t == 0)
+                uint8_t* bh = bring + (size_t)bs * kTcBSlot;
+                uint8_t* bl = bh + kTcBHalf;
+                if (n < nn) {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int u = u0 + e * 32 * kTcStageWarps + t;
-                        if (u >= nunits) continue;
-                        const int kc = u / nn, n = u - kc * nn;
+                        const int kc = kq + 2 * e;
+                        if (kc >= nkc) break;
                         uint4 h, l;
                         tc::split_tf32(vals[e][0], h.x, l.x);
                         tc::split_tf32(vals[e][1], h.y, l.y);
@@ -319,18 +367,43 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         *reinterpret_cast<uint4*>(bl + off) = l;
                     }
                 }
+                TC_TR(tra, t == 0)
                 tma::fence_proxy_async_smem();
                 __syncwarp();
+                TC_TR(trc, t == 0)
                 if (lane == 0) tma::mbar_arrive(&b_full[bs]);
             }
         }
     }
+    TC_TRACE_DUMP(warp < kTcConvWarps ? 0 : warp == kTcProdWarp ? 1 : warp == kTcMmaWarp ? 2 : 3,
+                  lane == 0 && (warp == 0 || warp == kTcProdWarp || warp == kTcMmaWarp || warp == kTcStageWarp0))
     tc::fence_before();
     __syncthreads();
     if (warp == kTcMmaWarp) {
         tc::fence_after();
         tc::tmem_free<512>(tbase);
     }
+}
+
+// Create time: flag set if any 32-bit word of a slab looks like an fp32 inf/NaN
+// (narrow formats can only add false positives, which just keep the guarded split).
+__global__ void k_scan_nonfinite(const uint32_t* __restrict__ w, int64_t n, int* flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if ((w[i] & 0x7f800000u) == 0x7f800000u) {
+            *flag = 1;
+            return;
+        }
+}
+
+static int slab_finite(const void* slab, size_t bytes) {
+    int* d = nullptr;
+    if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return 0;
+    int h = 0;
+    cudaMemset(d, 0, sizeof(int));
+    k_scan_nonfinite<<<148 * 4, 256>>>((const uint32_t*)slab, (int64_t)(bytes / 4), d);
+    if (cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) h = 1;
+    cudaFree(d);
+    return h == 0;
 }
 
 // Item slab relayout (create time): one thread per (chunk, item, column quad, row).
@@ -409,7 +482,7 @@ inline int ta_nraw(const TcAView& a) {
 __global__ void __launch_bounds__(kTaThreads, 1)
     k_tc_a(PlanView p, const __grid_constant__ MrView m, const __grid_constant__ TcAView a,
            const float* __restrict__ x, int64_t ldx, int64_t s, int spad, int nblk, float* __restrict__ partial,
-           float* __restrict__ tbuf, int nraw) {
+           float* __restrict__ tbuf, int nraw, int dbg) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const size_t rslot = ta_raw_slot(a);
     uint8_t* ring = smem_raw;
@@ -480,12 +553,12 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         // epilogue of chunk ci (the lc-th chunk of this CTA): D -> running sums,
         // flushed at the node's last chunk of the run
         auto epilogue = [&](int ci, int q0) {
-            tma::mbar_wait(acc_full, (unsigned)(lc & 1));
+            tma::mbar_wait_sleep(acc_full, (unsigned)(lc & 1));
             tc::fence_after();
             // flush decision for this row's level (the whole warp loads D regardless)
             bool flush = false;
             float* dst = nullptr;
-            if (lv >= 0) {
+            if (lv >= 0 && !(dbg & 16)) {
                 const int node = p.chunk_nodes[(int64_t)ci * p.nlev + lv];
                 flush = !(ci + 1 < c_end && p.chunk_nodes[(int64_t)(ci + 1) * p.nlev + lv] == node);
                 if (flush) {
@@ -526,19 +599,26 @@ __global__ void __launch_bounds__(kTaThreads, 1)
             for (int ci = c_beg; ci < c_end; ++ci) {
                 for (int it = 0; it < kItems; ++it, ++g) {
                     const int rs = (int)(g % nraw), as = (int)(g % nas);
-                    tma::mbar_wait(&raw_full[rs], (unsigned)((g / nraw) & 1));
-                    if (g >= nas) tma::mbar_wait(&a_empty[as], (unsigned)(((g / nas) & 1) ^ 1));
+                    tma::mbar_wait_sleep(&raw_full[rs], (unsigned)((g / nraw) & 1));
+                    if (g >= nas) tma::mbar_wait_sleep(&a_empty[as], (unsigned)(((g / nas) & 1) ^ 1));
                     tc::fence_after();
                     uint32_t hi[16], lo[16];
-                    if (lv >= 0) {
+                    if (lv >= 0 && !(dbg & 4)) {
                         const uint8_t* rp = ring + (size_t)rs * rslot + seg + (size_t)c * 4 * w;
 #pragma unroll
                         for (int kc = 0; kc < 4; ++kc) {
                             const float4 f = load_quad(fmt, rp + (size_t)kc * r8 * 4 * w);
-                            tc::split_tf32(f.x, hi[4 * kc], lo[4 * kc]);
-                            tc::split_tf32(f.y, hi[4 * kc + 1], lo[4 * kc + 1]);
-                            tc::split_tf32(f.z, hi[4 * kc + 2], lo[4 * kc + 2]);
-                            tc::split_tf32(f.w, hi[4 * kc + 3], lo[4 * kc + 3]);
+                            if (a.finite) {
+                                tc::split_tf32_fast(f.x, hi[4 * kc], lo[4 * kc]);
+                                tc::split_tf32_fast(f.y, hi[4 * kc + 1], lo[4 * kc + 1]);
+                                tc::split_tf32_fast(f.z, hi[4 * kc + 2], lo[4 * kc + 2]);
+                                tc::split_tf32_fast(f.w, hi[4 * kc + 3], lo[4 * kc + 3]);
+                            } else {
+                                tc::split_tf32(f.x, hi[4 * kc], lo[4 * kc]);
+                                tc::split_tf32(f.y, hi[4 * kc + 1], lo[4 * kc + 1]);
+                                tc::split_tf32(f.z, hi[4 * kc + 2], lo[4 * kc + 2]);
+                                tc::split_tf32(f.w, hi[4 * kc + 3], lo[4 * kc + 3]);
+                            }
                         }
                     } else {
 #pragma unroll
@@ -578,7 +658,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                     const uint8_t* src = a.slab + (int64_t)ci * a.chunk_bytes;
                     for (int it = 0; it < kItems; ++it, ++g) {
                         const int rs = (int)(g % nraw);
-                        if (g >= nraw) tma::mbar_wait(&raw_empty[rs], (unsigned)(((g / nraw) & 1) ^ 1));
+                        if (g >= nraw) tma::mbar_wait_sleep(&raw_empty[rs], (unsigned)(((g / nraw) & 1) ^ 1));
                         tma::mbar_arrive_tx(&raw_full[rs], (unsigned)a.item_bytes);
                         tma::bulk_g2s(ring + (size_t)rs * rslot, src + (int64_t)it * a.item_bytes,
                                       (unsigned)a.item_bytes, &raw_full[rs], pol);
@@ -596,11 +676,11 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                 const uint32_t idesc = tc::idesc_tf32(128, nn);
                 const uint32_t lbo = (uint32_t)(nn / 8) * 128;
                 for (int ci = c_beg; ci < c_end; ++ci, ++lc) {
-                    if (lc >= 1) tma::mbar_wait(acc_empty, (unsigned)((lc - 1) & 1));
+                    if (lc >= 1) tma::mbar_wait_sleep(acc_empty, (unsigned)((lc - 1) & 1));
                     for (int it = 0; it < kItems; ++it, ++g) {
                         const int as = (int)(g % nas), bs = (int)(g % kTaBStages);
-                        tma::mbar_wait(&a_full[as], (unsigned)((g / nas) & 1));
-                        tma::mbar_wait(&b_full[bs], (unsigned)((g / kTaBStages) & 1));
+                        tma::mbar_wait_sleep(&a_full[as], (unsigned)((g / nas) & 1));
+                        tma::mbar_wait_sleep(&b_full[bs], (unsigned)((g / kTaBStages) & 1));
                         tc::fence_after();
                         const uint32_t bh = tc::smem_u32(bring + (size_t)bs * kTaBSlot), bl = bh + kTaBHalf;
 #pragma unroll
@@ -610,9 +690,10 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                             for (int t = 0; t < a.nmt; ++t) {
                                 const uint32_t d = tbase + kTaAcc + t * 64;
                                 const uint32_t ah = tbase + abase + as * astride + t * 32 + j;
+                                if (dbg & 2) continue;
                                 tc::mma_tf32_ts(d, ah, dh, idesc, (it | j) != 0);
                                 tc::mma_tf32_ts(d, ah, dl, idesc, 1);
-                                if ((a.tile_full >> t) & 1) tc::mma_tf32_ts(d, ah + 16, dh, idesc, 1);
+                                if (((a.tile_full >> t) & 1) && !(dbg & 1)) tc::mma_tf32_ts(d, ah + 16, dh, idesc, 1);
                             }
                         }
                         tc::commit(&a_empty[as]);
@@ -635,7 +716,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                 const int64_t row0 = p.chunks[ci].row0;
                 for (int it = 0; it < kItems; ++it, ++g) {
                     const int bs = (int)(g % kTaBStages);
-                    if (g >= kTaBStages) tma::mbar_wait(&b_empty[bs], (unsigned)(((g / kTaBStages) & 1) ^ 1));
+                    if (g >= kTaBStages) tma::mbar_wait_sleep(&b_empty[bs], (unsigned)(((g / kTaBStages) & 1) ^ 1));
                     uint8_t* bh = bring + (size_t)bs * kTaBSlot;
                     uint8_t* bl = bh + kTaBHalf;
                     const float* src = x + (row0 + it * kTcAItemRows) * ldx + q0;
@@ -646,7 +727,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                         const int kc = u / nn, n = u - kc * nn;
                         const bool ok = u < nunits && q0 + n < s;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) vals[e][k] = ok ? __ldg(src + (int64_t)(kc * 4 + k) * ldx + n) : 0.f;
+                        for (int k = 0; k < 4; ++k) vals[e][k] = ok && !(dbg & 8) ? __ldg(src + (int64_t)(kc * 4 + k) * ldx + n) : 0.f;
                     }
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
@@ -776,6 +857,7 @@ hodlr_status tc_prepare(const MrInput& in, MrPlan& mr) {
         return HODLR_ERR_CUDA;
     }
     v.slab = (const uint8_t*)d;
+    v.finite = slab_finite(d, bytes);
     mr.tc_dev = d;
     mr.tc_ok = true;
     (void)nodes;
@@ -803,7 +885,7 @@ bool tc_a_candidate(const MrInput& in, const MrView& v) {
             if ((fmt >= 0 && fmt != nd.v_fmt) || nd.v_fmt == HODLR_FMT_FP64) return false;
             fmt = nd.v_fmt;
         }
-        mtot += (L.rv_max + 7) / 8 * 8;
+        mtot += L.rv_max;
     }
     return mtot > 0 && mtot <= 128 * kTcAMaxTiles;
 }
@@ -820,7 +902,7 @@ static hodlr_status tca_prepare(const MrInput& in, MrPlan& mr) {
             if ((*in.nodes)[id].rv > 0) fmt = (*in.nodes)[id].v_fmt;
         TcALevel& T = a.lev[lv];
         T.mbase = mb;
-        T.r8 = (L.rv_max + 7) / 8 * 8;
+        T.r8 = L.rv_max;  // rows stacked without padding (any row -> TMEM lane mapping works)
         T.fmt = fmt;
         T.seg = seg;
         if (fmt == HODLR_FMT_FP32)
@@ -847,6 +929,7 @@ static hodlr_status tca_prepare(const MrInput& in, MrPlan& mr) {
         return HODLR_ERR_CUDA;
     }
     a.slab = (const uint8_t*)d;
+    a.finite = slab_finite(d, bytes);
     mr.tca_dev = d;
     mr.tca_ok = true;
     return HODLR_OK;
@@ -863,7 +946,7 @@ cudaError_t tc_phase_a(const PlanView& p, const MrPlan& mr, const float* x, int6
     if (e != cudaSuccess) return e;
     const int nblk = (int)((s + kTcN - 1) / kTcN);
     k_tc_a<<<mr.view.nb, kTaThreads, sm, st>>>(p, mr.view, mr.tcav, x, ldx, s, (int)mr_spad(s), nblk, partial,
-                                                tbuf, nraw);
+                                                tbuf, nraw, getenv("HODLR_TC_DBG") ? atoi(getenv("HODLR_TC_DBG")) : 0);
     return cudaGetLastError();
 }
 
@@ -884,7 +967,8 @@ cudaError_t tc_phase_b(const PlanView& p, const MrPlan& mr, const float* x, int6
     const int nblk = (int)((s + kTcN - 1) / kTcN);
     const int nwork = p.nchunks * nblk;
     const int grid = std::min(nwork, sms);
-    k_tc_b<<<grid, kTcThreads, kTcSmem, st>>>(p, mr.tcv, x, ldx, tbuf, b, ldb, s, nblk);
+    k_tc_b<<<grid, kTcThreads, kTcSmem, st>>>(p, mr.tcv, x, ldx, tbuf, b, ldb, s, nblk,
+                                               getenv("HODLR_TC_DBG") ? atoi(getenv("HODLR_TC_DBG")) : 0);
     return cudaGetLastError();
 }
 

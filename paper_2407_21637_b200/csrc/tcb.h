@@ -37,6 +37,7 @@ struct TcItem {
 struct TcView {
     int32_t nitems;
     int32_t nlev;
+    int32_t finite;         // every stored value finite: converters use the fast hi/lo split
     int64_t leaf_bytes;     // bytes of one leaf region
     const uint8_t* slab;    // [chunk][leaf_bytes]
     TcItem item[kTcMaxItems];
@@ -51,12 +52,13 @@ constexpr int kTcAMaxTiles = 4;
 constexpr int kTcAItemRows = 16;
 struct TcALevel {
     int32_t mbase;     // first stacked M row of the level
-    int32_t r8;        // rv_max rounded up to 8
+    int32_t r8;        // rows of the level in the stack (= rv_max, no padding)
     int32_t fmt;       // V' storage format
     int32_t seg;       // byte offset of the level's segment inside an item
 };
 struct TcAView {
     int32_t nlev, mtot, nmt;
+    int32_t finite;           // every stored value finite (fast split)
     int32_t item_bytes;       // bytes of one item (16 rows, all levels)
     int64_t chunk_bytes;      // 16 items
     uint32_t tile_full;       // bit t: tile t holds an fp32 level (needs the A_lo pass)
