@@ -666,36 +666,29 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_b(PlanView p, const __grid_co
 // already-quantised values (no rounding), zero fill for padding.
 template <class Pol>
 __global__ void k_slab_a(PlanView p, const __grid_constant__ Mr2View v, uint8_t* __restrict__ slab) {
-    // one thread per (chunk, level, m-tile, k-block, lane, a): 4 consecutive rows of one V' column
-    int64_t per_chunk = 0;
-    for (int lv = v.alev_lo; lv < v.nlev; ++lv) per_chunk += (int64_t)v.lev[lv].nmt * 16 * 32 * Pol::AR;
+    // one thread per (chunk, task, k-block, lane, a): 4 consecutive rows of one V' column
+    const int64_t per_chunk = (int64_t)v.ntasks * 16 * 32 * Pol::AR;
     const int64_t total = per_chunk * p.nchunks;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int chunk = (int)(i / per_chunk);
         int64_t r = i - (int64_t)chunk * per_chunk;
-        int lv = v.alev_lo;
-        for (;; ++lv) {
-            const int64_t c = (int64_t)v.lev[lv].nmt * 16 * 32 * Pol::AR;
-            if (r < c) break;
-            r -= c;
-        }
         const int a = (int)(r % Pol::AR);
         r /= Pol::AR;
         const int lane = (int)(r % 32);
         r /= 32;
         const int kb = (int)(r % 16);
-        const int mt = (int)(r / 16);
-        const Mr2Level L = v.lev[lv];
-        const int fb = fmt_bytes(L.vfmt);
-        uint8_t* blk = slab + (int64_t)chunk * v.a_chunk_bytes + (int64_t)kb * v.arow + L.aoff + (int64_t)mt * L.ablk;
+        const int t = (int)(r / 16);
+        const int fb = fmt_bytes(v.task_fmt[t]);
+        uint8_t* blk = slab + (int64_t)chunk * v.a_chunk_bytes + (int64_t)kb * v.arow + v.task_off[t];
+        const int m = t * Pol::MR + (lane >> 2) + 8 * a;  // stacked row
+        const int lv = v.row_lv[m], c = v.row_c[m];
         const ChunkDesc ch = p.chunks[chunk];
-        const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
-        const int c = mt * Pol::MR + (lane >> 2) + 8 * a;
         const int row = kb * 16 + 4 * (lane & 3);
+        const NodeDesc* nd = lv >= 0 ? &p.nodes[p.chunk_nodes[chunk * p.nlev + lv]] : nullptr;
         for (int j = 0; j < 4; ++j) {
             uint8_t* dst = blk + frag_byte(lane, a * 4 + j, fb, Pol::AR * 4);
-            if (c < nd.rv) {
-                const uint8_t* src = p.arena + nd.v_off + ((int64_t)c * nd.v_ld + (ch.row0 - nd.row0) + row + j) * fb;
+            if (nd && c < nd->rv) {
+                const uint8_t* src = p.arena + nd->v_off + ((int64_t)c * nd->v_ld + (ch.row0 - nd->row0) + row + j) * fb;
                 for (int b = 0; b < fb; ++b) dst[b] = src[b];
             } else {
                 for (int b = 0; b < fb; ++b) dst[b] = 0;
@@ -1000,22 +993,16 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
 
     // ---------------- compute warps
     const int g = lane >> 2, tig = lane & 3;
-    int tlv[MAXTW], tmt[MAXTW], toff[MAXTW], tfmt[MAXTW];
+    int toff[MAXTW], tfmt[MAXTW];
     int ntw = 0;
 #pragma unroll
     for (int i = 0; i < MAXTW; ++i) {
         const int t = warp + i * kAWarps;
-        tlv[i] = v.lev_lo;
-        tmt[i] = 0;
         toff[i] = 0;
         tfmt[i] = HODLR_FMT_FP32;
         if (t < v.ntasks) {
-            int mt = t, lv = v.alev_lo;
-            while (mt >= v.lev[lv].nmt) { mt -= v.lev[lv].nmt; ++lv; }
-            tlv[i] = lv;
-            tmt[i] = mt;
-            toff[i] = (int)v.lev[lv].aoff + mt * v.lev[lv].ablk;
-            tfmt[i] = v.lev[lv].vfmt;
+            toff[i] = v.task_off[t];
+            tfmt[i] = v.task_fmt[t];
             ntw = i + 1;
         }
     }
@@ -1080,43 +1067,54 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
         }
         __syncwarp();
         if (lane == 0) tma::mbar_arrive(&xempty[buf]);
-        // accumulate into the task tiles; flush at a node's last chunk of this run
+        // accumulate into the task tiles; flush a row at its level node's last chunk of this run
 #pragma unroll
         for (int i = 0; i < MAXTW; ++i) {
             if (i >= ntw) continue;
-            const int t = warp + i * kAWarps, lv = tlv[i], mt = tmt[i];
-            const int node = p.chunk_nodes[ci * p.nlev + lv];
-            const bool more = ci + 1 < c_end && p.chunk_nodes[(ci + 1) * p.nlev + lv] == node;
-            const MrLevel L = m.lev[lv];
-            const MrSlot sl = m.slots[node];
-            const int64_t pslot = (int64_t)blockIdx.x + sl.jrel;
-            // a node inside this CTA's run has one slot: its sum IS the coefficient
-            int direct_rv = -1;
-            int64_t toff = 0;
-            if (!more && sl.b0 == sl.b1) {
-                const NodeDesc nd = p.nodes[node];
-                if (nd.ext_slot < 0) {
-                    direct_rv = nd.rv;
-                    toff = nd.t_off * s;
-                }
-            }
+            const int t = warp + i * kAWarps;
 #pragma unroll
-            for (int nt = 0; nt < NCT; ++nt) {
-                W* my = accs + (((size_t)t * NCT + nt) * 32 + lane) * Pol::CR;
-#pragma unroll
-                for (int e = 0; e < Pol::CR; ++e) {
-                    const W val = my[e] + acc[i][0][nt][e];
-                    if (more) {
-                        my[e] = val;
-                    } else {
-                        const int c = mt * Pol::MR + g + 8 * (e >> 1);
-                        const int q = nt * 8 + 2 * tig + (e & 1);
-                        if (direct_rv >= 0) {
-                            if (c < direct_rv && q0 + q < s) tbuf[toff + (int64_t)c * s + q0 + q] = val;
-                        } else if (c < L.rv_max && q0 + q < spad) {
-                            partial[(L.part_rows + pslot * L.rv_pad + c) * spad + q0 + q] = val;
+            for (int a = 0; a < Pol::AR; ++a) {
+                // accumulator elements e with (e >> 1) == a belong to stacked row m
+                const int srow = t * Pol::MR + g + 8 * a;
+                const int lv = v.row_lv[srow], c = v.row_c[srow];
+                bool more = true, direct = false;
+                int64_t dst = -1;  // element offset of column q0 in tbuf / partial
+                if (lv >= 0) {
+                    const int node = p.chunk_nodes[ci * p.nlev + lv];
+                    more = ci + 1 < c_end && p.chunk_nodes[(ci + 1) * p.nlev + lv] == node;
+                    if (!more) {
+                        const MrSlot sl = m.slots[node];
+                        const NodeDesc nd = p.nodes[node];
+                        // a node inside this CTA's run has one slot: its sum IS the coefficient
+                        if (sl.b0 == sl.b1 && nd.ext_slot < 0) {
+                            direct = true;
+                            if (c < nd.rv) dst = nd.t_off * s + (int64_t)c * s + q0;
+                        } else {
+                            const MrLevel L = m.lev[lv];
+                            if (c < L.rv_max) dst = (L.part_rows + ((int64_t)blockIdx.x + sl.jrel) * L.rv_pad + c) * spad + q0;
                         }
-                        my[e] = W(0);
+                    }
+                }
+#pragma unroll
+                for (int nt = 0; nt < NCT; ++nt) {
+                    W* my = accs + (((size_t)t * NCT + nt) * 32 + lane) * Pol::CR;
+#pragma unroll
+                    for (int e = 0; e < Pol::CR; ++e) {
+                        if ((e >> 1) != a) continue;
+                        const W val = my[e] + acc[i][0][nt][e];
+                        if (more) {
+                            my[e] = val;
+                        } else {
+                            const int q = nt * 8 + 2 * tig + (e & 1);
+                            if (dst >= 0) {
+                                if (direct) {
+                                    if (q0 + q < s) tbuf[dst + q] = val;
+                                } else if (q0 + q < spad) {
+                                    partial[dst + q] = val;
+                                }
+                            }
+                            my[e] = W(0);
+                        }
                     }
                 }
             }
@@ -1631,6 +1629,12 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
     const int lfb = fmt_bytes(in.leaf_fmt);
     v.d_item = MT * 32 * Pol::AR * 4 * lfb;
     int64_t aoff = 0, uoff = 0;  // uoff: offset inside the chunk's U area
+    int srows = 0, sfmt = -1;    // stacked phase-A rows so far, format of the open m-tile
+    for (int i = 0; i < kMr2MaxRows; ++i) {
+        v.row_lv[i] = -1;
+        v.row_c[i] = 0;
+    }
+    for (int i = 0; i < kMr2MaxTasks; ++i) v.task_fmt[i] = HODLR_FMT_FP32;
     for (int lv = 0; lv < nlev; ++lv) {
         const MrLevel& L = mr.view.lev[lv];
         Mr2Level& M = v.lev[lv];
@@ -1650,12 +1654,19 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
         if (M.vfmt < 0) M.vfmt = HODLR_FMT_FP32;
         if (M.ufmt < 0) M.ufmt = HODLR_FMT_FP32;
         if (sizeof(typename Pol::W) == 4 && (M.vfmt == HODLR_FMT_FP64 || M.ufmt == HODLR_FMT_FP64)) return HODLR_OK;
-        M.nmt = (L.rv_max + Pol::MR - 1) / Pol::MR;
-        M.ablk = 32 * Pol::AR * 4 * fmt_bytes(M.vfmt);
-        M.aoff = aoff;
-        aoff += (int64_t)M.nmt * M.ablk;
-        v.ntasks += M.nmt;
-        v.max_ablk = std::max(v.max_ablk, M.ablk);
+        // stack this level's V' columns after the previous level's when the format
+        // matches (shared m-tiles), else start a new m-tile
+        if (L.rv_max > 0) {
+            if (srows % Pol::MR != 0 && sfmt != M.vfmt) srows = (srows + Pol::MR - 1) / Pol::MR * Pol::MR;
+            if (srows + L.rv_max > kMr2MaxRows) return HODLR_OK;
+            for (int c = 0; c < L.rv_max; ++c) {
+                v.row_lv[srows + c] = (int16_t)lv;
+                v.row_c[srows + c] = (int16_t)c;
+            }
+            for (int tt = srows / Pol::MR; tt <= (srows + L.rv_max - 1) / Pol::MR; ++tt) v.task_fmt[tt] = M.vfmt;
+            srows += L.rv_max;
+            sfmt = M.vfmt;
+        }
         if (!bpart) continue;
         M.steps = (L.ru_max + Pol::KU - 1) / Pol::KU;
         M.usz = MT * 32 * Pol::AR * Pol::UV * fmt_bytes(M.ufmt);
@@ -1666,6 +1677,14 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
         M.uoff = uoff;
         uoff += (int64_t)M.steps * sstep;
         v.nu_items += M.steps;
+    }
+    v.ntasks = (srows + Pol::MR - 1) / Pol::MR;
+    if (v.ntasks > kMr2MaxTasks) return HODLR_OK;
+    for (int t = 0; t < v.ntasks; ++t) {
+        const int blk = 32 * Pol::AR * 4 * fmt_bytes(v.task_fmt[t]);
+        v.task_off[t] = (int32_t)aoff;
+        aoff += blk;
+        v.max_ablk = std::max(v.max_ablk, blk);
     }
     if (v.max_ablk == 0) v.max_ablk = 128;
     if (v.d_item & (v.d_item - 1)) return HODLR_OK;

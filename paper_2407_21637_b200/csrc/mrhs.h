@@ -29,6 +29,8 @@
 namespace hodlr {
 
 constexpr int kMrMaxLevels = 31;
+constexpr int kMr2MaxTasks = 64;           // 16 compute warps x <= 4 tasks
+constexpr int kMr2MaxRows = 1024;          // kMr2MaxTasks x MR (16 for TF32)
 
 struct MrLevel {
     int32_t node0, nnodes;   // node ids of the level: [node0, node0 + nnodes)
@@ -86,6 +88,13 @@ struct Mr2View {
     int32_t leaf_fmt;
     int32_t max_ablk;
     int32_t arow;              // A bytes of one k-step, all tasks ([kb][task] layout)
+    // Phase-A tasks stack the levels' V' columns along M (a run of levels with
+    // one storage format shares m-tiles; a format change starts a new tile):
+    // stacked row m -> (level, column), level -1 = padding.
+    int32_t task_fmt[kMr2MaxTasks];
+    int32_t task_off[kMr2MaxTasks];   // byte offset of the task's block inside one k-step
+    int16_t row_lv[kMr2MaxRows];
+    int16_t row_c[kMr2MaxRows];
     const uint8_t* slab_a;
     const uint8_t* slab_b;
     Mr2Level lev[kMrMaxLevels];
