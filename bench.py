@@ -195,6 +195,10 @@ def cpu_time_oracle(H, X, seconds):
 
 def main():
     args = parse()
+    # the driver reads ONE JSON line from stdout: keep NCCL's version banner off it
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
