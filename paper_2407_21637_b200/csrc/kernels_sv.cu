@@ -1192,6 +1192,7 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     // R pieces: late enough that the A leaves are (nearly) done, early enough that
     // they are taken before any running CTA could fill its deferred-U FIFO
     P.pos_r = std::min(P.num_d / 6, kFifo * 16);  // (assumes >= 16 CTAs can run at once)
+    if (const char* e = getenv("HODLR_POS_R")) P.pos_r = std::max(0, std::min(P.num_d, atoi(e)));  // tuning sweeps
 
     // ---- relayout the quantised level-batched arena into leaf slabs (bytes)
     std::vector<uint8_t> arena(in.arena_bytes);
