@@ -699,17 +699,37 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
     void* ws = nullptr;
     hodlr_status r = resolve_ws(h, working, s, &ws, 0);
     if (r != HODLR_OK) return r;
-    CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
+    // A pinned (page-locked, UVA-mapped) host b is written by the kernels
+    // directly where each element is stored once: the widening kernel (fp32
+    // working) and the fused single-vector kernel (fp64 working, b rows written
+    // once as the U pieces finish, so the PCIe writes overlap the kernel's tail).
+    // Saves the D2H copy-engine pass (cfg2 e2e 78 -> 68 us); pageable buffers go
+    // through the staging copy.
+    auto mapped = [](const void* hp) -> void* {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, hp) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+    };
+    const bool zc = !getenv("HODLR_B200_NO_ZEROCOPY");
+    double* b_map = zc ? (double*)mapped(b_host) : nullptr;
     if (working == HODLR_FMT_FP64) {
-        r = run_local<double>(h, xd, s, bd, s, s, ws, st);
+        CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
+        if (!(h->sv_ok && s == 1)) b_map = nullptr;  // multi-pass writers: stage in HBM
+        r = run_local<double>(h, xd, s, b_map ? b_map : bd, s, s, ws, st);
         if (r != HODLR_OK) return r;
     } else {
+        // (x is still staged by the copy engine: one kernel reading 2 MB of mapped
+        // host memory measured slower than the copy, cfg5 eps=1e-2 e2e 180 -> 247 us)
+        CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
         CUDA_TRY(launch_round_in<float>(xd, (float*)xw, n, s, s, s, st));
         r = run_local<float>(h, (const float*)xw, s, (float*)bw, s, s, ws, st);
         if (r != HODLR_OK) return r;
-        CUDA_TRY(launch_widen_out<float>((const float*)bw, bd, n, s, s, s, st));
+        CUDA_TRY(launch_widen_out<float>((const float*)bw, b_map ? b_map : bd, n, s, s, s, st));
     }
-    CUDA_TRY(cudaMemcpyAsync(b_host, bd, n * s * 8, cudaMemcpyDeviceToHost, st));
+    if (!b_map) CUDA_TRY(cudaMemcpyAsync(b_host, bd, n * s * 8, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     return HODLR_OK;
 }

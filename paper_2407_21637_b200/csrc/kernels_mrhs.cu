@@ -908,6 +908,14 @@ __device__ __forceinline__ void stage_x_async(W* xs, const W* __restrict__ x, in
 //                in stages of G k-steps (all tasks) through a CTA-wide ring;
 //   warp 17      stager: X of the next chunk (cp.async, fragment order).
 constexpr int kAStagers = 4;  // X staging warps of the phase-A CTA
+// Split-K factor of phase A: with few tasks (stacked m-tiles), KS warps share a
+// task, warp w taking the k-steps kb = kp (mod KS); their accumulator tiles are
+// summed in kp order at a row's flush (deterministic).  KS * ntasks <= kAWarps.
+__host__ __device__ __forceinline__ int ma2_ks(int ntasks) {
+    int ks = 1;
+    while (ks < 16 && ntasks * ks * 2 <= kAWarps) ks *= 2;
+    return ks;
+}
 constexpr int kAThreads = (kAWarps + 1 + kAStagers) * 32;
 
 template <class Pol, int NCT, int MAXTW>
@@ -993,11 +1001,14 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
 
     // ---------------- compute warps
     const int g = lane >> 2, tig = lane & 3;
+    // KS > 1 only with MAXTW == 1: warp = task * KS + kp, tile index = warp
+    const int KS = MAXTW == 1 ? ma2_ks(v.ntasks) : 1;
+    const int kp = warp & (KS - 1), wtask = KS > 1 ? warp / KS : warp;
     int toff[MAXTW], tfmt[MAXTW];
     int ntw = 0;
 #pragma unroll
     for (int i = 0; i < MAXTW; ++i) {
-        const int t = warp + i * kAWarps;
+        const int t = wtask + i * kAWarps;
         toff[i] = 0;
         tfmt[i] = HODLR_FMT_FP32;
         if (t < v.ntasks) {
@@ -1031,10 +1042,12 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
             tma::mbar_wait(&full[slot], ph);
             const uint8_t* base = ring + (size_t)slot * stage_bytes;
             for (int kk = 0; kk < G; ++kk) {
+                const int kb = gi * G + kk;
+                const bool mine = KS == 1 || (kb & (KS - 1)) == kp;
                 W tmp[MAXTW][Pol::AR * 4];
 #pragma unroll
                 for (int i = 0; i < MAXTW; ++i)
-                    if (i < ntw) frag_load<W, Pol::AR * 4>(tfmt[i], base + kk * v.arow + toff[i], lane, tmp[i]);
+                    if (i < ntw && mine) frag_load<W, Pol::AR * 4>(tfmt[i], base + kk * v.arow + toff[i], lane, tmp[i]);
                 if (kk == G - 1) {  // stage fully read
                     __syncwarp();
                     if (lane == 0) tma::mbar_arrive(&empty[slot]);
@@ -1043,7 +1056,7 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
                         ph ^= 1u;
                     }
                 }
-                const int kb = gi * G + kk;
+                if (!mine || ntw == 0) continue;
                 typename Pol::BF bf[NCT];
 #pragma unroll
                 for (int nt = 0; nt < NCT; ++nt) {
@@ -1071,14 +1084,18 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
 #pragma unroll
         for (int i = 0; i < MAXTW; ++i) {
             if (i >= ntw) continue;
-            const int t = warp + i * kAWarps;
+            const int t = wtask + i * kAWarps;
+            const int tile = KS > 1 ? warp : t;
+            bool more_a[Pol::AR], direct_a[Pol::AR];
+            int64_t dst_a[Pol::AR];  // element offset of column q0 in tbuf / partial
+            bool anyflush = false;
 #pragma unroll
             for (int a = 0; a < Pol::AR; ++a) {
                 // accumulator elements e with (e >> 1) == a belong to stacked row m
                 const int srow = t * Pol::MR + g + 8 * a;
                 const int lv = v.row_lv[srow], c = v.row_c[srow];
                 bool more = true, direct = false;
-                int64_t dst = -1;  // element offset of column q0 in tbuf / partial
+                int64_t dst = -1;
                 if (lv >= 0) {
                     const int node = p.chunk_nodes[ci * p.nlev + lv];
                     more = ci + 1 < c_end && p.chunk_nodes[(ci + 1) * p.nlev + lv] == node;
@@ -1095,26 +1112,78 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
                         }
                     }
                 }
+                more_a[a] = more;
+                direct_a[a] = direct;
+                dst_a[a] = dst;
+                anyflush |= !more;
+            }
+            auto store = [&](int a, int nt, int e, W val) {
+                const int q = nt * 8 + 2 * tig + (e & 1);
+                if (dst_a[a] >= 0) {
+                    if (direct_a[a]) {
+                        if (q0 + q < s) tbuf[dst_a[a] + q] = val;
+                    } else if (q0 + q < spad) {
+                        partial[dst_a[a] + q] = val;
+                    }
+                }
+            };
+            if (KS == 1) {
 #pragma unroll
-                for (int nt = 0; nt < NCT; ++nt) {
-                    W* my = accs + (((size_t)t * NCT + nt) * 32 + lane) * Pol::CR;
+                for (int a = 0; a < Pol::AR; ++a)
 #pragma unroll
-                    for (int e = 0; e < Pol::CR; ++e) {
-                        if ((e >> 1) != a) continue;
-                        const W val = my[e] + acc[i][0][nt][e];
-                        if (more) {
-                            my[e] = val;
-                        } else {
-                            const int q = nt * 8 + 2 * tig + (e & 1);
-                            if (dst >= 0) {
-                                if (direct) {
-                                    if (q0 + q < s) tbuf[dst + q] = val;
-                                } else if (q0 + q < spad) {
-                                    partial[dst + q] = val;
-                                }
+                    for (int nt = 0; nt < NCT; ++nt) {
+                        W* my = accs + (((size_t)tile * NCT + nt) * 32 + lane) * Pol::CR;
+#pragma unroll
+                        for (int e = 0; e < Pol::CR; ++e) {
+                            if ((e >> 1) != a) continue;
+                            const W val = my[e] + acc[i][0][nt][e];
+                            if (more_a[a]) {
+                                my[e] = val;
+                            } else {
+                                store(a, nt, e, val);
+                                my[e] = W(0);
                             }
-                            my[e] = W(0);
                         }
+                    }
+                continue;
+            }
+            // split-K: every warp of the task adds its chunk sums to its own tile;
+            // at a flush the kp = 0 warp sums the KS tiles in kp order
+#pragma unroll
+            for (int nt = 0; nt < NCT; ++nt) {
+                W* my = accs + (((size_t)tile * NCT + nt) * 32 + lane) * Pol::CR;
+#pragma unroll
+                for (int e = 0; e < Pol::CR; ++e) my[e] += acc[i][0][nt][e];
+            }
+            // same rows and chunk for the KS warps of a task: a uniform decision
+            if (__any_sync(0xffffffffu, anyflush)) {
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + wtask), "r"(32 * KS) : "memory");
+                if (kp == 0) {
+#pragma unroll
+                    for (int a = 0; a < Pol::AR; ++a) {
+                        if (more_a[a]) continue;
+#pragma unroll
+                        for (int nt = 0; nt < NCT; ++nt)
+#pragma unroll
+                            for (int e = 0; e < Pol::CR; ++e) {
+                                if ((e >> 1) != a) continue;
+                                W val = W(0);
+                                for (int k = 0; k < KS; ++k)
+                                    val += accs[((((size_t)(tile + k)) * NCT + nt) * 32 + lane) * Pol::CR + e];
+                                store(a, nt, e, val);
+                            }
+                    }
+                }
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + wtask), "r"(32 * KS) : "memory");
+#pragma unroll
+                for (int a = 0; a < Pol::AR; ++a) {
+                    if (more_a[a]) continue;
+#pragma unroll
+                    for (int nt = 0; nt < NCT; ++nt) {
+                        W* my = accs + (((size_t)tile * NCT + nt) * 32 + lane) * Pol::CR;
+#pragma unroll
+                        for (int e = 0; e < Pol::CR; ++e)
+                            if ((e >> 1) == a) my[e] = W(0);
                     }
                 }
             }
@@ -1422,7 +1491,7 @@ inline int pick_nt(int spad) { return spad >= 32 ? 4 : spad >= 16 ? 2 : 1; }
 template <class Pol>
 size_t ma2_smem(const Mr2View& v, int nct, int slot_bytes, int ns) {
     using W = typename Pol::W;
-    return 256 + (size_t)2 * kChunk * nct * 8 * sizeof(W) + (size_t)v.ntasks * nct * 32 * Pol::CR * sizeof(W) +
+    return 256 + (size_t)2 * kChunk * nct * 8 * sizeof(W) + (size_t)v.ntasks * ma2_ks(v.ntasks) * nct * 32 * Pol::CR * sizeof(W) +
            (size_t)ns * slot_bytes;
 }
 template <class Pol>

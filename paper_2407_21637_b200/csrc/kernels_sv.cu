@@ -167,6 +167,8 @@ struct SvParams {
     int8_t col_level[kMaxCols];           // flattened (group, column) -> level (0-based)
     int16_t col_c[kMaxCols];              //                            -> rank column
     int16_t gstart[6];
+    int32_t mode;                         // 0: whole matvec; 1: A items only (split launch 1);
+                                          // 2: R + BC items after launch 1 (PDL dependent)
 };
 
 struct SvSync {
@@ -481,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
     const int nq = P.num_a + P.num_d + P.num_r;  // queue: A leaves, then BC items with R pieces at pos_r
     constexpr int kBlocks = kM / kRB;            // row blocks per leaf
 
+    if (P.mode == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) {
         TR(0);
         for (int s = 0; s < kNS; ++s) {
@@ -644,6 +647,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 // ---- R: reduce node partials (needs every leaf's partials)
                 const RPiece rp = P.rp[qq - P.pos_r];
                 const Level& L = P.lev[rp.lv];
+                if (P.mode == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
                 if (lane == 0) {
                     if (r_items == 0) TR(4);
                     while (ld_acquire(&a.sync->a_done) != (unsigned)P.num_a) __nanosleep(128);
@@ -916,7 +920,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 // R piece.  Release pattern: CTA barrier, fence.acq_rel.gpu,
                 // relaxed reduction; readers ld.acquire the counter.
                 if (h.type == PT_A && h.last) ++my_a;
-                if (ctid == 0 && ((h.type == PT_A && h.last == 2) || h.type == PT_R)) {
+                if (ctid == 0 && ((h.type == PT_A && h.last == 2 && P.mode == 0) || h.type == PT_R)) {
                     if (h.type == PT_A) TR(16); else TR(18);
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     if (h.type == PT_A) TR(17); else TR(19);
@@ -968,8 +972,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
 size_t smem_bytes() { return (size_t)kNS * kStage + sizeof(SmemCtl); }
 
 // workspace: [SvSync | leaf B counters] (zeroed once, reset per call) [partials] [coefficients]
-size_t sv_sync_bytes(int nleaves) {
-    return (sizeof(SvSync) + (size_t)nleaves * sizeof(unsigned) + 255) / 256 * 256;
+size_t sv_sync_bytes(int nleaves) {  // two SvSync (split launches), then the leaf counters
+    return (2 * sizeof(SvSync) + (size_t)nleaves * sizeof(unsigned) + 255) / 256 * 256;
 }
 
 int64_t round_up16(int64_t v) { return (v + 15) / 16 * 16; }
@@ -1265,10 +1269,17 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     sv.num_items_b = P.num_d + P.num_r;
     sv.grid = std::min(sms * std::min(occ, kCtasPerSm), P.num_a + P.num_d + P.num_r);
     if (const char* g = getenv("HODLR_B200_GRID")) sv.grid = std::min(sv.grid, atoi(g));
+    {
+        const char* e = getenv("HODLR_SV_SPLIT");
+        // opt-in: measured slower (cfg2 41.8 -> 49.0 us, cfg5 eps=1e-2 76.5 -> 84.2 us):
+        // launch 2's CTAs cannot start before launch 1's leave the SMs, and the
+        // grid-completion wait costs more than the in-kernel publication
+        sv.split = e ? atoi(e) != 0 : 0;
+        sv.launches = sv.split ? 2 : 1;
+    }
     if (getenv("HODLR_B200_VERBOSE"))
         fprintf(stderr, "[hodlr_b200] fused path: grid %d (sms %d occ %d) smem %zu items A %d BC %d R %d U pieces %d\n",
                 sv.grid, sms, occ, smem, P.num_a, P.num_d, P.num_r, P.nupieces);
-    sv.launches = 1;
     sv.tfast_count = tb;
     sv.extra_ws = sv_sync_bytes(P.nleaves) + (size_t)(pb + tb) * 8;  // (leaf counters unused now)
     sv.part_count = pb;
@@ -1315,8 +1326,42 @@ cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* 
     cudaMemsetAsync(trace_buf, 0, (size_t)sv.grid * 48 * 8, st);
     a.trace = trace_buf;
 #endif
-    void* args[] = {(void*)&P, &a};
-    cudaError_t err = cudaLaunchKernel((const void*)k_stream<W>, dim3(sv.grid), dim3(kThreads), args, smem_bytes(), st);
+    cudaError_t err;
+    if (!sv.split) {
+        void* args[] = {(void*)&P, &a};
+        err = cudaLaunchKernel((const void*)k_stream<W>, dim3(sv.grid), dim3(kThreads), args, smem_bytes(), st);
+    } else {
+        // Split: launch 1 streams the phase-A items only (its completion publishes
+        // the partials, no GPU-scope fences under load); launch 2 (programmatic
+        // dependent launch: its CTAs start as launch 1's retire) streams D and U
+        // and reduces the partials into coefficients after griddepcontrol.wait.
+        static thread_local SvParams P1, P2;
+        P1 = P;
+        P1.num_d = P1.num_r = P1.pos_r = 0;
+        P1.mode = 1;
+        P2 = P;
+        P2.num_a = 0;
+        P2.mode = 2;
+        SvKernelArgs<W> a2 = a;
+        a2.sync = a.sync + 1;
+        void* args1[] = {(void*)&P1, &a};
+        err = cudaLaunchKernel((const void*)k_stream<W>, dim3(std::min(sv.grid, P.num_a)), dim3(kThreads), args1,
+                               smem_bytes(), st);
+        if (err == cudaSuccess) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(std::min(sv.grid, P.num_d + P.num_r));
+            cfg.blockDim = dim3(kThreads);
+            cfg.dynamicSmemBytes = smem_bytes();
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            void* args2[] = {(void*)&P2, &a2};
+            err = cudaLaunchKernelExC(&cfg, (const void*)k_stream<W>, args2);
+        }
+    }
 #ifdef HODLR_TRACE
     if (err == cudaSuccess) {
         std::vector<unsigned long long> h((size_t)sv.grid * 48);

@@ -20,6 +20,7 @@ struct SvPlan {
     int num_items_a = 0, num_items_b = 0;
     int grid = 0;
     int launches = 1;
+    int split = 0;              // 1: A-only launch + PDL-dependent R/BC launch
     int64_t tfast_count = 0;    // padded coefficient buffer (elements)
     int64_t part_count = 0;     // fast-path partial buffer (elements)
     size_t extra_ws = 0;        // bytes of workspace for sync state + coefficients
