@@ -167,6 +167,7 @@ struct SvParams {
     int8_t col_level[kMaxCols];           // flattened (group, column) -> level (0-based)
     int16_t col_c[kMaxCols];              //                            -> rank column
     int16_t gstart[6];
+    int32_t rdefer;                       // 1: park R pieces until the A partials exist
     int32_t mode;                         // 0: whole matvec; 1: A items only (split launch 1);
                                           // 2: R + BC items after launch 1 (PDL dependent)
 };
@@ -583,7 +584,57 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 next_stage();
             }
         };
+        // R pieces wait for every A leaf's partials.  A producer that takes one
+        // before that keeps streaming BC items and parks the piece (<= kRPend),
+        // emitting it at the first item boundary that sees a_done complete.
+        bool a_ready = false;
+        auto check_a = [&](bool block) {
+            if (a_ready) return;
+            unsigned v = 0;
+            if (lane == 0) {
+                v = ld_acquire(&a.sync->a_done);
+                while (block && v != (unsigned)P.num_a) {
+                    __nanosleep(128);
+                    v = ld_acquire(&a.sync->a_done);
+                }
+            }
+            a_ready = __shfl_sync(0xffffffffu, v, 0) == (unsigned)P.num_a;
+            if (a_ready) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // partials read by TMA below
+                if (lane == 0) TR(5);
+            }
+        };
+        auto emit_r = [&](int ri) {
+            const RPiece rp = P.rp[ri];
+            const Level& L = P.lev[rp.lv];
+            ++r_items;
+            if (lane == 0) TRV(13, r_items);
+            uint8_t* st = claim();
+            const int64_t cnt = (int64_t)(rp.j1 - rp.j0) * (rp.c1 - rp.c0) * L.cst;
+            const unsigned bytes = (unsigned)round_up16_d(cnt * (int64_t)sizeof(W));
+            if (lane == 0) {
+                PieceHdr& h = C.hdr[stage];
+                h.type = PT_R;
+                h.a = ri;
+                mbar_arrive_tx(&C.full[stage], bytes);
+                bulk_g2s(st, a.partial + L.pbase + ((int64_t)rp.j0 * L.r + rp.c0) * L.cst, bytes, &C.full[stage]);
+                TR(20);
+            }
+            __syncwarp();
+            next_stage();
+        };
+        constexpr int kRPend = 4;
+        int rpend[kRPend];
+        int nrp = 0;
+        auto flush_r = [&](bool block) {
+            if (nrp == 0) return;
+            check_a(block);
+            if (!a_ready) return;
+            for (int i = 0; i < nrp; ++i) emit_r(rpend[i]);
+            nrp = 0;
+        };
         auto flush_u = [&](bool block) {
+            if (block) flush_r(true);  // never wait for the coefficients while holding an R piece
             if (fh == ft) return;
             check_r(block);
             if (!r_ready) return;
@@ -645,31 +696,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             const int qq = q - P.num_a;
             if (qq >= P.pos_r && qq < P.pos_r + P.num_r) {
                 // ---- R: reduce node partials (needs every leaf's partials)
-                const RPiece rp = P.rp[qq - P.pos_r];
-                const Level& L = P.lev[rp.lv];
                 if (P.mode == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
-                if (lane == 0) {
-                    if (r_items == 0) TR(4);
-                    while (ld_acquire(&a.sync->a_done) != (unsigned)P.num_a) __nanosleep(128);
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
-                    if (r_items == 0) TR(5);
-                    TRV(13, r_items + 1);
-                }
-                __syncwarp();
-                ++r_items;
-                uint8_t* st = claim();
-                const int64_t cnt = (int64_t)(rp.j1 - rp.j0) * (rp.c1 - rp.c0) * L.cst;
-                const unsigned bytes = (unsigned)round_up16_d(cnt * (int64_t)sizeof(W));
-                if (lane == 0) {
-                    PieceHdr& h = C.hdr[stage];
-                    h.type = PT_R;
-                    h.a = qq - P.pos_r;
-                    mbar_arrive_tx(&C.full[stage], bytes);
-                    bulk_g2s(st, a.partial + L.pbase + ((int64_t)rp.j0 * L.r + rp.c0) * L.cst, bytes, &C.full[stage]);
-                    TR(20);
-                }
-                __syncwarp();
-                next_stage();
+                if (lane == 0 && r_items + nrp == 0) TR(4);
+                if (nrp == kRPend) flush_r(true);
+                rpend[nrp++] = qq - P.pos_r;
+                flush_r(P.mode == 2 || P.rdefer == 0);
                 continue;
             }
             // ---- BC: y = D x now (kept in this CTA's y slot), b = U t + y once t exists
@@ -707,6 +738,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
             if (lane == 0) C.fifo[ft % kFifo] = (leaf << 8) | rb;
             __syncwarp();
             ++ft;
+            flush_r(false);
             flush_u(false);
         }
         if (lane == 0) TR(7);
@@ -1168,6 +1200,8 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     P.num_d = nleaves * (kM / kRB);
     // node-reduction pieces (R items): a level's partials are [node][column][leaf]
     P.num_r = 0;
+    int64_t rcap = kStage;  // R piece bytes (HODLR_R_BYTES: sweeps)
+    if (const char* e = getenv("HODLR_R_BYTES")) rcap = std::max<int64_t>(1024, std::min<int64_t>(kStage, atoll(e)));
     for (int k = 0; k < depth; ++k) {
         const Level& L = P.lev[k];
         if (L.r == 0) continue;
@@ -1180,13 +1214,13 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
             P.rp[P.num_r++] = RPiece{(int16_t)k, 0, j0, j1, c0, c1};
             return true;
         };
-        if (node_bytes <= kStage) {
-            int per = (int)std::min<int64_t>(nodes_k, kStage / node_bytes);
+        if (node_bytes <= rcap) {
+            int per = (int)std::min<int64_t>(nodes_k, rcap / node_bytes);
             if (per >= 4) per = per / 4 * 4;
             for (int j0 = 0; j0 < nodes_k; j0 += per)
                 if (!add(j0, std::min(nodes_k, j0 + per), 0, L.r)) return HODLR_OK;
         } else {
-            const int cols = (int)(kStage / (nch * 8));
+            const int cols = (int)(rcap / (nch * 8));
             if (cols < 1) return HODLR_OK;
             for (int j = 0; j < nodes_k; ++j)
                 for (int c0 = 0; c0 < L.r; c0 += cols)
@@ -1196,6 +1230,11 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     // R pieces: late enough that the A leaves are (nearly) done, early enough that
     // they are taken before any running CTA could fill its deferred-U FIFO
     P.pos_r = std::min(P.num_d / 6, kFifo * 16);  // (assumes >= 16 CTAs can run at once)
+    // parking R pieces (HODLR_R_DEFER=1) measured slower on cfg2 (42.5 -> 45.1 us):
+    // a parked piece is only re-checked at BC item boundaries, so the partial
+    // reduction starts ~6 us later than with the blocking wait
+    P.rdefer = 0;
+    if (const char* e = getenv("HODLR_R_DEFER")) P.rdefer = atoi(e) != 0;
     if (const char* e = getenv("HODLR_POS_R")) P.pos_r = std::max(0, std::min(P.num_d, atoi(e)));  // tuning sweeps
 
     // ---- relayout the quantised level-batched arena into leaf slabs (bytes)
