@@ -51,17 +51,17 @@ constexpr int kRB = 64;                 // rows of a BC item (one leaf row block
 constexpr int kRPL = kRB / 32;          // rows per lane in B / C pieces
 // (HODLR_KNS / HODLR_KSTAGE override the ring geometry for tools/build_variants.sh sweeps)
 #ifndef HODLR_KNS
-#define HODLR_KNS 3
+#define HODLR_KNS 2
 #endif
 #ifndef HODLR_KSTAGE
-#define HODLR_KSTAGE 33280
+#define HODLR_KSTAGE 49920
 #endif
 constexpr int kNS = HODLR_KNS;          // ring stages per CTA
 #ifndef HODLR_CTAS
 #define HODLR_CTAS 2
 #endif
 constexpr int kCtasPerSm = HODLR_CTAS;  // independent pipelines per SM
-constexpr int kStage = HODLR_KSTAGE;    // bytes per stage (= 512 B of x + a 64 x 64 fp64 D block)
+constexpr int kStage = HODLR_KSTAGE;    // bytes per stage (2 x 48.75 KB: 2 CTAs/SM; measured 3-4% faster than 3 x 32.5 KB on cfg2)
 constexpr int kConsumers = 8;           // consumer warps (= column subsets of B/C pieces)
 constexpr int kThreads = 32 * (kConsumers + 1);  // + producer warp
 constexpr int kFifo = 8;                // BC items whose U piece waits for the coefficients
@@ -167,6 +167,7 @@ struct SvParams {
     int8_t col_level[kMaxCols];           // flattened (group, column) -> level (0-based)
     int16_t col_c[kMaxCols];              //                            -> rank column
     int16_t gstart[6];
+    int32_t static_first;                 // 1: CTA b starts with queue entry b
     int32_t rdefer;                       // 1: park R pieces until the A partials exist
     int32_t mode;                         // 0: whole matvec; 1: A items only (split launch 1);
                                           // 2: R + BC items after launch 1 (PDL dependent)
@@ -604,27 +605,49 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 if (lane == 0) TR(5);
             }
         };
-        auto emit_r = [&](int ri) {
+        // An R piece's descriptor and source are resolved when the piece is taken,
+        // before the wait for the A partials: the parameter-table reads (cold in
+        // the constant cache, ~us under full HBM load) stay off the critical path,
+        // and the consumer gets the piece from the stage header.
+        struct RJob {
+            const W* src;
+            unsigned bytes;
+            int lv, j0, j1, c01;
+        };
+        auto make_r = [&](int ri) {
             const RPiece rp = P.rp[ri];
             const Level& L = P.lev[rp.lv];
+            const int64_t cnt = (int64_t)(rp.j1 - rp.j0) * (rp.c1 - rp.c0) * L.cst;
+            RJob j;
+            j.src = a.partial + L.pbase + ((int64_t)rp.j0 * L.r + rp.c0) * L.cst;
+            j.bytes = (unsigned)round_up16_d(cnt * (int64_t)sizeof(W));
+            j.lv = rp.lv;
+            j.j0 = rp.j0;
+            j.j1 = rp.j1;
+            j.c01 = rp.c0 | (rp.c1 << 16);
+            asm volatile("" ::"l"(j.src), "r"(j.bytes), "r"(j.lv), "r"(j.j0), "r"(j.j1), "r"(j.c01));
+            return j;
+        };
+        auto emit_r = [&](const RJob& j) {
             ++r_items;
             if (lane == 0) TRV(13, r_items);
             uint8_t* st = claim();
-            const int64_t cnt = (int64_t)(rp.j1 - rp.j0) * (rp.c1 - rp.c0) * L.cst;
-            const unsigned bytes = (unsigned)round_up16_d(cnt * (int64_t)sizeof(W));
             if (lane == 0) {
                 PieceHdr& h = C.hdr[stage];
                 h.type = PT_R;
-                h.a = ri;
-                mbar_arrive_tx(&C.full[stage], bytes);
-                bulk_g2s(st, a.partial + L.pbase + ((int64_t)rp.j0 * L.r + rp.c0) * L.cst, bytes, &C.full[stage]);
+                h.a = j.lv;
+                h.leaf = j.j0;
+                h.b = j.j1;
+                h.last = j.c01;
+                mbar_arrive_tx(&C.full[stage], j.bytes);
+                bulk_g2s(st, j.src, j.bytes, &C.full[stage]);
                 TR(20);
             }
             __syncwarp();
             next_stage();
         };
         constexpr int kRPend = 4;
-        int rpend[kRPend];
+        RJob rpend[kRPend];
         int nrp = 0;
         auto flush_r = [&](bool block) {
             if (nrp == 0) return;
@@ -649,18 +672,32 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
         // Every cross-CTA wait (R on all A leaves, U on all R pieces) targets work
         // that sits EARLIER in the queue, i.e. was already taken by a running CTA,
         // so progress never depends on CTAs being co-resident.
+        // static_first: CTA b's first entry is b (no contended atomic before the
+        // first load; the counter then hands out entries from gridDim.x on).
+        // Progress still only needs every CTA of the grid to start eventually.
+        const int qoff = P.static_first ? (int)gridDim.x : 0;
         int n1 = 0, n2 = 0;
         if (lane == 0) {
-            n1 = (int)atomicAdd(&a.sync->queue, 2u);
-            n2 = n1 + 1;
+            if (P.static_first) {
+                n1 = (int)blockIdx.x;
+                n2 = (int)atomicAdd(&a.sync->queue, 1u) + qoff;
+            } else {
+                n1 = (int)atomicAdd(&a.sync->queue, 2u);
+                n2 = n1 + 1;
+            }
             TR(23);
         }
         const int dsz = fmt_sz(P.leaf_fmt);
+        bool first_q = true;
         for (;;) {
             const int q = __shfl_sync(0xffffffffu, n1, 0);
+            if (first_q) {
+                first_q = false;
+                if (lane == 0) TR(30);
+            }
             if (q >= nq) break;
             n1 = n2;
-            if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u);
+            if (lane == 0) n2 = (int)atomicAdd(&a.sync->queue, 1u) + qoff;
             if (q < P.num_a) {
                 // ---- A: partial V'^T x of one (leaf, piece) or one whole leaf
                 const int per_leaf = P.napieces / P.a_group;
@@ -699,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 if (P.mode == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
                 if (lane == 0 && r_items + nrp == 0) TR(4);
                 if (nrp == kRPend) flush_r(true);
-                rpend[nrp++] = qq - P.pos_r;
+                rpend[nrp++] = make_r(qq - P.pos_r);
                 flush_r(P.mode == 2 || P.rdefer == 0);
                 continue;
             }
@@ -885,7 +922,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_stream(const __grid_co
                 }
             } else if (h.type == PT_R) {
                 // t for (node, column) pairs: fixed-order sums over the node's leaves
-                const RPiece rp = P.rp[h.a];
+                RPiece rp;
+                rp.lv = (int16_t)h.a;
+                rp.j0 = h.leaf;
+                rp.j1 = h.b;
+                rp.c0 = h.last & 0xffff;
+                rp.c1 = h.last >> 16;
                 const Level& L = P.lev[rp.lv];
                 const int nch = (1 << (nlev - 1 - rp.lv)) * L.npc;  // partials per (node, column)
                 const int ncol = rp.c1 - rp.c0;
@@ -1234,6 +1276,8 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     // a parked piece is only re-checked at BC item boundaries, so the partial
     // reduction starts ~6 us later than with the blocking wait
     P.rdefer = 0;
+    P.static_first = 0;
+    if (const char* e = getenv("HODLR_SV_STATIC")) P.static_first = atoi(e) != 0;
     if (const char* e = getenv("HODLR_R_DEFER")) P.rdefer = atoi(e) != 0;
     if (const char* e = getenv("HODLR_POS_R")) P.pos_r = std::max(0, std::min(P.num_d, atoi(e)));  // tuning sweeps
 

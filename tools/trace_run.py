@@ -32,7 +32,7 @@ def summarize(path):
         print(f"  {name:28s} n={len(v):4d} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us")
 
     print(f"grid {grid}  A leaves {num_a}  R pieces {num_r}")
-    for name, i in [("entry", 0), ("epoch loaded", 21), ("tables ready", 22), ("first queue items", 23), ("first piece issued", 1), ("A piece 1 arrived", 24), ("A piece 2 arrived", 25),
+    for name, i in [("entry", 0), ("epoch loaded", 21), ("tables ready", 22), ("first queue items", 23), ("first entry known", 30), ("first piece issued", 1), ("A piece 1 arrived", 24), ("A piece 2 arrived", 25),
                     ("A piece 3 arrived", 26), ("A piece 4 arrived", 27), ("last A piece issued", 2), ("first BC item", 3), ("R wait start", 4),
                     ("R wait end (all A done)", 5), ("coefficients ready", 6), ("queue exhausted", 7),
                     ("first U issued", 14), ("first U consumed", 15), ("last U issued", 8), ("consumers done", 9), ("exit", 10),
