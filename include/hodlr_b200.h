@@ -115,7 +115,11 @@ hodlr_status hodlr_matvec(hodlr_handle* h, int32_t working, const void* x, int64
 /* End-to-end call with HOST buffers (the reference-facing drop-in): x_host and
  * b_host are binary64, n x s row-major.  Copies x in, rounds it to `working`,
  * runs the matvec, widens b to binary64 and copies it out; returns after the
- * result is in b_host.  Not valid on sharded handles. */
+ * result is in b_host.  Not valid on sharded handles.  When b_host is
+ * page-locked (cudaHostAlloc / torch pin_memory) the kernel that stores each b
+ * element once (the widening kernel, or the fused s = 1 kernel for binary64
+ * working) writes it through the mapped address instead of a D2H copy
+ * (HODLR_B200_NO_ZEROCOPY=1 disables this). */
 hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x_host,
                                double* b_host, int64_t s, void* stream);
 

@@ -51,17 +51,18 @@ constexpr int kRB = 64;                 // rows of a BC item (one leaf row block
 constexpr int kRPL = kRB / 32;          // rows per lane in B / C pieces
 // (HODLR_KNS / HODLR_KSTAGE override the ring geometry for tools/build_variants.sh sweeps)
 #ifndef HODLR_KNS
-#define HODLR_KNS 2
+#define HODLR_KNS 3
 #endif
 #ifndef HODLR_KSTAGE
-#define HODLR_KSTAGE 49920
+#define HODLR_KSTAGE 33280
 #endif
 constexpr int kNS = HODLR_KNS;          // ring stages per CTA
 #ifndef HODLR_CTAS
 #define HODLR_CTAS 2
 #endif
 constexpr int kCtasPerSm = HODLR_CTAS;  // independent pipelines per SM
-constexpr int kStage = HODLR_KSTAGE;    // bytes per stage (2 x 48.75 KB: 2 CTAs/SM; measured 3-4% faster than 3 x 32.5 KB on cfg2)
+constexpr int kStage = HODLR_KSTAGE;    // bytes per stage (= 512 B of x + a 64 x 64 fp64 D block; 2 x 48.75 KB measured
+                                        // level on cfg2, 7-9% slower on cfg5 fp32 working)
 constexpr int kConsumers = 8;           // consumer warps (= column subsets of B/C pieces)
 constexpr int kThreads = 32 * (kConsumers + 1);  // + producer warp
 constexpr int kFifo = 8;                // BC items whose U piece waits for the coefficients
