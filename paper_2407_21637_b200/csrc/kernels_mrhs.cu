@@ -1041,22 +1041,14 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
         for (int gi = 0; gi < nst; ++gi) {
             tma::mbar_wait(&full[slot], ph);
             const uint8_t* base = ring + (size_t)slot * stage_bytes;
-            for (int kk = 0; kk < G; ++kk) {
+            // this warp's k-steps of the stage: kb = gi * G + kk with kb = kp (mod KS)
+            const int kk0 = ((kp - gi * G) % KS + KS) % KS;
+            for (int kk = ntw > 0 ? kk0 : G; kk < G; kk += KS) {
                 const int kb = gi * G + kk;
-                const bool mine = KS == 1 || (kb & (KS - 1)) == kp;
                 W tmp[MAXTW][Pol::AR * 4];
 #pragma unroll
                 for (int i = 0; i < MAXTW; ++i)
-                    if (i < ntw && mine) frag_load<W, Pol::AR * 4>(tfmt[i], base + kk * v.arow + toff[i], lane, tmp[i]);
-                if (kk == G - 1) {  // stage fully read
-                    __syncwarp();
-                    if (lane == 0) tma::mbar_arrive(&empty[slot]);
-                    if (++slot == ns) {
-                        slot = 0;
-                        ph ^= 1u;
-                    }
-                }
-                if (!mine || ntw == 0) continue;
+                    if (i < ntw) frag_load<W, Pol::AR * 4>(tfmt[i], base + kk * v.arow + toff[i], lane, tmp[i]);
                 typename Pol::BF bf[NCT];
 #pragma unroll
                 for (int nt = 0; nt < NCT; ++nt) {
@@ -1076,6 +1068,13 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
                         Pol::prep_a(af[0], av);
                         Pol::template mma16_tile<1, NCT>(acc[i], af, bf);
                     }
+            }
+            // stage read (the A fragments are in registers): release it
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&empty[slot]);
+            if (++slot == ns) {
+                slot = 0;
+                ph ^= 1u;
             }
         }
         __syncwarp();
