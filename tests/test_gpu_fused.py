@@ -202,3 +202,23 @@ def test_fused_leaf_vs_working_precision_stress(cuda, leaf_working, call_working
     for _ in range(150):
         again = op.matvec(xd, working=w).double().cpu().numpy()
         assert np.array_equal(first, again)
+
+
+@pytest.mark.parametrize("working", ["fp64", "fp32"])
+@pytest.mark.parametrize("s", [1, 3])
+def test_host_call_pinned_matches_pageable(cuda, working, s):
+    """hodlr_matvec_host with a page-locked b (written by the kernels through the
+    mapped address) equals the staged pageable path and the oracle."""
+    torch = cuda
+    fmts = ["fp32", "bf16", "q52"] if working == "fp64" else ["bf16", "fp16", "fp32"]
+    H = random_hodlr(2048, 3, fmts, [12, 9, 5], working, seed=7)
+    op = make_op(H)
+    X = np.random.default_rng(3).standard_normal((H.n, s))
+    xh = torch.from_numpy(X.copy()).pin_memory()
+    bh = torch.full_like(xh, float("nan")).pin_memory()
+    op.matvec_host_ptr(xh.data_ptr(), bh.data_ptr(), s)
+    b_pinned = bh.numpy().copy()
+    b_pageable = op.matvec_host(X if s > 1 else X[:, 0]).reshape(H.n, s)
+    assert np.array_equal(b_pinned, b_pageable)
+    ref = np.stack([matvec_oracle(H, X[:, j]) for j in range(s)], axis=1)
+    assert rel(b_pinned, ref) <= (1e-12 if working == "fp64" else 1e-5)

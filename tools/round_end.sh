@@ -17,7 +17,7 @@ done
 timeout 600 python bench.py --sharded --steps 200 --warmup 5 --no-cpu-baseline > $O/bench_sharded1_cfg2.json 2> $O/bench_sharded1.err
 CMD="python bench.py --steps 20 --warmup 3 --no-cpu-baseline"
 $CMD > $O/ncu_plain_cfg2.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $O/launches_cfg2.csv $CMD > $O/ncu_launch_cfg2.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_stream|k_gen|k_ext|k_round|k_widen" -c 60 --csv --log-file $O/launches_cfg2.csv $CMD > $O/ncu_launch_cfg2.log 2>&1
 for c in 3 4; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_tc_|k_mr|k_stream|k_gen|k_ext" -c 40 --csv \
     --log-file $O/launches_cfg$c.csv python tools/time_configs.py $c > $O/ncu_launch_cfg$c.log 2>&1
