@@ -717,7 +717,7 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
     double* b_map = zc ? (double*)mapped(b_host) : nullptr;
     if (working == HODLR_FMT_FP64) {
         CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
-        if (!(h->sv_ok && s == 1)) b_map = nullptr;  // multi-pass writers: stage in HBM
+        if (!(h->sv_ok && s == 1) || ((uintptr_t)b_map & 15)) b_map = nullptr;  // multi-pass writers / unaligned: stage in HBM
         r = run_local<double>(h, xd, s, b_map ? b_map : bd, s, s, ws, st);
         if (r != HODLR_OK) return r;
     } else {
