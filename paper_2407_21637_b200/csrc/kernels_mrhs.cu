@@ -932,10 +932,12 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
     uint64_t* empty = full + kRingMax;
     uint64_t* xfull = empty + kRingMax;                      // [2]
     uint64_t* xempty = xfull + 2;
+    uint64_t* rawfull = xempty + 2;                          // [1]
     const int stage_bytes = G * v.arow;
     uint8_t* ring = smem_raw + 256;
     W* xsb = reinterpret_cast<W*>(ring + (size_t)ns * stage_bytes);  // [2][256 x ncol]
     W* accs = xsb + 2 * kChunk * ncol;                              // [task][NCT][32][CR]
+    W* xraw = accs + (size_t)v.ntasks * ma2_ks(v.ntasks) * NCT * 32 * Pol::CR;  // [256 x ncol] row-major
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t q0 = (int64_t)blockIdx.y * ncol;
     const int c_beg = (int)((int64_t)blockIdx.x * p.nchunks / gridDim.x);
@@ -951,6 +953,7 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
             tma::mbar_init(&xfull[i], 32 * kAStagers);
             tma::mbar_init(&xempty[i], kAWarps);
         }
+        tma::mbar_init(rawfull, 1);
         tma::fence_mbar_init();
     }
     __syncthreads();
@@ -979,6 +982,50 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
     if (warp > kAWarps) {
         // ---------------- stagers
         const int sl = threadIdx.x - (kAWarps + 1) * 32;
+        // Contiguous X chunks (all columns of a row-major X with ldx = ncol): one
+        // bulk copy of the chunk into a raw row-major buffer, then a shared-memory
+        // permutation into fragment order (destination-ordered: conflict-free
+        // stores), instead of ncol x 256 element cp.async requests through L1/L2.
+        const bool raw_ok = q0 == 0 && ldx == ncol && s >= ncol && (((uintptr_t)x) & 15) == 0;
+        if (raw_ok) {
+            auto issue = [&](int ci) {
+                if (sl == 0) {
+                    const ChunkDesc ch = p.chunks[ci];
+                    const unsigned bytes = (unsigned)(ch.nrows * ncol * sizeof(W));
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // raw reads done (barrier) before the refill
+                    tma::mbar_arrive_tx(rawfull, bytes);
+                    tma::bulk_g2s_plain(xraw, x + ch.row0 * ldx, bytes, rawfull);
+                }
+            };
+            if (c_beg < c_end) issue(c_beg);
+            for (int ci = c_beg; ci < c_end; ++ci) {
+                const int k = ci - c_beg, buf = k & 1, use = k >> 1;
+                if (use > 0) tma::mbar_wait(&xempty[buf], (unsigned)((use - 1) & 1));
+                tma::mbar_wait(rawfull, (unsigned)(k & 1));
+                const int nrows = p.chunks[ci].nrows;
+                W* xs = xsb + buf * kChunk * ncol;
+                for (int d = sl; d < kChunk * ncol; d += 32 * kAStagers) {
+                    // inverse of xfrag: element d of fragment order -> (r, q)
+                    const int blk = d >> 7, o = d & 127;
+                    int ln, e;
+                    if constexpr (sizeof(W) == 8) {
+                        ln = (o & 63) >> 1;
+                        e = ((o >> 6) << 1) | (o & 1);
+                    } else {
+                        ln = o >> 2;
+                        e = o & 3;
+                    }
+                    const int r = 16 * (blk / NCT) + 4 * (ln & 3) + e;
+                    const int q = 8 * (blk % NCT) + (ln >> 2);
+                    xs[d] = r < nrows ? xraw[r * ncol + q] : W(0);
+                }
+                asm volatile("bar.sync 15, %0;" ::"r"(32 * kAStagers) : "memory");  // raw fully read
+                if (ci + 1 < c_end) issue(ci + 1);
+                asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tma::smem_u32(&xfull[buf]))
+                             : "memory");
+            }
+            return;
+        }
         for (int ci = c_beg; ci < c_end; ++ci) {
             const int k = ci - c_beg, buf = k & 1, use = k >> 1;
             if (use > 0) tma::mbar_wait(&xempty[buf], (unsigned)((use - 1) & 1));
@@ -1490,7 +1537,7 @@ inline int pick_nt(int spad) { return spad >= 32 ? 4 : spad >= 16 ? 2 : 1; }
 template <class Pol>
 size_t ma2_smem(const Mr2View& v, int nct, int slot_bytes, int ns) {
     using W = typename Pol::W;
-    return 256 + (size_t)2 * kChunk * nct * 8 * sizeof(W) + (size_t)v.ntasks * ma2_ks(v.ntasks) * nct * 32 * Pol::CR * sizeof(W) +
+    return 256 + (size_t)3 * kChunk * nct * 8 * sizeof(W) + (size_t)v.ntasks * ma2_ks(v.ntasks) * nct * 32 * Pol::CR * sizeof(W) +
            (size_t)ns * slot_bytes;
 }
 template <class Pol>
