@@ -1181,9 +1181,23 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     int sms_now = 148, dev_now = 0;
     cudaGetDevice(&dev_now);
     cudaDeviceGetAttribute(&sms_now, cudaDevAttrMultiProcessorCount, dev_now);
-    P.a_group = nleaves >= 2 * kCtasPerSm * sms_now ? P.napieces : 1;
-    if (getenv("HODLR_B200_A_GROUP")) P.a_group = atoi(getenv("HODLR_B200_A_GROUP")) > 1 ? P.napieces : 1;
-    for (int i = 0; i < P.napieces; ++i) {
+    // (pairs of pieces when leaves are scarce and one column group: half the
+    // partials for the reduction; cfg2 42.5 -> 41.5 us, profiles/round1_sv_sweep_cfg2.txt)
+    P.a_group = nleaves >= 2 * kCtasPerSm * sms_now ? P.napieces
+                : (P.nag == 1 && P.napieces > 2 && P.napieces % 2 == 0) ? 2 : 1;
+    if (getenv("HODLR_B200_A_GROUP")) {
+        // 1: single pieces; k (one format group, k | napieces): k consecutive row
+        // pieces per item, npc = napieces / k partials per leaf; else whole leaves
+        const int k = atoi(getenv("HODLR_B200_A_GROUP"));
+        P.a_group = k <= 1 ? 1 : (P.nag == 1 && k < P.napieces && P.napieces % k == 0) ? k : P.napieces;
+    }
+    if (P.a_group > 1 && P.a_group < P.napieces) {
+        for (int i = 0; i < P.napieces; ++i) {
+            P.ap[i].chunk = i / P.a_group;
+            P.ap[i].npc = P.napieces / P.a_group;
+            P.ap[i].last_of_group = i % P.a_group == P.a_group - 1;
+        }
+    } else for (int i = 0; i < P.napieces; ++i) {
         if (P.a_group > 1) {
             P.ap[i].chunk = 0;
             P.ap[i].npc = 1;
