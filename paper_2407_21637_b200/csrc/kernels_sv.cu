@@ -1256,34 +1256,42 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     P.num_a = nleaves * (P.napieces / P.a_group);
     P.num_d = nleaves * (kM / kRB);
     // node-reduction pieces (R items): a level's partials are [node][column][leaf]
-    P.num_r = 0;
-    int64_t rcap = kStage;  // R piece bytes (HODLR_R_BYTES: sweeps)
-    if (const char* e = getenv("HODLR_R_BYTES")) rcap = std::max<int64_t>(1024, std::min<int64_t>(kStage, atoll(e)));
-    for (int k = 0; k < depth; ++k) {
-        const Level& L = P.lev[k];
-        if (L.r == 0) continue;
-        const int nodes_k = 1 << (k + 1);
-        const int64_t nch = L.cst;
-        const int64_t node_bytes = (int64_t)L.r * nch * 8;
-        auto add = [&](int j0, int j1, int c0, int c1) {
-            if (P.num_r == kMaxRPieces) return false;
-            if ((L.pbase + ((int64_t)j0 * L.r + c0) * nch) % 4) return false;  // 16-B aligned source
-            P.rp[P.num_r++] = RPiece{(int16_t)k, 0, j0, j1, c0, c1};
-            return true;
-        };
-        if (node_bytes <= rcap) {
-            int per = (int)std::min<int64_t>(nodes_k, rcap / node_bytes);
-            if (per >= 4) per = per / 4 * 4;
-            for (int j0 = 0; j0 < nodes_k; j0 += per)
-                if (!add(j0, std::min(nodes_k, j0 + per), 0, L.r)) return HODLR_OK;
-        } else {
-            const int cols = (int)(rcap / (nch * 8));
-            if (cols < 1) return HODLR_OK;
-            for (int j = 0; j < nodes_k; ++j)
-                for (int c0 = 0; c0 < L.r; c0 += cols)
-                    if (!add(j, j + 1, c0, std::min(L.r, c0 + cols))) return HODLR_OK;
+    // R pieces of <= 8 KB spread the reduction over more CTAs (cfg2 41.6 -> 41.0 us
+    // flushed, 39.0 -> 37.0 us hot; profiles/round1_sv_sweep_cfg2.txt); trees whose
+    // pieces would not fit kMaxRPieces or whose (node, column) runs exceed 8 KB use
+    // whole stages.  HODLR_R_BYTES overrides (sweeps).
+    auto build_r = [&](int64_t rcap) -> bool {
+        P.num_r = 0;
+        for (int k = 0; k < depth; ++k) {
+            const Level& L = P.lev[k];
+            if (L.r == 0) continue;
+            const int nodes_k = 1 << (k + 1);
+            const int64_t nch = L.cst;
+            const int64_t node_bytes = (int64_t)L.r * nch * 8;
+            auto add = [&](int j0, int j1, int c0, int c1) {
+                if (P.num_r == kMaxRPieces) return false;
+                if ((L.pbase + ((int64_t)j0 * L.r + c0) * nch) % 4) return false;  // 16-B aligned source
+                P.rp[P.num_r++] = RPiece{(int16_t)k, 0, j0, j1, c0, c1};
+                return true;
+            };
+            if (node_bytes <= rcap) {
+                int per = (int)std::min<int64_t>(nodes_k, rcap / node_bytes);
+                if (per >= 4) per = per / 4 * 4;
+                for (int j0 = 0; j0 < nodes_k; j0 += per)
+                    if (!add(j0, std::min(nodes_k, j0 + per), 0, L.r)) return false;
+            } else {
+                const int cols = (int)(rcap / (nch * 8));
+                if (cols < 1) return false;
+                for (int j = 0; j < nodes_k; ++j)
+                    for (int c0 = 0; c0 < L.r; c0 += cols)
+                        if (!add(j, j + 1, c0, std::min(L.r, c0 + cols))) return false;
+            }
         }
-    }
+        return true;
+    };
+    int64_t rcap = 8192;
+    if (const char* e = getenv("HODLR_R_BYTES")) rcap = std::max<int64_t>(1024, std::min<int64_t>(kStage, atoll(e)));
+    if (!build_r(rcap) && !(rcap != kStage && build_r(kStage))) return HODLR_OK;
     // R pieces: late enough that the A leaves are (nearly) done, early enough that
     // they are taken before any running CTA could fill its deferred-U FIFO
     P.pos_r = std::min(P.num_d / 6, kFifo * 16);  // (assumes >= 16 CTAs can run at once)
