@@ -63,7 +63,10 @@ constexpr int kNS = HODLR_KNS;          // ring stages per CTA
 constexpr int kCtasPerSm = HODLR_CTAS;  // independent pipelines per SM
 constexpr int kStage = HODLR_KSTAGE;    // bytes per stage (= 512 B of x + a 64 x 64 fp64 D block; 2 x 48.75 KB measured
                                         // level on cfg2, 7-9% slower on cfg5 fp32 working)
-constexpr int kConsumers = 8;           // consumer warps (= column subsets of B/C pieces)
+#ifndef HODLR_CONSUMERS
+#define HODLR_CONSUMERS 8
+#endif
+constexpr int kConsumers = HODLR_CONSUMERS;  // consumer warps (= column subsets of B/C pieces)
 constexpr int kThreads = 32 * (kConsumers + 1);  // + producer warp
 constexpr int kFifo = 8;                // BC items whose U piece waits for the coefficients
 #ifndef HODLR_MAX_R
