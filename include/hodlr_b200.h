@@ -102,8 +102,10 @@ hodlr_status hodlr_workspace_size(const hodlr_handle* h, int64_t s, size_t* byte
 /* b = H x  (Algorithm 3) on `stream`.  x, b: device, row-major n_local x s
  * with leading dimensions ldx, ldb (elements), element type = working format
  * (HODLR_FMT_FP64 -> double, HODLR_FMT_FP32 -> float).  Stream-ordered: no host
- * synchronisation, no allocation.  ws may be NULL (the handle's own workspace is
- * used; then calls on one handle must not overlap) or a caller buffer of
+ * synchronisation, no allocation once warm.  ws may be NULL: the handle keeps
+ * one workspace per CUDA stream (allocated on the first call on that stream and
+ * zeroed with cudaMemsetAsync on it), so calls on different streams may overlap
+ * and calls on one stream are ordered by it; or ws is a caller buffer of
  * hodlr_workspace_size bytes, zero-filled once before its first use and not
  * modified by the caller afterwards (the fused kernel keeps its per-call
  * synchronisation state there); concurrent calls with distinct ws are safe

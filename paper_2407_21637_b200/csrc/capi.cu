@@ -77,7 +77,16 @@ struct hodlr_handle {
     std::vector<std::vector<int>> node_id;
     std::vector<int64_t> factor_rows;  // for unpack: rows of U / V of each desc factor
     int64_t part_count = 0, t_count = 0, ext_count = 0;
-    DeviceBuf arena, tables, ws, e2e;
+    DeviceBuf arena, tables, e2e;
+    // NULL-workspace calls: one zero-initialised workspace per CUDA stream, so
+    // concurrent calls on different streams never share the fused kernel's
+    // synchronisation state (matvec is safe to call concurrently)
+    struct StreamWs {
+        void* stream;
+        DeviceBuf buf;
+    };
+    std::vector<StreamWs> ws;
+    std::mutex ws_mu;
     size_t arena_bytes = 0;
     PlanView view{};
     bool sv_ok = false;  // single-vector fast path usable
@@ -478,7 +487,7 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
             if (const char* r = getenv("HODLR_B200_SHARD_RESERVE_SMS")) reserve = atoi(r);
             reserve = std::max(0, std::min(reserve, sms - 1));
-            h->sv.grid = std::max(1, std::min(h->sv.grid, 2 * (sms - reserve)));
+            sv_set_grid(h->sv, 2 * (sms - reserve));
         }
     }
     *out = h;
@@ -543,20 +552,34 @@ hodlr_status check_working(int working) {
     return fail(HODLR_ERR_INVALID, "unknown working format code");
 }
 
-hodlr_status resolve_ws(hodlr_handle* h, int working, int64_t s, void** ws, size_t ws_bytes) {
+hodlr_status resolve_ws(hodlr_handle* h, int working, int64_t s, void** ws, size_t ws_bytes, void* stream) {
     size_t need = working == HODLR_FMT_FP64 ? ws_bytes_for<double>(h, s) : ws_bytes_for<float>(h, s);
     if (*ws) {
         if (ws_bytes < need) return fail(HODLR_ERR_INVALID, "workspace too small");
         return HODLR_OK;
     }
-    if (h->ws.bytes < need) {
-        cudaError_t e = h->ws.ensure(std::max<size_t>(need, kAlign));
-        if (e == cudaSuccess) e = cudaMemset(h->ws.p, 0, h->ws.bytes);
+    std::lock_guard<std::mutex> lock(h->ws_mu);
+    hodlr_handle::StreamWs* w = nullptr;
+    for (auto& e : h->ws)
+        if (e.stream == stream) w = &e;
+    if (!w) {
+        h->ws.push_back(hodlr_handle::StreamWs{stream, DeviceBuf{}});
+        w = &h->ws.back();
+    }
+    if (w->buf.bytes < need) {
+        // (growing: cudaFree waits for the device, so earlier calls on this
+        // stream are done with the old buffer; the zeroing is ordered on the
+        // caller's stream before the call's kernels)
+        CUDA_TRY(cudaSetDevice(h->device));
+        cudaError_t e = w->buf.ensure(std::max<size_t>(need, kAlign));
+        if (e == cudaSuccess) e = cudaMemsetAsync(w->buf.p, 0, w->buf.bytes, (cudaStream_t)stream);
         if (e != cudaSuccess) return fail(HODLR_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
     }
-    *ws = h->ws.p;
+    *ws = w->buf.p;
     return HODLR_OK;
 }
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 template <typename W>
 hodlr_status run_local(hodlr_handle* h, const W* x, int64_t ldx, W* b, int64_t ldb, int64_t s,
@@ -565,7 +588,7 @@ hodlr_status run_local(hodlr_handle* h, const W* x, int64_t ldx, W* b, int64_t l
     void* extra;
     carve<W>(h, s, ws, &partial, &tbuf, &extra);
     cudaError_t e;
-    if (h->sv_ok && s == 1 && ldx == 1 && ldb == 1 && h->nranks == 1) {
+    if (h->sv_ok && s == 1 && ldx == 1 && ldb == 1 && h->nranks == 1 && aligned16(x) && aligned16(b)) {
         e = sv_matvec<W>(h->view, h->sv, x, b, partial, tbuf, extra, st);
     } else if (h->nranks == 1 && mr_usable(h->mr, sizeof(W) == 8 ? HODLR_FMT_FP64 : HODLR_FMT_FP32)) {
         e = mr_matvec<W>(h->view, h->mr, 0, x, ldx, b, ldb, s, partial, tbuf, st);
@@ -579,6 +602,8 @@ hodlr_status run_local(hodlr_handle* h, const W* x, int64_t ldx, W* b, int64_t l
 
 // the single-vector fused kernel runs a rank's subtree (its own phase A)
 bool shard_sv_local(const hodlr_handle* h, int64_t s, int64_t ldx) { return h->sv_ok && s == 1 && ldx == 1; }
+// (shard_local falls back to the generic kernels for unaligned single vectors:
+// the same choice as run_local)
 
 template <typename W>
 cudaError_t shard_local_impl(hodlr_handle* h, const W* x, int64_t ldx, W* b, int64_t ldb, int64_t s, void* ws,
@@ -586,7 +611,8 @@ cudaError_t shard_local_impl(hodlr_handle* h, const W* x, int64_t ldx, W* b, int
     W *partial, *tbuf;
     void* extra;
     carve<W>(h, s, ws, &partial, &tbuf, &extra);
-    if (h->sv_ok && s == 1 && ldx == 1 && ldb == 1) return sv_matvec<W>(h->view, h->sv, x, b, partial, tbuf, extra, st);
+    if (h->sv_ok && s == 1 && ldx == 1 && ldb == 1 && aligned16(x) && aligned16(b))
+        return sv_matvec<W>(h->view, h->sv, x, b, partial, tbuf, extra, st);
     // multi-RHS kernels over the subtree levels (L+1..l) and the leaves; the
     // external levels are added by shard_end.  With fragment slabs, shard_begin
     // already ran phase A (all levels): only phase B is left.
@@ -626,7 +652,7 @@ hodlr_status hodlr_destroy(hodlr_handle* h) {
     cudaSetDevice(h->device);
     h->arena.release();
     h->tables.release();
-    h->ws.release();
+    for (auto& w : h->ws) w.buf.release();
     h->e2e.release();
     sv_release(h->sv);
     mr_release(h->mr);
@@ -668,7 +694,7 @@ hodlr_status hodlr_matvec(hodlr_handle* h, int32_t working, const void* x, int64
     if (stc != HODLR_OK) return stc;
     if (s < 1 || ldx < s || ldb < s) return fail(HODLR_ERR_INVALID, "need s >= 1, ldx >= s, ldb >= s");
     if (!x || !b) return fail(HODLR_ERR_INVALID, "null x or b");
-    hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes);
+    hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes, stream);
     if (r != HODLR_OK) return r;
     cudaStream_t st = (cudaStream_t)stream;
     if (working == HODLR_FMT_FP64)
@@ -697,7 +723,7 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
     void* xw = base + 2 * xb;
     void* bw = base + 2 * xb + wbytes;
     void* ws = nullptr;
-    hodlr_status r = resolve_ws(h, working, s, &ws, 0);
+    hodlr_status r = resolve_ws(h, working, s, &ws, 0, stream);
     if (r != HODLR_OK) return r;
     // A pinned (page-locked, UVA-mapped) host b is written by the kernels
     // directly where each element is stored once: the widening kernel (fp32
@@ -748,7 +774,7 @@ hodlr_status hodlr_matvec_shard_begin(hodlr_handle* h, int32_t working, const vo
     if (stc != HODLR_OK) return stc;
     if (s < 1 || ldx < s || !x_local) return fail(HODLR_ERR_INVALID, "bad x / s");
     if (h->ext_count > 0 && !send) return fail(HODLR_ERR_INVALID, "null send buffer");
-    hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes);
+    hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes, stream);
     if (r != HODLR_OK) return r;
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
@@ -783,7 +809,7 @@ hodlr_status hodlr_matvec_shard_local(hodlr_handle* h, int32_t working, const vo
     hodlr_status stc = check_working(working);
     if (stc != HODLR_OK) return stc;
     if (s < 1 || ldx < s || ldb < s || !x_local || !b_local) return fail(HODLR_ERR_INVALID, "bad x / b / s");
-    hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes);
+    hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes, stream);
     if (r != HODLR_OK) return r;
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = working == HODLR_FMT_FP64
@@ -801,7 +827,7 @@ hodlr_status hodlr_matvec_shard_end(hodlr_handle* h, int32_t working, const void
     if (stc != HODLR_OK) return stc;
     if (s < 1 || ldx < s || ldb < s || !x_local || !b_local) return fail(HODLR_ERR_INVALID, "bad x / b / s");
     if (h->ext_count > 0 && !recv) return fail(HODLR_ERR_INVALID, "null recv buffer");
-    hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes);
+    hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes, stream);
     if (r != HODLR_OK) return r;
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;

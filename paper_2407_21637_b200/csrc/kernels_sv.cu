@@ -16,19 +16,24 @@
 // all pieces of a work item; warps combine once per item through shared memory.
 //
 // Schedule (one CTA per pipeline, kCtasPerSm per SM; no co-residency needed):
-//   producer warp  pulls work and streams it with cp.async.bulk (1-D TMA,
-//                  complete_tx on the stage's "full" mbarrier) into a ring of
-//                  kNS stages;
-//   consumer warps compute from shared memory and release stages ("empty");
-//   reducer warps  count finished leaves into their l ancestor nodes; the last
-//                  leaf of a node reduces the node's partials in leaf order
-//                  (deterministic) into t (Alg. 3's V^T x) and publishes it.
-//   Phase A  (static round-robin over CTAs): leaf -> partial V'^T x per column.
-//   Phase B  (atomic queue): (leaf, 64-row block) -> y = D x, written to b.
-//   Phase C  (same queue, after all B items): (leaf, 64-row block) ->
-//            b = U t + y, with t (all levels) and y bulk-copied next to U.
-// By the time phase C starts every coefficient exists, so the grid-wide
-// dependency of the level-1 inner product never idles the memory pipe.
+//   producer warp  pulls work from ONE atomic queue (fetched two ahead) and
+//                  streams it with cp.async.bulk (1-D TMA, complete_tx on the
+//                  stage's "full" mbarrier) into a ring of kNS stages;
+//   consumer warps compute from shared memory and release stages ("empty").
+// Queue = [A items][BC items, with the R pieces inserted at position pos_r]:
+//   A  (leaf, row pair) -> partial V'^T x per column of every level, stored to
+//      the partial buffer; each CTA publishes its A completions once
+//      (fence + counter) after its last A item;
+//   R  (level, node range) -> fixed-order sum of the nodes' partials (leaf
+//      order: deterministic) into the coefficients t, published per piece;
+//   BC (leaf, 64-row block) -> y = D x kept in a CTA-local slot; its U piece
+//      (b = U t + y over every level, t bulk-copied next to U) is deferred in a
+//      kFifo-deep FIFO until every R piece is published, then b is written
+//      once (disjoint rows, no atomics).
+// Every cross-CTA wait targets work EARLIER in the queue (R waits on all A
+// items, U waits on all R pieces), so progress never assumes co-residency;
+// pos_r is bounded by grid * (kFifo - 2) so the R pieces are always taken
+// before running CTAs could fill their FIFOs (sv_prepare / sv_set_grid).
 // Per-call state (queue, counters, epoch) lives in the zero-initialised
 // workspace; the last CTA resets it and bumps the epoch.
 #include <cuda_runtime.h>
@@ -1393,9 +1398,19 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     sv.extra_ws = sv_sync_bytes(P.nleaves) + (size_t)(pb + tb) * 8;  // (leaf counters unused now)
     sv.part_count = pb;
     sv.leaf_fmt = lf;
+    // every CTA parks at most kFifo - 2 deferred U pieces before it must see
+    // the R pieces: with fewer CTAs than pos_r / (kFifo - 2) the R pieces could
+    // sit behind full FIFOs forever, so pos_r follows the final grid
+    P.pos_r = std::min(P.pos_r, sv.grid * (kFifo - 2));
     sv.params = new SvParams(P);
     *ok = true;
     return HODLR_OK;
+}
+
+void sv_set_grid(SvPlan& sv, int grid) {
+    sv.grid = std::max(1, std::min(sv.grid, grid));
+    SvParams& P = *reinterpret_cast<SvParams*>(sv.params);
+    P.pos_r = std::min(P.pos_r, sv.grid * (kFifo - 2));
 }
 
 void sv_release(SvPlan& sv) {

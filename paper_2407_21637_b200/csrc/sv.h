@@ -41,6 +41,9 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok);
 void sv_release(SvPlan& sv);
 size_t sv_extra_ws(const SvPlan& sv, int64_t s);
 int sv_launches(const SvPlan& sv);
+// shrink the persistent grid (e.g. to leave SMs to a concurrent all-gather);
+// keeps the R-piece queue position within what that grid can reach
+void sv_set_grid(SvPlan& sv, int grid);
 template <typename W>
 cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* partial, W* tbuf,
                       void* extra, cudaStream_t st);

@@ -197,6 +197,28 @@ class HodlrOperator:
                    "hodlr_matvec_host")
 
     # ---------------------------------------------------------------- sharded
+    def as_working(self, x, working=None):
+        """x as a CUDA tensor of the working dtype on this operator's device
+        (fp64 -> fp32 is one RNE rounding); raises on a host or foreign-device tensor."""
+        torch = _torch()
+        code = _working_code(self, working)
+        dt = torch.float64 if code == 4 else torch.float32
+        if not (isinstance(x, torch.Tensor) and x.is_cuda):
+            raise TypeError("expected a CUDA tensor")
+        if x.device.index != self.device:
+            raise ValueError(f"tensor on cuda:{x.device.index}, operator on cuda:{self.device}")
+        return x if x.dtype == dt else x.to(dt)
+
+    def _check_shard_io(self, code, *tensors):
+        torch = _torch()
+        dt = torch.float64 if code == 4 else torch.float32
+        for t in tensors:
+            if t is None or t.numel() == 0:
+                continue
+            if not t.is_cuda or t.device.index != self.device or t.dtype != dt:
+                raise ValueError(f"shard buffers must be {dt} tensors on cuda:{self.device} "
+                                 f"(got {t.dtype} on {t.device})")
+
     def exchange_count(self, s: int = 1) -> int:
         c = _lib.c_i64()
         _lib.check(_lib.lib().hodlr_shard_exchange_count(self._h, s, ctypes.byref(c)))
@@ -205,6 +227,7 @@ class HodlrOperator:
     def shard_begin(self, x, send, working=None, stream=None):
         torch = _torch()
         code = _working_code(self, working)
+        self._check_shard_io(code, x, send)
         st = stream if stream is not None else torch.cuda.current_stream(x.device)
         _lib.check(_lib.lib().hodlr_matvec_shard_begin(
             self._h, code, x.data_ptr(), x.stride(0), x.shape[1],
@@ -214,6 +237,7 @@ class HodlrOperator:
     def shard_local(self, x, out, working=None, stream=None):
         torch = _torch()
         code = _working_code(self, working)
+        self._check_shard_io(code, x, out)
         st = stream if stream is not None else torch.cuda.current_stream(x.device)
         _lib.check(_lib.lib().hodlr_matvec_shard_local(
             self._h, code, x.data_ptr(), x.stride(0), out.data_ptr(), out.stride(0), x.shape[1],
@@ -222,6 +246,7 @@ class HodlrOperator:
     def shard_end(self, x, recv, out, working=None, stream=None):
         torch = _torch()
         code = _working_code(self, working)
+        self._check_shard_io(code, x, recv, out)
         st = stream if stream is not None else torch.cuda.current_stream(x.device)
         _lib.check(_lib.lib().hodlr_matvec_shard_end(
             self._h, code, x.data_ptr(), x.stride(0),

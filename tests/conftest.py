@@ -14,17 +14,6 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200); run with -m gpu")
-    config.addinivalue_line("markers", "slow: long-running")
-
-
-def pytest_collection_modifyitems(config, items):
-    """Full-size BASELINE builds (``slow``) run only with HODLR_SLOW=1."""
-    if os.environ.get("HODLR_SLOW") == "1":
-        return
-    skip = pytest.mark.skip(reason="full-size config: set HODLR_SLOW=1")
-    for it in items:
-        if "slow" in it.keywords:
-            it.add_marker(skip)
 
 
 def golden_cases():

@@ -42,6 +42,11 @@ class EmulatedShard:
         a, _ = self.H.tree.ranges[k][j]
         return j, self.row0 - a
 
+    def as_working(self, X):
+        if not isinstance(X, torch.Tensor) or X.is_cuda:
+            raise TypeError("the CPU emulator takes CPU tensors")
+        return X.to(torch.float64)
+
     def shard_begin(self, X, send):
         x = X.numpy()
         s = x.shape[1]
