@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HODLR_B200_ABI_VERSION 2
+#define HODLR_B200_ABI_VERSION 3
 
 typedef enum {
     HODLR_OK = 0,
@@ -61,7 +61,8 @@ typedef struct {
     int32_t fmt;            /* hodlr_format of the block (PrecisionPlan level format) */
     int32_t rank;
     int64_t rows, cols;     /* U is rows x rank, V is cols x rank */
-    const double* U;        /* U[i,c] = U[i*u_rs + c*u_cs] */
+    const double* U;        /* U[i,c] = U[i*u_rs + c*u_cs]  (void* of the fmt encoding
+                               when hodlr_desc.payload_encoded = 1; same for V, leaves) */
     int64_t u_rs, u_cs;
     const double* V;        /* V[j,c] = V[j*v_rs + c*v_cs] */
     int64_t v_rs, v_cs;
@@ -77,6 +78,13 @@ typedef struct {
     const int64_t* leaf_ld;   /* row stride (elements) of each leaf, >= m_i */
     const hodlr_factor_in* factors; /* 2*(2^depth - 1) entries, offdiag_blocks()
                                       order: level-major, pair-major, [upper, lower] */
+    int32_t payload_encoded;  /* 0: every payload is binary64 (the reference's in-memory
+                                 model and container v1, hodlr.py:297-363).
+                                 1: narrow payloads (container v2): leaf i points at its
+                                 leaf_fmt encoding and each factor's U / V at their `fmt`
+                                 encoding (q52: 1 byte, bf16 / fp16: 2, fp32: 4, fp64: 8
+                                 per element; strides still in elements), so a stored
+                                 matrix reaches the device without a binary64 copy */
 } hodlr_desc;
 
 typedef struct hodlr_handle hodlr_handle;
@@ -109,10 +117,30 @@ hodlr_status hodlr_workspace_size(const hodlr_handle* h, int64_t s, size_t* byte
  * hodlr_workspace_size bytes, zero-filled once before its first use and not
  * modified by the caller afterwards (the fused kernel keeps its per-call
  * synchronisation state there); concurrent calls with distinct ws are safe
- * (SPEC.md:403-404).  Sharded handles: see hodlr_matvec_shard_* below. */
+ * (SPEC.md:403-404).  Sharded handles: see hodlr_matvec_shard_* below.
+ * Narrow working formats (HODLR_FMT_Q52 / BF16 / FP16, the paper's bf16-working
+ * experiment): x and b are binary64 carrying working-format
+ * values (the reference's own representation); x is rounded to `working` on
+ * entry and the call runs the strict-order kernels (see hodlr_matvec_strict);
+ * a caller workspace must then have hodlr_workspace_size_for bytes. */
 hodlr_status hodlr_matvec(hodlr_handle* h, int32_t working, const void* x, int64_t ldx,
                           void* b, int64_t ldb, int64_t s, void* ws, size_t ws_bytes,
                           void* stream);
+
+/* Strict-order matvec: Algorithm 3 evaluated exactly as the reference's
+ * Arithmetic(working) does (arithmetic.py:14-67: every product and partial sum
+ * rounded to `working`, contractions strictly left to right, level-major
+ * accumulation, leaves last) -- bit-identical to the reference arithmetic for
+ * any of the five named working formats (fp64: sequential binary64, which
+ * differs from the reference's BLAS order in the last bits).  x, b: device
+ * binary64, row-major n x s.  One thread per output chain: the fidelity path of
+ * the sweep harness, not the throughput path.  Unsharded handles only. */
+hodlr_status hodlr_matvec_strict(hodlr_handle* h, int32_t working, const double* x, int64_t ldx,
+                                 double* b, int64_t ldb, int64_t s, void* ws, size_t ws_bytes,
+                                 void* stream);
+/* Workspace bytes of a call in `working` (strict != 0: hodlr_matvec_strict). */
+hodlr_status hodlr_workspace_size_for(const hodlr_handle* h, int32_t working, int32_t strict,
+                                      int64_t s, size_t* bytes);
 
 /* End-to-end call with HOST buffers (the reference-facing drop-in): x_host and
  * b_host are binary64, n x s row-major.  Copies x in, rounds it to `working`,
@@ -197,7 +225,8 @@ typedef enum {
     HODLR_PATH_FUSED_SV = 1,
     HODLR_PATH_MRHS = 2,
     HODLR_PATH_MRHS_SLAB = 3,
-    HODLR_PATH_MRHS_TC = 4
+    HODLR_PATH_MRHS_TC = 4,
+    HODLR_PATH_STRICT = 5   /* strict-order kernels (narrow working formats) */
 } hodlr_path;
 hodlr_status hodlr_matvec_path(const hodlr_handle* h, int32_t working, int64_t s, int32_t* path,
                                int32_t* launches);

@@ -17,10 +17,10 @@ c_i32, c_i64, c_sz, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctyp
 c_dp = ctypes.POINTER(ctypes.c_double)
 
 HODLR_OK, HODLR_ERR_INVALID, HODLR_ERR_UNSUPPORTED, HODLR_ERR_CUDA = 0, 1, 2, 3
-PATH_GENERIC, PATH_FUSED_SV, PATH_MRHS, PATH_MRHS_SLAB, PATH_MRHS_TC = 0, 1, 2, 3, 4
+PATH_GENERIC, PATH_FUSED_SV, PATH_MRHS, PATH_MRHS_SLAB, PATH_MRHS_TC, PATH_STRICT = 0, 1, 2, 3, 4, 5
 PATH_NAMES = {PATH_GENERIC: "generic", PATH_FUSED_SV: "fused_sv", PATH_MRHS: "mrhs", PATH_MRHS_SLAB: "mrhs_slab",
-              PATH_MRHS_TC: "mrhs_tc"}
-ABI_VERSION = 2
+              PATH_MRHS_TC: "mrhs_tc", PATH_STRICT: "strict"}
+ABI_VERSION = 3
 
 
 class FactorIn(ctypes.Structure):
@@ -32,7 +32,8 @@ class FactorIn(ctypes.Structure):
 class Desc(ctypes.Structure):
     _fields_ = [("n", c_i64), ("depth", c_i32), ("leaf_fmt", c_i32),
                 ("leaf_bounds", ctypes.POINTER(c_i64)), ("leaves", ctypes.POINTER(c_dp)),
-                ("leaf_ld", ctypes.POINTER(c_i64)), ("factors", ctypes.POINTER(FactorIn))]
+                ("leaf_ld", ctypes.POINTER(c_i64)), ("factors", ctypes.POINTER(FactorIn)),
+                ("payload_encoded", c_i32)]
 
 
 class Shard(ctypes.Structure):
@@ -53,6 +54,8 @@ EXPORTS = {
     "hodlr_destroy": (c_i32, [c_vp]),
     "hodlr_workspace_size": (c_i32, [c_vp, c_i64, ctypes.POINTER(c_sz)]),
     "hodlr_matvec": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_sz, c_vp]),
+    "hodlr_matvec_strict": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_sz, c_vp]),
+    "hodlr_workspace_size_for": (c_i32, [c_vp, c_i32, c_i32, c_i64, ctypes.POINTER(c_sz)]),
     "hodlr_matvec_host": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i64, c_vp]),
     "hodlr_shard_exchange_count": (c_i32, [c_vp, c_i64, ctypes.POINTER(c_i64)]),
     "hodlr_matvec_shard_begin": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_i64, c_vp, c_vp, c_sz, c_vp]),

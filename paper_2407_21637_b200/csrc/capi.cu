@@ -135,12 +135,20 @@ struct ColumnSrc {  // a factor restricted to rows [r0, r0+nrows)
     int64_t rs, cs, r0;
 };
 
+// element i of a payload: binary64, or (container v2) the narrow encoding of `enc`
+inline double payload_at(const void* base, int enc, int64_t i) {
+    return enc == HODLR_FMT_FP64 ? ((const double*)base)[i] : dec_any(enc, base, i);
+}
+
 hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_handle** out) {
     if (!d || !out) return fail(HODLR_ERR_INVALID, "null descriptor or output pointer");
     *out = nullptr;
     if (d->depth < 0 || d->depth > 30) return fail(HODLR_ERR_INVALID, "depth out of range");
     if (d->n < 1) return fail(HODLR_ERR_INVALID, "dimension must be positive");
     if (!valid_fmt(d->leaf_fmt)) return fail(HODLR_ERR_UNSUPPORTED, "unsupported leaf format");
+    if (d->payload_encoded != 0 && d->payload_encoded != 1)
+        return fail(HODLR_ERR_INVALID, "payload_encoded must be 0 or 1");
+    const bool enc = d->payload_encoded == 1;
     const int depth = d->depth;
     const int64_t nleaf = int64_t(1) << depth;
     if (nleaf > d->n) return fail(HODLR_ERR_INVALID, "tree too deep for dimension");
@@ -388,7 +396,8 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
                 return cleanup(fail(HODLR_ERR_INVALID, "bad leaf pointer or stride"));
             }
             for (int r = 0; r < l.m; ++r) {
-                for (int c = 0; c < l.m; ++c) w.put(src[(int64_t)r * ld + c]);
+                for (int c = 0; c < l.m; ++c)
+                    w.put(payload_at(src, enc ? d->leaf_fmt : HODLR_FMT_FP64, (int64_t)r * ld + c));
                 for (int c = l.m; c < l.ld; ++c) w.put(0.0);
             }
         }
@@ -406,7 +415,8 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
             if (col.fmt != f) continue;
             int64_t ld = round_up(col.nrows, elems_per_16B(f));
             for (int64_t r = 0; r < col.nrows; ++r)
-                w.put(col.src.base[(col.src.r0 + r) * col.src.rs + (int64_t)col.c * col.src.cs]);
+                w.put(payload_at(col.src.base, enc ? f : HODLR_FMT_FP64,
+                                 (col.src.r0 + r) * col.src.rs + (int64_t)col.c * col.src.cs));
             for (int64_t r = col.nrows; r < ld; ++r) w.put(0.0);
         }
         w.flush();
@@ -514,7 +524,14 @@ size_t ws_bytes_for(const hodlr_handle* h, int64_t s) {
            (size_t)round_up((h->t_count * s) * sizeof(W), kAlign) + ext_ws_bytes<W>(h, s);
 }
 
-int working_bytes(int working) { return working == HODLR_FMT_FP64 ? 8 : working == HODLR_FMT_FP32 ? 4 : 0; }
+// narrow working formats (q52 / bf16 / fp16) run the strict-order kernels
+// (kernels_seq.cu) on binary64 carriers
+bool narrow_working(int working) { return working >= HODLR_FMT_Q52 && working <= HODLR_FMT_FP16; }
+int working_bytes(int working) { return working == HODLR_FMT_FP32 ? 4 : 8; }
+// workspace of a strict-order call: coefficients + the rounded copy of x
+size_t seq_ws_bytes(const hodlr_handle* h, int64_t s) {
+    return (size_t)round_up(h->t_count * s * 8, kAlign) + (size_t)round_up(h->n_local * s * 8, kAlign);
+}
 
 template <typename W>
 void carve(const hodlr_handle* h, int64_t s, void* ws, W** partial, W** tbuf, void** extra) {
@@ -544,16 +561,23 @@ ExtWs<W> carve_ext(const hodlr_handle* h, int64_t s, void* ws) {
     return e;
 }
 
-hodlr_status check_working(int working) {
+hodlr_status check_working(int working, bool allow_narrow = false) {
     if (working == HODLR_FMT_FP64 || working == HODLR_FMT_FP32) return HODLR_OK;
-    if (working >= HODLR_FMT_Q52 && working <= HODLR_FMT_FP16)
+    if (narrow_working(working)) {
+        if (allow_narrow) return HODLR_OK;
         return fail(HODLR_ERR_UNSUPPORTED,
-                    "working precision must be fp64 or fp32 on the B200 path (bf16/fp16/q52 working: not yet)");
+                    "sharded matvec: working precision must be fp64 or fp32 (bf16/fp16/q52 working run unsharded)");
+    }
     return fail(HODLR_ERR_INVALID, "unknown working format code");
 }
 
-hodlr_status resolve_ws(hodlr_handle* h, int working, int64_t s, void** ws, size_t ws_bytes, void* stream) {
-    size_t need = working == HODLR_FMT_FP64 ? ws_bytes_for<double>(h, s) : ws_bytes_for<float>(h, s);
+hodlr_status resolve_ws(hodlr_handle* h, int working, int64_t s, void** ws, size_t ws_bytes, void* stream,
+                        bool strict = false) {
+    size_t need = working == HODLR_FMT_FP32 ? ws_bytes_for<float>(h, s) : ws_bytes_for<double>(h, s);
+    // strict-order calls: the fused kernel's sync header stays untouched at the
+    // front (the workspace may be shared with fast calls on the same stream)
+    if (strict || narrow_working(working))
+        need = (size_t)round_up((int64_t)sv_extra_ws(h->sv, s), kAlign) + seq_ws_bytes(h, s);
     if (*ws) {
         if (ws_bytes < need) return fail(HODLR_ERR_INVALID, "workspace too small");
         return HODLR_OK;
@@ -597,6 +621,24 @@ hodlr_status run_local(hodlr_handle* h, const W* x, int64_t ldx, W* b, int64_t l
         if (e == cudaSuccess) e = gen_end<W>(h->view, x, ldx, tbuf, b, ldb, s, h->max_chunk_rows, st);
     }
     if (e != cudaSuccess) return fail(HODLR_ERR_CUDA, std::string("matvec launch: ") + cudaGetErrorString(e));
+    return HODLR_OK;
+}
+
+// Strict-order path (kernels_seq.cu): x and b are binary64 carriers; x is
+// rounded to `working` into the workspace first.
+hodlr_status run_seq(hodlr_handle* h, int working, const double* x, int64_t ldx, double* b, int64_t ldb, int64_t s,
+                     void* ws, cudaStream_t st) {
+    uint8_t* p = (uint8_t*)ws + round_up((int64_t)sv_extra_ws(h->sv, s), kAlign);
+    double* tbuf = (double*)p;
+    double* xr = (double*)(p + round_up(h->t_count * s * 8, kAlign));
+    cudaError_t e = cudaSuccess;
+    if (working != HODLR_FMT_FP64) {
+        e = seq_round(working, x, xr, h->n_local, s, ldx, s, st);
+        x = xr;
+        ldx = s;
+    }
+    if (e == cudaSuccess) e = seq_matvec(working, h->view, x, ldx, b, ldb, s, tbuf, st);
+    if (e != cudaSuccess) return fail(HODLR_ERR_CUDA, std::string("strict matvec launch: ") + cudaGetErrorString(e));
     return HODLR_OK;
 }
 
@@ -663,9 +705,12 @@ hodlr_status hodlr_destroy(hodlr_handle* h) {
 hodlr_status hodlr_matvec_path(const hodlr_handle* h, int32_t working, int64_t s, int32_t* path,
                                int32_t* launches) {
     if (!h || !path || !launches || s < 1) return fail(HODLR_ERR_INVALID, "bad arguments");
-    hodlr_status st = check_working(working);
+    hodlr_status st = check_working(working, true);
     if (st != HODLR_OK) return st;
-    if (h->sv_ok && s == 1) {
+    if (narrow_working(working)) {
+        *path = HODLR_PATH_STRICT;
+        *launches = 3;
+    } else if (h->sv_ok && s == 1) {
         *path = HODLR_PATH_FUSED_SV;
         *launches = sv_launches(h->sv);
     } else if (mr_usable(h->mr, working)) {
@@ -690,23 +735,49 @@ hodlr_status hodlr_matvec(hodlr_handle* h, int32_t working, const void* x, int64
                           int64_t ldb, int64_t s, void* ws, size_t ws_bytes, void* stream) {
     if (!h) return fail(HODLR_ERR_INVALID, "null handle");
     if (h->nranks != 1) return fail(HODLR_ERR_INVALID, "sharded handle: use hodlr_matvec_shard_begin/end");
-    hodlr_status stc = check_working(working);
+    hodlr_status stc = check_working(working, true);
     if (stc != HODLR_OK) return stc;
     if (s < 1 || ldx < s || ldb < s) return fail(HODLR_ERR_INVALID, "need s >= 1, ldx >= s, ldb >= s");
     if (!x || !b) return fail(HODLR_ERR_INVALID, "null x or b");
     hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes, stream);
     if (r != HODLR_OK) return r;
     cudaStream_t st = (cudaStream_t)stream;
+    if (narrow_working(working)) return run_seq(h, working, (const double*)x, ldx, (double*)b, ldb, s, ws, st);
     if (working == HODLR_FMT_FP64)
         return run_local<double>(h, (const double*)x, ldx, (double*)b, ldb, s, ws, st);
     return run_local<float>(h, (const float*)x, ldx, (float*)b, ldb, s, ws, st);
+}
+
+hodlr_status hodlr_matvec_strict(hodlr_handle* h, int32_t working, const double* x, int64_t ldx, double* b,
+                                 int64_t ldb, int64_t s, void* ws, size_t ws_bytes, void* stream) {
+    if (!h) return fail(HODLR_ERR_INVALID, "null handle");
+    if (h->nranks != 1) return fail(HODLR_ERR_INVALID, "strict-order matvec needs an unsharded handle");
+    hodlr_status stc = check_working(working, true);
+    if (stc != HODLR_OK) return stc;
+    if (s < 1 || ldx < s || ldb < s) return fail(HODLR_ERR_INVALID, "need s >= 1, ldx >= s, ldb >= s");
+    if (!x || !b) return fail(HODLR_ERR_INVALID, "null x or b");
+    hodlr_status r = resolve_ws(h, working, s, &ws, ws_bytes, stream, true);
+    if (r != HODLR_OK) return r;
+    return run_seq(h, working, x, ldx, b, ldb, s, ws, (cudaStream_t)stream);
+}
+
+hodlr_status hodlr_workspace_size_for(const hodlr_handle* h, int32_t working, int32_t strict, int64_t s,
+                                      size_t* bytes) {
+    if (!h || !bytes || s < 1) return fail(HODLR_ERR_INVALID, "bad arguments");
+    hodlr_status stc = check_working(working, true);
+    if (stc != HODLR_OK) return stc;
+    if (strict || narrow_working(working))
+        *bytes = (size_t)round_up((int64_t)sv_extra_ws(h->sv, s), kAlign) + seq_ws_bytes(h, s);
+    else
+        *bytes = working == HODLR_FMT_FP32 ? ws_bytes_for<float>(h, s) : ws_bytes_for<double>(h, s);
+    return HODLR_OK;
 }
 
 hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x_host,
                                double* b_host, int64_t s, void* stream) {
     if (!h) return fail(HODLR_ERR_INVALID, "null handle");
     if (h->nranks != 1) return fail(HODLR_ERR_INVALID, "host-buffer matvec needs an unsharded handle");
-    hodlr_status stc = check_working(working);
+    hodlr_status stc = check_working(working, true);
     if (stc != HODLR_OK) return stc;
     if (s < 1 || !x_host || !b_host) return fail(HODLR_ERR_INVALID, "bad arguments");
     std::lock_guard<std::mutex> lock(h->mu);
@@ -741,7 +812,12 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
     };
     const bool zc = !getenv("HODLR_B200_NO_ZEROCOPY");
     double* b_map = zc ? (double*)mapped(b_host) : nullptr;
-    if (working == HODLR_FMT_FP64) {
+    if (narrow_working(working)) {
+        CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
+        r = run_seq(h, working, xd, s, bd, s, s, ws, st);
+        if (r != HODLR_OK) return r;
+        b_map = nullptr;
+    } else if (working == HODLR_FMT_FP64) {
         CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
         if (!(h->sv_ok && s == 1) || ((uintptr_t)b_map & 15)) b_map = nullptr;  // multi-pass writers / unaligned: stage in HBM
         r = run_local<double>(h, xd, s, b_map ? b_map : bd, s, s, ws, st);

@@ -27,6 +27,13 @@ template <typename W>
 cudaError_t gen_end(const PlanView& p, const W* x, int64_t ldx, const W* tbuf, W* b, int64_t ldb,
                     int64_t s, int max_chunk_rows, cudaStream_t st);
 
+// Strict-order path (kernels_seq.cu): the reference's per-operation rounding in
+// any working format, bit-identical to arithmetic.py; binary64 carriers.
+cudaError_t seq_round(int fmt, const double* src, double* dst, int64_t rows, int64_t s, int64_t ldin, int64_t ldout,
+                      cudaStream_t st);
+cudaError_t seq_matvec(int fmt, const PlanView& p, const double* x, int64_t ldx, double* b, int64_t ldb, int64_t s,
+                       double* tbuf, cudaStream_t st);
+
 // Sharded path, external levels (kernels_shard.cu).
 int ext_v_blocks(int64_t n_local);
 template <typename W>

@@ -8,8 +8,11 @@ Algorithm 3 HODLR_MATVEC):
   package's ``model.HodlrMatrix`` (anything with ``n``, ``depth``,
   ``working_format``, ``offdiag_blocks()`` and ``leaves()``, hodlr.py:95-135);
 * ``x``: length-n real vector (or n x s block of right-hand sides);
-* ``working``: the working precision (default ``H.working_format``); fp64 and
-  fp32 run on the GPU, other formats raise ``NotImplementedError``;
+* ``working``: the working precision (default ``H.working_format``): fp64 and
+  fp32 run the throughput kernels; bf16 / fp16 / q52 (the paper's simulated
+  low working precisions) run the strict-order kernels,
+  bit-identical to the reference's ``Arithmetic(working)``; custom formats
+  raise ``NotImplementedError``;
 * length mismatch -> ``ValueError``; overflow propagates as inf.
 
 The matrix is packed once per ``H`` into the device layout (cached weakly by
@@ -33,6 +36,7 @@ from .formats import FP32, FP64, format_code
 __all__ = ["matvec", "HodlrOperator", "descriptor", "operator_for"]
 
 _WORKING_DTYPE = {4: np.float64, 3: np.float32}
+_NARROW = (0, 1, 2)  # q52, bf16, fp16 working: binary64 carriers, strict-order kernels
 
 
 def _f64(a) -> np.ndarray:
@@ -83,7 +87,49 @@ class _Descriptor:
         self.keep += [bounds, lds, lptrs, farr]
         self.desc = _lib.Desc(n, depth, format_code(H.working_format),
                               bounds.ctypes.data_as(ctypes.POINTER(_lib.c_i64)), lptrs,
-                              lds.ctypes.data_as(ctypes.POINTER(_lib.c_i64)), farr)
+                              lds.ctypes.data_as(ctypes.POINTER(_lib.c_i64)), farr, 0)
+
+
+class _EncodedDescriptor:
+    """``hodlr_desc`` with payload_encoded = 1 over the narrow arrays of a
+    container v2 (``model.EncodedHodlr``): nothing is widened on the host."""
+
+    def __init__(self, E):
+        from .model import ENCODED_DTYPE
+
+        n, depth = int(E.n), int(E.depth)
+        self.keep = []
+        rngs = E.tree.ranges[depth]
+        bounds = np.array([a for a, _ in rngs] + [n], dtype=np.int64)
+        wdt = np.dtype(ENCODED_DTYPE[E.working_format.name])
+        lptrs = (_lib.c_dp * len(rngs))()
+        lds = np.empty(len(rngs), dtype=np.int64)
+        for i, ((a, b), D) in enumerate(zip(rngs, E.leaf_blocks)):
+            if D.dtype != wdt or D.shape != (b - a, b - a):
+                raise ValueError(f"leaf {i}: expected {(b - a, b - a)} {wdt}, got {D.shape} {D.dtype}")
+            D = np.ascontiguousarray(D)
+            self.keep.append(D)
+            lptrs[i] = ctypes.cast(D.ctypes.data, _lib.c_dp)
+            lds[i] = D.shape[1]
+        facs = []
+        for k in range(1, depth + 1):
+            fmt = E.plan.chosen[k - 1]
+            dt = np.dtype(ENCODED_DTYPE[fmt.name])
+            for pair in E.blocks[k - 1]:
+                for U, V in pair:
+                    if U.dtype != dt or V.dtype != dt or U.ndim != 2 or V.ndim != 2 or U.shape[1] != V.shape[1]:
+                        raise ValueError(f"level {k}: bad encoded factor ({U.dtype} {U.shape}, {V.dtype} {V.shape})")
+                    self.keep += [U, V]
+                    it = dt.itemsize
+                    facs.append(_lib.FactorIn(
+                        format_code(fmt), U.shape[1], U.shape[0], V.shape[0],
+                        ctypes.cast(U.ctypes.data, _lib.c_dp), U.strides[0] // it, U.strides[1] // it,
+                        ctypes.cast(V.ctypes.data, _lib.c_dp), V.strides[0] // it, V.strides[1] // it))
+        farr = (_lib.FactorIn * max(len(facs), 1))(*facs)
+        self.keep += [bounds, lds, lptrs, farr]
+        self.desc = _lib.Desc(n, depth, format_code(E.working_format),
+                              bounds.ctypes.data_as(ctypes.POINTER(_lib.c_i64)), lptrs,
+                              lds.ctypes.data_as(ctypes.POINTER(_lib.c_i64)), farr, 1)
 
 
 def descriptor(H) -> _Descriptor:
@@ -97,12 +143,8 @@ def _torch():
 
 
 def _working_code(H, working) -> int:
-    code = format_code(working if working is not None else H.working_format)
-    if code not in _WORKING_DTYPE:
-        raise NotImplementedError(
-            "working precision must be fp64 or fp32 on the B200 path "
-            f"(got {working if working is not None else H.working_format})")
-    return code
+    # (format_code raises NotImplementedError for custom formats)
+    return format_code(working if working is not None else H.working_format)
 
 
 class HodlrOperator:
@@ -118,7 +160,7 @@ class HodlrOperator:
         self.n = int(H.n)
         self.depth = int(H.depth)
         self.rank, self.nranks = int(rank), int(nranks)
-        d = _Descriptor(H)
+        d = _EncodedDescriptor(H) if getattr(H, "encoded", False) else _Descriptor(H)
         h = _lib.c_vp()
         if nranks == 1:
             st = L.hodlr_create(ctypes.byref(d.desc), self.device, ctypes.byref(h))
@@ -137,6 +179,16 @@ class HodlrOperator:
         self.launches_per_matvec = int(info.launches_per_matvec)
         self._finalizer = weakref.finalize(self, L.hodlr_destroy, h)
 
+    @classmethod
+    def from_container(cls, path, device: int | None = None, rank: int = 0, nranks: int = 1):
+        """Device operator straight from a stored matrix (container v1 or v2,
+        hodlr.py:297-363): a v2 file's narrow payloads go to the packer as they
+        are, without a binary64 copy on the host."""
+        from .model import load_encoded, load_hodlr
+
+        E = load_encoded(path)
+        return cls(E if E.encoded else load_hodlr(path), device, rank, nranks)
+
     def path(self, s: int = 1, working=None) -> tuple[str, int]:
         """(kernel path, launches per matvec) for s right-hand sides:
         "fused_sv" (one persistent kernel), "mrhs" (tensor-core multi-RHS
@@ -149,10 +201,11 @@ class HodlrOperator:
     # ---------------------------------------------------------------- device
     def matvec(self, x, working=None, out=None, stream=None):
         """b = H x for a CUDA tensor x ((n,) or (n, s)), returns a CUDA tensor of
-        the working dtype.  Stream-ordered on ``stream`` (default: current)."""
+        the working dtype (float64 carrying working-format values for bf16 /
+        fp16 / q52 working).  Stream-ordered on ``stream`` (default: current)."""
         torch = _torch()
         code = _working_code(self, working)
-        dt = torch.float64 if code == 4 else torch.float32
+        dt = torch.float32 if code == 3 else torch.float64
         if not (isinstance(x, torch.Tensor) and x.is_cuda):
             raise TypeError("HodlrOperator.matvec expects a CUDA tensor; use matvec_host for host arrays")
         vec = x.dim() == 1
@@ -173,6 +226,31 @@ class HodlrOperator:
                 self._h, code, X.data_ptr(), X.stride(0), B.data_ptr(), B.stride(0), s, None, 0,
                 st.cuda_stream), "hodlr_matvec")
         return B[:, 0] if (vec and out is None) else B
+
+    def matvec_strict(self, x, working=None, stream=None):
+        """b = H x with the reference's arithmetic model in ``working``: every
+        product and partial sum rounded, strict left-to-right contractions
+        (arithmetic.py:14-67) -- bit-identical to ``Arithmetic(working)``.
+        x: CUDA float64 tensor; returns float64 carrying working-format values."""
+        torch = _torch()
+        code = _working_code(self, working)
+        if not (isinstance(x, torch.Tensor) and x.is_cuda):
+            raise TypeError("HodlrOperator.matvec_strict expects a CUDA tensor")
+        vec = x.dim() == 1
+        X = x.reshape(-1, 1) if vec else x
+        if X.dim() != 2 or X.shape[0] != self.n_local:
+            raise ValueError(f"length mismatch: x has {x.shape[0]} rows, operator has {self.n_local}")
+        X = X.to(torch.float64)
+        if X.stride(1) != 1:
+            X = X.contiguous()
+        s = X.shape[1]
+        B = torch.empty((self.n_local, s), dtype=torch.float64, device=X.device)
+        st = stream if stream is not None else torch.cuda.current_stream(X.device)
+        with self._lock:
+            _lib.check(_lib.lib().hodlr_matvec_strict(
+                self._h, code, X.data_ptr(), X.stride(0), B.data_ptr(), B.stride(0), s, None, 0,
+                st.cuda_stream), "hodlr_matvec_strict")
+        return B[:, 0] if vec else B
 
     # ---------------------------------------------------------------- host
     def matvec_host(self, x, working=None) -> np.ndarray:
@@ -202,6 +280,8 @@ class HodlrOperator:
         (fp64 -> fp32 is one RNE rounding); raises on a host or foreign-device tensor."""
         torch = _torch()
         code = _working_code(self, working)
+        if code in _NARROW:
+            raise NotImplementedError("sharded matvec: working precision must be fp64 or fp32")
         dt = torch.float64 if code == 4 else torch.float32
         if not (isinstance(x, torch.Tensor) and x.is_cuda):
             raise TypeError("expected a CUDA tensor")

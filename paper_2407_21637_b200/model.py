@@ -9,6 +9,14 @@ yielding ``(k, i, rows_first, rows_second, upper, lower)``) and ``leaves()``
 as a recursive node tree.  ``load_hodlr``/``save_hodlr`` read and write the
 reference's ``.npz`` container v1 (hodlr.py:297-363), so matrices move between
 the two packages bit-exactly.
+
+Container v2 (``save_hodlr(..., narrow=True)``) is the narrow-payload variant
+of the same schema: identical keys and metadata, ``container_version`` 2, and
+every payload stored in its own format's encoding instead of binary64 (q52: one
+byte, bf16 / fp16: two, fp32: four) -- 8x fewer bytes for a q52 level.
+``load_hodlr`` decodes it back to the binary64 object model (exact);
+``load_encoded`` keeps the narrow arrays so the device loader
+(``HodlrOperator.from_container``) hands them to the C ABI as they are.
 """
 
 from __future__ import annotations
@@ -22,10 +30,15 @@ from .formats import FP64, PrecisionFormat, format_spec, parse_format
 
 __all__ = [
     "ClusterTree", "build_tree", "LowRankFactor", "PrecisionPlan", "HodlrMatrix",
-    "storage_bits", "load_hodlr", "save_hodlr", "CONTAINER_VERSION",
+    "storage_bits", "load_hodlr", "save_hodlr", "load_encoded", "EncodedHodlr",
+    "CONTAINER_VERSION", "NARROW_CONTAINER_VERSION",
 ]
 
 CONTAINER_VERSION = 1
+NARROW_CONTAINER_VERSION = 2
+# numpy carrier of each named format's encoding (bf16 / q52 have no numpy type:
+# their bit patterns travel as unsigned integers)
+ENCODED_DTYPE = {"q52": np.uint8, "bf16": np.uint16, "fp16": np.float16, "fp32": np.float32, "fp64": np.float64}
 
 
 @dataclass(frozen=True)
@@ -137,39 +150,111 @@ def storage_bits(H) -> int:
     return total
 
 
-def save_hodlr(H, path) -> None:
-    """Container v1 writer (same schema as hodlr.py:297-324)."""
+def _encode(a: np.ndarray, fmt) -> np.ndarray:
+    """binary64 values representable in fmt -> the format's encoding, same
+    shape and memory order (K0's host build: exact for representable values)."""
+    from . import _lib
+    from .formats import format_code
+
+    code = format_code(fmt)
+    a = np.asarray(a, dtype=np.float64)
+    order = "F" if (a.ndim == 2 and a.flags.f_contiguous and not a.flags.c_contiguous) else "C"
+    flat = np.ascontiguousarray(a.ravel(order=order))
+    out = np.empty(flat.size, dtype=ENCODED_DTYPE[fmt.name])
+    if flat.size:
+        _lib.check(_lib.lib().hodlr_quantize_host(code, flat.ctypes.data, out.ctypes.data, flat.size))
+    return out.reshape(a.shape, order=order)
+
+
+def _decode(a: np.ndarray, fmt) -> np.ndarray:
+    """Inverse of _encode: exact widening to binary64, memory order kept."""
+    from . import _lib
+    from .formats import format_code
+
+    code = format_code(fmt)
+    want = np.dtype(ENCODED_DTYPE[fmt.name])
+    if a.dtype != want:
+        raise ValueError(f"payload dtype {a.dtype} is not the {fmt.name} encoding ({want})")
+    order = "F" if (a.ndim == 2 and a.flags.f_contiguous and not a.flags.c_contiguous) else "C"
+    flat = np.ascontiguousarray(a.ravel(order=order))
+    out = np.empty(flat.size, dtype=np.float64)
+    if flat.size:
+        _lib.check(_lib.lib().hodlr_dequantize_host(code, flat.ctypes.data, out.ctypes.data, flat.size))
+    return out.reshape(a.shape, order=order)
+
+
+def save_hodlr(H, path, narrow: bool = False) -> None:
+    """Container writer: v1 (the schema of hodlr.py:297-324, binary64 payloads)
+    or, with ``narrow=True``, v2 (same keys, payloads in their formats' encodings)."""
     meta = {
-        "container_version": CONTAINER_VERSION, "n": H.n, "depth": H.depth, "eps": H.eps,
+        "container_version": NARROW_CONTAINER_VERSION if narrow else CONTAINER_VERSION,
+        "n": H.n, "depth": H.depth, "eps": H.eps,
         "working": format_spec(H.working_format),
         "level_formats": [format_spec(f) for f in H.plan.chosen],
         "xi": H.plan.xi, "thresholds": H.plan.thresholds, "fallback": H.plan.fallback,
     }
-    arrays = {f"leaf{i}": blk for i, _, blk in H.leaves()}
+    enc = (lambda a, f: _encode(a, f)) if narrow else (lambda a, f: a)
+    arrays = {f"leaf{i}": enc(blk, H.working_format) for i, _, blk in H.leaves()}
     for k, i, _, _, up, lo in H.offdiag_blocks():
         for tag, f in (("upper", up), ("lower", lo)):
-            arrays[f"lvl{k}_pair{i}_{tag}_U"] = f.U
-            arrays[f"lvl{k}_pair{i}_{tag}_V"] = f.V
+            arrays[f"lvl{k}_pair{i}_{tag}_U"] = enc(f.U, f.fmt)
+            arrays[f"lvl{k}_pair{i}_{tag}_V"] = enc(f.V, f.fmt)
     np.savez(path, __meta__=json.dumps(meta), **arrays)
 
 
-def load_hodlr(path) -> HodlrMatrix:
-    """Container v1 reader (schema of hodlr.py:297-363) into the flat model."""
+@dataclass(eq=False)
+class EncodedHodlr:
+    """A stored matrix with its payloads still in their narrow encodings
+    (container v2) or binary64 (v1): what the device loader consumes."""
+
+    tree: ClusterTree
+    leaf_blocks: list            # encoded arrays, working format
+    blocks: list                 # blocks[k-1][i] = ((U, V), (U, V)) encoded arrays, level format
+    eps: float
+    plan: PrecisionPlan
+    working_format: PrecisionFormat
+    encoded: bool
+
+    n = property(lambda self: self.tree.n)
+    depth = property(lambda self: self.tree.depth)
+
+    def payload_bytes(self) -> int:
+        return sum(a.nbytes for a in self.leaf_blocks) + sum(
+            a.nbytes for lvl in self.blocks for pair in lvl for fac in pair for a in fac)
+
+
+def _read(path):
     with np.load(path, allow_pickle=False) as z:
         meta = json.loads(str(z["__meta__"][()]))
-        if meta.get("container_version") != CONTAINER_VERSION:
-            raise ValueError(f"unsupported container version {meta.get('container_version')!r}")
+        ver = meta.get("container_version")
+        if ver not in (CONTAINER_VERSION, NARROW_CONTAINER_VERSION):
+            raise ValueError(f"unsupported container version {ver!r}")
         tree = build_tree(int(meta["n"]), int(meta["depth"]))
         working = parse_format(meta["working"])
         chosen = [parse_format(s) for s in meta["level_formats"]]
+        if len(chosen) != tree.depth:
+            raise ValueError("level_formats does not match the tree depth")
         plan = PrecisionPlan(chosen, meta.get("xi"), meta.get("thresholds"), meta.get("fallback"))
         leaves = [z[f"leaf{i}"] for i in range(2 ** tree.depth)]
-        blocks = []
-        for k in range(1, tree.depth + 1):
-            fmt = chosen[k - 1]
-            blocks.append([
-                tuple(LowRankFactor(z[f"lvl{k}_pair{i}_{tag}_U"], z[f"lvl{k}_pair{i}_{tag}_V"], fmt)
-                      for tag in ("upper", "lower"))
-                for i in range(2 ** (k - 1))
-            ])
-    return HodlrMatrix(tree, leaves, blocks, float(meta["eps"]), plan, working)
+        blocks = [[tuple((z[f"lvl{k}_pair{i}_{tag}_U"], z[f"lvl{k}_pair{i}_{tag}_V"]) for tag in ("upper", "lower"))
+                   for i in range(2 ** (k - 1))] for k in range(1, tree.depth + 1)]
+    return EncodedHodlr(tree, leaves, blocks, float(meta["eps"]), plan, working, ver == NARROW_CONTAINER_VERSION)
+
+
+def load_encoded(path) -> EncodedHodlr:
+    """Container v1 or v2 with the payloads as stored (no widening)."""
+    return _read(path)
+
+
+def load_hodlr(path) -> HodlrMatrix:
+    """Container reader (v1: schema of hodlr.py:297-363; v2: narrow payloads,
+    widened exactly) into the flat binary64 model."""
+    E = _read(path)
+    dl = (lambda a: _decode(a, E.working_format)) if E.encoded else (lambda a: a)
+    leaves = [dl(a) for a in E.leaf_blocks]
+    blocks = []
+    for k in range(1, E.depth + 1):
+        fmt = E.plan.chosen[k - 1]
+        df = (lambda a, fmt=fmt: _decode(a, fmt)) if E.encoded else (lambda a: a)
+        blocks.append([tuple(LowRankFactor(df(U), df(V), fmt) for U, V in pair) for pair in E.blocks[k - 1]])
+    return HodlrMatrix(E.tree, leaves, blocks, E.eps, E.plan, E.working_format)

@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(L):
     for name in header_functions():
         assert hasattr(L, name), name
         assert name in _lib.EXPORTS, f"{name} not bound in _lib.EXPORTS"
-    assert L.hodlr_abi_version() == 2
+    assert L.hodlr_abi_version() == _lib.ABI_VERSION == 3
 
 
 def host_quantize(L, fmt, x):
@@ -98,7 +98,7 @@ def test_create_rejects_bad_descriptor_without_gpu(L):
     f = _lib.FactorIn(4, 1, 4, 4, U.ctypes.data_as(_lib.c_dp), 1, 1, U.ctypes.data_as(_lib.c_dp), 1, 1)
     fs = (_lib.FactorIn * 2)(f, f)
     d = _lib.Desc(8, 1, 4, bounds.ctypes.data_as(ctypes.POINTER(_lib.c_i64)), lptr,
-                  lds.ctypes.data_as(ctypes.POINTER(_lib.c_i64)), fs)
+                  lds.ctypes.data_as(ctypes.POINTER(_lib.c_i64)), fs, 0)
     h = _lib.c_vp()
     st = L.hodlr_create(ctypes.byref(d), 0, ctypes.byref(h))
     assert st == _lib.HODLR_ERR_INVALID  # factor rows 4 != leaf sizes 3 / 5
@@ -107,9 +107,11 @@ def test_create_rejects_bad_descriptor_without_gpu(L):
 
 
 def test_working_format_gate():
-    from paper_2407_21637_b200 import BF16, linops
+    from paper_2407_21637_b200 import linops
+    from paper_2407_21637_b200.formats import parse_format
     from conftest import load_case
 
     H, _, _ = load_case("g512_fp64")
+    custom = parse_format("custom:t=5,emin=-6,emax=7,bits=8")  # no GPU type: rejected before packing
     with pytest.raises(NotImplementedError):
-        linops.matvec(H, np.zeros(H.n), BF16)
+        linops.matvec(H, np.zeros(H.n), custom)

@@ -151,13 +151,14 @@ def test_working_override_fp32_on_fp64_matrix(cuda):
 
 
 def test_errors(cuda):
-    from paper_2407_21637_b200 import BF16, linops
+    from paper_2407_21637_b200 import linops
+    from paper_2407_21637_b200.formats import parse_format
 
     H, vec, _ = load_case("g512_fp64")
     with pytest.raises(ValueError):
         linops.matvec(H, np.ones(H.n - 1))
     with pytest.raises(NotImplementedError):
-        linops.matvec(H, np.ones(H.n), BF16)
+        linops.matvec(H, np.ones(H.n), parse_format("custom:t=5,emin=-6,emax=7,bits=8"))
 
 
 def test_overflow_propagates_inf(cuda):
