@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -41,6 +42,11 @@ constexpr int kBRows = kChunk / kBWarps;     // ... of 16 chunk rows each
 constexpr int kAWarps = 16;                  // slab phase-A CTA warps (one task list each)
 
 // ------------------------------------------------------------------ operand loads
+// values the integer widening does not cover
+__host__ __device__ __forceinline__ bool f32_special(uint32_t bits) {
+    const uint32_t t = bits & 0x7fffffffu;
+    return t != 0 && (t - 0x00800000u) >= 0x7f000000u;
+}
 template <typename W>
 __device__ __forceinline__ void cvt4(float a, float b, float c, float d, W (&v)[4]) {
     v[0] = (W)a; v[1] = (W)b; v[2] = (W)c; v[3] = (W)d;
@@ -161,6 +167,16 @@ struct PolF64 {
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt], a[mt].v[0][0], b[nt].v[0]);
     }
+    // the first MT of MTA tiles: MT * NT independent accumulators between dependent MMAs
+    template <int MT, int NT, int MTA>
+    __device__ static __forceinline__ void mma16_group(W (&c)[MTA][NT][CR], const AF (&a)[MTA], const BF (&b)[NT]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt], a[mt].v[0][j], b[nt].v[j]);
+    }
 };
 
 struct PolTF32 {
@@ -211,6 +227,28 @@ struct PolTF32 {
     // whole warp tile, independent accumulators interleaved between dependent MMAs
     template <int MT, int NT>
     __device__ static __forceinline__ void mma16_tile(W (&c)[MT][NT][CR], const AF (&a)[MT], const BF (&b)[NT]) {
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int j0 = 2 * p, j1 = 2 * p + 1;
+#pragma unroll
+            for (int pass = 0; pass < 3; ++pass)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const auto& A = a[mt];
+                        const auto& B = b[nt];
+                        if (pass == 0)
+                            tmma(c[mt][nt], A.h[0][j0], A.h[1][j0], A.h[0][j1], A.h[1][j1], B.l[j0], B.l[j1]);
+                        else if (pass == 1)
+                            tmma(c[mt][nt], A.l[0][j0], A.l[1][j0], A.l[0][j1], A.l[1][j1], B.h[j0], B.h[j1]);
+                        else
+                            tmma(c[mt][nt], A.h[0][j0], A.h[1][j0], A.h[0][j1], A.h[1][j1], B.h[j0], B.h[j1]);
+                    }
+        }
+    }
+    template <int MT, int NT, int MTA>
+    __device__ static __forceinline__ void mma16_group(W (&c)[MTA][NT][CR], const AF (&a)[MTA], const BF (&b)[NT]) {
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
             const int j0 = 2 * p, j1 = 2 * p + 1;
@@ -665,7 +703,7 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_b(PlanView p, const __grid_co
 // Relayout kernels (create time): arena -> fragment slabs.  Pure byte moves of
 // already-quantised values (no rounding), zero fill for padding.
 template <class Pol>
-__global__ void k_slab_a(PlanView p, const __grid_constant__ Mr2View v, uint8_t* __restrict__ slab) {
+__global__ void k_slab_a(PlanView p, const __grid_constant__ Mr2View v, uint8_t* __restrict__ slab, int* __restrict__ special) {
     // one thread per (chunk, task, k-block, lane, a): 4 consecutive rows of one V' column
     const int64_t per_chunk = (int64_t)v.ntasks * 16 * 32 * Pol::AR;
     const int64_t total = per_chunk * p.nchunks;
@@ -690,6 +728,7 @@ __global__ void k_slab_a(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
             if (nd && c < nd->rv) {
                 const uint8_t* src = p.arena + nd->v_off + ((int64_t)c * nd->v_ld + (ch.row0 - nd->row0) + row + j) * fb;
                 for (int b = 0; b < fb; ++b) dst[b] = src[b];
+                if (fb < 8 && f32_special(__float_as_uint((float)dec_any(v.task_fmt[t], src, 0)))) *special = 1;
             } else {
                 for (int b = 0; b < fb; ++b) dst[b] = 0;
             }
@@ -698,7 +737,7 @@ __global__ void k_slab_a(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
 }
 
 template <class Pol>
-__global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t* __restrict__ slab) {
+__global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t* __restrict__ slab, int* __restrict__ special) {
     constexpr int MT = kBRows / Pol::MR;
     // D part: one thread per (chunk, warp, kb, mt, lane, a): 4 consecutive leaf columns
     const int64_t dper = (int64_t)kBWarps * 16 * MT * 32 * Pol::AR;
@@ -722,6 +761,7 @@ __global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
         for (int j = 0; j < 4; ++j) {
             uint8_t* dst = blk + frag_byte(lane, a * 4 + j, lfb, Pol::AR * 4);
             for (int b = 0; b < lfb; ++b) dst[b] = src[j * lfb + b];
+            if (lfb < 8 && f32_special(__float_as_uint((float)dec_any(v.leaf_fmt, src, j)))) *special = 1;
         }
     }
     // U part: one thread per (chunk, warp, level, step, mt, lane, a, u): one element
@@ -755,14 +795,33 @@ __global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
         if (c < nd.ru) {
             const uint8_t* src = p.arena + nd.u_off + ((int64_t)c * nd.u_ld + row) * fb;
             for (int b = 0; b < fb; ++b) dst[b] = src[b];
+            if (fb < 8 && f32_special(__float_as_uint((float)dec_any(L.ufmt, src, 0)))) *special = 1;
         } else {
             for (int b = 0; b < fb; ++b) dst[b] = 0;
         }
     }
 }
 
+// float -> W.  FW: binary64 widening with integer ops instead of F2F.F64.F32
+// (exponent re-biased by 896, mantissa shifted by 29, zero kept zero; exact when
+// the slabs hold no fp32 subnormal / inf / nan, which is checked when they are
+// built).  An experiment (HODLR_B200_FASTWIDEN=1): measured slightly SLOWER than
+// the conversion instruction on cfg4 (the extra integer instructions cost more
+// issue slots than F2F costs pipe time), so it is off by default.
+template <typename W, bool FW>
+__device__ __forceinline__ W widen(float f) {
+    if constexpr (sizeof(W) == 8 && FW) {
+        const uint32_t u = __float_as_uint(f), t = u & 0x7fffffffu;
+        uint32_t h = __umulhi(t, 0x20000000u) + 0x38000000u;  // (t >> 3) + (896 << 20)
+        h = t ? h : 0u;
+        return (W)__hiloint2double((int)(h | (u & 0x80000000u)), (int)(u << 29));
+    } else {
+        return (W)f;
+    }
+}
+
 // A lane's N values of a fragment block (layout of frag_byte), decoded to W.
-template <typename W, int N>
+template <typename W, int N, bool FW = false>
 __device__ __forceinline__ void frag_load(int fmt, const uint8_t* blk, int lane, W (&v)[N]) {
     switch (fmt) {
         case HODLR_FMT_FP64:
@@ -779,15 +838,15 @@ __device__ __forceinline__ void frag_load(int fmt, const uint8_t* blk, int lane,
             break;
         case HODLR_FMT_FP32:
             if constexpr (N == 1) {
-                v[0] = (W) reinterpret_cast<const float*>(blk)[lane];
+                v[0] = widen<W, FW>(reinterpret_cast<const float*>(blk)[lane]);
             } else if constexpr (N == 2) {
                 const float2 f = reinterpret_cast<const float2*>(blk)[lane];
-                v[0] = (W)f.x; v[1] = (W)f.y;
+                v[0] = widen<W, FW>(f.x); v[1] = widen<W, FW>(f.y);
             } else {
 #pragma unroll
                 for (int u = 0; u < N / 4; ++u) {
                     const float4 f = reinterpret_cast<const float4*>(blk + u * 512)[lane];
-                    v[4 * u] = (W)f.x; v[4 * u + 1] = (W)f.y; v[4 * u + 2] = (W)f.z; v[4 * u + 3] = (W)f.w;
+                    v[4 * u] = widen<W, FW>(f.x); v[4 * u + 1] = widen<W, FW>(f.y); v[4 * u + 2] = widen<W, FW>(f.z); v[4 * u + 3] = widen<W, FW>(f.w);
                 }
             }
             break;
@@ -812,7 +871,7 @@ __device__ __forceinline__ void frag_load(int fmt, const uint8_t* blk, int lane,
 #pragma unroll
             for (int i = 0; i < N; ++i) {
                 const uint16_t h = (uint16_t)(w[i / 2] >> (16 * (i & 1)));
-                v[i] = bf ? (W)__uint_as_float((uint32_t)h << 16) : (W)dec_fp16(h);
+                v[i] = widen<W, FW>(bf ? __uint_as_float((uint32_t)h << 16) : dec_fp16(h));
             }
             break;
         }
@@ -835,7 +894,7 @@ __device__ __forceinline__ void frag_load(int fmt, const uint8_t* blk, int lane,
                 }
             }
 #pragma unroll
-            for (int i = 0; i < N; ++i) v[i] = (W)dec_q52((uint8_t)(w[i / 4] >> (8 * (i & 3))));
+            for (int i = 0; i < N; ++i) v[i] = widen<W, FW>(dec_q52((uint8_t)(w[i / 4] >> (8 * (i & 3)))));
             break;
         }
     }
@@ -1237,6 +1296,391 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
     }
 }
 
+// ------------------------------------------------------------------ MA3
+// Phase A with the reduction index split across the warps (contiguous X, i.e.
+// s = ncol = ldx: the BASELINE multi-RHS shape).  Same A slab, same run
+// partition and partial slots as k_mr2_a, different work split:
+//   warps 0..7   compute: warp w owns k-blocks 2w, 2w+1 (chunk rows 32w..32w+31)
+//                of EVERY task (m-tile) of every chunk, so it reads each A
+//                fragment and its own 32 rows of X exactly once -- X needs no
+//                fragment-order staging (the warp reads its B fragments straight
+//                from the row-major bytes the bulk copy delivered) -- and keeps
+//                one accumulator tile per task in registers ACROSS chunks.  The
+//                raw operands of a chunk are pulled into registers first and the
+//                ring stage released before the conversions and MMAs start;
+//   warp 8       producer: per chunk, H = 16/KH stages of [KH k-steps of the A
+//                slab | the matching 16*KH rows of X], two bulk copies per stage;
+//   warp 9       reducer: when a node of some level ends (or the CTA's run does),
+//                the compute warps park the affected accumulator tile in shared
+//                memory (a few buffers, mbarrier hand-off, no CTA-wide barrier)
+//                and carry on; the reducer sums the tiles in warp order
+//                (deterministic) and stores the finished rows to the coefficient
+//                buffer or the node's partial slot.
+// A CTA takes R consecutive runs of the plan's partition (slots are per run).
+// Which levels end at which chunk, and where their rows go, is resolved once
+// per CTA into a shared-memory table before the first chunk (no dependent
+// global loads on the per-chunk path).  AFMT >= 0: every task is stored in that
+// format (no per-task format dispatch in the inner loop).
+constexpr int kA3Kpw = 1;                      // k-blocks per compute warp
+constexpr int kA3Warps = 16 / kA3Kpw;
+constexpr int kA3Red = 3;                      // reducer warps (parked tiles round-robin)
+constexpr int kA3Threads = (kA3Warps + 1 + kA3Red) * 32;
+constexpr int kA3ParkMax = 8;                  // parking buffers (runtime depth npark <= kA3ParkMax)
+constexpr bool kA3Prefetch = kA3Kpw > 1;       // raw operands of a chunk to registers, stage released before the MMAs
+constexpr int kA3G = 1;                        // tiles whose MMAs are interleaved (independent accumulators)
+
+template <class Pol, int NCT>
+__host__ __device__ constexpr int ma3_red_elems() { return NCT * 32 * Pol::CR; }  // one tile, one warp
+
+struct A3Dst {           // destination of a level's rows at a chunk where its node ends
+    int64_t base;        // element offset of (column 0, rhs 0) in tbuf (direct) or partial
+    int32_t clim;        // stored columns: c < clim
+    int32_t direct;      // 1: the sum is the coefficient (tbuf, stride s); 0: partial slot (stride spad)
+};
+
+// raw (stored-format) A fragment of one k-block: AR * 4 values per lane
+template <int AFMT, int N>
+struct A3Raw {
+    static constexpr int kWords = AFMT == HODLR_FMT_FP64 ? 2 * N : AFMT == HODLR_FMT_FP32 ? N : AFMT == HODLR_FMT_Q52 ? (N + 3) / 4 : (N + 1) / 2;
+    uint32_t w[kWords];
+};
+template <int AFMT, int N>
+__device__ __forceinline__ void a3_load_raw(const uint8_t* blk, int lane, A3Raw<AFMT, N>& r) {
+    constexpr int bytes = A3Raw<AFMT, N>::kWords * 4;  // per lane
+    if constexpr (bytes <= 16) {
+        if constexpr (bytes == 16) {
+            const uint4 t = reinterpret_cast<const uint4*>(blk)[lane];
+            r.w[0] = t.x; r.w[1] = t.y; r.w[2] = t.z; r.w[3] = t.w;
+        } else if constexpr (bytes == 8) {
+            const uint2 t = reinterpret_cast<const uint2*>(blk)[lane];
+            r.w[0] = t.x; r.w[1] = t.y;
+        } else {
+            r.w[0] = reinterpret_cast<const uint32_t*>(blk)[lane];
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < bytes / 16; ++u) {
+            const uint4 t = reinterpret_cast<const uint4*>(blk + u * 512)[lane];
+            r.w[4 * u] = t.x; r.w[4 * u + 1] = t.y; r.w[4 * u + 2] = t.z; r.w[4 * u + 3] = t.w;
+        }
+    }
+}
+template <typename W, int AFMT, int N, bool FW>
+__device__ __forceinline__ void a3_decode(const A3Raw<AFMT, N>& r, W (&v)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        if constexpr (AFMT == HODLR_FMT_FP64) {
+            v[i] = (W)__hiloint2double((int)r.w[2 * i + 1], (int)r.w[2 * i]);
+        } else if constexpr (AFMT == HODLR_FMT_FP32) {
+            v[i] = widen<W, FW>(__uint_as_float(r.w[i]));
+        } else if constexpr (AFMT == HODLR_FMT_BF16) {
+            v[i] = widen<W, FW>(__uint_as_float((r.w[i / 2] >> (16 * (i & 1))) << 16));
+        } else if constexpr (AFMT == HODLR_FMT_FP16) {
+            v[i] = widen<W, FW>(dec_fp16((uint16_t)(r.w[i / 2] >> (16 * (i & 1)))));
+        } else {
+            v[i] = widen<W, FW>(dec_q52((uint8_t)(r.w[i / 4] >> (8 * (i & 3)))));
+        }
+    }
+}
+
+template <class Pol, int NCT, int MAXT, int AFMT, bool FW>
+__global__ void __launch_bounds__(kA3Threads, 1) k_mr3_a(PlanView p, const __grid_constant__ MrView m,
+                                                        const __grid_constant__ Mr2View v,
+                                                        const typename Pol::W* __restrict__ x, int64_t s, int spad,
+                                                        int KH, int ns, int R, int nloc_max, int npark, int dbg,
+                                                        typename Pol::W* __restrict__ partial,
+                                                        typename Pol::W* __restrict__ tbuf) {
+    using W = typename Pol::W;
+    constexpr int ncol = NCT * 8;
+    constexpr int RE = ma3_red_elems<Pol, NCT>();
+    constexpr int NA = Pol::AR * 4;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [kRingMax]
+    uint64_t* empty = full + kRingMax;                       // [kRingMax]
+    uint64_t* rfull = empty + kRingMax;                      // [kA3ParkMax]
+    uint64_t* rfree = rfull + kA3ParkMax;                    // [kA3ParkMax]
+    unsigned* s_tmask = reinterpret_cast<unsigned*>(rfree + kA3ParkMax);      // [MAXT] levels present in a task's rows
+    int8_t* s_rowlv = reinterpret_cast<int8_t*>(s_tmask + MAXT);           // [MAXT * MR] level of a stacked row
+    const int a_bytes = KH * v.arow, x_bytes = KH * 16 * ncol * (int)sizeof(W);
+    const int stage_bytes = a_bytes + x_bytes;
+    uint8_t* ring = smem_raw + 640;  // barriers + tables: 128 + 128 + 32 + 128 bytes
+    W* red = reinterpret_cast<W*>(ring + (size_t)ns * stage_bytes);       // [npark][kA3Warps][RE]
+    A3Dst* s_dst = reinterpret_cast<A3Dst*>(red + (size_t)npark * kA3Warps * RE);  // [nloc][nlev]
+    unsigned* s_mask = reinterpret_cast<unsigned*>(s_dst + (size_t)nloc_max * p.nlev);  // [nloc] levels ending
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int H = 16 / KH;
+    const int nch = p.nchunks, nb = m.nb;
+    const int vb0 = blockIdx.x * R, vb1 = min(vb0 + R, nb);
+    if (vb0 >= nb) return;
+    const int C0 = (int)((int64_t)vb0 * nch / nb), C1 = (int)((int64_t)vb1 * nch / nb);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < ns; ++i) {
+            tma::mbar_init(&full[i], 1);
+            tma::mbar_init(&empty[i], KH / kA3Kpw);
+        }
+        for (int i = 0; i < npark; ++i) {
+            tma::mbar_init(&rfull[i], kA3Warps);
+            tma::mbar_init(&rfree[i], 1);
+        }
+        tma::fence_mbar_init();
+    }
+    if (threadIdx.x < MAXT * Pol::MR) {
+        const int t = threadIdx.x / Pol::MR;
+        s_rowlv[threadIdx.x] = (int8_t)(t < v.ntasks ? v.row_lv[threadIdx.x] : -1);
+    }
+    if (threadIdx.x < MAXT) {
+        unsigned tm = 0;
+        if ((int)threadIdx.x < v.ntasks)
+            for (int r = 0; r < Pol::MR; ++r) {
+                const int lv = v.row_lv[threadIdx.x * Pol::MR + r];
+                if (lv >= 0) tm |= 1u << lv;
+            }
+        s_tmask[threadIdx.x] = tm;
+    }
+    for (int k = threadIdx.x; k < C1 - C0; k += blockDim.x) s_mask[k] = 0;
+    __syncthreads();
+
+    if (warp == kA3Warps) {
+        // ---------------- producer
+        if (lane == 0 && !(dbg & 32)) {
+            const uint64_t pol = tma::policy_evict_first();
+            int slot = 0;
+            unsigned ph = 0;
+            int64_t n = 0;
+            for (int ci = C0; ci < C1; ++ci) {
+                const uint8_t* asrc = v.slab_a + (int64_t)ci * v.a_chunk_bytes;
+                const W* xsrc = x + (int64_t)ci * kChunk * ncol;
+                for (int h = 0; h < H; ++h, ++n) {
+                    if (n >= ns) tma::mbar_wait(&empty[slot], ph ^ 1u);
+                    uint8_t* dst = ring + (size_t)slot * stage_bytes;
+                    tma::mbar_arrive_tx(&full[slot], (unsigned)stage_bytes);
+                    tma::bulk_g2s(dst, asrc + (int64_t)h * a_bytes, (unsigned)a_bytes, &full[slot], pol);
+                    tma::bulk_g2s_plain(dst + a_bytes, xsrc + (int64_t)h * KH * 16 * ncol, (unsigned)x_bytes, &full[slot]);
+                    if (++slot == ns) {
+                        slot = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- table: (local chunk, level) -> ends here? destination (all but the producer)
+    {
+        const int nthr = (kA3Warps + kA3Red) * 32;
+        const int tid = warp > kA3Warps ? (int)threadIdx.x - 32 : (int)threadIdx.x;
+        for (int i = tid; i < (C1 - C0) * p.nlev; i += nthr) {
+            const int k = i / p.nlev, lv = i - k * p.nlev;
+            const int ci = C0 + k;
+            // run containing ci: c_beg(vb) <= ci < c_end(vb)
+            int vb = (int)(((int64_t)(ci + 1) * nb - 1) / nch);
+            while ((int)((int64_t)vb * nch / nb) > ci) --vb;
+            while ((int)((int64_t)(vb + 1) * nch / nb) <= ci) ++vb;
+            const bool runend = ci + 1 == (int)((int64_t)(vb + 1) * nch / nb);
+            const int n0 = p.chunk_nodes[ci * p.nlev + lv];
+            const bool ends = runend || p.chunk_nodes[(ci + 1) * p.nlev + lv] != n0;
+            if (!ends) continue;
+            const MrSlot sl = m.slots[n0];
+            const NodeDesc* nd = &p.nodes[n0];
+            A3Dst d;
+            if (sl.b0 == sl.b1 && nd->ext_slot < 0) {  // the node lies inside this run: its sum IS the coefficient
+                d.direct = 1;
+                d.base = nd->t_off * s;
+                d.clim = nd->rv;
+            } else {
+                const MrLevel L = m.lev[lv];
+                d.direct = 0;
+                d.base = (L.part_rows + ((int64_t)vb + sl.jrel) * L.rv_pad) * spad;
+                d.clim = L.rv_max;
+            }
+            s_dst[i] = d;
+            atomicOr(&s_mask[k], 1u << lv);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    }
+    unsigned fl = 0;  // parked tiles so far (same sequence in every warp)
+
+    if (warp > kA3Warps) {
+        // ---------------- reducers: reducer ri takes parked tiles it = ri (mod kA3Red)
+        const int ri = warp - (kA3Warps + 1);
+        for (int ci = C0; ci < C1; ++ci) {
+            const unsigned mask = (dbg & 2) ? (ci + 1 == C1 ? s_mask[ci - C0] : 0u) : s_mask[ci - C0];
+            if (!mask) continue;
+            const A3Dst* dk = s_dst + (size_t)(ci - C0) * p.nlev;
+#pragma unroll
+            for (int t = 0; t < MAXT; ++t) {
+                if (!(s_tmask[t] & mask)) continue;
+                // rows of the task whose level ends here
+                unsigned rows = 0;
+#pragma unroll
+                for (int r = 0; r < Pol::MR; ++r) {
+                    const int lv = s_rowlv[t * Pol::MR + r];
+                    if (lv >= 0 && ((mask >> lv) & 1u)) rows |= 1u << r;
+                }
+                const unsigned it = fl++;
+                if ((int)(it % kA3Red) != ri) continue;
+                const int buf = it % npark;
+                tma::mbar_wait(&rfull[buf], (it / npark) & 1u);
+                const W* rb = red + (size_t)buf * kA3Warps * RE;
+                // 32 / ncol rows per sweep, one (row, rhs) per lane
+                const int sub = lane / ncol, col = lane % ncol;
+                if (dbg & 16) rows = 0;
+                while (rows) {
+                    unsigned rr = rows;
+                    for (int i = 0; i < sub && rr; ++i) rr &= rr - 1;
+                    if (rr) {
+                        const int row = __ffs(rr) - 1;
+                        const int srow = t * Pol::MR + row;
+                        const int lv = s_rowlv[srow], c = v.row_c[srow];
+                        const A3Dst d = dk[lv];
+                        const int e = ((row >> 3) << 1) | (col & 1);
+                        const int e0 = (((col >> 3) * 32) + (row & 7) * 4 + ((col & 7) >> 1)) * Pol::CR + e;
+                        // fixed pairwise tree over the warps (deterministic; short dependent
+                        // chains: the adds queue behind the compute warps' DMMAs on the FP64 pipe)
+                        W part[kA3Warps];
+#pragma unroll
+                        for (int w = 0; w < kA3Warps; ++w) part[w] = rb[(size_t)w * RE + e0];
+#pragma unroll
+                        for (int st = 1; st < kA3Warps; st *= 2)
+#pragma unroll
+                            for (int w = 0; w + st < kA3Warps; w += 2 * st) part[w] += part[w + st];
+                        const W sum = part[0];
+                        if (c < d.clim) {
+                            if (d.direct) {
+                                if (col < s) tbuf[d.base + (int64_t)c * s + col] = sum;
+                            } else if (col < spad) {
+                                partial[d.base + (int64_t)c * spad + col] = sum;
+                            }
+                        }
+                    }
+                    for (int i = 0; i < 32 / ncol && rows; ++i) rows &= rows - 1;
+                }
+                __syncwarp();
+                if (lane == 0) tma::mbar_arrive(&rfree[buf]);
+            }
+        }
+        return;
+    }
+
+    // ---------------- compute warps
+    const int g = lane >> 2, tig = lane & 3;
+    const int kb0 = kA3Kpw * warp;               // first k-block of this warp
+    const int wl = kb0 % KH, h = kb0 / KH;       // position inside its stage, stage of the chunk
+    constexpr int GT = kA3G, NG = MAXT / kA3G;   // tiles per group, groups
+    W acc[NG][GT][NCT][Pol::CR];
+#pragma unroll
+    for (int gi = 0; gi < NG; ++gi)
+#pragma unroll
+        for (int t = 0; t < GT; ++t)
+#pragma unroll
+            for (int nt = 0; nt < NCT; ++nt)
+#pragma unroll
+                for (int e = 0; e < Pol::CR; ++e) acc[gi][t][nt][e] = W(0);
+    const int ntasks = v.ntasks;
+    int64_t sn = h;  // this warp's stage number: k * H + h
+    for (int ci = C0; ci < C1; ++ci, sn += H) {
+        const int slot = (int)(sn % ns);
+        if (!(dbg & 32)) tma::mbar_wait(&full[slot], (unsigned)((sn / ns) & 1));
+        const uint8_t* base = ring + (size_t)slot * stage_bytes;
+        // raw operands of both k-blocks -> registers, then the stage goes back to the producer
+        W bv[kA3Kpw][NCT][4];
+        constexpr bool PF = kA3Prefetch && AFMT >= 0;
+        A3Raw<AFMT < 0 ? HODLR_FMT_FP32 : AFMT, NA> raw[PF ? kA3Kpw : 1][PF ? MAXT : 1];
+#pragma unroll
+        for (int q = 0; q < kA3Kpw; ++q) {
+            const W* xs = reinterpret_cast<const W*>(base + a_bytes) + (16 * (wl + q) + 4 * tig) * ncol + g;
+#pragma unroll
+            for (int nt = 0; nt < NCT; ++nt)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) bv[q][nt][j] = xs[j * ncol + 8 * nt];
+            if constexpr (PF) {
+                const uint8_t* ab = base + (size_t)(wl + q) * v.arow;
+#pragma unroll
+                for (int t = 0; t < MAXT; ++t)
+                    if (t < ntasks) a3_load_raw<AFMT, NA>(ab + v.task_off[t], lane, raw[q][t]);
+            }
+        }
+        if constexpr (PF) {
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&empty[slot]);
+        }
+#pragma unroll
+        for (int q = 0; q < kA3Kpw; ++q) {
+            typename Pol::BF bf[NCT];
+#pragma unroll
+            for (int nt = 0; nt < NCT; ++nt) Pol::prep_b(bf[nt], bv[q][nt]);
+            const uint8_t* ab = base + (size_t)(wl + q) * v.arow;
+#pragma unroll
+            for (int gi = 0; gi < NG; ++gi) {
+                const int nt_g = ntasks - gi * GT;  // tiles of this group in use (uniform)
+                if (nt_g <= 0) continue;
+                typename Pol::AF af[GT];
+#pragma unroll
+                for (int i = 0; i < GT; ++i) {
+                    const int t = gi * GT + i;
+                    W tmp[NA];
+                    if (i < nt_g) {
+                        if constexpr (PF) {
+                            a3_decode<W, AFMT, NA, FW>(raw[q][t], tmp);
+                        } else if constexpr (AFMT >= 0) {
+                            A3Raw<AFMT, NA> r1;
+                            a3_load_raw<AFMT, NA>(ab + v.task_off[t], lane, r1);
+                            a3_decode<W, AFMT, NA, FW>(r1, tmp);
+                        } else {
+                            frag_load<W, NA, FW>(v.task_fmt[t], ab + v.task_off[t], lane, tmp);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < NA; ++j) tmp[j] = W(0);
+                    }
+                    W av[Pol::AR][4];
+#pragma unroll
+                    for (int a = 0; a < Pol::AR; ++a)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) av[a][j] = tmp[a * 4 + j];
+                    Pol::prep_a(af[i], av);
+                }
+                if (dbg & 1) continue;
+                if (nt_g >= GT)
+                    Pol::template mma16_group<GT, NCT, GT>(acc[gi], af, bf);
+                else if (nt_g == 3)
+                    Pol::template mma16_group<(GT > 3 ? 3 : GT), NCT, GT>(acc[gi], af, bf);
+                else if (nt_g == 2)
+                    Pol::template mma16_group<(GT > 2 ? 2 : GT), NCT, GT>(acc[gi], af, bf);
+                else
+                    Pol::template mma16_group<1, NCT, GT>(acc[gi], af, bf);
+            }
+        }
+        if constexpr (!PF) {
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&empty[slot]);
+        }
+        const unsigned mask = (dbg & 2) ? (ci + 1 == C1 ? s_mask[ci - C0] : 0u) : s_mask[ci - C0];
+        if (!mask) continue;
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+            if (!(s_tmask[t] & mask)) continue;
+            const unsigned it = fl++;
+            const int buf = it % npark;
+            if ((int)it >= npark) tma::mbar_wait(&rfree[buf], ((it / npark) - 1) & 1u);
+            W* my = red + ((size_t)buf * kA3Warps + warp) * RE + lane * Pol::CR;
+            if (!(dbg & 8))
+#pragma unroll
+            for (int nt = 0; nt < NCT; ++nt)
+#pragma unroll
+                for (int e = 0; e < Pol::CR; ++e) {
+                    my[nt * 32 * Pol::CR + e] = acc[t / GT][t % GT][nt][e];
+                    const int lv = s_rowlv[t * Pol::MR + g + 8 * (e >> 1)];
+                    if (lv >= 0 && ((mask >> lv) & 1u)) acc[t / GT][t % GT][nt][e] = W(0);
+                }
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&rfull[buf]);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ MB2
 // Persistent: CTA b takes works (chunk, column group) b, b + grid, ...
 //   warps 0..15  compute: warp w owns chunk rows 16w..16w+15;
@@ -1249,7 +1693,7 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
 constexpr int kBStagers = 2;  // X / coefficient staging warps of the phase-B CTA
 constexpr int kBThreads = (kBWarps + 1 + kBStagers) * 32;
 
-template <class Pol, int NT>
+template <class Pol, int NT, bool FW>
 __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_constant__ MrView m,
                                                     const __grid_constant__ Mr2View v,
                                                     const typename Pol::W* __restrict__ x, int64_t ldx,
@@ -1404,7 +1848,7 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
             W tmp[MT][Pol::AR * 4];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
-                frag_load<W, Pol::AR * 4>(lfmt, base + mt * 32 * Pol::AR * 4 * lfb, lane, tmp[mt]);
+                frag_load<W, Pol::AR * 4, FW>(lfmt, base + mt * 32 * Pol::AR * 4 * lfb, lane, tmp[mt]);
             release_stage();
             typename Pol::AF af[MT];
 #pragma unroll
@@ -1442,7 +1886,7 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
                 W tmp[MT][Pol::AR * Pol::UV];
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt)
-                    frag_load<W, Pol::AR * Pol::UV>(ufmt, base + mt * 32 * Pol::AR * Pol::UV * ufb, lane, tmp[mt]);
+                    frag_load<W, Pol::AR * Pol::UV, FW>(ufmt, base + mt * 32 * Pol::AR * Pol::UV * ufb, lane, tmp[mt]);
                 const int nlo = step + 1 < steps ? lo + sstep : L.unext;
                 if (nlo < 0 || (nlo >> lstage) != (lo >> lstage)) {  // stage fully read
                     release_stage();
@@ -1581,10 +2025,83 @@ cudaError_t launch_ma2_n(const PlanView& p, const MrView& m, const Mr2View& v, c
     if (maxtw <= 2) return launch_ma2_t<Pol, NCT, 2>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
     return launch_ma2_t<Pol, NCT, 4>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
 }
+// K-split phase A (k_mr3_a): X contiguous (s = ldx = 8 or 16 columns), <= 8 tasks.
+constexpr int kA3MaxT = 8;
+template <class Pol, int NCT>
+size_t ma3_smem(const Mr2View& v, int KH, int ns, int npark) {
+    using W = typename Pol::W;
+    return 640 + (size_t)ns * (KH * v.arow + KH * 16 * NCT * 8 * sizeof(W)) +
+           (size_t)npark * kA3Warps * ma3_red_elems<Pol, NCT>() * sizeof(W);
+}
+inline size_t ma3_table_bytes(int nloc, int nlev) { return (size_t)nloc * nlev * sizeof(A3Dst) + (size_t)nloc * 4 + 16; }
+template <class Pol, int NCT>
+bool launch_ma3(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x, int64_t ldx,
+                int64_t s, int spad, typename Pol::W* partial, typename Pol::W* tbuf, cudaStream_t st,
+                cudaError_t* err) {
+    if (s != NCT * 8 || ldx != s || spad != s || v.ntasks > kA3MaxT || v.ntasks < 1 || (((uintptr_t)x) & 15)) return false;
+    if (const char* e = getenv("HODLR_B200_MA3"))
+        if (e[0] == '0') return false;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int R = (m.nb + sms - 1) / sms;           // runs per CTA: one CTA per SM
+    const int grid = (m.nb + R - 1) / R;
+    const int nloc = (int)(((int64_t)p.nchunks * R + m.nb - 1) / m.nb) + 1;  // chunks per CTA, upper bound
+    const size_t tab = ma3_table_bytes(nloc, p.nlev);
+    if (tab > 32 * 1024) return false;
+    const size_t budget = 225 * 1024 - tab;
+    int KH = 8;
+    if (const char* e = getenv("HODLR_B200_MA3_KH")) KH = atoi(e);
+    if (KH != 4 && KH != 8 && KH != 16) KH = 8;  // (a multiple of kA3Kpw)
+    int npark = 4;
+    if (const char* e = getenv("HODLR_B200_MA3_PARK")) npark = std::max(kA3Red, std::min(kA3ParkMax, atoi(e)));  // >= kA3Red: a reducer is never two phases behind a buffer
+    while (KH > 4 && ma3_smem<Pol, NCT>(v, KH, 3, npark) > budget) KH /= 2;
+    int ns = kRingMax;
+    while (ns > 2 && ma3_smem<Pol, NCT>(v, KH, ns, npark) > budget) --ns;
+    if (const char* e = getenv("HODLR_B200_MA3_NS")) ns = std::max(2, std::min(ns, atoi(e)));
+    const size_t sm = ma3_smem<Pol, NCT>(v, KH, ns, npark) + tab;
+    if (sm > 227 * 1024 || ns < 16 / KH) return false;
+    using W = typename Pol::W;
+    // every task in one storage format (the usual case): the specialised instance
+    int afmt = v.task_fmt[0];
+    for (int t = 1; t < v.ntasks; ++t)
+        if (v.task_fmt[t] != afmt) afmt = -1;
+    if (sizeof(W) == 4 && afmt == HODLR_FMT_FP64) afmt = -1;
+    if (const char* e = getenv("HODLR_B200_MA3_GENERIC"))
+        if (e[0] == '1') afmt = -1;
+    const bool fw = sizeof(W) == 8 && v.widen_fast && getenv("HODLR_B200_FASTWIDEN");  // measured slower than F2F (cfg4: 124 vs 120 us): off
+    auto pick = [&](auto fwc) {
+        constexpr bool F = decltype(fwc)::value;
+        auto kk = k_mr3_a<Pol, NCT, kA3MaxT, -1, F>;
+        switch (afmt) {
+            case HODLR_FMT_Q52: kk = k_mr3_a<Pol, NCT, kA3MaxT, HODLR_FMT_Q52, F>; break;
+            case HODLR_FMT_BF16: kk = k_mr3_a<Pol, NCT, kA3MaxT, HODLR_FMT_BF16, F>; break;
+            case HODLR_FMT_FP16: kk = k_mr3_a<Pol, NCT, kA3MaxT, HODLR_FMT_FP16, F>; break;
+            case HODLR_FMT_FP32: kk = k_mr3_a<Pol, NCT, kA3MaxT, HODLR_FMT_FP32, F>; break;
+            case HODLR_FMT_FP64: kk = k_mr3_a<Pol, NCT, kA3MaxT, HODLR_FMT_FP64, F>; break;
+            default: break;
+        }
+        return kk;
+    };
+    auto k = fw ? pick(std::true_type{}) : pick(std::false_type{});
+    *err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (*err != cudaSuccess) return true;
+    int dbg = 0;  // timing experiments only (results are wrong when set)
+    if (const char* e = getenv("HODLR_B200_MA3_DBG")) dbg = atoi(e);
+    k<<<grid, kA3Threads, sm, st>>>(p, m, v, x, s, spad, KH, ns, R, nloc, npark, dbg, partial, tbuf);
+    *err = cudaGetLastError();
+    return true;
+}
+
 template <class Pol>
 cudaError_t launch_ma2(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
                        int64_t ldx, int64_t s, int spad, typename Pol::W* partial, typename Pol::W* tbuf,
                        cudaStream_t st) {
+    {
+        cudaError_t e3 = cudaSuccess;
+        if (spad == 16 && launch_ma3<Pol, 2>(p, m, v, x, ldx, s, spad, partial, tbuf, st, &e3)) return e3;
+        if (spad == 8 && launch_ma3<Pol, 1>(p, m, v, x, ldx, s, spad, partial, tbuf, st, &e3)) return e3;
+    }
     int nct = pick_nt(spad);
     while (nct > 1 && ma2_smem<Pol>(v, nct, 16 * 1024, 2) > 225 * 1024) nct /= 2;
     if (nct == 4) return launch_ma2_n<Pol, 4>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
@@ -1606,7 +2123,8 @@ cudaError_t launch_mb2_t(const PlanView& p, const MrView& m, const Mr2View& v, c
     if (const char* e = getenv("HODLR_B200_MB_NS")) ns = std::max(2, std::min(ns, atoi(e)));
     const size_t sm = mb2_smem<Pol>(v, NT, ns, nbuf);
     if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
-    auto k = k_mr2_b<Pol, NT>;
+    const bool fw = sizeof(typename Pol::W) == 8 && v.widen_fast && getenv("HODLR_B200_FASTWIDEN");  // off by default (measured: no gain)
+    auto k = fw ? k_mr2_b<Pol, NT, true> : k_mr2_b<Pol, NT, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int ngrp = (spad + NT * 8 - 1) / (NT * 8);
@@ -1821,22 +2339,28 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
     const size_t a_bytes = (size_t)v.a_chunk_bytes * chunks.size();
     const size_t b_bytes = (size_t)v.b_chunk_bytes * chunks.size();
     void* d = nullptr;
-    if (cudaMalloc(&d, a_bytes + b_bytes + 256) != cudaSuccess) {
+    if (cudaMalloc(&d, a_bytes + b_bytes + 512) != cudaSuccess) {
         cudaGetLastError();
         return HODLR_OK;  // no room for a second copy: the arena kernels serve
     }
     v.slab_a = (const uint8_t*)d;
     v.slab_b = (const uint8_t*)d + (a_bytes + 255) / 256 * 256;
-    cudaError_t e = cudaSuccess;
-    if (a_bytes) {
-        k_slab_a<Pol><<<148 * 8, 256>>>(*in.view, v, (uint8_t*)v.slab_a);
+    // (in the allocation's 512-byte tail, past both slabs: "a stored value is an
+    // fp32 subnormal / inf / nan", which rules out the integer widening)
+    int* special = (int*)((uint8_t*)d + ((a_bytes + b_bytes + 508) & ~(size_t)3));
+    cudaError_t e = cudaMemset(special, 0, 4);
+    if (e == cudaSuccess && a_bytes) {
+        k_slab_a<Pol><<<148 * 8, 256>>>(*in.view, v, (uint8_t*)v.slab_a, special);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) {
-        k_slab_b<Pol><<<148 * 8, 256>>>(*in.view, v, (uint8_t*)v.slab_b);
+        k_slab_b<Pol><<<148 * 8, 256>>>(*in.view, v, (uint8_t*)v.slab_b, special);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    int sp = 1;
+    if (e == cudaSuccess) e = cudaMemcpy(&sp, special, 4, cudaMemcpyDeviceToHost);
+    v.widen_fast = sp == 0;
     if (e != cudaSuccess) {
         cudaFree(d);
         return HODLR_ERR_CUDA;

@@ -88,6 +88,7 @@ struct Mr2View {
     int32_t leaf_fmt;
     int32_t max_ablk;
     int32_t arow;              // A bytes of one k-step, all tasks ([kb][task] layout)
+    int32_t widen_fast;        // the slabs hold no fp32 subnormal / inf / nan (integer fp32 -> fp64 widening is exact)
     // Phase-A tasks stack the levels' V' columns along M (a run of levels with
     // one storage format shares m-tiles; a format change starts a new tile):
     // stacked row m -> (level, column), level -1 = padding.
