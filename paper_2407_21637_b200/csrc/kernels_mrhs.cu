@@ -764,6 +764,43 @@ __global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
             if (lfb < 8 && f32_special(__float_as_uint((float)dec_any(v.leaf_fmt, src, j)))) *special = 1;
         }
     }
+    if (v.ustack) {
+        // stacked U: one thread per (chunk, warp, k-block, mt, lane, a): 4 consecutive stacked columns
+        const int fb = fmt_bytes(v.ufmt_all);
+        const int64_t uper = (int64_t)kBWarps * v.nku * MT * 32 * Pol::AR;
+        const int64_t utotal = uper * p.nchunks;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < utotal; i += (int64_t)gridDim.x * blockDim.x) {
+            const int chunk = (int)(i / uper);
+            int64_t r = i - (int64_t)chunk * uper;
+            const int a = (int)(r % Pol::AR); r /= Pol::AR;
+            const int lane = (int)(r % 32); r /= 32;
+            const int mt = (int)(r % MT); r /= MT;
+            const int kb = (int)(r % v.nku);
+            const int w = (int)(r / v.nku);
+            const ChunkDesc ch = p.chunks[chunk];
+            uint8_t* blk = slab + (int64_t)chunk * v.b_chunk_bytes + 16LL * kBWarps * v.d_item +
+                           ((int64_t)kb * kBWarps + w) * v.u_item + (int64_t)mt * 32 * Pol::AR * 4 * fb;
+            for (int j = 0; j < 4; ++j) {
+                const int sc = kb * 16 + 4 * (lane & 3) + j;
+                const int lv = v.urow_lv[sc], c = v.urow_c[sc];
+                uint8_t* dst = blk + frag_byte(lane, a * 4 + j, fb, Pol::AR * 4);
+                bool put = false;
+                if (lv >= 0) {
+                    const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
+                    if (c < nd.ru) {
+                        const int row = (ch.row0 - nd.row0) + kBRows * w + mt * Pol::MR + (lane >> 2) + 8 * a;
+                        const uint8_t* src = p.arena + nd.u_off + ((int64_t)c * nd.u_ld + row) * fb;
+                        for (int b = 0; b < fb; ++b) dst[b] = src[b];
+                        if (fb < 8 && f32_special(__float_as_uint((float)dec_any(v.ufmt_all, src, 0)))) *special = 1;
+                        put = true;
+                    }
+                }
+                if (!put)
+                    for (int b = 0; b < fb; ++b) dst[b] = 0;
+            }
+        }
+        return;
+    }
     // U part: one thread per (chunk, warp, level, step, mt, lane, a, u): one element
     int64_t uper = 0;
     for (int lv = v.lev_lo; lv < v.nlev; ++lv) uper += (int64_t)v.lev[lv].steps * MT * 32 * Pol::AR * Pol::UV;
@@ -1716,7 +1753,8 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwork = p.nchunks * ngrp;
     const int64_t dbytes = 16LL << lstage;                           // D region of a chunk
-    const int nstage = 16 + (v.warp_bytes + stage_bytes - 1) / stage_bytes;
+    const int ustage = kBWarps * v.u_item;  // stacked U: one U k-block per stage
+    const int nstage = v.ustack ? 16 + v.nku : 16 + (v.warp_bytes + stage_bytes - 1) / stage_bytes;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < ns; ++i) {
@@ -1747,6 +1785,9 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
                     if (st < 16) {
                         off = (int64_t)st << lstage;
                         bytes = stage_bytes;
+                    } else if (v.ustack) {
+                        off = dbytes + (int64_t)(st - 16) * ustage;
+                        bytes = ustage;
                     } else {
                         off = dbytes + ((int64_t)(st - 16) << lstage);
                         bytes = min((int64_t)stage_bytes, dbytes + v.warp_bytes - off);
@@ -1782,8 +1823,25 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
                     *dst = W(0);
             }
             W* ts = tsb + buf * trows * ncol;
+            if (v.ustack) {
+                // coefficients of the stacked U columns, fragment order (like X)
+                for (int i = sl; i < v.nku * 16 * ncol; i += 32 * kBStagers) {
+                    const int r = i / ncol, q = i - r * ncol;
+                    W* dst = ts + xfrag<W>(r, q, NT);
+                    const int lv = v.urow_lv[r], c = v.urow_c[r];
+                    bool put = false;
+                    if (lv >= 0 && q0 + q < s) {
+                        const NodeDesc* nd = &p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
+                        if (c < nd->ru) {
+                            cp_async(dst, tbuf + (nd->tsrc_off + c) * s + q0 + q, (int)sizeof(W));
+                            put = true;
+                        }
+                    }
+                    if (!put) *dst = W(0);
+                }
+            }
             int base = 0;
-            for (int lv = v.lev_lo; lv < v.nlev; ++lv) {
+            for (int lv = v.ustack ? v.nlev : v.lev_lo; lv < v.nlev; ++lv) {
                 const int steps = v.lev[lv].steps;
                 if (steps == 0) continue;
                 const NodeDesc nd = p.nodes[p.chunk_nodes[chunk * p.nlev + lv]];
@@ -1869,10 +1927,41 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
             }
             Pol::template mma16_tile<MT, NT>(acc, af, bf);
         }
+        // stacked U: nku more k-blocks, same shape as the D items
+        if (v.ustack) {
+            const int ufmt = v.ufmt_all;
+            const int ufb = fmt_bytes(ufmt);
+            for (int kb = 0; kb < v.nku; ++kb) {
+                const uint8_t* base = next_stage() + warp * v.u_item;
+                W tmp[MT][Pol::AR * 4];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+                    frag_load<W, Pol::AR * 4, FW>(ufmt, base + mt * 32 * Pol::AR * 4 * ufb, lane, tmp[mt]);
+                release_stage();
+                typename Pol::AF af[MT];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    W av[Pol::AR][4];
+#pragma unroll
+                    for (int a = 0; a < Pol::AR; ++a)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) av[a][j] = tmp[mt][a * 4 + j];
+                    Pol::prep_a(af[mt], av);
+                }
+                typename Pol::BF bf[NT];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    W bv[4];
+                    load_bfrag<W>(ts + (kb * NT + nt) * 128, lane, bv);
+                    Pol::prep_b(bf[nt], bv);
+                }
+                Pol::template mma16_tile<MT, NT>(acc, af, bf);
+            }
+        }
         // U: per step, the 16 warps' blocks are adjacent; several steps per stage
         int tbase = 0;
         const uint8_t* sbase = nullptr;
-        for (int lv = v.lev_lo; lv < v.nlev; ++lv) {
+        for (int lv = v.ustack ? v.nlev : v.lev_lo; lv < v.nlev; ++lv) {
             const Mr2Level& L = v.lev[lv];
             const int steps = L.steps;
             if (steps == 0) continue;
@@ -1986,6 +2075,7 @@ size_t ma2_smem(const Mr2View& v, int nct, int slot_bytes, int ns) {
 }
 template <class Pol>
 int mb2_trows(const Mr2View& v) {
+    if (v.ustack) return v.nku * 16;
     int trows = 0;
     for (int lv = v.lev_lo; lv < v.nlev; ++lv) trows += v.lev[lv].steps * Pol::KU;
     return trows;
@@ -2313,6 +2403,35 @@ hodlr_status build_slab(const MrInput& in, MrPlan& mr) {
     }
     v.ntasks = (srows + Pol::MR - 1) / Pol::MR;
     if (v.ntasks > kMr2MaxTasks) return HODLR_OK;
+    // stacked U layout when every level with U columns stores them in one format
+    {
+        int ufmt = -1, ucols = 0;
+        bool same = true;
+        for (int lv = 0; lv < nlev; ++lv) {
+            const MrLevel& L = mr.view.lev[lv];
+            if (L.ru_max <= 0) continue;
+            if (ufmt >= 0 && v.lev[lv].ufmt != ufmt) same = false;
+            ufmt = v.lev[lv].ufmt;
+            ucols += L.ru_max;
+        }
+        for (int i = 0; i < kMr2MaxRows; ++i) {
+            v.urow_lv[i] = -1;
+            v.urow_c[i] = 0;
+        }
+        if (same && ufmt >= 0 && ucols <= kMr2MaxRows && !getenv("HODLR_B200_NO_USTACK")) {
+            int r = 0;
+            for (int lv = 0; lv < nlev; ++lv)
+                for (int c = 0; c < mr.view.lev[lv].ru_max; ++c, ++r) {
+                    v.urow_lv[r] = (int16_t)lv;
+                    v.urow_c[r] = (int16_t)c;
+                }
+            v.ustack = 1;
+            v.nku = (ucols + 15) / 16;
+            v.ufmt_all = ufmt;
+            v.u_item = MT * 32 * Pol::AR * 4 * fmt_bytes(ufmt);
+            uoff = (int64_t)v.nku * kBWarps * v.u_item;  // U area bytes per chunk
+        }
+    }
     for (int t = 0; t < v.ntasks; ++t) {
         const int blk = 32 * Pol::AR * 4 * fmt_bytes(v.task_fmt[t]);
         v.task_off[t] = (int32_t)aoff;

@@ -89,6 +89,16 @@ struct Mr2View {
     int32_t max_ablk;
     int32_t arow;              // A bytes of one k-step, all tasks ([kb][task] layout)
     int32_t widen_fast;        // the slabs hold no fp32 subnormal / inf / nan (integer fp32 -> fp64 widening is exact)
+    // Stacked U (every level's U in one storage format): the levels' U columns are
+    // concatenated (no per-level padding) and cut into nku 16-column k-blocks laid
+    // out exactly like the D items ([k-block][warp][m-tile][lane][4 columns]), so
+    // the U part of phase B is nku more iterations of the D loop.
+    int32_t ustack;            // 1: stacked U layout (else per-level U steps)
+    int32_t nku;               // 16-column U k-blocks per chunk
+    int32_t ufmt_all;          // the common U storage format
+    int32_t u_item;            // bytes of one warp's block of one U k-block
+    int16_t urow_lv[kMr2MaxRows];  // stacked U column -> level (-1: padding)
+    int16_t urow_c[kMr2MaxRows];   //                  -> rank column
     // Phase-A tasks stack the levels' V' columns along M (a run of levels with
     // one storage format shares m-tiles; a format change starts a new tile):
     // stacked row m -> (level, column), level -1 = padding.
