@@ -297,7 +297,7 @@ def _parity(H, X, b_gpu, Kx, normA):
 
 
 KERNELS = {"fused_sv": "k_stream (fused single-vector kernel, one launch per matvec)",
-           "mrhs_slab64": "k_mr2_a + k_mr_reduce + k_mr2_b (multi-RHS, fragment slabs, DMMA fp64)",
+           "mrhs_slab64": "k_mr3_a (K-split phase A) + k_mr_reduce + k_mr2_b (multi-RHS, fragment slabs, DMMA fp64)",
            "mrhs_slab32": "k_mr2_a + k_mr_reduce + k_mr2_b (multi-RHS, fragment slabs, 3xTF32 mma.sync)",
            "mrhs": "k_mr_a + k_mr_reduce + k_mr_b (multi-RHS, arena)",
            "mrhs_tc": "k_tc_a + k_mr_reduce + k_tc_b (multi-RHS, tcgen05 kind::tf32 3xTF32, A in TMEM)",
@@ -564,7 +564,9 @@ def _run_sharded(args, rank, world, local, dev):
     s = x.shape[1]
     wb = wbytes_of(H)
     dt = torch.float64 if wb == 8 else torch.float32
-    sop = dist.ShardedOperator(H, rank, world, device=local)
+    # the whole step (phase A, all-gather, phase B) replayed as one CUDA graph per
+    # buffer pair; falls back to eager launches if the capture fails
+    sop = dist.ShardedOperator(H, rank, world, device=local, use_graph=os.environ.get("HODLR_B200_SHARD_GRAPH", "1") == "1")
     op = sop.op
     r0, nl = sop.row0, sop.n_local
     xd = torch.from_numpy(np.ascontiguousarray(x[r0:r0 + nl])).to(dev).to(dt)
@@ -648,6 +650,7 @@ def _run_sharded(args, rank, world, local, dev):
             "l2": "flushed before every timed step (256 MiB read, untimed)",
             "build_seconds": t_build, "parallelism": f"tree sharded at level {L} over {world} GPUs, "
                                                      "NCCL all-gather of V^T x coefficients",
+            "cuda_graph_replays": sop.graph_replays,
             "native_lib": _native_lib(),
         },
         "parity": parity,

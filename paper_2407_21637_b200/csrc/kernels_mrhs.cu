@@ -460,10 +460,27 @@ template <typename W>
 __global__ void __launch_bounds__(256) k_mr_reduce(PlanView p, const __grid_constant__ MrView m, int node_lo,
                                                    int64_t s, int spad, const W* __restrict__ partial,
                                                    W* __restrict__ tbuf, W* __restrict__ send,
-                                                   const int32_t* __restrict__ list) {
+                                                   const int32_t* __restrict__ list, int nbig = 0, int ty_big = 0,
+                                                   int ty_small = 0) {
     // one warp per output coefficient: lane l sums slots b0+l, b0+l+32, ... in
     // order, then a fixed xor tree combines the lanes (deterministic)
-    const int node = list ? list[blockIdx.x] : node_lo + blockIdx.x;
+    // ty_big > 0: ONE 1-D launch over the listed nodes, the first nbig (many
+    // slots) with ty_big tiles each, the others with ty_small (no idle CTAs, one
+    // launch instead of two); else grid (nodes, tiles)
+    int bx = blockIdx.x, by = blockIdx.y, gy = gridDim.y;
+    if (ty_big > 0) {
+        if (bx < nbig * ty_big) {
+            by = bx % ty_big;
+            bx /= ty_big;
+            gy = ty_big;
+        } else {
+            bx -= nbig * ty_big;
+            by = bx % ty_small;
+            bx = nbig + bx / ty_small;
+            gy = ty_small;
+        }
+    }
+    const int node = list ? list[bx] : node_lo + bx;
     const NodeDesc nd = p.nodes[node];
     const MrSlot sl = m.slots[node];
     const MrLevel L = m.lev[sl.lv];
@@ -476,11 +493,11 @@ __global__ void __launch_bounds__(256) k_mr_reduce(PlanView p, const __grid_cons
     const int64_t stride = (int64_t)L.rv_pad * spad;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nb = sl.b1 - sl.b0 + 1;
-    const int64_t i0 = (int64_t)blockIdx.y * 256;
+    const int64_t i0 = (int64_t)by * 256;
     if (nb <= 32) {
         if (i0 >= cnt_out) return;
         // few slots: one thread per coefficient, slots in order
-        for (int64_t i = i0 + threadIdx.x; i < cnt_out; i += (int64_t)gridDim.y * 256) {
+        for (int64_t i = i0 + threadIdx.x; i < cnt_out; i += (int64_t)gy * 256) {
             W acc = W(0);
             if (i < cnt) {
                 const int64_t c = i / s, q = i - c * s;
@@ -501,7 +518,7 @@ __global__ void __launch_bounds__(256) k_mr_reduce(PlanView p, const __grid_cons
     }
     // many slots (upper levels): one warp per coefficient, lane l sums slots
     // l, l+32, ... in order, then a fixed xor tree (deterministic)
-    for (int64_t base = (int64_t)blockIdx.y * 8; base < cnt_out; base += (int64_t)gridDim.y * 8) {
+    for (int64_t base = (int64_t)by * 8; base < cnt_out; base += (int64_t)gy * 8) {
         {
             const int64_t i = base + warp;
             if (i >= cnt_out) break;
@@ -1475,7 +1492,6 @@ __global__ void __launch_bounds__(kA3Threads, 1) k_mr3_a(PlanView p, const __gri
             }
         s_tmask[threadIdx.x] = tm;
     }
-    for (int k = threadIdx.x; k < C1 - C0; k += blockDim.x) s_mask[k] = 0;
     __syncthreads();
 
     if (warp == kA3Warps) {
@@ -1504,37 +1520,19 @@ __global__ void __launch_bounds__(kA3Threads, 1) k_mr3_a(PlanView p, const __gri
         return;
     }
 
-    // ---------------- table: (local chunk, level) -> ends here? destination (all but the producer)
+    // ---------------- flush table of this CTA's chunks -> shared memory (all but the producer)
     {
         const int nthr = (kA3Warps + kA3Red) * 32;
         const int tid = warp > kA3Warps ? (int)threadIdx.x - 32 : (int)threadIdx.x;
         for (int i = tid; i < (C1 - C0) * p.nlev; i += nthr) {
-            const int k = i / p.nlev, lv = i - k * p.nlev;
-            const int ci = C0 + k;
-            // run containing ci: c_beg(vb) <= ci < c_end(vb)
-            int vb = (int)(((int64_t)(ci + 1) * nb - 1) / nch);
-            while ((int)((int64_t)vb * nch / nb) > ci) --vb;
-            while ((int)((int64_t)(vb + 1) * nch / nb) <= ci) ++vb;
-            const bool runend = ci + 1 == (int)((int64_t)(vb + 1) * nch / nb);
-            const int n0 = p.chunk_nodes[ci * p.nlev + lv];
-            const bool ends = runend || p.chunk_nodes[(ci + 1) * p.nlev + lv] != n0;
-            if (!ends) continue;
-            const MrSlot sl = m.slots[n0];
-            const NodeDesc* nd = &p.nodes[n0];
+            const MrFlush f = m.flush[(size_t)C0 * p.nlev + i];
             A3Dst d;
-            if (sl.b0 == sl.b1 && nd->ext_slot < 0) {  // the node lies inside this run: its sum IS the coefficient
-                d.direct = 1;
-                d.base = nd->t_off * s;
-                d.clim = nd->rv;
-            } else {
-                const MrLevel L = m.lev[lv];
-                d.direct = 0;
-                d.base = (L.part_rows + ((int64_t)vb + sl.jrel) * L.rv_pad) * spad;
-                d.clim = L.rv_max;
-            }
+            d.base = f.row * (f.direct ? s : (int64_t)spad);
+            d.clim = f.clim;
+            d.direct = f.direct;
             s_dst[i] = d;
-            atomicOr(&s_mask[k], 1u << lv);
         }
+        for (int k = tid; k < C1 - C0; k += nthr) s_mask[k] = m.flush_mask[C0 + k];
         asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
     }
     unsigned fl = 0;  // parked tiles so far (same sequence in every warp)
@@ -2244,20 +2242,14 @@ template <typename W>
 cudaError_t launch_reduce(const PlanView& p, const MrPlan& mr, int64_t s, int spad, const W* partial, W* tbuf,
                           W* send, cudaStream_t st) {
     const int nsmall = mr.nmulti - mr.nbig;
-    if (mr.nbig > 0) {
-        const int64_t t = ((int64_t)mr.rmax_big * s + 7) / 8;
-        dim3 gr(mr.nbig, (unsigned)std::max<int64_t>(1, std::min<int64_t>(t, 1024)));
-        k_mr_reduce<W><<<gr, 256, 0, st>>>(p, mr.view, 0, s, spad, partial, tbuf, send, mr.multi);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
-    if (nsmall > 0) {
-        const int64_t t = ((int64_t)mr.rmax_small * s + 255) / 256;
-        dim3 gr(nsmall, (unsigned)std::max<int64_t>(1, std::min<int64_t>(t, 1024)));
-        k_mr_reduce<W><<<gr, 256, 0, st>>>(p, mr.view, 0, s, spad, partial, tbuf, send, mr.multi + mr.nbig);
-        return cudaGetLastError();
-    }
-    return cudaSuccess;
+    const int64_t tb = ((int64_t)mr.rmax_big * s + 7) / 8, ts = ((int64_t)mr.rmax_small * s + 255) / 256;
+    const int ty_big = (int)std::max<int64_t>(1, std::min<int64_t>(tb, 1024));
+    const int ty_small = (int)std::max<int64_t>(1, std::min<int64_t>(ts, 1024));
+    const int64_t blocks = (int64_t)mr.nbig * ty_big + (int64_t)nsmall * ty_small;
+    if (blocks <= 0) return cudaSuccess;
+    k_mr_reduce<W><<<(unsigned)blocks, 256, 0, st>>>(p, mr.view, 0, s, spad, partial, tbuf, send, mr.multi, mr.nbig,
+                                                      ty_big, ty_small);
+    return cudaGetLastError();
 }
 
 template <class Pol>
@@ -2534,6 +2526,17 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
     mr.tca_cand = !mr.has_fp64_operand && in.view && in.d_arena && !getenv("HODLR_B200_NO_SLAB") &&
                   tc_a_candidate(in, v);
     if (mr.tca_cand) v.nb = std::max(1, std::min(nch, sms));
+    // fragment-slab handles (uniform 256-row leaves): the slab phase-A kernels run
+    // one CTA per SM, so one run per SM (fewer run-end flushes and partial slots)
+    {
+        bool uniform = in.view && in.d_arena && !getenv("HODLR_B200_NO_SLAB");
+        for (const ChunkDesc& c : chunks) {
+            const LeafDesc& l = (*in.leaves)[c.leaf];
+            if (c.nrows != kChunk || l.m != kChunk || l.row0 != c.row0 || l.fmt != in.leaf_fmt) uniform = false;
+        }
+        if (uniform && (in.leaf_fmt == HODLR_FMT_FP64 || in.leaf_fmt == HODLR_FMT_FP32) && !getenv("HODLR_B200_NB2"))
+            v.nb = std::max(1, std::min(nch, sms));
+    }
     int64_t rows = 0;
     for (int lv = 0; lv < nlev; ++lv) {
         MrLevel& L = v.lev[lv];
@@ -2596,6 +2599,45 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
         return HODLR_ERR_CUDA;
     }
     v.slots = (const MrSlot*)mr.dev;
+    {
+        // flush table of the K-split phase A: per chunk, the levels whose node ends
+        // there (inside the chunk's run) and the destination of their rows
+        std::vector<MrFlush> fl((size_t)nch * nlev, MrFlush{0, 0, 0});
+        std::vector<uint32_t> fm((size_t)nch, 0u);
+        for (int b = 0; b < v.nb; ++b) {
+            const int c0 = (int)((int64_t)b * nch / v.nb), c1 = (int)((int64_t)(b + 1) * nch / v.nb);
+            for (int ci = c0; ci < c1; ++ci)
+                for (int lv = 0; lv < nlev; ++lv) {
+                    const int n0 = cn[(size_t)ci * nlev + lv];
+                    if (ci + 1 < c1 && cn[(size_t)(ci + 1) * nlev + lv] == n0) continue;
+                    const MrSlot& sl = slots[n0];
+                    const NodeDesc& nd = nodes[n0];
+                    const MrLevel& L = v.lev[lv];
+                    MrFlush& f = fl[(size_t)ci * nlev + lv];
+                    if (sl.b0 == sl.b1 && nd.ext_slot < 0) {
+                        f.direct = 1;
+                        f.row = nd.t_off;
+                        f.clim = nd.rv;
+                    } else {
+                        f.direct = 0;
+                        f.row = L.part_rows + ((int64_t)b + sl.jrel) * L.rv_pad;
+                        f.clim = L.rv_max;
+                    }
+                    fm[ci] |= 1u << lv;
+                }
+        }
+        const size_t fbytes = fl.size() * sizeof(MrFlush);
+        e = cudaMalloc(&mr.flush_dev, fbytes + fm.size() * 4 + 16);
+        if (e == cudaSuccess) e = cudaMemcpy(mr.flush_dev, fl.data(), fbytes, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = cudaMemcpy((uint8_t*)mr.flush_dev + fbytes, fm.data(), fm.size() * 4, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            mr_release(mr);
+            return HODLR_ERR_CUDA;
+        }
+        v.flush = (const MrFlush*)mr.flush_dev;
+        v.flush_mask = (const uint32_t*)((uint8_t*)mr.flush_dev + fbytes);
+    }
     mr.ok = true;
     if (in.view && in.d_arena && !getenv("HODLR_B200_NO_SLAB")) {
         hodlr_status st = HODLR_OK;
@@ -2614,6 +2656,8 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
 
 void mr_release(MrPlan& mr) {
     if (mr.dev) cudaFree(mr.dev);
+    if (mr.flush_dev) cudaFree(mr.flush_dev);
+    mr.flush_dev = nullptr;
     if (mr.slab_dev) cudaFree(mr.slab_dev);
     if (mr.tc_dev) cudaFree(mr.tc_dev);
     if (mr.tca_dev) cudaFree(mr.tca_dev);

@@ -46,11 +46,21 @@ struct MrSlot {
     int32_t b0, b1, jrel, lv;
 };
 
+// Phase-A flush table (k_mr3_a), per (chunk, level): does the level's node end at
+// this chunk of its run, and where do its rows go.
+struct MrFlush {
+    int64_t row;             // direct: t_off of the node; else the partial row of its (run, node) slot
+    int32_t clim;            // stored columns: c < clim
+    int32_t direct;          // 1: the run holds the whole node, its sum IS the coefficient
+};
+
 struct MrView {
     int32_t nlev;            // levels 0..nlev-1 = tree levels 1..nlev
     int32_t nb;              // phase-A CTAs; slots per level = nb + nnodes
     int64_t part_rows;       // total partial rows (x spad values)
     const MrSlot* slots;     // device, indexed by node id
+    const MrFlush* flush;    // device, [nchunks][nlev]
+    const uint32_t* flush_mask;  // device, [nchunks]: bit lv = level lv's node ends at this chunk of its run
     MrLevel lev[kMrMaxLevels];
 };
 
@@ -122,6 +132,7 @@ struct MrPlan {
     int leaf_fmt = HODLR_FMT_FP64;
     MrView view{};
     void* dev = nullptr;
+    void* flush_dev = nullptr; // device: MrFlush table + masks
     int32_t* multi = nullptr;  // device: ids of nodes summed over several phase-A CTAs (or external)
     int nmulti = 0;
     int nbig = 0;              // the first nbig listed nodes sum more than 32 slots

@@ -75,8 +75,17 @@ class ShardedOperator:
     handle); any object with ``exchange_count/shard_begin/shard_local/shard_end``
     and ``row0/n_local`` works (the CPU tests pass an emulator)."""
 
-    def __init__(self, H, rank=None, nranks=None, device=None, group=None, backend_op=None):
+    def __init__(self, H, rank=None, nranks=None, device=None, group=None, backend_op=None, use_graph=None):
+        import os
+
         import torch.distributed as tdist
+
+        # use_graph: replay the whole step (phase A, all-gather, phase B: 4-6 launches
+        # of 5-70 us each at P = 8) as ONE captured CUDA graph per (x, out) buffer
+        # pair; any capture failure falls back to eager launches for that pair
+        self.use_graph = (os.environ.get("HODLR_B200_SHARD_GRAPH", "0") == "1") if use_graph is None else bool(use_graph)
+        self._graphs = {}
+        self.graph_replays = 0
 
         self.group = group
         self.rank = tdist.get_rank(group) if rank is None else int(rank)
@@ -126,6 +135,13 @@ class ShardedOperator:
                                 or B.stride(1) != 1):
             raise ValueError("out has the wrong shape / dtype / device / layout")
         send, recv = self._buffers(X.shape[1], X)
+        if not (self.use_graph and X.is_cuda and self._replay(X, B, send, recv)):
+            self._step(X, B, send, recv)
+        return B[:, 0] if (vec and out is None) else B
+
+    def _step(self, X, B, send, recv):
+        import torch.distributed as tdist
+
         self.op.shard_begin(X, send)
         work = None
         if send.numel():
@@ -134,4 +150,31 @@ class ShardedOperator:
         if work is not None:
             work.wait()
         self.op.shard_end(X, recv, B)
-        return B[:, 0] if (vec and out is None) else B
+
+    def _replay(self, X, B, send, recv) -> bool:
+        """Replay (capturing on first use) the step for this buffer pair; False -> run eagerly."""
+        import torch
+
+        key = (X.data_ptr(), B.data_ptr(), tuple(X.shape), X.stride(0), B.stride(0), X.dtype)
+        g = self._graphs.get(key)
+        if g is None:
+            try:
+                cur = torch.cuda.current_stream(X.device)
+                side = torch.cuda.Stream(X.device)
+                side.wait_stream(cur)
+                with torch.cuda.stream(side):
+                    for _ in range(2):  # warm up on the capture stream: its workspace, NCCL channels
+                        self._step(X, B, send, recv)
+                side.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=side):
+                    self._step(X, B, send, recv)
+                cur.wait_stream(side)
+            except Exception:  # capture not possible here: eager launches from now on
+                g = False
+            self._graphs[key] = g
+        if g is False:
+            return False
+        g.replay()
+        self.graph_replays += 1
+        return True

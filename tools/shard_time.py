@@ -1,7 +1,7 @@
 """Per-rank device time of the sharded matvec on ONE GPU:
 rank 0's handle of a P-way shard runs shard_begin / shard_local / shard_end
 with a zero-filled receive buffer (no other rank exists; the all-gather itself
-is not timed).  python tools/shard_time.py 4|2 [P ...]"""
+is not timed).  python tools/shard_time.py 4|2|s4 [P ...]   (s4: synthetic matrix of cfg4's shape)"""
 import os
 import sys
 
@@ -13,7 +13,15 @@ from paper_2407_21637_b200 import linops, problems, storage_bits
 
 cfg = sys.argv[1]
 Ps = [int(a) for a in sys.argv[2:]] or [1, 2, 4, 8]
-H, X, src = (problems.cfg4() if cfg == "4" else problems.cfg3() if cfg == "3" else problems.cfg2())
+if cfg == "s4":
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from synth_time import SHAPES, synthetic
+
+    n_, d_, f_, r_, w_, s_ = SHAPES["4"]
+    H = synthetic(n_, d_, f_, r_, w_)
+    X = np.random.default_rng(1).standard_normal((n_, s_))
+else:
+    H, X, src = (problems.cfg4() if cfg == "4" else problems.cfg3() if cfg == "3" else problems.cfg2())
 X = np.asarray(X).reshape(H.n, -1)
 s = X.shape[1]
 dt = torch.float64 if H.working_format.name == "fp64" else torch.float32
