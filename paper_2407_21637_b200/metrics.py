@@ -13,7 +13,31 @@ import math
 
 import numpy as np
 
-__all__ = ["matvec_bound", "matvec_backward_error", "hypothesis_holds"]
+__all__ = ["matvec_bound", "matvec_backward_error", "hypothesis_holds", "construction_bound",
+           "construction_error", "storage_ratio"]
+
+
+def construction_bound(depth: int, eps: float) -> float:
+    """Thm 3.1's global construction bound (2 sqrt(2 l) + 1) eps."""
+    if depth < 1:
+        raise ValueError("depth must be >= 1")
+    return (2.0 * math.sqrt(2.0 * depth) + 1.0) * eps
+
+
+def construction_error(A, H_dense) -> float:
+    """||A - reconstruct_dense(H)||_F / ||A||_F (SPEC.md:509-515); H_dense is the
+    densified HODLR matrix."""
+    na = float(np.linalg.norm(A))
+    if na == 0.0:
+        raise ValueError("zero matrix")
+    return float(np.linalg.norm(np.asarray(A) - np.asarray(H_dense)) / na)
+
+
+def storage_ratio(uniform, adaptive) -> float:
+    """storage_bits(uniform build) / storage_bits(adaptive build)."""
+    from .model import storage_bits
+
+    return storage_bits(uniform) / storage_bits(adaptive)
 
 
 def matvec_bound(depth: int, eps: float) -> float:
