@@ -1377,7 +1377,7 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
 // format (no per-task format dispatch in the inner loop).
 constexpr int kA3Kpw = 1;                      // k-blocks per compute warp
 constexpr int kA3Warps = 16 / kA3Kpw;
-constexpr int kA3Red = 3;                      // reducer warps (parked tiles round-robin)
+constexpr int kA3Red = 2;                      // reducer warps (parked tiles round-robin; 1: 112 us, 2: 102, 3: 106 on cfg4)
 constexpr int kA3Threads = (kA3Warps + 1 + kA3Red) * 32;
 constexpr int kA3ParkMax = 8;                  // parking buffers (runtime depth npark <= kA3ParkMax)
 constexpr bool kA3Prefetch = kA3Kpw > 1;       // raw operands of a chunk to registers, stage released before the MMAs
@@ -1706,9 +1706,12 @@ __global__ void __launch_bounds__(kA3Threads, 1) k_mr3_a(PlanView p, const __gri
             for (int nt = 0; nt < NCT; ++nt)
 #pragma unroll
                 for (int e = 0; e < Pol::CR; ++e) {
-                    my[nt * 32 * Pol::CR + e] = acc[t / GT][t % GT][nt][e];
+                    // only the rows whose node ends are parked (the reducers read no others)
                     const int lv = s_rowlv[t * Pol::MR + g + 8 * (e >> 1)];
-                    if (lv >= 0 && ((mask >> lv) & 1u)) acc[t / GT][t % GT][nt][e] = W(0);
+                    if (lv >= 0 && ((mask >> lv) & 1u)) {
+                        my[nt * 32 * Pol::CR + e] = acc[t / GT][t % GT][nt][e];
+                        acc[t / GT][t % GT][nt][e] = W(0);
+                    }
                 }
             __syncwarp();
             if (lane == 0) tma::mbar_arrive(&rfull[buf]);
