@@ -216,3 +216,42 @@ def test_mrhs_tc_phase_b_with_wide_stack(cuda):
     assert op.path(32)[0] == "mrhs_tc"
     X = np.random.default_rng(6).standard_normal((H.n, 32))
     assert rel(run(cuda, op, X, "fp32"), matvec_oracle(H, xin(X, "fp32"))) <= 1e-5
+
+
+@pytest.mark.parametrize("working,fmt", [("fp64", "fp32"), ("fp64", "bf16"), ("fp64", "q52"), ("fp64", "fp64"),
+                                         ("fp32", "fp32"), ("fp32", "fp16")])
+@pytest.mark.parametrize("s", [8, 16, 24])
+def test_slab_kernels_uniform_format(cuda, working, fmt, s):
+    """One storage format on every level: the stacked-U phase B (U columns of all
+    levels concatenated into 16-column k-blocks) and, for s = 8 / 16, the K-split
+    phase A with its format-specialised instance; mma.sync kinds for both working
+    precisions (tcgen05 off), variable ranks incl. rank-0 nodes, many chunks per
+    phase-A run (node ends inside runs: parked tiles) against the oracle."""
+    H = random_hodlr(256 * 64, 6, [fmt] * 6, [(0, 9), 7, (3, 12), 5, (1, 6), 4], working, seed=3 * s + len(fmt))
+    X = np.random.default_rng(s).standard_normal((H.n, s))
+    old = os.environ.get("HODLR_B200_NO_TC")
+    os.environ["HODLR_B200_NO_TC"] = "1"
+    try:
+        op = make_op(H)
+        assert op.path(s)[0] == "mrhs_slab"
+        B = run(cuda, op, X, working)
+        B2 = run(cuda, op, X, working)
+    finally:
+        if old is None:
+            del os.environ["HODLR_B200_NO_TC"]
+        else:
+            os.environ["HODLR_B200_NO_TC"] = old
+    assert np.array_equal(B, B2)  # deterministic
+    assert rel(B, matvec_oracle(H, xin(X, working))) <= (1e-12 if working == "fp64" else 1e-5)
+
+
+def test_slab_kernels_large_uniform_tree(cuda):
+    """cfg4's shape at 1/8 scale (n = 2^17, depth 9, fp32 factors, fp64 working,
+    16 rhs): every phase-A CTA runs several chunks, upper-level nodes span many
+    runs (partial slots + reduce), deep levels end inside runs (direct stores)."""
+    H = random_hodlr(1 << 17, 9, ["fp32"] * 9, [7, 7, 7, 5, 4, 3, 3, 2, 2], "fp64", seed=77)
+    X = np.random.default_rng(5).standard_normal((H.n, 16))
+    op = make_op(H)
+    assert op.path(16)[0] == "mrhs_slab"
+    B = run(cuda, op, X, "fp64")
+    assert rel(B, matvec_oracle(H, X)) <= 1e-12
