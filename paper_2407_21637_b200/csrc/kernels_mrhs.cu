@@ -1719,6 +1719,275 @@ __global__ void __launch_bounds__(kA3Threads, 1) k_mr3_a(PlanView p, const __gri
     }
 }
 
+// ------------------------------------------------------------------ MA4
+// The K-split phase A with a 4 x 4 warp arrangement: warp (tg, kg) owns the
+// tile group tg (tiles 2 tg, 2 tg + 1 of the stacked rows) and the k-blocks
+// 4 kg .. 4 kg + 3 of every chunk.  Against k_mr3_a (16 k-blocks x all tiles per
+// warp): 4 accumulator tiles per warp instead of 14-16 (no register spills under
+// the 96-register cap of a 19-warp CTA), and a tile's partial sums live in only 4
+// warps, so a parked tile is 4 pieces, not 16 -- and the deep levels, whose nodes
+// end every chunk or two, all sit in the last tile group: per chunk only its 4
+// warps (which carry half the MMA work when the tile count is odd) park anything.
+// Every tile group has its own parking channel (buffers, barriers, counters);
+// reducer r serves the groups g = r (mod kA3Red).  Same stages, producer, flush
+// table, slots and summation determinism (fixed pairwise tree) as k_mr3_a.
+constexpr int kA4TG = 2;                       // tiles per group
+constexpr int kA4NG = 4;                       // tile groups (MAXT = 8)
+constexpr int kA4KG = 4;                       // k-blocks per warp
+constexpr int kA4Park = 3;                     // parking buffers per channel
+
+template <class Pol, int NCT, int AFMT, bool FW>
+__global__ void __launch_bounds__(kA3Threads, 1) k_mr4_a(PlanView p, const __grid_constant__ MrView m,
+                                                        const __grid_constant__ Mr2View v,
+                                                        const typename Pol::W* __restrict__ x, int64_t s, int spad,
+                                                        int KH, int ns, int R, int nloc_max,
+                                                        typename Pol::W* __restrict__ partial,
+                                                        typename Pol::W* __restrict__ tbuf) {
+    using W = typename Pol::W;
+    constexpr int MAXT = kA4TG * kA4NG;
+    constexpr int ncol = NCT * 8;
+    constexpr int RE = ma3_red_elems<Pol, NCT>();
+    constexpr int NA = Pol::AR * 4;
+    constexpr int NCH = kA4NG * kA4Park;     // parking buffers in all
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [kRingMax]
+    uint64_t* empty = full + kRingMax;                       // [kRingMax]
+    uint64_t* rfull = empty + kRingMax;                      // [NCH]
+    uint64_t* rfree = rfull + NCH;                           // [NCH]
+    unsigned* s_tmask = reinterpret_cast<unsigned*>(rfree + NCH);          // [MAXT]
+    int8_t* s_rowlv = reinterpret_cast<int8_t*>(s_tmask + MAXT);           // [MAXT * MR]
+    const int a_bytes = KH * v.arow, x_bytes = KH * 16 * ncol * (int)sizeof(W);
+    const int stage_bytes = a_bytes + x_bytes;
+    uint8_t* ring = smem_raw + 640;  // barriers + tables: 128 + 192 + 32 + 128 bytes
+    W* red = reinterpret_cast<W*>(ring + (size_t)ns * stage_bytes);       // [NG][kA4Park][4 warps][RE]
+    A3Dst* s_dst = reinterpret_cast<A3Dst*>(red + (size_t)NCH * 4 * RE);   // [nloc][nlev]
+    unsigned* s_mask = reinterpret_cast<unsigned*>(s_dst + (size_t)nloc_max * p.nlev);  // [nloc]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int H = 16 / KH;
+    const int nch = p.nchunks, nb = m.nb;
+    const int vb0 = blockIdx.x * R, vb1 = min(vb0 + R, nb);
+    if (vb0 >= nb) return;
+    const int C0 = (int)((int64_t)vb0 * nch / nb), C1 = (int)((int64_t)vb1 * nch / nb);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < ns; ++i) {
+            tma::mbar_init(&full[i], 1);
+            tma::mbar_init(&empty[i], KH);   // (KH / 4 k-groups) x 4 tile groups
+        }
+        for (int i = 0; i < NCH; ++i) {
+            tma::mbar_init(&rfull[i], kA4KG);
+            tma::mbar_init(&rfree[i], 1);
+        }
+        tma::fence_mbar_init();
+    }
+    if (threadIdx.x < MAXT * Pol::MR) {
+        const int t = threadIdx.x / Pol::MR;
+        s_rowlv[threadIdx.x] = (int8_t)(t < v.ntasks ? v.row_lv[threadIdx.x] : -1);
+    }
+    if (threadIdx.x < MAXT) {
+        unsigned tm = 0;
+        if ((int)threadIdx.x < v.ntasks)
+            for (int r = 0; r < Pol::MR; ++r) {
+                const int lv = v.row_lv[threadIdx.x * Pol::MR + r];
+                if (lv >= 0) tm |= 1u << lv;
+            }
+        s_tmask[threadIdx.x] = tm;
+    }
+    __syncthreads();
+
+    if (warp == kA3Warps) {
+        // ---------------- producer (as k_mr3_a)
+        if (lane == 0) {
+            const uint64_t pol = tma::policy_evict_first();
+            int slot = 0;
+            unsigned ph = 0;
+            int64_t n = 0;
+            for (int ci = C0; ci < C1; ++ci) {
+                const uint8_t* asrc = v.slab_a + (int64_t)ci * v.a_chunk_bytes;
+                const W* xsrc = x + (int64_t)ci * kChunk * ncol;
+                for (int h = 0; h < H; ++h, ++n) {
+                    if (n >= ns) tma::mbar_wait(&empty[slot], ph ^ 1u);
+                    uint8_t* dst = ring + (size_t)slot * stage_bytes;
+                    tma::mbar_arrive_tx(&full[slot], (unsigned)stage_bytes);
+                    tma::bulk_g2s(dst, asrc + (int64_t)h * a_bytes, (unsigned)a_bytes, &full[slot], pol);
+                    tma::bulk_g2s_plain(dst + a_bytes, xsrc + (int64_t)h * KH * 16 * ncol, (unsigned)x_bytes, &full[slot]);
+                    if (++slot == ns) {
+                        slot = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- flush table of this CTA's chunks -> shared memory (all but the producer)
+    {
+        const int nthr = (kA3Warps + kA3Red) * 32;
+        const int tid = warp > kA3Warps ? (int)threadIdx.x - 32 : (int)threadIdx.x;
+        for (int i = tid; i < (C1 - C0) * p.nlev; i += nthr) {
+            const MrFlush f = m.flush[(size_t)C0 * p.nlev + i];
+            A3Dst d;
+            d.base = f.row * (f.direct ? s : (int64_t)spad);
+            d.clim = f.clim;
+            d.direct = f.direct;
+            s_dst[i] = d;
+        }
+        for (int k = tid; k < C1 - C0; k += nthr) s_mask[k] = m.flush_mask[C0 + k];
+        asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    }
+
+    if (warp > kA3Warps) {
+        // ---------------- reducers: reducer ri serves the tile groups g = ri (mod kA3Red)
+        const int ri = warp - (kA3Warps + 1);
+        unsigned fl[kA4NG];
+#pragma unroll
+        for (int g_ = 0; g_ < kA4NG; ++g_) fl[g_] = 0;
+        for (int ci = C0; ci < C1; ++ci) {
+            const unsigned mask = s_mask[ci - C0];
+            if (!mask) continue;
+            const A3Dst* dk = s_dst + (size_t)(ci - C0) * p.nlev;
+#pragma unroll
+            for (int t = 0; t < MAXT; ++t) {
+                const int grp = t / kA4TG;
+                if (grp % kA3Red != ri) continue;
+                if (!(s_tmask[t] & mask)) continue;
+                unsigned rows = 0;
+#pragma unroll
+                for (int r = 0; r < Pol::MR; ++r) {
+                    const int lv = s_rowlv[t * Pol::MR + r];
+                    if (lv >= 0 && ((mask >> lv) & 1u)) rows |= 1u << r;
+                }
+                const unsigned it = fl[grp]++;
+                const int buf = grp * kA4Park + (int)(it % kA4Park);
+                tma::mbar_wait(&rfull[buf], (it / kA4Park) & 1u);
+                const W* rb = red + (size_t)buf * kA4KG * RE;
+                const int sub = lane / ncol, col = lane % ncol;
+                while (rows) {
+                    unsigned rr = rows;
+                    for (int i = 0; i < sub && rr; ++i) rr &= rr - 1;
+                    if (rr) {
+                        const int row = __ffs(rr) - 1;
+                        const int srow = t * Pol::MR + row;
+                        const int lv = s_rowlv[srow], c = v.row_c[srow];
+                        const A3Dst d = dk[lv];
+                        const int e = ((row >> 3) << 1) | (col & 1);
+                        const int e0 = (((col >> 3) * 32) + (row & 7) * 4 + ((col & 7) >> 1)) * Pol::CR + e;
+                        // fixed order (deterministic): (kg0 + kg1) + (kg2 + kg3)
+                        const W sum = (rb[e0] + rb[RE + e0]) + (rb[2 * RE + e0] + rb[3 * RE + e0]);
+                        if (c < d.clim) {
+                            if (d.direct) {
+                                if (col < s) tbuf[d.base + (int64_t)c * s + col] = sum;
+                            } else if (col < spad) {
+                                partial[d.base + (int64_t)c * spad + col] = sum;
+                            }
+                        }
+                    }
+                    for (int i = 0; i < 32 / ncol && rows; ++i) rows &= rows - 1;
+                }
+                __syncwarp();
+                if (lane == 0) tma::mbar_arrive(&rfree[buf]);
+            }
+        }
+        return;
+    }
+
+    // ---------------- compute warps: warp = tg * 4 + kg (one warp of every tile group per sub-partition)
+    const int g = lane >> 2, tig = lane & 3;
+    const int tg = warp >> 2, kg = warp & 3;
+    const int kb0 = kA4KG * kg;                 // first k-block of this warp
+    const int wl = kb0 % KH, h = kb0 / KH;      // position inside its stage, stage of the chunk
+    const int t0 = tg * kA4TG;                  // first tile of the group
+    const int nt_g = min(kA4TG, v.ntasks - t0); // tiles of the group in use
+    W acc[kA4TG][NCT][Pol::CR];
+#pragma unroll
+    for (int i = 0; i < kA4TG; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NCT; ++nt)
+#pragma unroll
+            for (int e = 0; e < Pol::CR; ++e) acc[i][nt][e] = W(0);
+    int toff[kA4TG], tfmt[kA4TG];
+#pragma unroll
+    for (int i = 0; i < kA4TG; ++i) {
+        toff[i] = i < nt_g ? v.task_off[t0 + i] : 0;
+        tfmt[i] = i < nt_g ? v.task_fmt[t0 + i] : HODLR_FMT_FP32;
+    }
+    unsigned fl = 0;  // parked tiles of this group so far
+    int64_t sn = h;   // this warp's stage number: k * H + h
+    for (int ci = C0; ci < C1; ++ci, sn += H) {
+        const int slot = (int)(sn % ns);
+        tma::mbar_wait(&full[slot], (unsigned)((sn / ns) & 1));
+        const uint8_t* base = ring + (size_t)slot * stage_bytes;
+        if (nt_g > 0) {
+#pragma unroll
+            for (int q = 0; q < kA4KG; ++q) {
+                const W* xs = reinterpret_cast<const W*>(base + a_bytes) + (16 * (wl + q) + 4 * tig) * ncol + g;
+                typename Pol::BF bf[NCT];
+#pragma unroll
+                for (int nt = 0; nt < NCT; ++nt) {
+                    W bv[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) bv[j] = xs[j * ncol + 8 * nt];
+                    Pol::prep_b(bf[nt], bv);
+                }
+                const uint8_t* ab = base + (size_t)(wl + q) * v.arow;
+                typename Pol::AF af[kA4TG];
+#pragma unroll
+                for (int i = 0; i < kA4TG; ++i) {
+                    W tmp[NA];
+                    if (i < nt_g) {
+                        if constexpr (AFMT >= 0) {
+                            A3Raw<AFMT, NA> r1;
+                            a3_load_raw<AFMT, NA>(ab + toff[i], lane, r1);
+                            a3_decode<W, AFMT, NA, FW>(r1, tmp);
+                        } else {
+                            frag_load<W, NA, FW>(tfmt[i], ab + toff[i], lane, tmp);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < NA; ++j) tmp[j] = W(0);
+                    }
+                    W av[Pol::AR][4];
+#pragma unroll
+                    for (int a = 0; a < Pol::AR; ++a)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) av[a][j] = tmp[a * 4 + j];
+                    Pol::prep_a(af[i], av);
+                }
+                if (nt_g >= kA4TG)
+                    Pol::template mma16_group<kA4TG, NCT, kA4TG>(acc, af, bf);
+                else
+                    Pol::template mma16_group<1, NCT, kA4TG>(acc, af, bf);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) tma::mbar_arrive(&empty[slot]);
+        const unsigned mask = s_mask[ci - C0];
+        if (!mask) continue;
+#pragma unroll
+        for (int i = 0; i < kA4TG; ++i) {
+            const int t = t0 + i;
+            if (!(s_tmask[t] & mask)) continue;   // (s_tmask is 0 for unused tiles)
+            const unsigned it = fl++;
+            const int buf = tg * kA4Park + (int)(it % kA4Park);
+            if (it >= (unsigned)kA4Park) tma::mbar_wait(&rfree[buf], ((it / kA4Park) - 1) & 1u);
+            W* my = red + ((size_t)buf * kA4KG + kg) * RE + lane * Pol::CR;
+#pragma unroll
+            for (int nt = 0; nt < NCT; ++nt)
+#pragma unroll
+                for (int e = 0; e < Pol::CR; ++e) {
+                    const int lv = s_rowlv[t * Pol::MR + g + 8 * (e >> 1)];
+                    if (lv >= 0 && ((mask >> lv) & 1u)) {
+                        my[nt * 32 * Pol::CR + e] = acc[i][nt][e];
+                        acc[i][nt][e] = W(0);
+                    }
+                }
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&rfull[buf]);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ MB2
 // Persistent: CTA b takes works (chunk, column group) b, b + grid, ...
 //   warps 0..15  compute: warp w owns chunk rows 16w..16w+15;
@@ -2179,6 +2448,38 @@ bool launch_ma3(const PlanView& p, const MrView& m, const Mr2View& v, const type
     if (*err != cudaSuccess) return true;
     int dbg = 0;  // timing experiments only (results are wrong when set)
     if (const char* e = getenv("HODLR_B200_MA3_DBG")) dbg = atoi(e);
+    bool use4 = true;
+    if (const char* e = getenv("HODLR_B200_MA4")) use4 = e[0] != '0';
+    if (use4) {
+        // the 4 x 4 arrangement: its own parking geometry (4 channels x kA4Park buffers of 4 pieces)
+        const size_t red4 = (size_t)kA4NG * kA4Park * kA4KG * ma3_red_elems<Pol, NCT>() * sizeof(W);
+        const size_t stage = (size_t)KH * v.arow + (size_t)KH * 16 * NCT * 8 * sizeof(W);
+        int ns4 = kRingMax;
+        while (ns4 > 2 && 640 + ns4 * stage + red4 > budget) --ns4;
+        if (const char* e = getenv("HODLR_B200_MA3_NS")) ns4 = std::max(2, std::min(ns4, atoi(e)));
+        const size_t sm4 = 640 + ns4 * stage + red4 + tab;
+        if (sm4 <= 227 * 1024 && ns4 >= 16 / KH && KH >= kA4KG) {
+            auto pick4 = [&](auto fwc) {
+                constexpr bool F = decltype(fwc)::value;
+                auto kk = k_mr4_a<Pol, NCT, -1, F>;
+                switch (afmt) {
+                    case HODLR_FMT_Q52: kk = k_mr4_a<Pol, NCT, HODLR_FMT_Q52, F>; break;
+                    case HODLR_FMT_BF16: kk = k_mr4_a<Pol, NCT, HODLR_FMT_BF16, F>; break;
+                    case HODLR_FMT_FP16: kk = k_mr4_a<Pol, NCT, HODLR_FMT_FP16, F>; break;
+                    case HODLR_FMT_FP32: kk = k_mr4_a<Pol, NCT, HODLR_FMT_FP32, F>; break;
+                    case HODLR_FMT_FP64: kk = k_mr4_a<Pol, NCT, HODLR_FMT_FP64, F>; break;
+                    default: break;
+                }
+                return kk;
+            };
+            auto k4 = fw ? pick4(std::true_type{}) : pick4(std::false_type{});
+            *err = cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
+            if (*err != cudaSuccess) return true;
+            k4<<<grid, kA3Threads, sm4, st>>>(p, m, v, x, s, spad, KH, ns4, R, nloc, partial, tbuf);
+            *err = cudaGetLastError();
+            return true;
+        }
+    }
     k<<<grid, kA3Threads, sm, st>>>(p, m, v, x, s, spad, KH, ns, R, nloc, npark, dbg, partial, tbuf);
     *err = cudaGetLastError();
     return true;
