@@ -16,10 +16,12 @@
 //   fp32 working: mma.sync.m16n8k8.tf32, every operand split a = hi + lo
 //                 (hi = rna_tf32(a), lo = rna_tf32(a - hi)) and
 //                 acc += hi*lo' + lo*hi' + hi*hi'  (fp32-level accuracy).
+#include <cuda.h>  // CUtensorMap types only (the encoder is fetched through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -308,6 +310,24 @@ template <typename W>
 __device__ __forceinline__ int xfrag(int r, int q, int nct) {
     const int lane = ((q & 7) << 2) | ((r >> 2) & 3);
     return ((r >> 4) * nct + (q >> 3)) * 128 + frag_byte(lane, r & 3, (int)sizeof(W), 4) / (int)sizeof(W);
+}
+
+// Fragment slabs use their own bijection of a 16-wide k-block (any bijection
+// works as long as both operands share it): the lane at k position tig holds,
+// as its j-th value, row kperm_row(tig, j) = 2 tig + (j & 1) + 8 (j >> 1).  For a
+// fixed j the four tig lanes then sit on rows with distinct (row & 7) / 2, which
+// makes the B-fragment loads from a 128-byte-swizzled X tile (k_mr4_a)
+// bank-conflict free.  Phase A only (A slab, k_mr2_a / k_mr3_a / k_mr4_a); phase B
+// and the arena kernels keep rows 4 tig + j (measured: the bijection slows the
+// phase-B stagers' fragment-order stores, 428 -> 446 us on cfg4).
+__host__ __device__ __forceinline__ int kperm_row(int tig, int j) { return 2 * tig + (j & 1) + 8 * (j >> 1); }
+__host__ __device__ __forceinline__ int kperm_tig(int r) { return (r & 7) >> 1; }
+__host__ __device__ __forceinline__ int kperm_j(int r) { return (r & 1) | (((r >> 3) & 1) << 1); }
+// xfrag with the slab bijection (row r of a 16-row block -> lane k position, value index)
+template <typename W>
+__device__ __forceinline__ int xfrag2(int r, int q, int nct) {
+    const int lane = ((q & 7) << 2) | kperm_tig(r);
+    return ((r >> 4) * nct + (q >> 3)) * 128 + frag_byte(lane, kperm_j(r), (int)sizeof(W), 4) / (int)sizeof(W);
 }
 
 // A lane's B fragment (4 values) of block `blk` (128 elements).
@@ -738,12 +758,12 @@ __global__ void k_slab_a(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
         const int m = t * Pol::MR + (lane >> 2) + 8 * a;  // stacked row
         const int lv = v.row_lv[m], c = v.row_c[m];
         const ChunkDesc ch = p.chunks[chunk];
-        const int row = kb * 16 + 4 * (lane & 3);
         const NodeDesc* nd = lv >= 0 ? &p.nodes[p.chunk_nodes[chunk * p.nlev + lv]] : nullptr;
         for (int j = 0; j < 4; ++j) {
+            const int row = kb * 16 + kperm_row(lane & 3, j);
             uint8_t* dst = blk + frag_byte(lane, a * 4 + j, fb, Pol::AR * 4);
             if (nd && c < nd->rv) {
-                const uint8_t* src = p.arena + nd->v_off + ((int64_t)c * nd->v_ld + (ch.row0 - nd->row0) + row + j) * fb;
+                const uint8_t* src = p.arena + nd->v_off + ((int64_t)c * nd->v_ld + (ch.row0 - nd->row0) + row) * fb;
                 for (int b = 0; b < fb; ++b) dst[b] = src[b];
                 if (fb < 8 && f32_special(__float_as_uint((float)dec_any(v.task_fmt[t], src, 0)))) *special = 1;
             } else {
@@ -771,14 +791,14 @@ __global__ void k_slab_b(PlanView p, const __grid_constant__ Mr2View v, uint8_t*
         const ChunkDesc ch = p.chunks[chunk];
         const LeafDesc lf = p.leaves[ch.leaf];
         const int row = (ch.row0 - lf.row0) + kBRows * w + mt * Pol::MR + (lane >> 2) + 8 * a;
-        const int col = kb * 16 + 4 * (lane & 3);
-        const uint8_t* src = p.arena + lf.off + ((int64_t)row * lf.ld + col) * lfb;
         uint8_t* blk = slab + (int64_t)chunk * v.b_chunk_bytes + ((int64_t)kb * kBWarps + w) * v.d_item +
                        (int64_t)mt * 32 * Pol::AR * 4 * lfb;
         for (int j = 0; j < 4; ++j) {
+            const int col = kb * 16 + 4 * (lane & 3) + j;  // (phase B keeps rows 4 tig + j: its X / T staging stores are faster that way)
+            const uint8_t* src = p.arena + lf.off + ((int64_t)row * lf.ld + col) * lfb;
             uint8_t* dst = blk + frag_byte(lane, a * 4 + j, lfb, Pol::AR * 4);
-            for (int b = 0; b < lfb; ++b) dst[b] = src[j * lfb + b];
-            if (lfb < 8 && f32_special(__float_as_uint((float)dec_any(v.leaf_fmt, src, j)))) *special = 1;
+            for (int b = 0; b < lfb; ++b) dst[b] = src[b];
+            if (lfb < 8 && f32_special(__float_as_uint((float)dec_any(v.leaf_fmt, src, 0)))) *special = 1;
         }
     }
     if (v.ustack) {
@@ -1128,7 +1148,7 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
                         ln = o >> 2;
                         e = o & 3;
                     }
-                    const int r = 16 * (blk / NCT) + 4 * (ln & 3) + e;
+                    const int r = 16 * (blk / NCT) + kperm_row(ln & 3, e);
                     const int q = 8 * (blk % NCT) + (ln >> 2);
                     xs[d] = r < nrows ? xraw[r * ncol + q] : W(0);
                 }
@@ -1146,7 +1166,7 @@ __global__ void __launch_bounds__(kAThreads) k_mr2_a(PlanView p, const __grid_co
             W* xs = xsb + buf * kChunk * ncol;
             for (int i = sl; i < kChunk * ncol; i += 32 * kAStagers) {
                 const int r = i / ncol, q = i - r * ncol;
-                W* dst = xs + xfrag<W>(r, q, NCT);
+                W* dst = xs + xfrag2<W>(r, q, NCT);
                 if (r < ch.nrows && q0 + q < s)
                     cp_async(dst, x + (ch.row0 + r) * ldx + q0 + q, (int)sizeof(W));
                 else
@@ -1625,11 +1645,11 @@ __global__ void __launch_bounds__(kA3Threads, 1) k_mr3_a(PlanView p, const __gri
         A3Raw<AFMT < 0 ? HODLR_FMT_FP32 : AFMT, NA> raw[PF ? kA3Kpw : 1][PF ? MAXT : 1];
 #pragma unroll
         for (int q = 0; q < kA3Kpw; ++q) {
-            const W* xs = reinterpret_cast<const W*>(base + a_bytes) + (16 * (wl + q) + 4 * tig) * ncol + g;
+            const W* xs = reinterpret_cast<const W*>(base + a_bytes) + 16 * (wl + q) * ncol + g;
 #pragma unroll
             for (int nt = 0; nt < NCT; ++nt)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) bv[q][nt][j] = xs[j * ncol + 8 * nt];
+                for (int j = 0; j < 4; ++j) bv[q][nt][j] = xs[kperm_row(tig, j) * ncol + 8 * nt];
             if constexpr (PF) {
                 const uint8_t* ab = base + (size_t)(wl + q) * v.arow;
 #pragma unroll
@@ -1731,6 +1751,15 @@ __global__ void __launch_bounds__(kA3Threads, 1) k_mr3_a(PlanView p, const __gri
 // Every tile group has its own parking channel (buffers, barriers, counters);
 // reducer r serves the groups g = r (mod kA3Red).  Same stages, producer, flush
 // table, slots and summation determinism (fixed pairwise tree) as k_mr3_a.
+// X rows (128 B for 16 fp64 right-hand sides) all start at the same bank, so the
+// B-fragment loads (lanes = 8 columns x 4 rows) were 4-way bank conflicted and,
+// with four tile-group warps re-reading each k-block's X, took ~70% of the
+// shared-memory pipe.  With `use_tmap` the X tile of a stage arrives by ONE
+// tensor-map bulk copy (cp.async.bulk.tensor.2d) with the 128-byte swizzle: the
+// 16-byte unit of row r, column pair c/2 lands at unit (c/2) ^ (r & 7), which
+// spreads a lane group's rows over the banks: with the slab's k bijection
+// (kperm_row: the four tig lanes on rows with distinct (row & 7) / 2) the loads
+// are bank-conflict free.
 constexpr int kA4TG = 2;                       // tiles per group
 constexpr int kA4NG = 4;                       // tile groups (MAXT = 8)
 constexpr int kA4KG = 4;                       // k-blocks per warp
@@ -1742,7 +1771,8 @@ __global__ void __launch_bounds__(kA3Threads, 1) k_mr4_a(PlanView p, const __gri
                                                         const typename Pol::W* __restrict__ x, int64_t s, int spad,
                                                         int KH, int ns, int R, int nloc_max,
                                                         typename Pol::W* __restrict__ partial,
-                                                        typename Pol::W* __restrict__ tbuf) {
+                                                        typename Pol::W* __restrict__ tbuf,
+                                                        const __grid_constant__ CUtensorMap tmx, int use_tmap) {
     using W = typename Pol::W;
     constexpr int MAXT = kA4TG * kA4NG;
     constexpr int ncol = NCT * 8;
@@ -1758,7 +1788,9 @@ __global__ void __launch_bounds__(kA3Threads, 1) k_mr4_a(PlanView p, const __gri
     int8_t* s_rowlv = reinterpret_cast<int8_t*>(s_tmask + MAXT);           // [MAXT * MR]
     const int a_bytes = KH * v.arow, x_bytes = KH * 16 * ncol * (int)sizeof(W);
     const int stage_bytes = a_bytes + x_bytes;
-    uint8_t* ring = smem_raw + 640;  // barriers + tables: 128 + 192 + 32 + 128 bytes
+    // (barriers + tables: 128 + 192 + 32 + 128 bytes; stages 1024-byte aligned for the swizzled X tiles)
+    const uint32_t base_u32 = tma::smem_u32(smem_raw);
+    uint8_t* ring = smem_raw + (((base_u32 + 640u + 1023u) & ~1023u) - base_u32);
     W* red = reinterpret_cast<W*>(ring + (size_t)ns * stage_bytes);       // [NG][kA4Park][4 warps][RE]
     A3Dst* s_dst = reinterpret_cast<A3Dst*>(red + (size_t)NCH * 4 * RE);   // [nloc][nlev]
     unsigned* s_mask = reinterpret_cast<unsigned*>(s_dst + (size_t)nloc_max * p.nlev);  // [nloc]
@@ -1810,7 +1842,14 @@ __global__ void __launch_bounds__(kA3Threads, 1) k_mr4_a(PlanView p, const __gri
                     uint8_t* dst = ring + (size_t)slot * stage_bytes;
                     tma::mbar_arrive_tx(&full[slot], (unsigned)stage_bytes);
                     tma::bulk_g2s(dst, asrc + (int64_t)h * a_bytes, (unsigned)a_bytes, &full[slot], pol);
-                    tma::bulk_g2s_plain(dst + a_bytes, xsrc + (int64_t)h * KH * 16 * ncol, (unsigned)x_bytes, &full[slot]);
+                    if (use_tmap)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+                                "r"(tma::smem_u32(dst + a_bytes)),
+                            "l"(reinterpret_cast<uint64_t>(&tmx)), "r"(0), "r"(ci * kChunk + h * KH * 16), "r"(tma::smem_u32(&full[slot]))
+                            : "memory");
+                    else
+                        tma::bulk_g2s_plain(dst + a_bytes, xsrc + (int64_t)h * KH * 16 * ncol, (unsigned)x_bytes, &full[slot]);
                     if (++slot == ns) {
                         slot = 0;
                         ph ^= 1u;
@@ -1921,13 +1960,20 @@ __global__ void __launch_bounds__(kA3Threads, 1) k_mr4_a(PlanView p, const __gri
         if (nt_g > 0) {
 #pragma unroll
             for (int q = 0; q < kA4KG; ++q) {
-                const W* xs = reinterpret_cast<const W*>(base + a_bytes) + (16 * (wl + q) + 4 * tig) * ncol + g;
+                const uint8_t* xt = base + a_bytes;
+                const int r0 = 16 * (wl + q);
                 typename Pol::BF bf[NCT];
 #pragma unroll
                 for (int nt = 0; nt < NCT; ++nt) {
                     W bv[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) bv[j] = xs[j * ncol + 8 * nt];
+                    for (int j = 0; j < 4; ++j) {
+                        const int r = r0 + kperm_row(tig, j), c = 8 * nt + g;
+                        // swizzled tile: 16-byte unit (c / 2) of row r sits at unit (c / 2) ^ (r & 7)
+                        const int off = use_tmap ? r * 128 + ((((c >> 1) ^ (r & 7)) << 4) | ((c & 1) << 3))
+                                                 : (r * ncol + c) * (int)sizeof(W);
+                        bv[j] = *reinterpret_cast<const W*>(xt + off);
+                    }
                     Pol::prep_b(bf[nt], bv);
                 }
                 const uint8_t* ab = base + (size_t)(wl + q) * v.arow;
@@ -2385,6 +2431,32 @@ cudaError_t launch_ma2_n(const PlanView& p, const MrView& m, const Mr2View& v, c
     if (maxtw <= 2) return launch_ma2_t<Pol, NCT, 2>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
     return launch_ma2_t<Pol, NCT, 4>(p, m, v, x, ldx, s, spad, partial, tbuf, st);
 }
+// cuTensorMapEncodeTiled through the runtime (no libcuda link): a 2-D fp64 tensor
+// [nrows][16] (128-byte rows), boxes of box_rows rows, 128-byte swizzle.
+inline bool encode_x_tmap(CUtensorMap* tm, const void* x, uint64_t nrows, uint32_t box_rows) {
+    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            f = nullptr;
+        }
+        return (EncodeFn)f;
+    }();
+    if (!fn || box_rows > 256 || (((uintptr_t)x) & 15)) return false;
+    const cuuint64_t dims[2] = {16, nrows};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {16, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(x), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // K-split phase A (k_mr3_a): X contiguous (s = ldx = 8 or 16 columns), <= 8 tasks.
 constexpr int kA3MaxT = 8;
 template <class Pol, int NCT>
@@ -2455,9 +2527,9 @@ bool launch_ma3(const PlanView& p, const MrView& m, const Mr2View& v, const type
         const size_t red4 = (size_t)kA4NG * kA4Park * kA4KG * ma3_red_elems<Pol, NCT>() * sizeof(W);
         const size_t stage = (size_t)KH * v.arow + (size_t)KH * 16 * NCT * 8 * sizeof(W);
         int ns4 = kRingMax;
-        while (ns4 > 2 && 640 + ns4 * stage + red4 > budget) --ns4;
+        while (ns4 > 2 && 640 + 1024 + ns4 * stage + red4 > budget) --ns4;
         if (const char* e = getenv("HODLR_B200_MA3_NS")) ns4 = std::max(2, std::min(ns4, atoi(e)));
-        const size_t sm4 = 640 + ns4 * stage + red4 + tab;
+        const size_t sm4 = 640 + 1024 + ns4 * stage + red4 + tab;  // (+ slack: stages are 1024-byte aligned)
         if (sm4 <= 227 * 1024 && ns4 >= 16 / KH && KH >= kA4KG) {
             auto pick4 = [&](auto fwc) {
                 constexpr bool F = decltype(fwc)::value;
@@ -2475,7 +2547,13 @@ bool launch_ma3(const PlanView& p, const MrView& m, const Mr2View& v, const type
             auto k4 = fw ? pick4(std::true_type{}) : pick4(std::false_type{});
             *err = cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
             if (*err != cudaSuccess) return true;
-            k4<<<grid, kA3Threads, sm4, st>>>(p, m, v, x, s, spad, KH, ns4, R, nloc, partial, tbuf);
+            // X tiles by tensor-map bulk copies with the 128-byte swizzle (fp64, 16 rhs: 128-byte rows)
+            alignas(64) CUtensorMap tmx;
+            memset(&tmx, 0, sizeof(tmx));
+            int use_tmap = 0;
+            if (sizeof(W) == 8 && NCT == 2 && ((size_t)KH * v.arow) % 1024 == 0 && !getenv("HODLR_B200_MA4_NO_TMAP"))
+                use_tmap = encode_x_tmap(&tmx, x, (uint64_t)p.nchunks * kChunk, KH * 16) ? 1 : 0;
+            k4<<<grid, kA3Threads, sm4, st>>>(p, m, v, x, s, spad, KH, ns4, R, nloc, partial, tbuf, tmx, use_tmap);
             *err = cudaGetLastError();
             return true;
         }
