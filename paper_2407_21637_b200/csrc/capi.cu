@@ -78,6 +78,9 @@ struct hodlr_handle {
     std::vector<int64_t> factor_rows;  // for unpack: rows of U / V of each desc factor
     int64_t part_count = 0, t_count = 0, ext_count = 0;
     DeviceBuf arena, tables, e2e;
+    // host-buffer pipeline: device-to-host copies of finished row ranges on their own stream
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> slice_ev;
     // NULL-workspace calls: one zero-initialised workspace per CUDA stream, so
     // concurrent calls on different streams never share the fused kernel's
     // synchronisation state (matvec is safe to call concurrently)
@@ -696,6 +699,8 @@ hodlr_status hodlr_destroy(hodlr_handle* h) {
     h->tables.release();
     for (auto& w : h->ws) w.buf.release();
     h->e2e.release();
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    for (cudaEvent_t e : h->slice_ev) cudaEventDestroy(e);
     sv_release(h->sv);
     mr_release(h->mr);
     delete h;
@@ -817,6 +822,37 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
         r = run_seq(h, working, xd, s, bd, s, s, ws, st);
         if (r != HODLR_OK) return r;
         b_map = nullptr;
+    } else if (working == HODLR_FMT_FP64 && mr_sliceable(h->mr, working, s) && !(h->sv_ok && s == 1) &&
+               n * s * 8 >= (int64_t(8) << 20) && !getenv("HODLR_B200_NO_E2E_PIPELINE")) {
+        // Multi-RHS slab path with a large result (cfg4: 134 MB each way): phase A +
+        // reduce once, then phase B over row ranges; each finished range is copied out
+        // on a second stream while the next ranges are computed, so only the first
+        // range's kernel time stays in front of the 2.4 ms device-to-host copy.
+        CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
+        double *partial, *tbuf;
+        void* extra;
+        carve<double>(h, s, ws, &partial, &tbuf, &extra);
+        CUDA_TRY(mr_phase_a(h->view, h->mr, xd, s, s, partial, tbuf, st));
+        const int nch = h->view.nchunks;
+        const int nsl = std::max(1, std::min(8, nch / 64));
+        if (!h->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        while ((int)h->slice_ev.size() < nsl) {
+            cudaEvent_t ev;
+            CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            h->slice_ev.push_back(ev);
+        }
+        for (int i = 0; i < nsl; ++i) {
+            const int c0 = (int)((int64_t)i * nch / nsl), c1 = (int)((int64_t)(i + 1) * nch / nsl);
+            CUDA_TRY(mr_phase_b_range(h->view, h->mr, xd, s, bd, s, s, tbuf, c0, c1, st));
+            CUDA_TRY(cudaEventRecord(h->slice_ev[i], st));
+            CUDA_TRY(cudaStreamWaitEvent(h->copy_stream, h->slice_ev[i], 0));
+            const int64_t r0 = h->chunks[c0].row0, r1 = c1 < nch ? h->chunks[c1].row0 : n;
+            CUDA_TRY(cudaMemcpyAsync(b_host + r0 * s, bd + r0 * s, (size_t)(r1 - r0) * s * 8, cudaMemcpyDeviceToHost,
+                                     h->copy_stream));
+        }
+        CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return HODLR_OK;
     } else if (working == HODLR_FMT_FP64) {
         CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
         if (!(h->sv_ok && s == 1) || ((uintptr_t)b_map & 15)) b_map = nullptr;  // multi-pass writers / unaligned: stage in HBM

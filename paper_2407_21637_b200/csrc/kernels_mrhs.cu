@@ -2052,7 +2052,7 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
                                                     const typename Pol::W* __restrict__ x, int64_t ldx,
                                                     const typename Pol::W* __restrict__ tbuf,
                                                     typename Pol::W* __restrict__ b, int64_t ldb, int64_t s,
-                                                    int ngrp, int ns, int trows, int nbuf) {
+                                                    int ngrp, int ns, int trows, int nbuf, int chunk0, int chunk1) {
     using W = typename Pol::W;
     constexpr int MT = kBRows / Pol::MR;
     constexpr int ncol = NT * 8;
@@ -2067,7 +2067,7 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
     W* xsb = reinterpret_cast<W*>(ring + (size_t)ns * stage_bytes);  // [nbuf][256 x ncol]
     W* tsb = xsb + nbuf * kChunk * ncol;                            // [nbuf][trows x ncol]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nwork = p.nchunks * ngrp;
+    const int work0 = chunk0 * ngrp, nwork = chunk1 * ngrp;  // works [work0, nwork): chunks [chunk0, chunk1)
     const int64_t dbytes = 16LL << lstage;                           // D region of a chunk
     const int ustage = kBWarps * v.u_item;  // stacked U: one U k-block per stage
     const int nstage = v.ustack ? 16 + v.nku : 16 + (v.warp_bytes + stage_bytes - 1) / stage_bytes;
@@ -2092,7 +2092,7 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
             int slot = 0;
             unsigned ph = 0;
             int64_t n = 0;  // stages issued
-            for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
+            for (int work = work0 + blockIdx.x; work < nwork; work += gridDim.x) {
                 const int chunk = ngrp == 1 ? work : work / ngrp;
                 const uint8_t* src = v.slab_b + (int64_t)chunk * v.b_chunk_bytes;
                 for (int st = 0; st < nstage; ++st, ++n) {
@@ -2123,7 +2123,7 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
         // ---------------- stagers
         const int sl = threadIdx.x - (kBWarps + 1) * 32;
         int k = 0;
-        for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++k) {
+        for (int work = work0 + blockIdx.x; work < nwork; work += gridDim.x, ++k) {
             const int buf = nbuf == 2 ? (k & 1) : 0, use = nbuf == 2 ? (k >> 1) : k;
             if (use > 0) tma::mbar_wait(&xempty[buf], (unsigned)((use - 1) & 1));
             const int chunk = ngrp == 1 ? work : work / ngrp;
@@ -2200,7 +2200,7 @@ __global__ void __launch_bounds__(kBThreads) k_mr2_b(PlanView p, const __grid_co
     const int lfmt = v.leaf_fmt;
     const int lfb = fmt_bytes(lfmt);
     int k = 0;
-    for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++k) {
+    for (int work = work0 + blockIdx.x; work < nwork; work += gridDim.x, ++k) {
         const int buf = nbuf == 2 ? (k & 1) : 0, use = nbuf == 2 ? (k >> 1) : k;
         const int chunk = ngrp == 1 ? work : work / ngrp;
         const int64_t q0 = (int64_t)(work - chunk * ngrp) * ncol;
@@ -2582,7 +2582,7 @@ cudaError_t launch_ma2(const PlanView& p, const MrView& m, const Mr2View& v, con
 template <class Pol, int NT>
 cudaError_t launch_mb2_t(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
                          int64_t ldx, const typename Pol::W* tbuf, typename Pol::W* b, int64_t ldb, int64_t s,
-                         int spad, cudaStream_t st) {
+                         int spad, cudaStream_t st, int chunk0, int chunk1) {
     // one CTA per SM; X / coefficients double-buffered when it leaves >= 3 ring
     // stages, else single-buffered; the ring takes the rest of shared memory
     int nbuf = 2;
@@ -2602,20 +2602,22 @@ cudaError_t launch_mb2_t(const PlanView& p, const MrView& m, const Mr2View& v, c
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBThreads, sm);
-    const int nwork = p.nchunks * ngrp;
+    if (chunk1 <= chunk0) return cudaSuccess;
+    const int nwork = (chunk1 - chunk0) * ngrp;
     const int grid = std::max(1, std::min(nwork, sms * std::max(occ, 1)));
-    k<<<grid, kBThreads, sm, st>>>(p, m, v, x, ldx, tbuf, b, ldb, s, ngrp, ns, mb2_trows<Pol>(v), nbuf);
+    k<<<grid, kBThreads, sm, st>>>(p, m, v, x, ldx, tbuf, b, ldb, s, ngrp, ns, mb2_trows<Pol>(v), nbuf, chunk0, chunk1);
     return cudaGetLastError();
 }
 template <class Pol>
 cudaError_t launch_mb2(const PlanView& p, const MrView& m, const Mr2View& v, const typename Pol::W* x,
                        int64_t ldx, const typename Pol::W* tbuf, typename Pol::W* b, int64_t ldb, int64_t s,
-                       int spad, cudaStream_t st) {
+                       int spad, cudaStream_t st, int chunk0 = 0, int chunk1 = -1) {
+    if (chunk1 < 0) chunk1 = p.nchunks;
     int nt = pick_nt(spad);
     while (nt > 1 && mb2_smem<Pol>(v, nt, 2, 1) > 225 * 1024) nt /= 2;
-    if (nt == 4) return launch_mb2_t<Pol, 4>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st);
-    if (nt == 2) return launch_mb2_t<Pol, 2>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st);
-    return launch_mb2_t<Pol, 1>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st);
+    if (nt == 4) return launch_mb2_t<Pol, 4>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st, chunk0, chunk1);
+    if (nt == 2) return launch_mb2_t<Pol, 2>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st, chunk0, chunk1);
+    return launch_mb2_t<Pol, 1>(p, m, v, x, ldx, tbuf, b, ldb, s, spad, st, chunk0, chunk1);
 }
 
 // Fixed-order reduction of the listed multi-slot nodes (mr.multi: nbig
@@ -2637,7 +2639,7 @@ cudaError_t launch_reduce(const PlanView& p, const MrPlan& mr, int64_t s, int sp
 template <class Pol>
 cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typename Pol::W* x, int64_t ldx,
                    typename Pol::W* b, int64_t ldb, int64_t s, typename Pol::W* partial,
-                   typename Pol::W* tbuf, cudaStream_t st) {
+                   typename Pol::W* tbuf, cudaStream_t st, int phases = 3, int chunk0 = 0, int chunk1 = -1) {
     using W = typename Pol::W;
     const MrView& m = mr.view;
     const int spad = (int)mr_spad(s);
@@ -2646,7 +2648,7 @@ cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typena
     const int wfmt = sizeof(W) == 8 ? HODLR_FMT_FP64 : HODLR_FMT_FP32;
     if (mr_slab_used(mr, wfmt, lev_lo)) {
         cudaError_t e = cudaSuccess;
-        if (any_level) {
+        if (any_level && (phases & 1)) {
             bool done = false;
             if constexpr (sizeof(W) == 4) {
                 if (tca_usable(mr, s)) {
@@ -2660,11 +2662,11 @@ cudaError_t mr_run(const PlanView& p, const MrPlan& mr, int lev_lo, const typena
             if (e == cudaSuccess && nred > 0 && mr.nmulti > 0)  // single-slot nodes were written by phase A
                 e = launch_reduce<W>(p, mr, s, spad, partial, tbuf, nullptr, st);
         }
-        if (e == cudaSuccess) {
+        if (e == cudaSuccess && (phases & 2)) {
             if constexpr (sizeof(W) == 4) {
                 if (tc_usable(mr, s)) return tc_phase_b(p, mr, x, ldx, b, ldb, s, tbuf, st);
             }
-            e = launch_mb2<Pol>(p, m, mr.v2, x, ldx, tbuf, b, ldb, s, spad, st);
+            e = launch_mb2<Pol>(p, m, mr.v2, x, ldx, tbuf, b, ldb, s, spad, st, chunk0, chunk1);
         }
         return e;
     }
@@ -3104,6 +3106,21 @@ cudaError_t mr_slab_phase_b<float>(const PlanView& p, const MrPlan& mr, const fl
                                    int64_t ldb, int64_t s, const float* tbuf, cudaStream_t st) {
     if (tc_usable(mr, s)) return tc_phase_b(p, mr, x, ldx, b, ldb, s, tbuf, st);
     return launch_mb2<PolTF32>(p, mr.view, mr.v2, x, ldx, tbuf, b, ldb, s, (int)mr_spad(s), st);
+}
+
+// Host-buffer pipeline (capi.cu hodlr_matvec_host): phase A + reduce once, then
+// phase B over chunk ranges, so each range's device-to-host copy overlaps the
+// next ranges' kernels.  Fragment-slab DMMA path only (fp64 working).
+bool mr_sliceable(const MrPlan& mr, int working_fmt, int64_t s) {
+    return working_fmt == HODLR_FMT_FP64 && s > 1 && mr_slab_used(mr, working_fmt, 0);
+}
+cudaError_t mr_phase_a(const PlanView& p, const MrPlan& mr, const double* x, int64_t ldx, int64_t s, double* partial,
+                       double* tbuf, cudaStream_t st) {
+    return mr_run<PolF64>(p, mr, 0, x, ldx, nullptr, 0, s, partial, tbuf, st, 1);
+}
+cudaError_t mr_phase_b_range(const PlanView& p, const MrPlan& mr, const double* x, int64_t ldx, double* b, int64_t ldb,
+                             int64_t s, double* tbuf, int chunk0, int chunk1, cudaStream_t st) {
+    return mr_run<PolF64>(p, mr, 0, x, ldx, b, ldb, s, nullptr, tbuf, st, 2, chunk0, chunk1);
 }
 
 bool mr_slab_used(const MrPlan& mr, int working_fmt, int lev_lo) {

@@ -189,6 +189,14 @@ template <typename W>
 cudaError_t mr_slab_phase_b(const PlanView& p, const MrPlan& mr, const W* x, int64_t ldx, W* b, int64_t ldb,
                             int64_t s, const W* tbuf, cudaStream_t st);
 
+// Host-buffer pipeline: phase A + reduce, then phase B over chunk ranges [chunk0, chunk1)
+// (256-row chunks, in row order), so the copies of finished ranges overlap later kernels.
+bool mr_sliceable(const MrPlan& mr, int working_fmt, int64_t s);
+cudaError_t mr_phase_a(const PlanView& p, const MrPlan& mr, const double* x, int64_t ldx, int64_t s, double* partial,
+                       double* tbuf, cudaStream_t st);
+cudaError_t mr_phase_b_range(const PlanView& p, const MrPlan& mr, const double* x, int64_t ldx, double* b, int64_t ldb,
+                             int64_t s, double* tbuf, int chunk0, int chunk1, cudaStream_t st);
+
 // tcgen05 phase A / B (kernels_tc.cu)
 bool tc_a_candidate(const MrInput& in, const MrView& v);
 bool tca_usable(const MrPlan& mr, int64_t s);
