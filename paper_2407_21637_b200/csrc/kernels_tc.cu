@@ -319,26 +319,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tru[t] = nd.ru;
             }
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcStageWarps) : "memory");
-            for (int i = 0; i < nitems; ++i, ++g) {
+            // thread t: column n = t % 64, column quads kc = t / 64 + 2e (no division).  The
+            // loads of item i + 1 are issued before item i is split and stored (and before
+            // the wait for its slot), so one L2 latency per item leaves the critical path.
+            const int n = t & 63, kq = t >> 6;
+            const bool colok = n < nn && q0 + n < s && !(dbg & 8);
+            auto load_item = [&](int i, float (&vals)[4][4]) {
                 const TcItem it = v.item[i];
-                const int bs = (int)(g % kTcBStages);
-                // source rows [col0, col0 + ncols) of X (leaf rows) or of T of the sibling node
                 const float* src;
                 int64_t ld;
                 int nvalid;
-                if (it.lv < 0) {
+                if (it.lv < 0) {  // source rows [col0, col0 + ncols) of X (leaf rows)
                     src = x + (row0 + it.col0) * ldx + q0;
                     ld = ldx;
                     nvalid = it.ncols;
-                } else {
+                } else {          // ... or of T of the sibling node
                     src = tbuf + (toff[it.lv] + it.col0) * s + q0;
                     ld = s;
                     nvalid = max(0, min((int)it.ncols, tru[it.lv] - it.col0));
                 }
-                // thread t: column n = t % 64, column quads kc = t / 64 + 2e (no division)
-                const int n = t & 63, kq = t >> 6, nkc = it.ncols >> 2;
-                const bool colok = n < nn && q0 + n < s && !(dbg & 8);
-                float vals[4][4];
+                const int nkc = it.ncols >> 2;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int kc = kq + 2 * e;
@@ -348,6 +348,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         vals[e][k] = (colok && kc < nkc && r < nvalid) ? __ldg(src + (int64_t)r * ld + n) : 0.0f;
                     }
                 }
+            };
+            float nxt[4][4];
+            load_item(0, nxt);
+            for (int i = 0; i < nitems; ++i, ++g) {
+                const TcItem it = v.item[i];
+                const int bs = (int)(g % kTcBStages);
+                const int nkc = it.ncols >> 2;
+                float vals[4][4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) vals[e][k] = nxt[e][k];
+                if (i + 1 < nitems) load_item(i + 1, nxt);
                 if (g >= kTcBStages) tma::mbar_wait_sleep(&b_empty[bs], (unsigned)(((g / kTcBStages) & 1) ^ 1));
                 TC_TR(trw, t == 0)
                 uint8_t* bh = bring + (size_t)bs * kTcBSlot;
@@ -712,23 +725,36 @@ __global__ void __launch_bounds__(kTaThreads, 1)
             const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
             const int lbo = (nn / 8) * 128;
             const int nunits = 4 * nn;
+            // loads of the next item are issued before the current one is split and stored
+            // (and before the wait for its slot): one L2 latency per item off the critical path
+            auto load_item = [&](int ci, int it, float (&vals)[2][4]) {
+                const float* src = x + ((int64_t)p.chunks[ci].row0 + it * kTcAItemRows) * ldx + q0;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int u = e * 32 * kTaStageWarps + t;
+                    const int kc = u / nn, n = u - kc * nn;
+                    const bool ok = u < nunits && q0 + n < s;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) vals[e][k] = ok && !(dbg & 8) ? __ldg(src + (int64_t)(kc * 4 + k) * ldx + n) : 0.f;
+                }
+            };
+            float nxt[2][4];
+            if (c_beg < c_end) load_item(c_beg, 0, nxt);
             for (int ci = c_beg; ci < c_end; ++ci) {
-                const int64_t row0 = p.chunks[ci].row0;
                 for (int it = 0; it < kItems; ++it, ++g) {
                     const int bs = (int)(g % kTaBStages);
+                    float vals[2][4];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) vals[e][k] = nxt[e][k];
+                    if (it + 1 < kItems)
+                        load_item(ci, it + 1, nxt);
+                    else if (ci + 1 < c_end)
+                        load_item(ci + 1, 0, nxt);
                     if (g >= kTaBStages) tma::mbar_wait_sleep(&b_empty[bs], (unsigned)(((g / kTaBStages) & 1) ^ 1));
                     uint8_t* bh = bring + (size_t)bs * kTaBSlot;
                     uint8_t* bl = bh + kTaBHalf;
-                    const float* src = x + (row0 + it * kTcAItemRows) * ldx + q0;
-                    float vals[2][4];
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int u = e * 32 * kTaStageWarps + t;
-                        const int kc = u / nn, n = u - kc * nn;
-                        const bool ok = u < nunits && q0 + n < s;
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) vals[e][k] = ok && !(dbg & 8) ? __ldg(src + (int64_t)(kc * 4 + k) * ldx + n) : 0.f;
-                    }
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int u = e * 32 * kTaStageWarps + t;

@@ -22,11 +22,14 @@ CMD="python bench.py --steps 4 --warmup 3 --no-cpu-baseline"
 $CMD > $O/ncu_plain.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_mr|k_stream|k_gen|k_tc" -c 120 --csv --log-file $O/launches_bench.csv $CMD > $O/ncu_launch.log 2>&1
 # ncu --set full of the cfg4 kernels (synthetic matrix of cfg4's shape: same kernels, same bytes)
-for k in k_mr2_b k_mr3_a; do
+for k in k_mr2_b k_mr4_a; do
   python tools/synth_time.py 4 --iters 3 > $O/full_plain_$k.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 -o $O/full_$k -f python tools/synth_time.py 4 --iters 3 > $O/full_$k.log 2>&1
+  # (reports are 25 MB each and gpurun_out/ is capped at 64 MiB: keep the text summaries)
+  python tools/ncu_summary.py $O/full_$k.ncu-rep > $O/ncu_full_$k.txt 2>&1; python tools/ncu_sass.py $O/full_$k.ncu-rep 25 >> $O/ncu_full_$k.txt 2>&1; rm -f $O/full_$k.ncu-rep
 done
 python tools/synth_time.py 2 --iters 3 > $O/full_plain_sv.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stream -s 4 -c 1 -o $O/full_k_stream -f python tools/synth_time.py 2 --iters 3 > $O/full_k_stream.log 2>&1
+python tools/ncu_summary.py $O/full_k_stream.ncu-rep > $O/ncu_full_k_stream.txt 2>&1; python tools/ncu_sass.py $O/full_k_stream.ncu-rep 25 >> $O/ncu_full_k_stream.txt 2>&1; rm -f $O/full_k_stream.ncu-rep
 timeout 600 python tools/shard_time.py s4 1 2 4 8 2>&1 | grep -v -i warn > $O/shard_rank_times_cfg4.txt
 echo done > $O/DONE
