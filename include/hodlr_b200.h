@@ -149,7 +149,10 @@ hodlr_status hodlr_workspace_size_for(const hodlr_handle* h, int32_t working, in
  * page-locked (cudaHostAlloc / torch pin_memory) the kernel that stores each b
  * element once (the widening kernel, or the fused s = 1 kernel for binary64
  * working) writes it through the mapped address instead of a D2H copy
- * (HODLR_B200_NO_ZEROCOPY=1 disables this). */
+ * (HODLR_B200_NO_ZEROCOPY=1 disables this).  Multi-RHS calls with a large result
+ * (binary64 working, fragment-slab path, >= 8 MB) run phase B over row ranges and
+ * copy each finished range out on a second stream while the next ranges are
+ * computed (HODLR_B200_NO_E2E_PIPELINE=1 disables this). */
 hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x_host,
                                double* b_host, int64_t s, void* stream);
 
