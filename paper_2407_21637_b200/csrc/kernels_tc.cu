@@ -260,7 +260,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else if (warp == kTcMmaWarp) {
         // ---------------------------------------------------------- MMA issuer
-        if (lane == 0) {
+        // (whole warp, uniform control flow; the MMAs and commits are predicated on one elected lane)
+        const uint32_t leader = tc::elect_one();
+        {
             int64_t g = 0;
             int lc = 0;
             for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++lc) {
@@ -287,16 +289,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             if (dbg & 2) continue;
                             const uint32_t d = tbase + kTcAcc + m * 64;
                             const uint32_t ah = tbase + kTcAStage + ts * 128 + m * 64 + j;
-                            tc::mma_tf32_ts(d, ah, dh, idesc, (i | j) != 0);
-                            tc::mma_tf32_ts(d, ah, dl, idesc, 1);
-                            if (full && !(dbg & 1)) tc::mma_tf32_ts(d, ah + 32, dh, idesc, 1);
+                            tc::mma_tf32_ts_u(d, ah, dh, idesc, (i | j) != 0, leader);
+                            tc::mma_tf32_ts_u(d, ah, dl, idesc, 1, leader);
+                            if (full && !(dbg & 1)) tc::mma_tf32_ts_u(d, ah + 32, dh, idesc, 1, leader);
                         }
                     }
-                    tc::commit(&a_empty[ts]);
-                    tc::commit(&b_empty[bs]);
+                    tc::commit_u(&a_empty[ts], leader);
+                    tc::commit_u(&b_empty[bs], leader);
                     TC_TR(trc, true)
                 }
-                tc::commit(acc_full);
+                tc::commit_u(acc_full, leader);
             }
         }
     } else {
@@ -680,7 +682,10 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         }
     } else if (warp == kTaMmaWarp) {
         // ---------------------------------------------------------- MMA issuer
-        if (lane == 0) {
+        // (whole warp, uniform control flow; the MMAs and commits are predicated on one elected lane,
+        // see tc::mma_tf32_ts_u)
+        const uint32_t leader = tc::elect_one();
+        {
             int64_t g = 0;
             int lc = 0;
             for (int blk = 0; blk < nblk; ++blk) {
@@ -704,15 +709,15 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                                 const uint32_t d = tbase + kTaAcc + t * 64;
                                 const uint32_t ah = tbase + abase + as * astride + t * 32 + j;
                                 if (dbg & 2) continue;
-                                tc::mma_tf32_ts(d, ah, dh, idesc, (it | j) != 0);
-                                tc::mma_tf32_ts(d, ah, dl, idesc, 1);
-                                if (((a.tile_full >> t) & 1) && !(dbg & 1)) tc::mma_tf32_ts(d, ah + 16, dh, idesc, 1);
+                                tc::mma_tf32_ts_u(d, ah, dh, idesc, (it | j) != 0, leader);
+                                tc::mma_tf32_ts_u(d, ah, dl, idesc, 1, leader);
+                                if (((a.tile_full >> t) & 1) && !(dbg & 1)) tc::mma_tf32_ts_u(d, ah + 16, dh, idesc, 1, leader);
                             }
                         }
-                        tc::commit(&a_empty[as]);
-                        tc::commit(&b_empty[bs]);
+                        tc::commit_u(&a_empty[as], leader);
+                        tc::commit_u(&b_empty[bs], leader);
                     }
-                    tc::commit(acc_full);
+                    tc::commit_u(acc_full, leader);
                 }
             }
         }
