@@ -688,6 +688,8 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         {
             int64_t g = 0;
             int lc = 0;
+            int as = 0, bs = 0;
+            unsigned a_par = 0, b_par = 0;
             for (int blk = 0; blk < nblk; ++blk) {
                 const int q0 = blk * kTcN;
                 const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
@@ -696,16 +698,19 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                 for (int ci = c_beg; ci < c_end; ++ci, ++lc) {
                     if (lc >= 1) tma::mbar_wait_sleep(acc_empty, (unsigned)((lc - 1) & 1));
                     for (int it = 0; it < kItems; ++it, ++g) {
-                        const int as = (int)(g % nas), bs = (int)(g % kTaBStages);
-                        tma::mbar_wait_sleep(&a_full[as], (unsigned)((g / nas) & 1));
-                        tma::mbar_wait_sleep(&b_full[bs], (unsigned)((g / kTaBStages) & 1));
+                        // (stage indices and parities kept as counters: a 64-bit g % nas with a
+                        // runtime nas takes the operands out of the uniform datapath)
+                        tma::mbar_wait_sleep(&a_full[as], a_par);
+                        tma::mbar_wait_sleep(&b_full[bs], b_par);
                         tc::fence_after();
                         const uint32_t bh = tc::smem_u32(bring + (size_t)bs * kTaBSlot), bl = bh + kTaBHalf;
 #pragma unroll
                         for (int j = 0; j < kTcAItemRows; j += 8) {
                             const uint64_t dh = tc::smem_desc(bh + (uint32_t)(j >> 2) * lbo, lbo, 128);
                             const uint64_t dl = tc::smem_desc(bl + (uint32_t)(j >> 2) * lbo, lbo, 128);
-                            for (int t = 0; t < a.nmt; ++t) {
+#pragma unroll
+                            for (int t = 0; t < kTcAMaxTiles; ++t) {
+                                if (t >= a.nmt) break;
                                 const uint32_t d = tbase + kTaAcc + t * 64;
                                 const uint32_t ah = tbase + abase + as * astride + t * 32 + j;
                                 if (dbg & 2) continue;
@@ -716,6 +721,14 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                         }
                         tc::commit_u(&a_empty[as], leader);
                         tc::commit_u(&b_empty[bs], leader);
+                        if (++as == nas) {
+                            as = 0;
+                            a_par ^= 1u;
+                        }
+                        if (++bs == kTaBStages) {
+                            bs = 0;
+                            b_par ^= 1u;
+                        }
                     }
                     tc::commit_u(acc_full, leader);
                 }
