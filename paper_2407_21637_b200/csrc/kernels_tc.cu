@@ -60,7 +60,7 @@ constexpr int kTcConvWarps = 16;   // warp w: m-tile (w>>2)&1, lane quarter w&3,
 constexpr int kTcProdWarp = 16;
 constexpr int kTcMmaWarp = 17;
 constexpr int kTcStageWarp0 = 18;
-constexpr int kTcStageWarps = 4;
+constexpr int kTcStageWarps = 8;   // thread t: right-hand side t % 64, column quads t / 64 and t / 64 + 4
 constexpr int kTcThreads = (kTcStageWarp0 + kTcStageWarps) * 32;
 constexpr int kTcRawStages = 4;
 constexpr int kTcRawSlot = kTcRows * kTcItemCols * 4;  // 32 KB
@@ -71,7 +71,15 @@ constexpr int kTcBSlot = 2 * kTcBHalf;
 constexpr uint32_t kTcAcc = 0, kTcAStage = 128;        // accumulator [2 m-tiles][64]; A stages [3][2][hi 32 | lo 32]
 constexpr int kChunkRowsTa = 256;  // rows of a phase-A chunk (= leaf)
 constexpr int kTcBars = 2 * kTcRawStages + 2 * kTcAStages + 2 * kTcBStages + 2;
-constexpr size_t kTcSmem = (size_t)kTcRawStages * kTcRawSlot + (size_t)kTcBStages * kTcBSlot + kTcBars * 8 +
+constexpr int kTcBPrefetch = 3;                   // B rows in flight (cp.async groups) ahead of the item being staged
+constexpr int kTcBRawSlots = kTcBPrefetch + 1;
+constexpr int kTcBRawSlot = kTcItemCols * kTcN * 4;  // 8 KB: the fp32 source rows of one item
+struct BSrc {  // source rows of one item's B operand (X or T), first right-hand side of the pass
+    const float* p;
+    int32_t ld, nvalid;
+};
+constexpr size_t kTcSmem = (size_t)kTcRawStages * kTcRawSlot + (size_t)kTcBStages * kTcBSlot +
+                           (size_t)kTcBRawSlots * kTcBRawSlot + kTcBars * 8 + 2 * kTcMaxItems * sizeof(BSrc) +
                            2 * 2 * kMrMaxLevels * 8 + 16;
 
 __device__ __forceinline__ float4 load_quad(int fmt, const uint8_t* p) {
@@ -102,7 +110,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     uint8_t* ring = smem_raw;                                              // [4][32 KB]
     uint8_t* bring = ring + (size_t)kTcRawStages * kTcRawSlot;             // [3][hi 8 KB | lo 8 KB]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(bring + (size_t)kTcBStages * kTcBSlot);
+    float* rawb = reinterpret_cast<float*>(bring + (size_t)kTcBStages * kTcBSlot);  // [4][32 rows][64] fp32 source rows
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rawb + (size_t)kTcBRawSlots * (kTcBRawSlot / 4));
     uint64_t* raw_full = bars;
     uint64_t* raw_empty = raw_full + kTcRawStages;
     uint64_t* a_full = raw_empty + kTcRawStages;
@@ -112,7 +121,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t* acc_full = b_empty + kTcBStages;
     uint64_t* acc_empty = acc_full + 1;
     // stagers' per-leaf node table, double-buffered by leaf parity: [2][level] (tsrc_off, ru)
-    int64_t* ntab_off = reinterpret_cast<int64_t*>(acc_empty + 1);
+    BSrc* btab = reinterpret_cast<BSrc*>(acc_empty + 1);  // stagers' per-leaf source rows, double-buffered by leaf parity
+    int64_t* ntab_off = reinterpret_cast<int64_t*>(btab + 2 * kTcMaxItems);
     int32_t* ntab_ru = reinterpret_cast<int32_t*>(ntab_off + 2 * kMrMaxLevels);
     uint32_t* tbase_s = reinterpret_cast<uint32_t*>(ntab_ru + 2 * kMrMaxLevels);
 
@@ -284,14 +294,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     for (int j = 0; j < ncols; j += 8) {
                         const uint64_t dh = tc::smem_desc(bh + (uint32_t)(j >> 2) * lbo, lbo, 128);
                         const uint64_t dl = tc::smem_desc(bl + (uint32_t)(j >> 2) * lbo, lbo, 128);
-#pragma unroll
-                        for (int m = 0; m < 2; ++m) {
-                            if (dbg & 2) continue;
-                            const uint32_t d = tbase + kTcAcc + m * 64;
-                            const uint32_t ah = tbase + kTcAStage + ts * 128 + m * 64 + j;
-                            tc::mma_tf32_ts_u(d, ah, dh, idesc, (i | j) != 0, leader);
-                            tc::mma_tf32_ts_u(d, ah, dl, idesc, 1, leader);
-                            if (full && !(dbg & 1)) tc::mma_tf32_ts_u(d, ah + 32, dh, idesc, 1, leader);
+                        if (dbg & 2) continue;
+                        // the two m-tiles alternate: consecutive MMAs never accumulate into the same tile
+                        const uint32_t d0 = tbase + kTcAcc, d1 = d0 + 64;
+                        const uint32_t a0 = tbase + kTcAStage + ts * 128 + j, a1 = a0 + 64;
+                        tc::mma_tf32_ts_u(d0, a0, dh, idesc, (i | j) != 0, leader);
+                        tc::mma_tf32_ts_u(d1, a1, dh, idesc, (i | j) != 0, leader);
+                        tc::mma_tf32_ts_u(d0, a0, dl, idesc, 1, leader);
+                        tc::mma_tf32_ts_u(d1, a1, dl, idesc, 1, leader);
+                        if (full && !(dbg & 1)) {
+                            tc::mma_tf32_ts_u(d0, a0 + 32, dh, idesc, 1, leader);
+                            tc::mma_tf32_ts_u(d1, a1 + 32, dh, idesc, 1, leader);
                         }
                     }
                     tc::commit_u(&a_empty[ts], leader);
@@ -304,91 +317,204 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     } else {
         // ---------------------------------------------------------- B stagers
         const int t = threadIdx.x - kTcStageWarp0 * 32;
-        int64_t g = 0;
-        int lc = 0;
-        for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++lc) {
-            const int chunk = work / nblk;
-            const int q0 = (work % nblk) * kTcN;
-            const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
-            const int64_t row0 = p.chunks[chunk].row0;
-            const int lbo = (nn / 8) * 128;
-            // node table of this leaf (one dependent lookup per level, not per item)
-            int64_t* toff = ntab_off + (lc & 1) * kMrMaxLevels;
-            int32_t* tru = ntab_ru + (lc & 1) * kMrMaxLevels;
-            if (t < v.nlev) {
-                const NodeDesc& nd = p.nodes[p.chunk_nodes[(int64_t)chunk * p.nlev + t]];
-                toff[t] = nd.tsrc_off;
-                tru[t] = nd.ru;
-            }
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcStageWarps) : "memory");
-            // thread t: column n = t % 64, column quads kc = t / 64 + 2e (no division).  The
-            // loads of item i + 1 are issued before item i is split and stored (and before
-            // the wait for its slot), so one L2 latency per item leaves the critical path.
+        // Aligned operands: the source rows (X or T, fp32) of item g + 3 are copied into a
+        // 4-slot shared-memory ring with cp.async while item g is split and stored, so no
+        // L2 latency sits on the per-item chain.  Otherwise: register-staged loads below.
+        const bool fast = ((ldx | s) & 3) == 0 && ldx <= 0x7fffffff && s <= 0x7fffffff && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(tbuf)) & 15) == 0 &&
+                          !(dbg & 16);
+        if (fast) {
             const int n = t & 63, kq = t >> 6;
-            const bool colok = n < nn && q0 + n < s && !(dbg & 8);
-            auto load_item = [&](int i, float (&vals)[4][4]) {
-                const TcItem it = v.item[i];
-                const float* src;
-                int64_t ld;
-                int nvalid;
-                if (it.lv < 0) {  // source rows [col0, col0 + ncols) of X (leaf rows)
-                    src = x + (row0 + it.col0) * ldx + q0;
-                    ld = ldx;
-                    nvalid = it.ncols;
-                } else {          // ... or of T of the sibling node
-                    src = tbuf + (toff[it.lv] + it.col0) * s + q0;
-                    ld = s;
-                    nvalid = max(0, min((int)it.ncols, tru[it.lv] - it.col0));
-                }
-                const int nkc = it.ncols >> 2;
+            int iw = blockIdx.x, ii = 0, ilc = 0, islot = 0;  // issue side: work unit, item, leaf count, ring slot
+            int iq0 = 0;
+            auto issue_next = [&]() {
+                if (iw < nwork) {
+                    BSrc* tab = btab + (ilc & 1) * kTcMaxItems;
+                    if (ii == 0) {
+                        // per leaf: the source rows of every item (one dependent node lookup per item, once)
+                        const int chunk = iw / nblk;
+                        const int q0i = (iw % nblk) * kTcN;
+                        if (t < nitems) {
+                            const TcItem it = v.item[t];
+                            BSrc e;
+                            if (it.lv < 0) {  // rows [col0, col0 + ncols) of X (leaf rows)
+                                e.p = x + (p.chunks[chunk].row0 + it.col0) * ldx + q0i;
+                                e.ld = (int32_t)ldx;
+                                e.nvalid = it.ncols;
+                            } else {          // ... or of T of the sibling node
+                                const NodeDesc& nd = p.nodes[p.chunk_nodes[(int64_t)chunk * p.nlev + it.lv]];
+                                e.p = tbuf + (nd.tsrc_off + it.col0) * s + q0i;
+                                e.ld = (int32_t)s;
+                                e.nvalid = max(0, min((int)it.ncols, nd.ru - it.col0));
+                            }
+                            tab[t] = e;
+                        }
+                        iq0 = q0i;
+                        asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcStageWarps) : "memory");
+                    }
+                    const BSrc e = tab[ii];
+                    const int ncols = v.item[ii].ncols;
+                    float* dst = rawb + (size_t)islot * (kTcBRawSlot / 4);
+                    const int c = (t & 15) * 4;
+                    const bool cok = iq0 + c < s && !(dbg & 8);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int kc = kq + 2 * e;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int r = kc * 4 + k;
-                        vals[e][k] = (colok && kc < nkc && r < nvalid) ? __ldg(src + (int64_t)r * ld + n) : 0.0f;
+                    for (int u = 0; u < 2; ++u) {
+                        const int r = (t >> 4) + 16 * u;
+                        if (r < ncols) {
+                            const bool ok = cok && r < e.nvalid;
+                            tma::cp_async16(dst + r * kTcN + c, ok ? e.p + (int64_t)r * e.ld + c : x, ok ? 16u : 0u);
+                        }
+                    }
+                    if (++islot == kTcBRawSlots) islot = 0;
+                    if (++ii == nitems) {
+                        ii = 0;
+                        iw += gridDim.x;
+                        ++ilc;
                     }
                 }
+                tma::cp_async_commit();
             };
-            float nxt[4][4];
-            load_item(0, nxt);
-            for (int i = 0; i < nitems; ++i, ++g) {
-                const TcItem it = v.item[i];
-                const int bs = (int)(g % kTcBStages);
-                const int nkc = it.ncols >> 2;
-                float vals[4][4];
+#pragma unroll 1
+            for (int u = 0; u < kTcBPrefetch; ++u) issue_next();
+            int64_t g = 0;
+            int bs = 0, cslot = 0;
+            unsigned bpar = 0;  // parity of the b_empty wait (the first pass through the ring does not wait)
+            bool first_pass = true;
+            for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
+                const int q0 = (work % nblk) * kTcN;
+                const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
+                const int lbo = (nn / 8) * 128;
+                for (int i = 0; i < nitems; ++i, ++g) {
+                    const int nkc = v.item[i].ncols >> 2;
+                    tma::cp_async_wait<kTcBPrefetch - 1>();
+                    asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcStageWarps) : "memory");
+                    TC_TR(trw, t == 0)
+                    issue_next();  // item g + 3 -> the slot item g - 1 was read from (all reads done: barrier above)
+                    TC_TR(tra, t == 0)
+                    const float* rb = rawb + (size_t)cslot * (kTcBRawSlot / 4) + n;
+                    float vals[2][4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
+                    for (int e = 0; e < 2; ++e) {
+                        const int kc = kq + 4 * e;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) vals[e][k] = nxt[e][k];
-                if (i + 1 < nitems) load_item(i + 1, nxt);
-                if (g >= kTcBStages) tma::mbar_wait_sleep(&b_empty[bs], (unsigned)(((g / kTcBStages) & 1) ^ 1));
-                TC_TR(trw, t == 0)
-                uint8_t* bh = bring + (size_t)bs * kTcBSlot;
-                uint8_t* bl = bh + kTcBHalf;
-                if (n < nn) {
+                        for (int k = 0; k < 4; ++k) vals[e][k] = kc < nkc ? rb[(kc * 4 + k) * kTcN] : 0.0f;
+                    }
+                    if (!first_pass) tma::mbar_wait_sleep(&b_empty[bs], bpar);
+                    TC_TR(trb, t == 0)
+                    uint8_t* bh = bring + (size_t)bs * kTcBSlot;
+                    uint8_t* bl = bh + kTcBHalf;
+                    if (n < nn) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int kc = kq + 2 * e;
-                        if (kc >= nkc) break;
-                        uint4 h, l;
-                        tc::split_tf32(vals[e][0], h.x, l.x);
-                        tc::split_tf32(vals[e][1], h.y, l.y);
-                        tc::split_tf32(vals[e][2], h.z, l.z);
-                        tc::split_tf32(vals[e][3], h.w, l.w);
-                        const int off = kc * lbo + (n >> 3) * 128 + (n & 7) * 16;
-                        *reinterpret_cast<uint4*>(bh + off) = h;
-                        *reinterpret_cast<uint4*>(bl + off) = l;
+                        for (int e = 0; e < 2; ++e) {
+                            const int kc = kq + 4 * e;
+                            if (kc >= nkc) break;
+                            uint4 h, l;
+                            tc::split_tf32(vals[e][0], h.x, l.x);
+                            tc::split_tf32(vals[e][1], h.y, l.y);
+                            tc::split_tf32(vals[e][2], h.z, l.z);
+                            tc::split_tf32(vals[e][3], h.w, l.w);
+                            const int off = kc * lbo + (n >> 3) * 128 + (n & 7) * 16;
+                            *reinterpret_cast<uint4*>(bh + off) = h;
+                            *reinterpret_cast<uint4*>(bl + off) = l;
+                        }
+                    }
+                    tma::fence_proxy_async_smem();
+                    __syncwarp();
+                    TC_TR(trc, t == 0)
+                    if (lane == 0) tma::mbar_arrive(&b_full[bs]);
+                    if (++cslot == kTcBRawSlots) cslot = 0;
+                    if (++bs == kTcBStages) {
+                        bs = 0;
+                        if (first_pass) first_pass = false; else bpar ^= 1u;
                     }
                 }
-                TC_TR(tra, t == 0)
-                tma::fence_proxy_async_smem();
-                __syncwarp();
-                TC_TR(trc, t == 0)
-                if (lane == 0) tma::mbar_arrive(&b_full[bs]);
             }
-        }
+        } else {
+            int64_t g = 0;
+            int lc = 0;
+            for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++lc) {
+                const int chunk = work / nblk;
+                const int q0 = (work % nblk) * kTcN;
+                const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
+                const int64_t row0 = p.chunks[chunk].row0;
+                const int lbo = (nn / 8) * 128;
+                // node table of this leaf (one dependent lookup per level, not per item)
+                int64_t* toff = ntab_off + (lc & 1) * kMrMaxLevels;
+                int32_t* tru = ntab_ru + (lc & 1) * kMrMaxLevels;
+                if (t < v.nlev) {
+                    const NodeDesc& nd = p.nodes[p.chunk_nodes[(int64_t)chunk * p.nlev + t]];
+                    toff[t] = nd.tsrc_off;
+                    tru[t] = nd.ru;
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcStageWarps) : "memory");
+                // thread t: column n = t % 64, column quads kc = t / 64 + 2e (no division).  The
+                // loads of item i + 1 are issued before item i is split and stored (and before
+                // the wait for its slot), so one L2 latency per item leaves the critical path.
+                const int n = t & 63, kq = t >> 6;
+                const bool colok = n < nn && q0 + n < s && !(dbg & 8);
+                auto load_item = [&](int i, float (&vals)[2][4]) {
+                    const TcItem it = v.item[i];
+                    const float* src;
+                    int64_t ld;
+                    int nvalid;
+                    if (it.lv < 0) {  // source rows [col0, col0 + ncols) of X (leaf rows)
+                        src = x + (row0 + it.col0) * ldx + q0;
+                        ld = ldx;
+                        nvalid = it.ncols;
+                    } else {          // ... or of T of the sibling node
+                        src = tbuf + (toff[it.lv] + it.col0) * s + q0;
+                        ld = s;
+                        nvalid = max(0, min((int)it.ncols, tru[it.lv] - it.col0));
+                    }
+                    const int nkc = it.ncols >> 2;
+    #pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int kc = kq + 4 * e;
+    #pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int r = kc * 4 + k;
+                            vals[e][k] = (colok && kc < nkc && r < nvalid) ? __ldg(src + (int64_t)r * ld + n) : 0.0f;
+                        }
+                    }
+                };
+                float nxt[2][4];
+                load_item(0, nxt);
+                for (int i = 0; i < nitems; ++i, ++g) {
+                    const TcItem it = v.item[i];
+                    const int bs = (int)(g % kTcBStages);
+                    const int nkc = it.ncols >> 2;
+                    float vals[2][4];
+    #pragma unroll
+                    for (int e = 0; e < 2; ++e)
+    #pragma unroll
+                        for (int k = 0; k < 4; ++k) vals[e][k] = nxt[e][k];
+                    if (i + 1 < nitems) load_item(i + 1, nxt);
+                    if (g >= kTcBStages) tma::mbar_wait_sleep(&b_empty[bs], (unsigned)(((g / kTcBStages) & 1) ^ 1));
+                    TC_TR(trw, t == 0)
+                    uint8_t* bh = bring + (size_t)bs * kTcBSlot;
+                    uint8_t* bl = bh + kTcBHalf;
+                    if (n < nn) {
+    #pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int kc = kq + 4 * e;
+                            if (kc >= nkc) break;
+                            uint4 h, l;
+                            tc::split_tf32(vals[e][0], h.x, l.x);
+                            tc::split_tf32(vals[e][1], h.y, l.y);
+                            tc::split_tf32(vals[e][2], h.z, l.z);
+                            tc::split_tf32(vals[e][3], h.w, l.w);
+                            const int off = kc * lbo + (n >> 3) * 128 + (n & 7) * 16;
+                            *reinterpret_cast<uint4*>(bh + off) = h;
+                            *reinterpret_cast<uint4*>(bl + off) = l;
+                        }
+                    }
+                    TC_TR(tra, t == 0)
+                    tma::fence_proxy_async_smem();
+                    __syncwarp();
+                    TC_TR(trc, t == 0)
+                    if (lane == 0) tma::mbar_arrive(&b_full[bs]);
+                }
+            }
+    }
     }
     TC_TRACE_DUMP(warp < kTcConvWarps ? 0 : warp == kTcProdWarp ? 1 : warp == kTcMmaWarp ? 2 : 3,
                   lane == 0 && (warp == 0 || warp == kTcProdWarp || warp == kTcMmaWarp || warp == kTcStageWarp0))
