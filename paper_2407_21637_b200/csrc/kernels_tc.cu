@@ -192,45 +192,76 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) tma::mbar_arrive(acc_empty);
             ++lc;
         };
+        // Ring positions as counters (no 64-bit division per item).  Only converter warp 0
+        // polls the item's two mbarriers; the other 15 warps wait at a hardware barrier, so
+        // their waiting takes no issue slots from the warps that are working.
+        int rs = 0, ts = 0;
+        unsigned rpar = 0, apar = 0;
+        bool a_first = true;
+        const bool fin = v.finite != 0;
+        const uint8_t* rrow = ring + (size_t)row * 16;
         for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
             const int chunk = work / nblk;
             const int q0 = (work % nblk) * kTcN;
             for (int i = 0; i < nitems; ++i, ++g) {
                 const TcItem it = v.item[i];
-                const int rs = (int)(g % kTcRawStages), ts = (int)(g % kTcAStages);
-                tma::mbar_wait_sleep(&raw_full[rs], (unsigned)((g / kTcRawStages) & 1));
-                TC_TR(tra, warp == 0 && lane == 0)
-                if (g >= kTcAStages) tma::mbar_wait_sleep(&a_empty[ts], (unsigned)(((g / kTcAStages) & 1) ^ 1));
-                TC_TR(trb, warp == 0 && lane == 0)
+                if (warp == 0) {
+                    tma::mbar_wait_sleep(&raw_full[rs], rpar);
+                    TC_TR(tra, lane == 0)
+                    if (!a_first) tma::mbar_wait_sleep(&a_empty[ts], apar);
+                    TC_TR(trb, lane == 0)
+                }
+                asm volatile("bar.sync 2, %0;" ::"n"(32 * kTcConvWarps) : "memory");
                 tc::fence_after();
                 TC_TR(trc, warp == 0 && lane == 0)
-                const int w = fmt_bytes(it.fmt);
-                const uint8_t* rp = ring + (size_t)rs * kTcRawSlot + (size_t)row * 4 * w;
                 const uint32_t ah = tl + kTcAStage + ts * 128 + mt * 64;
-                const bool full = it.fmt == HODLR_FMT_FP32;
-                const int j0 = half * 16, j1 = min((int)it.ncols, j0 + 16);
-                for (int j = j0; j < j1; j += 8) {
-                    float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f), f1 = f0;
-                    if (!(dbg & 4)) {
-                        f0 = load_quad(it.fmt, rp + (size_t)(j >> 2) * kTcRows * 4 * w);
-                        f1 = load_quad(it.fmt, rp + (size_t)((j >> 2) + 1) * kTcRows * 4 * w);
-                    }
-                    const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-                    uint32_t hi[8], lo[8];
-                    if (full) {
+                if (it.fmt == HODLR_FMT_FP32 && it.ncols == kTcItemCols && !(dbg & 4)) {
+                    // full fp32 item: this thread's 16 columns = 4 column quads, one 16-byte load each
+                    const uint8_t* rp = rrow + (size_t)rs * kTcRawSlot + (size_t)half * 4 * (kTcRows * 16);
+                    float f[16];
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            if (v.finite)
-                                tc::split_tf32_fast(f[e], hi[e], lo[e]);
-                            else
-                                tc::split_tf32(f[e], hi[e], lo[e]);
-                        }
-                        tc::st_x8(ah + j, hi);
-                        tc::st_x8(ah + 32 + j, lo);
+                    for (int q = 0; q < 4; ++q) {
+                        const float4 u = *reinterpret_cast<const float4*>(rp + (size_t)q * (kTcRows * 16));
+                        f[4 * q] = u.x, f[4 * q + 1] = u.y, f[4 * q + 2] = u.z, f[4 * q + 3] = u.w;
+                    }
+                    uint32_t hi[16], lo[16];
+                    if (fin) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) tc::split_tf32_fast(f[e], hi[e], lo[e]);
                     } else {
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) hi[e] = __float_as_uint(f[e]);
-                        tc::st_x8(ah + j, hi);
+                        for (int e = 0; e < 16; ++e) tc::split_tf32(f[e], hi[e], lo[e]);
+                    }
+                    tc::st_x16(ah + half * 16, hi);
+                    tc::st_x16(ah + 32 + half * 16, lo);
+                } else {
+                    const int w = fmt_bytes(it.fmt);
+                    const uint8_t* rp = ring + (size_t)rs * kTcRawSlot + (size_t)row * 4 * w;
+                    const bool full = it.fmt == HODLR_FMT_FP32;
+                    const int j0 = half * 16, j1 = min((int)it.ncols, j0 + 16);
+                    for (int j = j0; j < j1; j += 8) {
+                        float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f), f1 = f0;
+                        if (!(dbg & 4)) {
+                            f0 = load_quad(it.fmt, rp + (size_t)(j >> 2) * kTcRows * 4 * w);
+                            f1 = load_quad(it.fmt, rp + (size_t)((j >> 2) + 1) * kTcRows * 4 * w);
+                        }
+                        const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+                        uint32_t hi[8], lo[8];
+                        if (full) {
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                if (fin)
+                                    tc::split_tf32_fast(f[e], hi[e], lo[e]);
+                                else
+                                    tc::split_tf32(f[e], hi[e], lo[e]);
+                            }
+                            tc::st_x8(ah + j, hi);
+                            tc::st_x8(ah + 32 + j, lo);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) hi[e] = __float_as_uint(f[e]);
+                            tc::st_x8(ah + j, hi);
+                        }
                     }
                 }
                 TC_TR(trw, warp == 0 && lane == 0)
@@ -240,6 +271,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 if (lane == 0) {
                     tma::mbar_arrive(&raw_empty[rs]);
                     tma::mbar_arrive(&a_full[ts]);
+                }
+                if (++rs == kTcRawStages) rs = 0, rpar ^= 1u;
+                if (++ts == kTcAStages) {
+                    ts = 0;
+                    if (a_first) a_first = false; else apar ^= 1u;
                 }
                 if (i == 0 && pend_chunk >= 0) {
                     epilogue(pend_chunk, pend_q0);
