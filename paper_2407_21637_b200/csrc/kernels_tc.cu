@@ -70,9 +70,8 @@ constexpr int kTcBHalf = kTcItemCols * kTcN * 4;       // 8 KB: hi (or lo) of on
 constexpr int kTcBSlot = 2 * kTcBHalf;
 constexpr uint32_t kTcAcc = 0, kTcAStage = 128;        // accumulator [2 m-tiles][64]; A stages [3][2][hi 32 | lo 32]
 constexpr int kChunkRowsTa = 256;  // rows of a phase-A chunk (= leaf)
-constexpr int kTcBars = 2 * kTcRawStages + 2 * kTcAStages + 2 * kTcBStages + 2;
-constexpr int kTcBPrefetch = 3;                   // B rows in flight (cp.async groups) ahead of the item being staged
-constexpr int kTcBRawSlots = kTcBPrefetch + 1;
+constexpr int kTcBRawSlots = 4;                   // B source rows (fp32) in flight, filled by the producer's bulk copies
+constexpr int kTcBars = 2 * kTcRawStages + 2 * kTcAStages + 2 * kTcBStages + 2 + 2 * kTcBRawSlots;
 constexpr int kTcBRawSlot = kTcItemCols * kTcN * 4;  // 8 KB: the fp32 source rows of one item
 struct BSrc {  // source rows of one item's B operand (X or T), first right-hand side of the pass
     const float* p;
@@ -120,8 +119,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t* b_empty = b_full + kTcBStages;
     uint64_t* acc_full = b_empty + kTcBStages;
     uint64_t* acc_empty = acc_full + 1;
-    // stagers' per-leaf node table, double-buffered by leaf parity: [2][level] (tsrc_off, ru)
-    BSrc* btab = reinterpret_cast<BSrc*>(acc_empty + 1);  // stagers' per-leaf source rows, double-buffered by leaf parity
+    uint64_t* braw_full = acc_empty + 1;
+    uint64_t* braw_empty = braw_full + kTcBRawSlots;
+    // per-leaf B source rows of every item (aligned path) / node table (register-staged path),
+    // both double-buffered by leaf parity
+    BSrc* btab = reinterpret_cast<BSrc*>(braw_empty + kTcBRawSlots);
     int64_t* ntab_off = reinterpret_cast<int64_t*>(btab + 2 * kTcMaxItems);
     int32_t* ntab_ru = reinterpret_cast<int32_t*>(ntab_off + 2 * kMrMaxLevels);
     uint32_t* tbase_s = reinterpret_cast<uint32_t*>(ntab_ru + 2 * kMrMaxLevels);
@@ -145,6 +147,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         tma::mbar_init(acc_full, 1);
         tma::mbar_init(acc_empty, kTcConvWarps);
+        for (int i = 0; i < kTcBRawSlots; ++i) {
+            tma::mbar_init(&braw_full[i], 1);
+            tma::mbar_init(&braw_empty[i], kTcStageWarps);
+        }
         tma::fence_mbar_init();
     }
     if (warp == kTcMmaWarp) tc::tmem_alloc<512>(tbase_s);
@@ -153,6 +159,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc::fence_after();
     const uint32_t tbase = *tbase_s;
     TC_TRACE_DECL
+    // Aligned fp32 operands: the producer warp bulk-copies every item's B source rows (X or
+    // T) into a 4-slot ring ahead of the stagers, so no L2 latency and no address work sits
+    // on the stagers' per-item chain.  Otherwise the stagers load through registers.
+    const bool bfast = ((ldx | s) & 3) == 0 && ldx <= 0x7fffffff && s <= 0x7fffffff &&
+                       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(tbuf)) & 15) == 0 && !(dbg & 16);
 
     if (warp < kTcConvWarps) {
         // ---------------------------------------------------------- converters + epilogue
@@ -288,19 +299,70 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (pend_chunk >= 0) epilogue(pend_chunk, pend_q0);
     } else if (warp == kTcProdWarp) {
         // ---------------------------------------------------------- producer
-        if (lane == 0) {
-            const uint64_t pol = tma::policy_evict_first();
-            int64_t g = 0;
-            for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
-                const uint8_t* src = v.slab + (int64_t)(work / nblk) * v.leaf_bytes;
-                for (int i = 0; i < nitems; ++i, ++g) {
-                    const int rs = (int)(g % kTcRawStages);
-                    if (g >= kTcRawStages) tma::mbar_wait_sleep(&raw_empty[rs], (unsigned)(((g / kTcRawStages) & 1) ^ 1));
+        // (whole warp: lane 0 moves the A item; the B source rows go row by row, one lane each,
+        // or as one copy when the rows are contiguous)
+        const uint64_t pol = tma::policy_evict_first();
+        int rs = 0, bslot = 0, lc = 0;
+        [[maybe_unused]] int64_t g = 0;
+        unsigned rpar = 1, bpar = 1;  // parity of the *_empty waits from the second pass on
+        bool r_first = true, b_first = true;
+        for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++lc) {
+            const int chunk = work / nblk;
+            const int q0 = (work % nblk) * kTcN;
+            const uint8_t* src = v.slab + (int64_t)chunk * v.leaf_bytes;
+            BSrc* tab = btab + (lc & 1) * kTcMaxItems;
+            const unsigned rowbytes = (unsigned)min((int64_t)kTcN, s - q0) * 4u;
+            if (bfast) {
+                // per leaf: the source rows of every item (one dependent node lookup per item, once)
+                const int64_t row0 = p.chunks[chunk].row0;
+                for (int t = lane; t < nitems; t += 32) {
+                    const TcItem it = v.item[t];
+                    BSrc e;
+                    if (it.lv < 0) {  // rows [col0, col0 + ncols) of X (leaf rows)
+                        e.p = x + (row0 + it.col0) * ldx + q0;
+                        e.ld = (int32_t)ldx;
+                        e.nvalid = it.ncols;
+                    } else {          // ... or of T of the sibling node
+                        const NodeDesc& nd = p.nodes[p.chunk_nodes[(int64_t)chunk * p.nlev + it.lv]];
+                        e.p = tbuf + (nd.tsrc_off + it.col0) * s + q0;
+                        e.ld = (int32_t)s;
+                        e.nvalid = max(0, min((int)it.ncols, nd.ru - it.col0));
+                    }
+                    tab[t] = e;
+                }
+                __syncwarp();
+            }
+            for (int i = 0; i < nitems; ++i, ++g) {
+                if (lane == 0) {
+                    if (!r_first) tma::mbar_wait_sleep(&raw_empty[rs], rpar ^ 1u);
                     TC_TR(trw, true)
                     const int bytes = v.item[i].bytes;
                     tma::mbar_arrive_tx(&raw_full[rs], (unsigned)bytes);
                     tma::bulk_g2s(ring + (size_t)rs * kTcRawSlot, src + v.item[i].off, (unsigned)bytes, &raw_full[rs],
                                   pol);
+                }
+                if (++rs == kTcRawStages) {
+                    rs = 0;
+                    if (r_first) r_first = false; else rpar ^= 1u;
+                }
+                if (bfast) {
+                    const BSrc e = tab[i];
+                    const int nv = (dbg & 8) ? 0 : e.nvalid;
+                    if (!b_first) tma::mbar_wait_sleep(&braw_empty[bslot], bpar ^ 1u);
+                    float* dst = rawb + (size_t)bslot * (kTcBRawSlot / 4);
+                    const bool one = (unsigned)e.ld * 4u == rowbytes && rowbytes == kTcN * 4;
+                    if (lane == 0) tma::mbar_arrive_tx(&braw_full[bslot], (unsigned)nv * rowbytes);
+                    __syncwarp();
+                    if (one) {
+                        if (lane == 0 && nv > 0)
+                            tma::bulk_g2s_plain(dst, e.p, (unsigned)nv * rowbytes, &braw_full[bslot]);
+                    } else if (lane < nv) {
+                        tma::bulk_g2s_plain(dst + lane * kTcN, e.p + (int64_t)lane * e.ld, rowbytes, &braw_full[bslot]);
+                    }
+                    if (++bslot == kTcBRawSlots) {
+                        bslot = 0;
+                        if (b_first) b_first = false; else bpar ^= 1u;
+                    }
                 }
             }
         }
@@ -311,6 +373,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         {
             int64_t g = 0;
             int lc = 0;
+            int ts = 0, bs = 0;
+            unsigned a_par = 0, b_par = 0;
             for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++lc) {
                 const int q0 = (work % nblk) * kTcN;
                 const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
@@ -318,34 +382,43 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t lbo = (uint32_t)(nn / 8) * 128;
                 if (lc >= 1) tma::mbar_wait_sleep(acc_empty, (unsigned)((lc - 1) & 1));
                 for (int i = 0; i < nitems; ++i, ++g) {
-                    const int ts = (int)(g % kTcAStages), bs = (int)(g % kTcBStages);
-                    tma::mbar_wait_sleep(&a_full[ts], (unsigned)((g / kTcAStages) & 1));
+                    tma::mbar_wait_sleep(&a_full[ts], a_par);
                     TC_TR(tra, true)
-                    tma::mbar_wait_sleep(&b_full[bs], (unsigned)((g / kTcBStages) & 1));
+                    tma::mbar_wait_sleep(&b_full[bs], b_par);
                     TC_TR(trb, true)
                     tc::fence_after();
                     const int ncols = v.item[i].ncols;
-                    const bool full = v.item[i].fmt == HODLR_FMT_FP32;
-                    const uint32_t bh = tc::smem_u32(bring + (size_t)bs * kTcBSlot), bl = bh + kTcBHalf;
-                    for (int j = 0; j < ncols; j += 8) {
-                        const uint64_t dh = tc::smem_desc(bh + (uint32_t)(j >> 2) * lbo, lbo, 128);
-                        const uint64_t dl = tc::smem_desc(bl + (uint32_t)(j >> 2) * lbo, lbo, 128);
-                        if (dbg & 2) continue;
-                        // the two m-tiles alternate: consecutive MMAs never accumulate into the same tile
-                        const uint32_t d0 = tbase + kTcAcc, d1 = d0 + 64;
-                        const uint32_t a0 = tbase + kTcAStage + ts * 128 + j, a1 = a0 + 64;
-                        tc::mma_tf32_ts_u(d0, a0, dh, idesc, (i | j) != 0, leader);
-                        tc::mma_tf32_ts_u(d1, a1, dh, idesc, (i | j) != 0, leader);
-                        tc::mma_tf32_ts_u(d0, a0, dl, idesc, 1, leader);
-                        tc::mma_tf32_ts_u(d1, a1, dl, idesc, 1, leader);
-                        if (full && !(dbg & 1)) {
-                            tc::mma_tf32_ts_u(d0, a0 + 32, dh, idesc, 1, leader);
-                            tc::mma_tf32_ts_u(d1, a1 + 32, dh, idesc, 1, leader);
+                    const bool full = v.item[i].fmt == HODLR_FMT_FP32 && !(dbg & 1);
+                    const uint32_t bh = tc::smem_u32(bring) + (uint32_t)bs * kTcBSlot;
+                    // descriptors of the item's first k-step; a k-step (two column quads) further = + 2 lbo bytes
+                    uint64_t dh = tc::smem_desc(bh, lbo, 128), dl = tc::smem_desc(bh + kTcBHalf, lbo, 128);
+                    const uint64_t dstep = (uint64_t)((2 * lbo) >> 4);
+                    const uint32_t d0 = tbase + kTcAcc, d1 = d0 + 64;
+                    uint32_t a0 = tbase + kTcAStage + ts * 128;
+                    uint32_t acc = i != 0;
+                    if (!(dbg & 2)) {
+#pragma unroll 1
+                        for (int j = 0; j < ncols; j += 8) {
+                            // the two m-tiles alternate: consecutive MMAs never accumulate into the same tile
+                            tc::mma_tf32_ts_u(d0, a0, dh, idesc, acc, leader);
+                            tc::mma_tf32_ts_u(d1, a0 + 64, dh, idesc, acc, leader);
+                            tc::mma_tf32_ts_u(d0, a0, dl, idesc, 1, leader);
+                            tc::mma_tf32_ts_u(d1, a0 + 64, dl, idesc, 1, leader);
+                            if (full) {
+                                tc::mma_tf32_ts_u(d0, a0 + 32, dh, idesc, 1, leader);
+                                tc::mma_tf32_ts_u(d1, a0 + 96, dh, idesc, 1, leader);
+                            }
+                            acc = 1;
+                            a0 += 8;
+                            dh += dstep;
+                            dl += dstep;
                         }
                     }
                     tc::commit_u(&a_empty[ts], leader);
                     tc::commit_u(&b_empty[bs], leader);
                     TC_TR(trc, true)
+                    if (++ts == kTcAStages) ts = 0, a_par ^= 1u;
+                    if (++bs == kTcBStages) bs = 0, b_par ^= 1u;
                 }
                 tc::commit_u(acc_full, leader);
             }
@@ -356,85 +429,38 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // Aligned operands: the source rows (X or T, fp32) of item g + 3 are copied into a
         // 4-slot shared-memory ring with cp.async while item g is split and stored, so no
         // L2 latency sits on the per-item chain.  Otherwise: register-staged loads below.
-        const bool fast = ((ldx | s) & 3) == 0 && ldx <= 0x7fffffff && s <= 0x7fffffff && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(tbuf)) & 15) == 0 &&
-                          !(dbg & 16);
-        if (fast) {
+        if (bfast) {
+            // thread: right-hand side n = t % 64, column quads t / 64 and t / 64 + 4.  Stager warp 0
+            // polls the two mbarriers of the item; the others wait at a hardware barrier.
             const int n = t & 63, kq = t >> 6;
-            int iw = blockIdx.x, ii = 0, ilc = 0, islot = 0;  // issue side: work unit, item, leaf count, ring slot
-            int iq0 = 0;
-            auto issue_next = [&]() {
-                if (iw < nwork) {
-                    BSrc* tab = btab + (ilc & 1) * kTcMaxItems;
-                    if (ii == 0) {
-                        // per leaf: the source rows of every item (one dependent node lookup per item, once)
-                        const int chunk = iw / nblk;
-                        const int q0i = (iw % nblk) * kTcN;
-                        if (t < nitems) {
-                            const TcItem it = v.item[t];
-                            BSrc e;
-                            if (it.lv < 0) {  // rows [col0, col0 + ncols) of X (leaf rows)
-                                e.p = x + (p.chunks[chunk].row0 + it.col0) * ldx + q0i;
-                                e.ld = (int32_t)ldx;
-                                e.nvalid = it.ncols;
-                            } else {          // ... or of T of the sibling node
-                                const NodeDesc& nd = p.nodes[p.chunk_nodes[(int64_t)chunk * p.nlev + it.lv]];
-                                e.p = tbuf + (nd.tsrc_off + it.col0) * s + q0i;
-                                e.ld = (int32_t)s;
-                                e.nvalid = max(0, min((int)it.ncols, nd.ru - it.col0));
-                            }
-                            tab[t] = e;
-                        }
-                        iq0 = q0i;
-                        asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcStageWarps) : "memory");
-                    }
-                    const BSrc e = tab[ii];
-                    const int ncols = v.item[ii].ncols;
-                    float* dst = rawb + (size_t)islot * (kTcBRawSlot / 4);
-                    const int c = (t & 15) * 4;
-                    const bool cok = iq0 + c < s && !(dbg & 8);
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int r = (t >> 4) + 16 * u;
-                        if (r < ncols) {
-                            const bool ok = cok && r < e.nvalid;
-                            tma::cp_async16(dst + r * kTcN + c, ok ? e.p + (int64_t)r * e.ld + c : x, ok ? 16u : 0u);
-                        }
-                    }
-                    if (++islot == kTcBRawSlots) islot = 0;
-                    if (++ii == nitems) {
-                        ii = 0;
-                        iw += gridDim.x;
-                        ++ilc;
-                    }
-                }
-                tma::cp_async_commit();
-            };
-#pragma unroll 1
-            for (int u = 0; u < kTcBPrefetch; ++u) issue_next();
             int64_t g = 0;
-            int bs = 0, cslot = 0;
-            unsigned bpar = 0;  // parity of the b_empty wait (the first pass through the ring does not wait)
+            int bs = 0, cslot = 0, lc = 0;
+            unsigned bpar = 0, cpar = 0;
             bool first_pass = true;
-            for (int work = blockIdx.x; work < nwork; work += gridDim.x) {
+            for (int work = blockIdx.x; work < nwork; work += gridDim.x, ++lc) {
                 const int q0 = (work % nblk) * kTcN;
                 const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
                 const int lbo = (nn / 8) * 128;
+                const bool colok = q0 + n < s;
+                const BSrc* tab = btab + (lc & 1) * kTcMaxItems;
                 for (int i = 0; i < nitems; ++i, ++g) {
                     const int nkc = v.item[i].ncols >> 2;
-                    tma::cp_async_wait<kTcBPrefetch - 1>();
+                    if (warp == kTcStageWarp0) {
+                        tma::mbar_wait_sleep(&braw_full[cslot], cpar);
+                        TC_TR(trw, t == 0)
+                        if (!first_pass) tma::mbar_wait_sleep(&b_empty[bs], bpar);
+                        TC_TR(tra, t == 0)
+                    }
                     asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcStageWarps) : "memory");
-                    TC_TR(trw, t == 0)
-                    issue_next();  // item g + 3 -> the slot item g - 1 was read from (all reads done: barrier above)
-                    TC_TR(tra, t == 0)
+                    const int nvalid = colok ? tab[i].nvalid : 0;
                     const float* rb = rawb + (size_t)cslot * (kTcBRawSlot / 4) + n;
                     float vals[2][4];
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int kc = kq + 4 * e;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) vals[e][k] = kc < nkc ? rb[(kc * 4 + k) * kTcN] : 0.0f;
+                        for (int k = 0; k < 4; ++k) vals[e][k] = kc * 4 + k < nvalid ? rb[(kc * 4 + k) * kTcN] : 0.0f;
                     }
-                    if (!first_pass) tma::mbar_wait_sleep(&b_empty[bs], bpar);
                     TC_TR(trb, t == 0)
                     uint8_t* bh = bring + (size_t)bs * kTcBSlot;
                     uint8_t* bl = bh + kTcBHalf;
@@ -456,8 +482,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     tma::fence_proxy_async_smem();
                     __syncwarp();
                     TC_TR(trc, t == 0)
-                    if (lane == 0) tma::mbar_arrive(&b_full[bs]);
-                    if (++cslot == kTcBRawSlots) cslot = 0;
+                    if (lane == 0) {
+                        tma::mbar_arrive(&b_full[bs]);
+                        tma::mbar_arrive(&braw_empty[cslot]);
+                    }
+                    if (++cslot == kTcBRawSlots) cslot = 0, cpar ^= 1u;
                     if (++bs == kTcBStages) {
                         bs = 0;
                         if (first_pass) first_pass = false; else bpar ^= 1u;
