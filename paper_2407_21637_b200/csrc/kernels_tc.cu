@@ -666,7 +666,9 @@ constexpr int kTaBHalf = kTcAItemRows * kTcN * 4;  // 4 KB
 constexpr int kTaBSlot = 2 * kTaBHalf;
 constexpr uint32_t kTaAcc = 0;
 constexpr int kTaMaxRaw = 6;
-constexpr int kTaBars = 2 * kTaMaxRaw + 2 * kTaMaxAStages + 2 * kTaBStages + 2;
+constexpr int kTaXRawSlots = 4;                          // X source rows (fp32) in flight, filled by the producer
+constexpr int kTaXRawSlot = kTcAItemRows * kTcN * 4;     // 4 KB
+constexpr int kTaBars = 2 * kTaMaxRaw + 2 * kTaMaxAStages + 2 * kTaBStages + 2 + 2 * kTaXRawSlots;
 // TMEM: D tiles at columns t*64, then A stages of nmt*32 columns (hi 16 | lo 16
 // per tile): 3 stages for <= 3 tiles (480 columns), 2 for 4 tiles (512)
 __host__ __device__ inline int ta_astages(const TcAView& a) { return a.nmt <= 3 ? 3 : 2; }
@@ -676,7 +678,8 @@ __host__ __device__ inline size_t ta_raw_slot(const TcAView& a) { return ((size_
 // running sums [64 columns][nmt * 128 rows] fp32 (thread m owns column j at j*rows + m)
 __host__ __device__ inline size_t ta_sum_bytes(const TcAView& a) { return (size_t)kTcN * ta_srows(a) * 4; }
 inline size_t ta_smem(const TcAView& a, int nraw) {
-    return nraw * ta_raw_slot(a) + (size_t)kTaBStages * kTaBSlot + ta_sum_bytes(a) + kTaBars * 8 + 16;
+    return nraw * ta_raw_slot(a) + (size_t)kTaBStages * kTaBSlot + (size_t)kTaXRawSlots * kTaXRawSlot +
+           ta_sum_bytes(a) + kTaBars * 8 + 16;
 }
 // raw ring depth: as many item slots (<= kTaMaxRaw) as fit next to the rest
 inline int ta_nraw(const TcAView& a) {
@@ -693,7 +696,8 @@ __global__ void __launch_bounds__(kTaThreads, 1)
     const size_t rslot = ta_raw_slot(a);
     uint8_t* ring = smem_raw;
     uint8_t* bring = ring + nraw * rslot;
-    float* sums = reinterpret_cast<float*>(bring + (size_t)kTaBStages * kTaBSlot);
+    float* xraw = reinterpret_cast<float*>(bring + (size_t)kTaBStages * kTaBSlot);  // [4][16 rows][64] fp32 X rows
+    float* sums = xraw + (size_t)kTaXRawSlots * (kTaXRawSlot / 4);
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sums) + ta_sum_bytes(a));
     uint64_t* raw_full = bars;
     uint64_t* raw_empty = raw_full + nraw;
@@ -703,7 +707,9 @@ __global__ void __launch_bounds__(kTaThreads, 1)
     uint64_t* b_empty = b_full + kTaBStages;
     uint64_t* acc_full = b_empty + kTaBStages;
     uint64_t* acc_empty = acc_full + 1;
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    uint64_t* xraw_full = acc_empty + 1;
+    uint64_t* xraw_empty = xraw_full + kTaXRawSlots;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(xraw_empty + kTaXRawSlots);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c_beg = (int)((int64_t)blockIdx.x * p.nchunks / gridDim.x);
@@ -725,6 +731,10 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         }
         tma::mbar_init(acc_full, 1);
         tma::mbar_init(acc_empty, kTaConvWarps);
+        for (int i = 0; i < kTaXRawSlots; ++i) {
+            tma::mbar_init(&xraw_full[i], 1);
+            tma::mbar_init(&xraw_empty[i], kTaStageWarps);
+        }
         tma::fence_mbar_init();
     }
     if (warp == kTaMmaWarp) tc::tmem_alloc<512>(tbase_s);
@@ -734,6 +744,9 @@ __global__ void __launch_bounds__(kTaThreads, 1)
     const uint32_t tbase = *tbase_s;
     const int nas = ta_astages(a);
     const uint32_t abase = (uint32_t)a.nmt * 64, astride = (uint32_t)a.nmt * 32;
+    // Aligned X: the producer warp bulk-copies every item's 16 X rows into a 4-slot ring
+    // ahead of the stagers (no L2 latency or address work on their per-item chain).
+    const bool xfast = ((ldx | s) & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && !(dbg & 32);
 
     if (warp < kTaConvWarps) {
         // ---------------------------------------------------------- converters + epilogue
@@ -800,13 +813,20 @@ __global__ void __launch_bounds__(kTaThreads, 1)
             ++lc;
         };
         int pend_ci = -1, pend_q0 = 0;
+        int rs = 0, as = 0;
+        unsigned rpar = 0, apar = 0;
+        bool a_first = true;
         for (int blk = 0; blk < nblk; ++blk) {
             const int q0 = blk * kTcN;
             for (int ci = c_beg; ci < c_end; ++ci) {
                 for (int it = 0; it < kItems; ++it, ++g) {
-                    const int rs = (int)(g % nraw), as = (int)(g % nas);
-                    tma::mbar_wait_sleep(&raw_full[rs], (unsigned)((g / nraw) & 1));
-                    if (g >= nas) tma::mbar_wait_sleep(&a_empty[as], (unsigned)(((g / nas) & 1) ^ 1));
+                    // only converter warp 0 polls the item's mbarriers; the others wait at a
+                    // hardware barrier (their waiting takes no issue slots)
+                    if (warp == 0) {
+                        tma::mbar_wait_sleep(&raw_full[rs], rpar);
+                        if (!a_first) tma::mbar_wait_sleep(&a_empty[as], apar);
+                    }
+                    asm volatile("bar.sync 2, %0;" ::"n"(32 * kTaConvWarps) : "memory");
                     tc::fence_after();
                     uint32_t hi[16], lo[16];
                     if (lv >= 0 && !(dbg & 4)) {
@@ -832,10 +852,8 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                     }
                     if (mt < a.nmt) {  // warp-uniform: warps past the last tile only keep the protocol
                         const uint32_t ah = tl + abase + as * astride + mt * 32;
-                        tc::st_x8(ah, *reinterpret_cast<const uint32_t(*)[8]>(&hi[0]));
-                        tc::st_x8(ah + 8, *reinterpret_cast<const uint32_t(*)[8]>(&hi[8]));
-                        tc::st_x8(ah + 16, *reinterpret_cast<const uint32_t(*)[8]>(&lo[0]));
-                        tc::st_x8(ah + 24, *reinterpret_cast<const uint32_t(*)[8]>(&lo[8]));
+                        tc::st_x16(ah, hi);
+                        tc::st_x16(ah + 16, lo);
                         tc::wait_st();
                     }
                     tc::fence_before();
@@ -843,6 +861,11 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                     if (lane == 0) {
                         tma::mbar_arrive(&raw_empty[rs]);
                         tma::mbar_arrive(&a_full[as]);
+                    }
+                    if (++rs == nraw) rs = 0, rpar ^= 1u;
+                    if (++as == nas) {
+                        as = 0;
+                        if (a_first) a_first = false; else apar ^= 1u;
                     }
                     if (it == 0 && pend_ci >= 0) {
                         epilogue(pend_ci, pend_q0);
@@ -856,20 +879,49 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         if (pend_ci >= 0) epilogue(pend_ci, pend_q0);
     } else if (warp == kTaProdWarp) {
         // ---------------------------------------------------------- producer
-        if (lane == 0) {
-            const uint64_t pol = tma::policy_evict_first();
-            int64_t g = 0;
-            for (int blk = 0; blk < nblk; ++blk)
-                for (int ci = c_beg; ci < c_end; ++ci) {
-                    const uint8_t* src = a.slab + (int64_t)ci * a.chunk_bytes;
-                    for (int it = 0; it < kItems; ++it, ++g) {
-                        const int rs = (int)(g % nraw);
-                        if (g >= nraw) tma::mbar_wait_sleep(&raw_empty[rs], (unsigned)(((g / nraw) & 1) ^ 1));
+        // (whole warp: lane 0 moves the A item; the 16 X rows go one lane each, or as one copy
+        // when they are contiguous)
+        const uint64_t pol = tma::policy_evict_first();
+        int rs = 0, xs = 0;
+        unsigned rpar = 0, xpar = 0;  // parity of the *_empty waits from the second pass on
+        bool r_first = true, x_first = true;
+        for (int blk = 0; blk < nblk; ++blk) {
+            const int q0 = blk * kTcN;
+            const unsigned rowbytes = (unsigned)min((int64_t)kTcN, s - q0) * 4u;
+            const bool one = (uint64_t)ldx * 4u == rowbytes && rowbytes == kTcN * 4;
+            for (int ci = c_beg; ci < c_end; ++ci) {
+                const uint8_t* src = a.slab + (int64_t)ci * a.chunk_bytes;
+                const float* xsrc = x + (int64_t)p.chunks[ci].row0 * ldx + q0;
+                for (int it = 0; it < kItems; ++it) {
+                    if (lane == 0) {
+                        if (!r_first) tma::mbar_wait_sleep(&raw_empty[rs], rpar);
                         tma::mbar_arrive_tx(&raw_full[rs], (unsigned)a.item_bytes);
                         tma::bulk_g2s(ring + (size_t)rs * rslot, src + (int64_t)it * a.item_bytes,
                                       (unsigned)a.item_bytes, &raw_full[rs], pol);
                     }
+                    if (++rs == nraw) {
+                        rs = 0;
+                        if (r_first) r_first = false; else rpar ^= 1u;
+                    }
+                    if (xfast) {
+                        if (!x_first) tma::mbar_wait_sleep(&xraw_empty[xs], xpar);
+                        float* dst = xraw + (size_t)xs * (kTaXRawSlot / 4);
+                        const float* xr = xsrc + (int64_t)it * kTcAItemRows * ldx;
+                        const unsigned nv = (dbg & 8) ? 0u : (unsigned)kTcAItemRows;
+                        if (lane == 0) tma::mbar_arrive_tx(&xraw_full[xs], nv * rowbytes);
+                        __syncwarp();
+                        if (one) {
+                            if (lane == 0 && nv) tma::bulk_g2s_plain(dst, xr, nv * rowbytes, &xraw_full[xs]);
+                        } else if (lane < (int)nv) {
+                            tma::bulk_g2s_plain(dst + lane * kTcN, xr + (int64_t)lane * ldx, rowbytes, &xraw_full[xs]);
+                        }
+                        if (++xs == kTaXRawSlots) {
+                            xs = 0;
+                            if (x_first) x_first = false; else xpar ^= 1u;
+                        }
+                    }
                 }
+            }
         }
     } else if (warp == kTaMmaWarp) {
         // ---------------------------------------------------------- MMA issuer
@@ -928,62 +980,123 @@ __global__ void __launch_bounds__(kTaThreads, 1)
     } else {
         // ---------------------------------------------------------- X stagers
         const int t = threadIdx.x - kTaStageWarp0 * 32;
-        int64_t g = 0;
-        for (int blk = 0; blk < nblk; ++blk) {
-            const int q0 = blk * kTcN;
-            const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
-            const int lbo = (nn / 8) * 128;
-            const int nunits = 4 * nn;
-            // loads of the next item are issued before the current one is split and stored
-            // (and before the wait for its slot): one L2 latency per item off the critical path
-            auto load_item = [&](int ci, int it, float (&vals)[2][4]) {
-                const float* src = x + ((int64_t)p.chunks[ci].row0 + it * kTcAItemRows) * ldx + q0;
+        if (xfast) {
+            // stager warp 0 polls the item's two mbarriers; the others wait at a hardware barrier
+            int bs = 0, xs = 0;
+            unsigned bpar = 0, xpar = 0;
+            bool b_first = true;
+            for (int blk = 0; blk < nblk; ++blk) {
+                const int q0 = blk * kTcN;
+                const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
+                const int lbo = (nn / 8) * 128;
+                const int nunits = 4 * nn;
+                // this thread's two (column quad kc, right-hand side n) units, fixed for the pass
+                int kcs[2], ns[2], offs[2];
+                bool oks[2], lds[2];
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int u = e * 32 * kTaStageWarps + t;
-                    const int kc = u / nn, n = u - kc * nn;
-                    const bool ok = u < nunits && q0 + n < s;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) vals[e][k] = ok && !(dbg & 8) ? __ldg(src + (int64_t)(kc * 4 + k) * ldx + n) : 0.f;
+                    kcs[e] = u / nn, ns[e] = u - kcs[e] * nn;
+                    oks[e] = u < nunits;
+                    lds[e] = oks[e] && q0 + ns[e] < s && !(dbg & 8);
+                    offs[e] = kcs[e] * lbo + (ns[e] >> 3) * 128 + (ns[e] & 7) * 16;
                 }
-            };
-            float nxt[2][4];
-            if (c_beg < c_end) load_item(c_beg, 0, nxt);
-            for (int ci = c_beg; ci < c_end; ++ci) {
-                for (int it = 0; it < kItems; ++it, ++g) {
-                    const int bs = (int)(g % kTaBStages);
-                    float vals[2][4];
+                for (int ci = c_beg; ci < c_end; ++ci) {
+                    for (int it = 0; it < kItems; ++it) {
+                        if (warp == kTaStageWarp0) {
+                            tma::mbar_wait_sleep(&xraw_full[xs], xpar);
+                            if (!b_first) tma::mbar_wait_sleep(&b_empty[bs], bpar);
+                        }
+                        asm volatile("bar.sync 1, %0;" ::"n"(32 * kTaStageWarps) : "memory");
+                        const float* rb = xraw + (size_t)xs * (kTaXRawSlot / 4);
+                        uint8_t* bh = bring + (size_t)bs * kTaBSlot;
+                        uint8_t* bl = bh + kTaBHalf;
 #pragma unroll
-                    for (int e = 0; e < 2; ++e)
+                        for (int e = 0; e < 2; ++e) {
+                            if (!oks[e]) continue;
+                            float v4[4];
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) vals[e][k] = nxt[e][k];
-                    if (it + 1 < kItems)
-                        load_item(ci, it + 1, nxt);
-                    else if (ci + 1 < c_end)
-                        load_item(ci + 1, 0, nxt);
-                    if (g >= kTaBStages) tma::mbar_wait_sleep(&b_empty[bs], (unsigned)(((g / kTaBStages) & 1) ^ 1));
-                    uint8_t* bh = bring + (size_t)bs * kTaBSlot;
-                    uint8_t* bl = bh + kTaBHalf;
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int u = e * 32 * kTaStageWarps + t;
-                        if (u >= nunits) continue;
-                        const int kc = u / nn, n = u - kc * nn;
-                        uint4 h, l;
-                        tc::split_tf32(vals[e][0], h.x, l.x);
-                        tc::split_tf32(vals[e][1], h.y, l.y);
-                        tc::split_tf32(vals[e][2], h.z, l.z);
-                        tc::split_tf32(vals[e][3], h.w, l.w);
-                        const int off = kc * lbo + (n >> 3) * 128 + (n & 7) * 16;
-                        *reinterpret_cast<uint4*>(bh + off) = h;
-                        *reinterpret_cast<uint4*>(bl + off) = l;
+                            for (int k = 0; k < 4; ++k) v4[k] = lds[e] ? rb[(kcs[e] * 4 + k) * kTcN + ns[e]] : 0.f;
+                            uint4 h, l;
+                            tc::split_tf32(v4[0], h.x, l.x);
+                            tc::split_tf32(v4[1], h.y, l.y);
+                            tc::split_tf32(v4[2], h.z, l.z);
+                            tc::split_tf32(v4[3], h.w, l.w);
+                            *reinterpret_cast<uint4*>(bh + offs[e]) = h;
+                            *reinterpret_cast<uint4*>(bl + offs[e]) = l;
+                        }
+                        tma::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma::mbar_arrive(&b_full[bs]);
+                            tma::mbar_arrive(&xraw_empty[xs]);
+                        }
+                        if (++xs == kTaXRawSlots) xs = 0, xpar ^= 1u;
+                        if (++bs == kTaBStages) {
+                            bs = 0;
+                            if (b_first) b_first = false; else bpar ^= 1u;
+                        }
                     }
-                    tma::fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) tma::mbar_arrive(&b_full[bs]);
                 }
             }
-        }
+        } else {
+            int64_t g = 0;
+            for (int blk = 0; blk < nblk; ++blk) {
+                const int q0 = blk * kTcN;
+                const int nn = (int)min((int64_t)kTcN, (s - q0 + 15) / 16 * 16);
+                const int lbo = (nn / 8) * 128;
+                const int nunits = 4 * nn;
+                // loads of the next item are issued before the current one is split and stored
+                // (and before the wait for its slot): one L2 latency per item off the critical path
+                auto load_item = [&](int ci, int it, float (&vals)[2][4]) {
+                    const float* src = x + ((int64_t)p.chunks[ci].row0 + it * kTcAItemRows) * ldx + q0;
+    #pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int u = e * 32 * kTaStageWarps + t;
+                        const int kc = u / nn, n = u - kc * nn;
+                        const bool ok = u < nunits && q0 + n < s;
+    #pragma unroll
+                        for (int k = 0; k < 4; ++k) vals[e][k] = ok && !(dbg & 8) ? __ldg(src + (int64_t)(kc * 4 + k) * ldx + n) : 0.f;
+                    }
+                };
+                float nxt[2][4];
+                if (c_beg < c_end) load_item(c_beg, 0, nxt);
+                for (int ci = c_beg; ci < c_end; ++ci) {
+                    for (int it = 0; it < kItems; ++it, ++g) {
+                        const int bs = (int)(g % kTaBStages);
+                        float vals[2][4];
+    #pragma unroll
+                        for (int e = 0; e < 2; ++e)
+    #pragma unroll
+                            for (int k = 0; k < 4; ++k) vals[e][k] = nxt[e][k];
+                        if (it + 1 < kItems)
+                            load_item(ci, it + 1, nxt);
+                        else if (ci + 1 < c_end)
+                            load_item(ci + 1, 0, nxt);
+                        if (g >= kTaBStages) tma::mbar_wait_sleep(&b_empty[bs], (unsigned)(((g / kTaBStages) & 1) ^ 1));
+                        uint8_t* bh = bring + (size_t)bs * kTaBSlot;
+                        uint8_t* bl = bh + kTaBHalf;
+    #pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int u = e * 32 * kTaStageWarps + t;
+                            if (u >= nunits) continue;
+                            const int kc = u / nn, n = u - kc * nn;
+                            uint4 h, l;
+                            tc::split_tf32(vals[e][0], h.x, l.x);
+                            tc::split_tf32(vals[e][1], h.y, l.y);
+                            tc::split_tf32(vals[e][2], h.z, l.z);
+                            tc::split_tf32(vals[e][3], h.w, l.w);
+                            const int off = kc * lbo + (n >> 3) * 128 + (n & 7) * 16;
+                            *reinterpret_cast<uint4*>(bh + off) = h;
+                            *reinterpret_cast<uint4*>(bl + off) = l;
+                        }
+                        tma::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) tma::mbar_arrive(&b_full[bs]);
+                    }
+                }
+            }
+    }
     }
     tc::fence_before();
     __syncthreads();
