@@ -2,6 +2,7 @@
 // the streaming kernels.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 namespace hodlr {
 namespace tma {
@@ -34,6 +35,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // to `ns` nanoseconds per try (instead of spinning): for role warps that wait
 // most of the time, so their polling does not take issue slots from the warps
 // doing the work.
+#ifdef HODLR_MBAR_WATCHDOG
+// Diagnostic build: a wait that does not complete in ~10^5 tries reports itself (block 0) and gives up.
+__device__ __noinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity, unsigned ns = 20000) {
+    for (int it = 0;; ++it) {
+        unsigned ok;
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, P;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+            : "memory");
+        if (ok) return;
+        if (it > 200000) {
+            if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
+                printf("WATCHDOG warp %d barrier@%u parity %u state %llx\n", (int)(threadIdx.x >> 5), smem_u32(bar), parity,
+                       *reinterpret_cast<volatile unsigned long long*>(bar));
+            return;
+        }
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity, unsigned ns = 20000) {
     asm volatile(
         "{\n\t.reg .pred P;\n"
@@ -43,6 +66,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity, 
         "r"(parity), "r"(ns)
         : "memory");
 }
+#endif
 // Streaming (read-once) bytes: L2 evict-first.
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;

@@ -31,7 +31,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <thread>
 #include <vector>
 
 #include "async.cuh"
@@ -54,6 +56,15 @@ namespace {
 #define TC_TRACE_DECL
 #define TC_TR(arr, cond)
 #define TC_TRACE_DUMP(role, lead)
+#endif
+
+// Build with -DHODLR_TC_PROGRESS: lane 0 of every warp of CTA 0 of k_tc_a publishes (item << 8 | step)
+// to host-mapped memory; a host thread prints the table 3 s after the launch (who is stuck where).
+#ifdef HODLR_TC_PROGRESS
+__device__ volatile int* g_progress = nullptr;
+#define TC_PROG(step) if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && g_progress) g_progress[threadIdx.x >> 5] = (int)(pg << 8) | (step);
+#else
+#define TC_PROG(step)
 #endif
 
 constexpr int kTcConvWarps = 16;   // warp w: m-tile (w>>2)&1, lane quarter w&3, column half w>>3
@@ -346,12 +357,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     if (r_first) r_first = false; else rpar ^= 1u;
                 }
                 if (bfast) {
+                    // (lane 0 does every mbarrier wait of this warp: the other lanes block at the
+                    // __syncwarp below instead of spinning on a divergent path next to lane 0's)
                     const BSrc e = tab[i];
                     const int nv = (dbg & 8) ? 0 : e.nvalid;
-                    if (!b_first) tma::mbar_wait_sleep(&braw_empty[bslot], bpar ^ 1u);
                     float* dst = rawb + (size_t)bslot * (kTcBRawSlot / 4);
                     const bool one = (unsigned)e.ld * 4u == rowbytes && rowbytes == kTcN * 4;
-                    if (lane == 0) tma::mbar_arrive_tx(&braw_full[bslot], (unsigned)nv * rowbytes);
+                    if (lane == 0) {
+                        if (!b_first) tma::mbar_wait_sleep(&braw_empty[bslot], bpar ^ 1u);
+                        tma::mbar_arrive_tx(&braw_full[bslot], (unsigned)nv * rowbytes);
+                    }
                     __syncwarp();
                     if (one) {
                         if (lane == 0 && nv > 0)
@@ -771,8 +786,11 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         int lc = 0;  // chunks consumed (epilogues done)
         // epilogue of chunk ci (the lc-th chunk of this CTA): D -> running sums,
         // flushed at the node's last chunk of the run
+        [[maybe_unused]] int pg = 0;
         auto epilogue = [&](int ci, int q0) {
+            TC_PROG(5)
             tma::mbar_wait_sleep(acc_full, (unsigned)(lc & 1));
+            TC_PROG(6)
             tc::fence_after();
             // flush decision for this row's level (the whole warp loads D regardless)
             bool flush = false;
@@ -822,11 +840,14 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                 for (int it = 0; it < kItems; ++it, ++g) {
                     // only converter warp 0 polls the item's mbarriers; the others wait at a
                     // hardware barrier (their waiting takes no issue slots)
-                    if (warp == 0) {
+                    TC_PROG(1)
+                    if (warp == 0 || (dbg & 128)) {
                         tma::mbar_wait_sleep(&raw_full[rs], rpar);
                         if (!a_first) tma::mbar_wait_sleep(&a_empty[as], apar);
                     }
+                    TC_PROG(2)
                     asm volatile("bar.sync 2, %0;" ::"n"(32 * kTaConvWarps) : "memory");
+                    TC_PROG(3)
                     tc::fence_after();
                     uint32_t hi[16], lo[16];
                     if (lv >= 0 && !(dbg & 4)) {
@@ -862,6 +883,8 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                         tma::mbar_arrive(&raw_empty[rs]);
                         tma::mbar_arrive(&a_full[as]);
                     }
+                    TC_PROG(4)
+                    ++pg;
                     if (++rs == nraw) rs = 0, rpar ^= 1u;
                     if (++as == nas) {
                         as = 0;
@@ -883,6 +906,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         // when they are contiguous)
         const uint64_t pol = tma::policy_evict_first();
         int rs = 0, xs = 0;
+        [[maybe_unused]] int pg = 0;
         unsigned rpar = 0, xpar = 0;  // parity of the *_empty waits from the second pass on
         bool r_first = true, x_first = true;
         for (int blk = 0; blk < nblk; ++blk) {
@@ -894,7 +918,9 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                 const float* xsrc = x + (int64_t)p.chunks[ci].row0 * ldx + q0;
                 for (int it = 0; it < kItems; ++it) {
                     if (lane == 0) {
+                        TC_PROG(1)
                         if (!r_first) tma::mbar_wait_sleep(&raw_empty[rs], rpar);
+                        TC_PROG(2)
                         tma::mbar_arrive_tx(&raw_full[rs], (unsigned)a.item_bytes);
                         tma::bulk_g2s(ring + (size_t)rs * rslot, src + (int64_t)it * a.item_bytes,
                                       (unsigned)a.item_bytes, &raw_full[rs], pol);
@@ -904,11 +930,18 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                         if (r_first) r_first = false; else rpar ^= 1u;
                     }
                     if (xfast) {
-                        if (!x_first) tma::mbar_wait_sleep(&xraw_empty[xs], xpar);
+                        // (lane 0 does every mbarrier wait of this warp: the other lanes block at the
+                        // __syncwarp below instead of spinning on a divergent path next to lane 0's)
                         float* dst = xraw + (size_t)xs * (kTaXRawSlot / 4);
                         const float* xr = xsrc + (int64_t)it * kTcAItemRows * ldx;
-                        const unsigned nv = (dbg & 8) ? 0u : (unsigned)kTcAItemRows;
-                        if (lane == 0) tma::mbar_arrive_tx(&xraw_full[xs], nv * rowbytes);
+                        const unsigned nv = ((dbg & 8) && !(dbg & 64)) ? 0u : (unsigned)kTcAItemRows;
+                        if (lane == 0) {
+                            TC_PROG(3)
+                            if (!x_first) tma::mbar_wait_sleep(&xraw_empty[xs], xpar);
+                            TC_PROG(4)
+                            tma::mbar_arrive_tx(&xraw_full[xs], nv * rowbytes);
+                        }
+                        ++pg;
                         __syncwarp();
                         if (one) {
                             if (lane == 0 && nv) tma::bulk_g2s_plain(dst, xr, nv * rowbytes, &xraw_full[xs]);
@@ -932,6 +965,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
             int64_t g = 0;
             int lc = 0;
             int as = 0, bs = 0;
+            [[maybe_unused]] int pg = 0;
             unsigned a_par = 0, b_par = 0;
             for (int blk = 0; blk < nblk; ++blk) {
                 const int q0 = blk * kTcN;
@@ -939,12 +973,17 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                 const uint32_t idesc = tc::idesc_tf32(128, nn);
                 const uint32_t lbo = (uint32_t)(nn / 8) * 128;
                 for (int ci = c_beg; ci < c_end; ++ci, ++lc) {
+                    TC_PROG(1)
                     if (lc >= 1) tma::mbar_wait_sleep(acc_empty, (unsigned)((lc - 1) & 1));
                     for (int it = 0; it < kItems; ++it, ++g) {
                         // (stage indices and parities kept as counters: a 64-bit g % nas with a
                         // runtime nas takes the operands out of the uniform datapath)
+                        TC_PROG(2)
                         tma::mbar_wait_sleep(&a_full[as], a_par);
+                        TC_PROG(3)
                         tma::mbar_wait_sleep(&b_full[bs], b_par);
+                        TC_PROG(4)
+                        ++pg;
                         tc::fence_after();
                         const uint32_t bh = tc::smem_u32(bring + (size_t)bs * kTaBSlot), bl = bh + kTaBHalf;
 #pragma unroll
@@ -983,6 +1022,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         if (xfast) {
             // stager warp 0 polls the item's two mbarriers; the others wait at a hardware barrier
             int bs = 0, xs = 0;
+            [[maybe_unused]] int pg = 0;
             unsigned bpar = 0, xpar = 0;
             bool b_first = true;
             for (int blk = 0; blk < nblk; ++blk) {
@@ -1003,11 +1043,16 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                 }
                 for (int ci = c_beg; ci < c_end; ++ci) {
                     for (int it = 0; it < kItems; ++it) {
-                        if (warp == kTaStageWarp0) {
+                        TC_PROG(1)
+                        if (warp == kTaStageWarp0 || (dbg & 256)) {
                             tma::mbar_wait_sleep(&xraw_full[xs], xpar);
+                            TC_PROG(2)
                             if (!b_first) tma::mbar_wait_sleep(&b_empty[bs], bpar);
                         }
+                        TC_PROG(3)
                         asm volatile("bar.sync 1, %0;" ::"n"(32 * kTaStageWarps) : "memory");
+                        TC_PROG(4)
+                        ++pg;
                         const float* rb = xraw + (size_t)xs * (kTaXRawSlot / 4);
                         uint8_t* bh = bring + (size_t)bs * kTaBSlot;
                         uint8_t* bl = bh + kTaBHalf;
@@ -1283,7 +1328,9 @@ static hodlr_status tca_prepare(const MrInput& in, MrPlan& mr) {
     return HODLR_OK;
 }
 
-bool tca_usable(const MrPlan& mr, int64_t s) { return mr.tca_ok && s > 1 && !getenv("HODLR_B200_NO_TC"); }
+bool tca_usable(const MrPlan& mr, int64_t s) {
+    return mr.tca_ok && s > 1 && !getenv("HODLR_B200_NO_TC") && !getenv("HODLR_B200_NO_TCA");
+}
 
 cudaError_t tc_phase_a(const PlanView& p, const MrPlan& mr, const float* x, int64_t ldx, int64_t s, float* partial,
                        float* tbuf, cudaStream_t st) {
@@ -1293,12 +1340,32 @@ cudaError_t tc_phase_a(const PlanView& p, const MrPlan& mr, const float* x, int6
     cudaError_t e = cudaFuncSetAttribute(k_tc_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int nblk = (int)((s + kTcN - 1) / kTcN);
+#ifdef HODLR_TC_PROGRESS
+    {
+        static int* host = nullptr;
+        if (!host) {
+            cudaHostAlloc(&host, 64 * sizeof(int), cudaHostAllocMapped);
+            int* dev = nullptr;
+            cudaHostGetDevicePointer(&dev, host, 0);
+            cudaMemcpyToSymbol(g_progress, &dev, sizeof(dev));
+        }
+        for (int i = 0; i < 64; ++i) host[i] = -1;
+        std::thread([] {
+            std::this_thread::sleep_for(std::chrono::seconds(3));
+            fprintf(stderr, "PROGRESS");
+            for (int i = 0; i < kTaThreads / 32; ++i) fprintf(stderr, " w%d:%d.%d", i, host[i] >> 8, host[i] & 255);
+            fprintf(stderr, "\n");
+        }).detach();
+    }
+#endif
     k_tc_a<<<mr.view.nb, kTaThreads, sm, st>>>(p, mr.view, mr.tcav, x, ldx, s, (int)mr_spad(s), nblk, partial,
                                                 tbuf, nraw, getenv("HODLR_TC_DBG") ? atoi(getenv("HODLR_TC_DBG")) : 0);
     return cudaGetLastError();
 }
 
-bool tc_usable(const MrPlan& mr, int64_t s) { return mr.tc_ok && s > 1 && !getenv("HODLR_B200_NO_TC"); }
+bool tc_usable(const MrPlan& mr, int64_t s) {
+    return mr.tc_ok && s > 1 && !getenv("HODLR_B200_NO_TC") && !getenv("HODLR_B200_NO_TCB");
+}
 
 cudaError_t tc_phase_b(const PlanView& p, const MrPlan& mr, const float* x, int64_t ldx, float* b, int64_t ldb,
                        int64_t s, const float* tbuf, cudaStream_t st) {

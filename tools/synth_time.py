@@ -141,3 +141,4 @@ def main():
 
 if __name__ == "__main__":
     main()
+    time.sleep(float(os.environ.get("SYNTH_SLEEP", "0")))  # (diagnostic builds with a delayed host-side report)
