@@ -482,8 +482,6 @@ __global__ void __launch_bounds__(256) k_mr_reduce(PlanView p, const __grid_cons
                                                    W* __restrict__ tbuf, W* __restrict__ send,
                                                    const int32_t* __restrict__ list, int nbig = 0, int ty_big = 0,
                                                    int ty_small = 0) {
-    // one warp per output coefficient: lane l sums slots b0+l, b0+l+32, ... in
-    // order, then a fixed xor tree combines the lanes (deterministic)
     // ty_big > 0: ONE 1-D launch over the listed nodes, the first nbig (many
     // slots) with ty_big tiles each, the others with ty_small (no idle CTAs, one
     // launch instead of two); else grid (nodes, tiles)
@@ -536,31 +534,36 @@ __global__ void __launch_bounds__(256) k_mr_reduce(PlanView p, const __grid_cons
         }
         return;
     }
-    // many slots (upper levels): one warp per coefficient, lane l sums slots
-    // l, l+32, ... in order, then a fixed xor tree (deterministic)
-    for (int64_t base = (int64_t)by * 8; base < cnt_out; base += (int64_t)gy * 8) {
-        {
-            const int64_t i = base + warp;
-            if (i >= cnt_out) break;
-            W acc = W(0);
-            if (i < cnt) {
-                const int64_t c = i / s, q = i - c * s;
-                const W* src = partial + (L.part_rows + (int64_t)(sl.b0 + sl.jrel) * L.rv_pad + c) * spad + q;
-                int b = lane;
-                for (; b + 96 < nb; b += 128) {
-                    const W v0 = src[(int64_t)b * stride], v1 = src[(int64_t)(b + 32) * stride];
-                    const W v2 = src[(int64_t)(b + 64) * stride], v3 = src[(int64_t)(b + 96) * stride];
-                    acc += v0;
-                    acc += v1;
-                    acc += v2;
-                    acc += v3;
-                }
-                for (; b < nb; b += 32) acc += src[(int64_t)b * stride];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    // many slots (upper levels): a CTA owns 32 consecutive coefficients per step (one 128/256-byte
+    // row segment of every slot: coalesced).  Warp w sums slots w, w + 8, ... in order, four loads
+    // in flight; the 8 warp sums are combined in warp order through shared memory (deterministic).
+    __shared__ W red[8][33];
+    for (int64_t base = (int64_t)by * 32; base < cnt_out; base += (int64_t)gy * 32) {
+        const int64_t i = base + lane;
+        W acc = W(0);
+        if (i < cnt) {
+            const int64_t c = i / s, q = i - c * s;
+            const W* src = partial + (L.part_rows + (int64_t)(sl.b0 + sl.jrel) * L.rv_pad + c) * spad + q;
+            int bb = warp;
+            for (; bb + 24 < nb; bb += 32) {
+                const W v0 = src[(int64_t)bb * stride], v1 = src[(int64_t)(bb + 8) * stride];
+                const W v2 = src[(int64_t)(bb + 16) * stride], v3 = src[(int64_t)(bb + 24) * stride];
+                acc += v0;
+                acc += v1;
+                acc += v2;
+                acc += v3;
             }
-            if (lane == 0) dst[i] = acc;
+            for (; bb < nb; bb += 8) acc += src[(int64_t)bb * stride];
         }
+        red[warp][lane] = acc;
+        __syncthreads();
+        if (warp == 0 && i < cnt_out) {
+            W t = red[0][lane];
+#pragma unroll
+            for (int w = 1; w < 8; ++w) t += red[w][lane];
+            dst[i] = t;
+        }
+        __syncthreads();
     }
 }
 
@@ -2626,7 +2629,7 @@ template <typename W>
 cudaError_t launch_reduce(const PlanView& p, const MrPlan& mr, int64_t s, int spad, const W* partial, W* tbuf,
                           W* send, cudaStream_t st) {
     const int nsmall = mr.nmulti - mr.nbig;
-    const int64_t tb = ((int64_t)mr.rmax_big * s + 7) / 8, ts = ((int64_t)mr.rmax_small * s + 255) / 256;
+    const int64_t tb = ((int64_t)mr.rmax_big * s + 31) / 32, ts = ((int64_t)mr.rmax_small * s + 255) / 256;
     const int ty_big = (int)std::max<int64_t>(1, std::min<int64_t>(tb, 1024));
     const int ty_small = (int)std::max<int64_t>(1, std::min<int64_t>(ts, 1024));
     const int64_t blocks = (int64_t)mr.nbig * ty_big + (int64_t)nsmall * ty_small;

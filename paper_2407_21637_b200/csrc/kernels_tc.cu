@@ -687,7 +687,8 @@ constexpr int kTaBars = 2 * kTaMaxRaw + 2 * kTaMaxAStages + 2 * kTaBStages + 2 +
 // TMEM: D tiles at columns t*64, then A stages of nmt*32 columns (hi 16 | lo 16
 // per tile): 3 stages for <= 3 tiles (480 columns), 2 for 4 tiles (512)
 __host__ __device__ inline int ta_astages(const TcAView& a) { return a.nmt <= 3 ? 3 : 2; }
-__host__ __device__ inline int ta_srows(const TcAView& a) { return (a.mtot + 31) / 32 * 32; }
+// (odd row count: the per-row flush reads a row across the 64 columns without bank conflicts)
+__host__ __device__ inline int ta_srows(const TcAView& a) { return (a.mtot + 31) / 32 * 32 + 1; }
 
 __host__ __device__ inline size_t ta_raw_slot(const TcAView& a) { return ((size_t)a.item_bytes + 127) / 128 * 128; }
 // running sums [64 columns][nmt * 128 rows] fp32 (thread m owns column j at j*rows + m)
@@ -818,16 +819,34 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                 tc::wait_ld();
                 if (lv >= 0) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const float val = my[(cc + j) * srows] + __uint_as_float(v[j]);
-                        my[(cc + j) * srows] = flush ? 0.f : val;
-                        if (dst && cc + j < qn) dst[cc + j] = val;
-                    }
+                    for (int j = 0; j < 16; ++j) my[(cc + j) * srows] += __uint_as_float(v[j]);
                 }
             }
+            // the accumulator is free again: the MMA warp can start the next chunk while the
+            // finished rows are written out
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tma::mbar_arrive(acc_empty);
+            // flush, a row at a time with the lanes along the right-hand sides (coalesced 128-byte
+            // stores instead of one strided store per thread and column)
+            unsigned zm = __ballot_sync(0xffffffffu, flush);
+            const unsigned wm = __ballot_sync(0xffffffffu, flush && dst != nullptr);
+            const unsigned long long dbits = reinterpret_cast<unsigned long long>(dst);
+            while (zm) {
+                const int r = __ffs(zm) - 1;
+                zm &= zm - 1;
+                float* drow = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, dbits, r));
+                const bool wr = (wm >> r) & 1u;
+                float* srow = sums + (mt * 128 + qd * 32 + r);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = lane + 32 * h;
+                    const float val = srow[j * srows];
+                    if (wr && j < qn) drow[j] = val;
+                    srow[j * srows] = 0.f;
+                }
+            }
+            __syncwarp();
             ++lc;
         };
         int pend_ci = -1, pend_q0 = 0;
