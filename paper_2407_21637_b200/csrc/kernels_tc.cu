@@ -853,6 +853,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         int rs = 0, as = 0;
         unsigned rpar = 0, apar = 0;
         bool a_first = true;
+        const bool fin = a.finite != 0;
         for (int blk = 0; blk < nblk; ++blk) {
             const int q0 = blk * kTcN;
             for (int ci = c_beg; ci < c_end; ++ci) {
@@ -871,20 +872,26 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                     uint32_t hi[16], lo[16];
                     if (lv >= 0 && !(dbg & 4)) {
                         const uint8_t* rp = ring + (size_t)rs * rslot + seg + (size_t)c * 4 * w;
+                        float f[16];
+                        if (fmt == HODLR_FMT_FP32) {  // the four 16-byte loads issue back to back
 #pragma unroll
-                        for (int kc = 0; kc < 4; ++kc) {
-                            const float4 f = load_quad(fmt, rp + (size_t)kc * r8 * 4 * w);
-                            if (a.finite) {
-                                tc::split_tf32_fast(f.x, hi[4 * kc], lo[4 * kc]);
-                                tc::split_tf32_fast(f.y, hi[4 * kc + 1], lo[4 * kc + 1]);
-                                tc::split_tf32_fast(f.z, hi[4 * kc + 2], lo[4 * kc + 2]);
-                                tc::split_tf32_fast(f.w, hi[4 * kc + 3], lo[4 * kc + 3]);
-                            } else {
-                                tc::split_tf32(f.x, hi[4 * kc], lo[4 * kc]);
-                                tc::split_tf32(f.y, hi[4 * kc + 1], lo[4 * kc + 1]);
-                                tc::split_tf32(f.z, hi[4 * kc + 2], lo[4 * kc + 2]);
-                                tc::split_tf32(f.w, hi[4 * kc + 3], lo[4 * kc + 3]);
+                            for (int kc = 0; kc < 4; ++kc) {
+                                const float4 u = *reinterpret_cast<const float4*>(rp + (size_t)kc * r8 * 16);
+                                f[4 * kc] = u.x, f[4 * kc + 1] = u.y, f[4 * kc + 2] = u.z, f[4 * kc + 3] = u.w;
                             }
+                        } else {
+#pragma unroll
+                            for (int kc = 0; kc < 4; ++kc) {
+                                const float4 u = load_quad(fmt, rp + (size_t)kc * r8 * 4 * w);
+                                f[4 * kc] = u.x, f[4 * kc + 1] = u.y, f[4 * kc + 2] = u.z, f[4 * kc + 3] = u.w;
+                            }
+                        }
+                        if (fin) {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) tc::split_tf32_fast(f[e], hi[e], lo[e]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) tc::split_tf32(f[e], hi[e], lo[e]);
                         }
                     } else {
 #pragma unroll
