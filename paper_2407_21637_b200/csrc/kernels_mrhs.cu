@@ -476,6 +476,8 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_a(PlanView p, const __grid_co
 // ------------------------------------------------------------------ MR
 // grid.x = nodes, grid.y = tiles of 256 (c, q) coefficients: T[c][q] = sum
 // over the node's slots in CTA order (fixed order: deterministic).
+// nodes with more slots than this are summed by 8 warps per coefficient tile (k_mr_reduce)
+constexpr int kMrBigSlots = 32;
 template <typename W>
 __global__ void __launch_bounds__(256) k_mr_reduce(PlanView p, const __grid_constant__ MrView m, int node_lo,
                                                    int64_t s, int spad, const W* __restrict__ partial,
@@ -512,7 +514,7 @@ __global__ void __launch_bounds__(256) k_mr_reduce(PlanView p, const __grid_cons
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nb = sl.b1 - sl.b0 + 1;
     const int64_t i0 = (int64_t)by * 256;
-    if (nb <= 32) {
+    if (nb <= kMrBigSlots) {
         if (i0 >= cnt_out) return;
         // few slots: one thread per coefficient, slots in order
         for (int64_t i = i0 + threadIdx.x; i < cnt_out; i += (int64_t)gy * 256) {
@@ -2965,7 +2967,7 @@ hodlr_status mr_prepare(const MrInput& in, MrPlan& mr) {
     std::vector<int32_t> multi, small;
     for (size_t id = 0; id < nodes.size(); ++id)
         if (slots[id].b1 > slots[id].b0 || nodes[id].ext_slot >= 0) {
-            const bool big = slots[id].b1 - slots[id].b0 + 1 > 32;
+            const bool big = slots[id].b1 - slots[id].b0 + 1 > kMrBigSlots;
             const int w = std::max(nodes[id].rv, nodes[id].ext_slot >= 0 ? v.lev[nodes[id].level - 1].ext_w : 0);
             (big ? multi : small).push_back((int32_t)id);
             int& r = big ? mr.rmax_big : mr.rmax_small;
