@@ -680,22 +680,18 @@ constexpr int kTaBStages = 4;
 constexpr int kTaBHalf = kTcAItemRows * kTcN * 4;  // 4 KB
 constexpr int kTaBSlot = 2 * kTaBHalf;
 constexpr uint32_t kTaAcc = 0;
-constexpr int kTaMaxRaw = 6;
+constexpr int kTaMaxRaw = 8;
 constexpr int kTaXRawSlots = 4;                          // X source rows (fp32) in flight, filled by the producer
 constexpr int kTaXRawSlot = kTcAItemRows * kTcN * 4;     // 4 KB
 constexpr int kTaBars = 2 * kTaMaxRaw + 2 * kTaMaxAStages + 2 * kTaBStages + 2 + 2 * kTaXRawSlots;
 // TMEM: D tiles at columns t*64, then A stages of nmt*32 columns (hi 16 | lo 16
 // per tile): 3 stages for <= 3 tiles (480 columns), 2 for 4 tiles (512)
 __host__ __device__ inline int ta_astages(const TcAView& a) { return a.nmt <= 3 ? 3 : 2; }
-// (odd row count: the per-row flush reads a row across the 64 columns without bank conflicts)
-__host__ __device__ inline int ta_srows(const TcAView& a) { return (a.mtot + 31) / 32 * 32 + 1; }
 
 __host__ __device__ inline size_t ta_raw_slot(const TcAView& a) { return ((size_t)a.item_bytes + 127) / 128 * 128; }
-// running sums [64 columns][nmt * 128 rows] fp32 (thread m owns column j at j*rows + m)
-__host__ __device__ inline size_t ta_sum_bytes(const TcAView& a) { return (size_t)kTcN * ta_srows(a) * 4; }
 inline size_t ta_smem(const TcAView& a, int nraw) {
     return nraw * ta_raw_slot(a) + (size_t)kTaBStages * kTaBSlot + (size_t)kTaXRawSlots * kTaXRawSlot +
-           ta_sum_bytes(a) + kTaBars * 8 + 16;
+           kTaBars * 8 + 16;
 }
 // raw ring depth: as many item slots (<= kTaMaxRaw) as fit next to the rest
 inline int ta_nraw(const TcAView& a) {
@@ -713,8 +709,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
     uint8_t* ring = smem_raw;
     uint8_t* bring = ring + nraw * rslot;
     float* xraw = reinterpret_cast<float*>(bring + (size_t)kTaBStages * kTaBSlot);  // [4][16 rows][64] fp32 X rows
-    float* sums = xraw + (size_t)kTaXRawSlots * (kTaXRawSlot / 4);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sums) + ta_sum_bytes(a));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xraw + (size_t)kTaXRawSlots * (kTaXRawSlot / 4));
     uint64_t* raw_full = bars;
     uint64_t* raw_empty = raw_full + nraw;
     uint64_t* a_full = raw_empty + nraw;
@@ -779,21 +774,19 @@ __global__ void __launch_bounds__(kTaThreads, 1)
             }
         const int w = fmt_bytes(fmt);
         const uint32_t tl = tbase + ((uint32_t)(qd * 32) << 16);
-        const int srows = ta_srows(a);
-        float* my = sums + mrow;  // column j at my[j * srows]; rows >= mtot have no sums
-        if (lv >= 0)
-            for (int j = 0; j < kTcN; ++j) my[j * srows] = 0.f;
         int64_t g = 0;
         int lc = 0;  // chunks consumed (epilogues done)
-        // epilogue of chunk ci (the lc-th chunk of this CTA): D -> running sums,
-        // flushed at the node's last chunk of the run
+        // Epilogue of chunk ci (the lc-th chunk of this CTA).  The accumulator D stays in tensor
+        // memory ACROSS the chunks of a node (the MMAs keep accumulating): a warp touches D only
+        // when one of its rows ends its node's run here -- it reads D, writes the finished rows
+        // (to the coefficient buffer when this CTA holds the whole node, else to the node's
+        // partial slot), and stores D back with those rows zeroed.
         [[maybe_unused]] int pg = 0;
         auto epilogue = [&](int ci, int q0) {
             TC_PROG(5)
             tma::mbar_wait_sleep(acc_full, (unsigned)(lc & 1));
             TC_PROG(6)
             tc::fence_after();
-            // flush decision for this row's level (the whole warp loads D regardless)
             bool flush = false;
             float* dst = nullptr;
             if (lv >= 0 && !(dbg & 16)) {
@@ -811,42 +804,38 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                     }
                 }
             }
-            const int qn = (int)min((int64_t)kTcN, s - q0);
+            if (mt < a.nmt && __any_sync(0xffffffffu, flush)) {
+                const int qn = (int)min((int64_t)kTcN, s - q0);
+                const bool vec = dst && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
 #pragma unroll 1
-            for (int cc = 0; cc < kTcN; cc += 16) {
-                uint32_t v[16];
-                tc::ld_x16(tl + kTaAcc + mt * 64 + cc, v);
-                tc::wait_ld();
-                if (lv >= 0) {
+                for (int cc = 0; cc < kTcN; cc += 16) {
+                    uint32_t v[16];
+                    tc::ld_x16(tl + kTaAcc + mt * 64 + cc, v);
+                    tc::wait_ld();
+                    if (flush) {
+                        if (dst) {
+                            if (vec && cc + 16 <= qn) {  // 64 contiguous bytes per row: whole sectors
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) my[(cc + j) * srows] += __uint_as_float(v[j]);
+                                for (int j = 0; j < 16; j += 4)
+                                    *reinterpret_cast<float4*>(dst + cc + j) =
+                                        make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                    __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 16; ++j)
+                                    if (cc + j < qn) dst[cc + j] = __uint_as_float(v[j]);
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = 0u;
+                    }
+                    tc::st_x16(tl + kTaAcc + mt * 64 + cc, v);
                 }
+                tc::wait_st();
             }
-            // the accumulator is free again: the MMA warp can start the next chunk while the
-            // finished rows are written out
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tma::mbar_arrive(acc_empty);
-            // flush, a row at a time with the lanes along the right-hand sides (coalesced 128-byte
-            // stores instead of one strided store per thread and column)
-            unsigned zm = __ballot_sync(0xffffffffu, flush);
-            const unsigned wm = __ballot_sync(0xffffffffu, flush && dst != nullptr);
-            const unsigned long long dbits = reinterpret_cast<unsigned long long>(dst);
-            while (zm) {
-                const int r = __ffs(zm) - 1;
-                zm &= zm - 1;
-                float* drow = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, dbits, r));
-                const bool wr = (wm >> r) & 1u;
-                float* srow = sums + (mt * 128 + qd * 32 + r);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int j = lane + 32 * h;
-                    const float val = srow[j * srows];
-                    if (wr && j < qn) drow[j] = val;
-                    srow[j * srows] = 0.f;
-                }
-            }
-            __syncwarp();
             ++lc;
         };
         int pend_ci = -1, pend_q0 = 0;
@@ -1022,7 +1011,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                                 const uint32_t d = tbase + kTaAcc + t * 64;
                                 const uint32_t ah = tbase + abase + as * astride + t * 32 + j;
                                 if (dbg & 2) continue;
-                                tc::mma_tf32_ts_u(d, ah, dh, idesc, (it | j) != 0, leader);
+                                tc::mma_tf32_ts_u(d, ah, dh, idesc, (lc | it | j) != 0, leader);
                                 tc::mma_tf32_ts_u(d, ah, dl, idesc, 1, leader);
                                 if (((a.tile_full >> t) & 1) && !(dbg & 1)) tc::mma_tf32_ts_u(d, ah + 16, dh, idesc, 1, leader);
                             }
