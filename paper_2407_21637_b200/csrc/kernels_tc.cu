@@ -689,17 +689,29 @@ constexpr int kTaBars = 2 * kTaMaxRaw + 2 * kTaMaxAStages + 2 * kTaBStages + 2 +
 __host__ __device__ inline int ta_astages(const TcAView& a) { return a.nmt <= 3 ? 3 : 2; }
 
 __host__ __device__ inline size_t ta_raw_slot(const TcAView& a) { return ((size_t)a.item_bytes + 127) / 128 * 128; }
-inline size_t ta_smem(const TcAView& a, int nraw) {
+// Cross-chunk running sums of the accurate variant: [stacked row][64 columns + 4 pad] fp32 in
+// shared memory (the pad makes the per-thread 16-byte row accesses conflict-free)
+constexpr int kTaSumLd = kTcN + 4;
+__host__ __device__ inline size_t ta_sum_bytes(const TcAView& a, bool tmem_sums) {
+    return tmem_sums ? 0 : (size_t)((a.mtot + 31) / 32 * 32) * kTaSumLd * 4;
+}
+inline size_t ta_smem(const TcAView& a, int nraw, bool tmem_sums) {
     return nraw * ta_raw_slot(a) + (size_t)kTaBStages * kTaBSlot + (size_t)kTaXRawSlots * kTaXRawSlot +
-           kTaBars * 8 + 16;
+           ta_sum_bytes(a, tmem_sums) + kTaBars * 8 + 16;
 }
 // raw ring depth: as many item slots (<= kTaMaxRaw) as fit next to the rest
-inline int ta_nraw(const TcAView& a) {
+inline int ta_nraw(const TcAView& a, bool tmem_sums) {
     int n = kTaMaxRaw;
-    while (n > 2 && ta_smem(a, n) > 227 * 1024) --n;
+    if (const char* e = getenv("HODLR_B200_TA_NRAW")) n = std::max(2, std::min(kTaMaxRaw, atoi(e)));  // (ring-depth sweeps)
+    while (n > 2 && ta_smem(a, n, tmem_sums) > 227 * 1024) --n;
     return n;
 }
 
+// TSUM = true: the accumulator stays in tensor memory across a node's chunks (fastest; the
+// tensor core's truncating fp32 accumulation then runs over the whole run: error ~4x larger).
+// TSUM = false (default): per-chunk accumulator, cross-chunk sums added in fp32 (round to
+// nearest) by the converter warps in shared memory.
+template <bool TSUM>
 __global__ void __launch_bounds__(kTaThreads, 1)
     k_tc_a(PlanView p, const __grid_constant__ MrView m, const __grid_constant__ TcAView a,
            const float* __restrict__ x, int64_t ldx, int64_t s, int spad, int nblk, float* __restrict__ partial,
@@ -709,7 +721,8 @@ __global__ void __launch_bounds__(kTaThreads, 1)
     uint8_t* ring = smem_raw;
     uint8_t* bring = ring + nraw * rslot;
     float* xraw = reinterpret_cast<float*>(bring + (size_t)kTaBStages * kTaBSlot);  // [4][16 rows][64] fp32 X rows
-    uint64_t* bars = reinterpret_cast<uint64_t*>(xraw + (size_t)kTaXRawSlots * (kTaXRawSlot / 4));
+    float* sums = xraw + (size_t)kTaXRawSlots * (kTaXRawSlot / 4);  // (TSUM = false only)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sums) + ta_sum_bytes(a, TSUM));
     uint64_t* raw_full = bars;
     uint64_t* raw_empty = raw_full + nraw;
     uint64_t* a_full = raw_empty + nraw;
@@ -776,6 +789,11 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         const uint32_t tl = tbase + ((uint32_t)(qd * 32) << 16);
         int64_t g = 0;
         int lc = 0;  // chunks consumed (epilogues done)
+        if constexpr (!TSUM) {
+            if (lv >= 0)
+                for (int j = 0; j < kTcN; j += 4)
+                    *reinterpret_cast<float4*>(sums + (size_t)mrow * kTaSumLd + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         // Epilogue of chunk ci (the lc-th chunk of this CTA).  The accumulator D stays in tensor
         // memory ACROSS the chunks of a node (the MMAs keep accumulating): a warp touches D only
         // when one of its rows ends its node's run here -- it reads D, writes the finished rows
@@ -804,38 +822,85 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                     }
                 }
             }
-            if (mt < a.nmt && __any_sync(0xffffffffu, flush)) {
-                const int qn = (int)min((int64_t)kTcN, s - q0);
-                const bool vec = dst && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+            if constexpr (TSUM) {
+                if (mt < a.nmt && __any_sync(0xffffffffu, flush)) {
+                    const int qn = (int)min((int64_t)kTcN, s - q0);
+                    const bool vec = dst && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+    #pragma unroll 1
+                    for (int cc = 0; cc < kTcN; cc += 16) {
+                        uint32_t v[16];
+                        tc::ld_x16(tl + kTaAcc + mt * 64 + cc, v);
+                        tc::wait_ld();
+                        if (flush) {
+                            if (dst) {
+                                if (vec && cc + 16 <= qn) {  // 64 contiguous bytes per row: whole sectors
+    #pragma unroll
+                                    for (int j = 0; j < 16; j += 4)
+                                        *reinterpret_cast<float4*>(dst + cc + j) =
+                                            make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                        __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+                                } else {
+    #pragma unroll
+                                    for (int j = 0; j < 16; ++j)
+                                        if (cc + j < qn) dst[cc + j] = __uint_as_float(v[j]);
+                                }
+                            }
+    #pragma unroll
+                            for (int j = 0; j < 16; ++j) v[j] = 0u;
+                        }
+                        tc::st_x16(tl + kTaAcc + mt * 64 + cc, v);
+                    }
+                    tc::wait_st();
+                }
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tma::mbar_arrive(acc_empty);
+            } else {
+                // D (this chunk) -> running sums of this thread's row, 16 bytes at a time
+                float* my = sums + (size_t)mrow * kTaSumLd;
+                if (mt < a.nmt) {
 #pragma unroll 1
-                for (int cc = 0; cc < kTcN; cc += 16) {
-                    uint32_t v[16];
-                    tc::ld_x16(tl + kTaAcc + mt * 64 + cc, v);
-                    tc::wait_ld();
-                    if (flush) {
-                        if (dst) {
-                            if (vec && cc + 16 <= qn) {  // 64 contiguous bytes per row: whole sectors
+                    for (int cc = 0; cc < kTcN; cc += 16) {
+                        uint32_t v[16];
+                        tc::ld_x16(tl + kTaAcc + mt * 64 + cc, v);
+                        tc::wait_ld();
+                        if (lv >= 0) {
 #pragma unroll
-                                for (int j = 0; j < 16; j += 4)
-                                    *reinterpret_cast<float4*>(dst + cc + j) =
-                                        make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                                    __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-                            } else {
-#pragma unroll
-                                for (int j = 0; j < 16; ++j)
-                                    if (cc + j < qn) dst[cc + j] = __uint_as_float(v[j]);
+                            for (int j = 0; j < 16; j += 4) {
+                                float4 t = *reinterpret_cast<float4*>(my + cc + j);
+                                t.x += __uint_as_float(v[j]), t.y += __uint_as_float(v[j + 1]);
+                                t.z += __uint_as_float(v[j + 2]), t.w += __uint_as_float(v[j + 3]);
+                                *reinterpret_cast<float4*>(my + cc + j) = t;
                             }
                         }
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) v[j] = 0u;
                     }
-                    tc::st_x16(tl + kTaAcc + mt * 64 + cc, v);
                 }
-                tc::wait_st();
+                // the accumulator is free again: the MMA warp starts the next chunk while the
+                // finished rows are written out
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tma::mbar_arrive(acc_empty);
+                // flush a row at a time, lanes along the right-hand sides (coalesced stores)
+                const int qn = (int)min((int64_t)kTcN, s - q0);
+                unsigned zm = __ballot_sync(0xffffffffu, flush);
+                const unsigned wm = __ballot_sync(0xffffffffu, flush && dst != nullptr);
+                const unsigned long long dbits = reinterpret_cast<unsigned long long>(dst);
+                while (zm) {
+                    const int r = __ffs(zm) - 1;
+                    zm &= zm - 1;
+                    float* drow = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, dbits, r));
+                    const bool wr = (wm >> r) & 1u;
+                    float* srow = sums + (size_t)(mt * 128 + qd * 32 + r) * kTaSumLd;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int j = lane + 32 * h;
+                        const float val = srow[j];
+                        if (wr && j < qn) drow[j] = val;
+                        srow[j] = 0.f;
+                    }
+                }
+                __syncwarp();
             }
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) tma::mbar_arrive(acc_empty);
             ++lc;
         };
         int pend_ci = -1, pend_q0 = 0;
@@ -1011,7 +1076,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
                                 const uint32_t d = tbase + kTaAcc + t * 64;
                                 const uint32_t ah = tbase + abase + as * astride + t * 32 + j;
                                 if (dbg & 2) continue;
-                                tc::mma_tf32_ts_u(d, ah, dh, idesc, (lc | it | j) != 0, leader);
+                                tc::mma_tf32_ts_u(d, ah, dh, idesc, ((TSUM ? lc : 0) | it | j) != 0, leader);
                                 tc::mma_tf32_ts_u(d, ah, dl, idesc, 1, leader);
                                 if (((a.tile_full >> t) & 1) && !(dbg & 1)) tc::mma_tf32_ts_u(d, ah + 16, dh, idesc, 1, leader);
                             }
@@ -1322,7 +1387,7 @@ static hodlr_status tca_prepare(const MrInput& in, MrPlan& mr) {
     a.nmt = (mb + 127) / 128;
     a.item_bytes = seg;
     a.chunk_bytes = (int64_t)seg * (kChunkRowsTa / kTcAItemRows);
-    if (ta_smem(a, 2) > 227 * 1024) return HODLR_OK;
+    if (ta_smem(a, 2, false) > 227 * 1024) return HODLR_OK;
     const size_t bytes = (size_t)a.chunk_bytes * in.chunks->size();
     void* d = nullptr;
     if (cudaMalloc(&d, bytes) != cudaSuccess) {
@@ -1350,9 +1415,14 @@ bool tca_usable(const MrPlan& mr, int64_t s) {
 cudaError_t tc_phase_a(const PlanView& p, const MrPlan& mr, const float* x, int64_t ldx, int64_t s, float* partial,
                        float* tbuf, cudaStream_t st) {
     if (p.nchunks == 0) return cudaSuccess;
-    const int nraw = ta_nraw(mr.tcav);
-    const size_t sm = ta_smem(mr.tcav, nraw);
-    cudaError_t e = cudaFuncSetAttribute(k_tc_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    // HODLR_B200_TC_SUMS=tmem: keep a node's running sums in tensor memory (faster, ~4x the
+    // rounding error: the tensor core accumulates with truncation); default: fp32 sums in smem
+    const char* sums_env = getenv("HODLR_B200_TC_SUMS");
+    const bool tsum = sums_env && sums_env[0] == 't';
+    const int nraw = ta_nraw(mr.tcav, tsum);
+    const size_t sm = ta_smem(mr.tcav, nraw, tsum);
+    auto kern = tsum ? k_tc_a<true> : k_tc_a<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int nblk = (int)((s + kTcN - 1) / kTcN);
 #ifdef HODLR_TC_PROGRESS
@@ -1373,7 +1443,7 @@ cudaError_t tc_phase_a(const PlanView& p, const MrPlan& mr, const float* x, int6
         }).detach();
     }
 #endif
-    k_tc_a<<<mr.view.nb, kTaThreads, sm, st>>>(p, mr.view, mr.tcav, x, ldx, s, (int)mr_spad(s), nblk, partial,
+    kern<<<mr.view.nb, kTaThreads, sm, st>>>(p, mr.view, mr.tcav, x, ldx, s, (int)mr_spad(s), nblk, partial,
                                                 tbuf, nraw, getenv("HODLR_TC_DBG") ? atoi(getenv("HODLR_TC_DBG")) : 0);
     return cudaGetLastError();
 }
