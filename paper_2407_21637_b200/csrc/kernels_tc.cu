@@ -15,19 +15,26 @@
 // Accumulation is fp32 in tensor memory.
 //
 // Warp roles (one CTA per SM, persistent over (leaf, column block) work units):
-//   warps 0-7  converters: warp w owns m-tile w/4 (leaf rows 128*(w/4) ..) and
-//              TMEM lane quarter w%4; thread = one leaf row.  Per item: wait for
-//              the raw bytes, load the row's values (one vector load per column
-//              quad), split, tcgen05.st hi/lo into the item's TMEM A stage.
-//              They also run the epilogue of the previous leaf (tcgen05.ld of
-//              the accumulator, b written once: disjoint rows, no atomics),
-//              deferred by one item so it overlaps the next leaf's first MMAs.
-//   warp 8     producer: one cp.async.bulk per item into a 4-slot ring.
-//   warp 9     MMA issuer (one thread) and TMEM owner (512 columns).
-//   warps 10-13 B stagers: X / T rows -> tf32 hi/lo in the K-major no-swizzle
-//              canonical layout (core matrix = 8 columns x 4 k), 3-slot ring.
-// TMEM columns: accumulators [2 buffers][2 m-tiles][64] at 0..255, A stages
-// [2][2 m-tiles][hi 32 | lo 32] at 256..511.
+//   warps 0-15  converters: warp w owns m-tile (w/4)%2 (leaf rows 128*m ..), TMEM lane
+//               quarter w%4 and column half w/8 of the item; thread = one leaf row.
+//               Per item: warp 0 polls the item's two mbarriers (raw bytes landed, A stage
+//               free), the other 15 wait at a hardware barrier (no polling instructions);
+//               then four 16-byte loads, split, two tcgen05.st.x16 (hi, lo) into the item's
+//               TMEM A stage.  They also run the epilogue of the previous leaf (tcgen05.ld
+//               of the accumulator, b written once: disjoint rows, no atomics), deferred by
+//               one item so it overlaps the next leaf's first MMAs.
+//   warp 16     producer: lane 0 moves the A item (one cp.async.bulk into a 4-slot ring) and
+//               does every mbarrier wait of the warp; the B source rows (X or T, fp32) of
+//               the item go as one bulk copy (contiguous rows) or one row per lane into a
+//               second 4-slot ring.  A per-leaf table holds every item's source pointer.
+//   warp 17     MMA issuer (whole warp in uniform control flow, the tcgen05.mma / commit
+//               predicated on one elected lane: tc::mma_tf32_ts_u) and TMEM owner.
+//   warps 18-25 B stagers: source rows (shared memory) -> tf32 hi/lo in the K-major
+//               no-swizzle canonical layout (core matrix = 8 columns x 4 k), 3-slot ring;
+//               warp 18 polls, the others wait at a hardware barrier.  Operands that are
+//               not 16-byte aligned take the register-staged path (loads from global).
+// TMEM columns: accumulator [2 m-tiles][64] at 0..127, A stages [3][2 m-tiles][hi 32 | lo 32]
+// at 128..511.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -663,12 +670,14 @@ __global__ void k_tc_slab(PlanView p, const __grid_constant__ TcView v, int64_t 
 
 // ====================================================================== phase A
 // Warp roles: 0-15 converters / epilogue (warp w: M-tile w/4, TMEM lane quarter
-// w%4; thread = one stacked rank row m), 16 producer, 17 MMA issuer + TMEM
-// owner, 18-21 X stagers.  CTA b owns chunks [b*nch/nb, (b+1)*nch/nb) (the
-// MrView slot layout), per chunk D = sum over 16 items; the converters keep a
-// running sum per (row m, column) in registers across the chunks of the node
-// and flush it at the node's last chunk of the run: to the coefficient buffer
-// when this CTA holds the whole node, else to the node's partial slot.
+// w%4; thread = one stacked rank row m; warp 0 polls the item's mbarriers, the
+// others wait at a hardware barrier), 16 producer (A item by lane 0, the item's
+// 16 X rows by bulk copy into a 4-slot ring), 17 MMA issuer + TMEM owner, 18-21 X
+// stagers (warp 18 polls).  CTA b owns chunks [b*nch/nb, (b+1)*nch/nb) (the MrView
+// slot layout), per chunk D = sum over 16 items.  Cross-chunk sums of a node's
+// run: see the TSUM template parameter of k_tc_a; a finished row is written to
+// the coefficient buffer when this CTA holds the whole node, else to the node's
+// partial slot (fixed-order reduce afterwards).
 constexpr int kTaConvWarps = 4 * kTcAMaxTiles;
 constexpr int kTaProdWarp = kTaConvWarps;
 constexpr int kTaMmaWarp = kTaConvWarps + 1;
