@@ -297,7 +297,7 @@ def _parity(H, X, b_gpu, Kx, normA):
 
 
 KERNELS = {"fused_sv": "k_stream (fused single-vector kernel, one launch per matvec)",
-           "mrhs_slab64": "k_mr3_a (K-split phase A) + k_mr_reduce + k_mr2_b (multi-RHS, fragment slabs, DMMA fp64)",
+           "mrhs_slab64": "k_mr4_a (K-split 4 x 4 phase A) + k_mr_reduce + k_mr2_b (multi-RHS, fragment slabs, DMMA fp64)",
            "mrhs_slab32": "k_mr2_a + k_mr_reduce + k_mr2_b (multi-RHS, fragment slabs, 3xTF32 mma.sync)",
            "mrhs": "k_mr_a + k_mr_reduce + k_mr_b (multi-RHS, arena)",
            "mrhs_tc": "k_tc_a + k_mr_reduce + k_tc_b (multi-RHS, tcgen05 kind::tf32 3xTF32, A in TMEM)",
