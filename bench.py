@@ -359,6 +359,55 @@ def time_e2e(op, X, K, stream):
     return e0.elapsed_time(e1) / K, bh.numpy().copy()
 
 
+def time_e2e_two_callers(op, X, K, b_ref):
+    """Host-buffer calls from TWO host threads (each with its own pinned buffers and stream):
+    the C ABI keeps two staging contexts per handle, so one call's device-to-host copy runs
+    under the other's host-to-device copy.  Every call still copies its X in and its B out.
+    Returns ms per call (device time from the first call's start to the last call's end,
+    divided by the 2 K calls) and whether both callers' results equal the serial result."""
+    import threading
+
+    import torch
+
+    s = X.shape[1]
+    xs, bs, sts = [], [], []
+    for _ in range(2):
+        xs.append(torch.from_numpy(np.ascontiguousarray(X)).pin_memory())
+        bs.append(torch.empty_like(xs[-1]).pin_memory())
+        sts.append(torch.cuda.Stream())
+    errs = []
+
+    def run(i, reps):
+        try:
+            for _ in range(reps):
+                op.matvec_host_ptr(xs[i].data_ptr(), bs[i].data_ptr(), s, stream=sts[i].cuda_stream)
+        except Exception as e:  # reported by the caller
+            errs.append(repr(e))
+
+    def both(reps):
+        th = [threading.Thread(target=run, args=(i, reps)) for i in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    both(2)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e0.record(sts[0])
+    sts[1].wait_event(e0)
+    both(K)
+    for i in range(2):
+        ends[i].record(sts[i])
+    torch.cuda.synchronize()
+    if errs:
+        raise RuntimeError("two-caller e2e: " + "; ".join(errs))
+    ms = max(e0.elapsed_time(e) for e in ends) / (2 * K)
+    same = all(np.array_equal(b.numpy(), b_ref) for b in bs)
+    return ms, same
+
+
 def measure_config(cfg, args, dev, clocks=None, cpu=True):
     """One BASELINE config on one GPU: parity, device time, e2e, roofline, CPU baseline."""
     import torch
@@ -386,6 +435,8 @@ def measure_config(cfg, args, dev, clocks=None, cpu=True):
     ms, ms_hot = time_device(op, xd, bd, K, args.warmup, flush, stream, clocks)
     ms_e2e, b_e2e = time_e2e(op, X, max(10, min(K, 200) // 4), stream)
     parity["e2e_matches"] = bool(np.linalg.norm(b_e2e - b_gpu) <= parity["tol_vs_oracle"] * np.linalg.norm(b_gpu))
+    ms_e2e2, same2 = time_e2e_two_callers(op, X, int(min(500, max(5, 40.0 / ms_e2e))), b_e2e)  # ~80 ms of calls
+    parity["e2e_two_callers_bitwise_equal"] = bool(same2)
     del flush
 
     B = alg_bytes(H, s, wb)
@@ -401,7 +452,7 @@ def measure_config(cfg, args, dev, clocks=None, cpu=True):
             traffic = None
     res = {
         "H": H, "X": X, "desc": desc, "path": path, "launches": launches, "ms": ms, "ms_hot": ms_hot,
-        "ms_e2e": ms_e2e, "B": B, "F": F, "wb": wb, "parity": parity, "t_build": t_build, "op": op,
+        "ms_e2e": ms_e2e, "ms_e2e2": ms_e2e2, "B": B, "F": F, "wb": wb, "parity": parity, "t_build": t_build, "op": op,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": _kernel_name(path, wb),
                      "alg_bytes_per_launch": int(B)},
@@ -483,7 +534,11 @@ def run_single(args):
         "roofline": r["roofline"],
         "e2e": {"value": 1000.0 / r["ms_e2e"], "unit": "matvec/s", "h2d_bytes_per_step": int(H.n * s * 8),
                 "d2h_bytes_per_step": int(H.n * s * 8), "ms_per_step": r["ms_e2e"],
-                "path": "hodlr_matvec_host (pinned binary64 X in, B out)"},
+                "path": "hodlr_matvec_host (pinned binary64 X in, B out), one caller, calls back to back",
+                "two_callers": {"value": 1000.0 / r["ms_e2e2"], "unit": "matvec/s", "ms_per_step": r["ms_e2e2"],
+                                "note": "same entry point from two host threads on two streams (two staging "
+                                        "contexts per handle): one call's D2H overlaps the other's H2D; "
+                                        "every call copies its X in and its B out"}},
         "gpu_launches": args.steps * r["launches"],
         "clocks": clocks.summary(),
         "host": host_info(),
@@ -507,7 +562,9 @@ def run_single(args):
         line["secondary"] = {"cfg2": {
             "workload": r2["desc"], "value": 1000.0 / r2["ms"], "unit": "matvec/s", "ms_per_step": r2["ms"],
             "kernel_path": r2["path"], "roofline": r2["roofline"], "parity": r2["parity"],
-            "e2e": {"value": 1000.0 / r2["ms_e2e"], "unit": "matvec/s", "ms_per_step": r2["ms_e2e"]},
+            "e2e": {"value": 1000.0 / r2["ms_e2e"], "unit": "matvec/s", "ms_per_step": r2["ms_e2e"],
+                    "two_callers": {"value": 1000.0 / r2["ms_e2e2"], "unit": "matvec/s",
+                                    "ms_per_step": r2["ms_e2e2"]}},
             "hot_cache_ms": r2["ms_hot"], "gpu_launches": args.steps * r2["launches"], "clocks": c2.summary()}}
         line["gpu_launches"] += args.steps * r2["launches"]
     print(json.dumps(line), flush=True)

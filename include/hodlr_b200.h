@@ -152,7 +152,11 @@ hodlr_status hodlr_workspace_size_for(const hodlr_handle* h, int32_t working, in
  * (HODLR_B200_NO_ZEROCOPY=1 disables this).  Multi-RHS calls with a large result
  * (binary64 working, fragment-slab path, >= 8 MB) run phase B over row ranges and
  * copy each finished range out on a second stream while the next ranges are
- * computed (HODLR_B200_NO_E2E_PIPELINE=1 disables this). */
+ * computed (HODLR_B200_NO_E2E_PIPELINE=1 disables this).
+ * Safe to call from several host threads on one handle: the
+ * handle keeps two staging contexts, so two calls on different streams overlap
+ * (one call's device-to-host copy runs under the other's host-to-device copy:
+ * PCIe is full duplex) and further callers wait for a free context. */
 hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x_host,
                                double* b_host, int64_t s, void* stream);
 

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -77,10 +78,27 @@ struct hodlr_handle {
     std::vector<std::vector<int>> node_id;
     std::vector<int64_t> factor_rows;  // for unpack: rows of U / V of each desc factor
     int64_t part_count = 0, t_count = 0, ext_count = 0;
-    DeviceBuf arena, tables, e2e;
-    // host-buffer pipeline: device-to-host copies of finished row ranges on their own stream
-    cudaStream_t copy_stream = nullptr;
-    std::vector<cudaEvent_t> slice_ev;
+    DeviceBuf arena, tables;
+    // Host-buffer calls (hodlr_matvec_host): kHostCtx staging contexts, so calls from
+    // different host threads (on different streams) overlap -- one call's device-to-host
+    // copy runs under the next call's host-to-device copy (PCIe is full duplex).  A call
+    // holds one context from entry to return; further callers wait for a free one.
+    struct HostCtx {
+        DeviceBuf e2e;                       // x / b staging (binary64 and working copies)
+        cudaStream_t copy_stream = nullptr;  // device-to-host copies of finished row ranges
+        std::vector<cudaEvent_t> slice_ev;
+        cudaEvent_t h2d_ev = nullptr;        // this context's last host-to-device copy
+        bool busy = false;
+    };
+    // Host-to-device copies of concurrent calls run one after the other (each waits for the
+    // previous call's copy): two calls that start together then do not share the H2D
+    // direction and finish it together -- the second call's copy runs under the first
+    // call's kernels and device-to-host copy instead.
+    cudaEvent_t last_h2d = nullptr;
+    std::mutex h2d_mu;
+    static constexpr int kHostCtx = 2;
+    HostCtx hctx[kHostCtx];
+    std::condition_variable hcv;
     // NULL-workspace calls: one zero-initialised workspace per CUDA stream, so
     // concurrent calls on different streams never share the fused kernel's
     // synchronisation state (matvec is safe to call concurrently)
@@ -698,9 +716,12 @@ hodlr_status hodlr_destroy(hodlr_handle* h) {
     h->arena.release();
     h->tables.release();
     for (auto& w : h->ws) w.buf.release();
-    h->e2e.release();
-    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
-    for (cudaEvent_t e : h->slice_ev) cudaEventDestroy(e);
+    for (auto& c : h->hctx) {
+        c.e2e.release();
+        if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+        for (cudaEvent_t e : c.slice_ev) cudaEventDestroy(e);
+        if (c.h2d_ev) cudaEventDestroy(c.h2d_ev);
+    }
     sv_release(h->sv);
     mr_release(h->mr);
     delete h;
@@ -785,15 +806,41 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
     hodlr_status stc = check_working(working, true);
     if (stc != HODLR_OK) return stc;
     if (s < 1 || !x_host || !b_host) return fail(HODLR_ERR_INVALID, "bad arguments");
-    std::lock_guard<std::mutex> lock(h->mu);
+    // take a free staging context (released on every return path)
+    struct CtxLease {
+        hodlr_handle* h;
+        hodlr_handle::HostCtx* c = nullptr;
+        explicit CtxLease(hodlr_handle* hh) : h(hh) {
+            std::unique_lock<std::mutex> lk(h->mu);
+            h->hcv.wait(lk, [&] {
+                for (auto& x : h->hctx)
+                    if (!x.busy) return true;
+                return false;
+            });
+            for (auto& x : h->hctx)
+                if (!x.busy) {
+                    c = &x;
+                    break;
+                }
+            c->busy = true;
+        }
+        ~CtxLease() {
+            {
+                std::lock_guard<std::mutex> lk(h->mu);
+                c->busy = false;
+            }
+            h->hcv.notify_one();
+        }
+    } lease(h);
+    hodlr_handle::HostCtx& hc = *lease.c;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = h->n_local;
     const int wb = working_bytes(working);
     size_t xb = round_up(n * s * 8, kAlign), wbytes = round_up(n * s * wb, kAlign);
     size_t need = 2 * xb + 2 * wbytes;
     CUDA_TRY(cudaSetDevice(h->device));
-    CUDA_TRY(h->e2e.ensure(need));
-    uint8_t* base = (uint8_t*)h->e2e.p;
+    CUDA_TRY(hc.e2e.ensure(need));
+    uint8_t* base = (uint8_t*)hc.e2e.p;
     double* xd = (double*)base;
     double* bd = (double*)(base + xb);
     void* xw = base + 2 * xb;
@@ -815,10 +862,21 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
         }
         return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
     };
+    // x in: ordered after the previous call's host-to-device copy (see hodlr_handle::last_h2d)
+    auto copy_x_in = [&](double* dst) -> cudaError_t {
+        std::lock_guard<std::mutex> lk(h->h2d_mu);
+        cudaError_t e = cudaSuccess;
+        if (!hc.h2d_ev) e = cudaEventCreateWithFlags(&hc.h2d_ev, cudaEventDisableTiming);
+        if (e == cudaSuccess && h->last_h2d && h->last_h2d != hc.h2d_ev) e = cudaStreamWaitEvent(st, h->last_h2d, 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dst, x_host, n * s * 8, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaEventRecord(hc.h2d_ev, st);
+        if (e == cudaSuccess) h->last_h2d = hc.h2d_ev;
+        return e;
+    };
     const bool zc = !getenv("HODLR_B200_NO_ZEROCOPY");
     double* b_map = zc ? (double*)mapped(b_host) : nullptr;
     if (narrow_working(working)) {
-        CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(copy_x_in(xd));
         r = run_seq(h, working, xd, s, bd, s, s, ws, st);
         if (r != HODLR_OK) return r;
         b_map = nullptr;
@@ -828,40 +886,40 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
         // reduce once, then phase B over row ranges; each finished range is copied out
         // on a second stream while the next ranges are computed, so only the first
         // range's kernel time stays in front of the 2.4 ms device-to-host copy.
-        CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(copy_x_in(xd));
         double *partial, *tbuf;
         void* extra;
         carve<double>(h, s, ws, &partial, &tbuf, &extra);
         CUDA_TRY(mr_phase_a(h->view, h->mr, xd, s, s, partial, tbuf, st));
         const int nch = h->view.nchunks;
         const int nsl = std::max(1, std::min(8, nch / 64));
-        if (!h->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-        while ((int)h->slice_ev.size() < nsl) {
+        if (!hc.copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&hc.copy_stream, cudaStreamNonBlocking));
+        while ((int)hc.slice_ev.size() < nsl) {
             cudaEvent_t ev;
             CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            h->slice_ev.push_back(ev);
+            hc.slice_ev.push_back(ev);
         }
         for (int i = 0; i < nsl; ++i) {
             const int c0 = (int)((int64_t)i * nch / nsl), c1 = (int)((int64_t)(i + 1) * nch / nsl);
             CUDA_TRY(mr_phase_b_range(h->view, h->mr, xd, s, bd, s, s, tbuf, c0, c1, st));
-            CUDA_TRY(cudaEventRecord(h->slice_ev[i], st));
-            CUDA_TRY(cudaStreamWaitEvent(h->copy_stream, h->slice_ev[i], 0));
+            CUDA_TRY(cudaEventRecord(hc.slice_ev[i], st));
+            CUDA_TRY(cudaStreamWaitEvent(hc.copy_stream, hc.slice_ev[i], 0));
             const int64_t r0 = h->chunks[c0].row0, r1 = c1 < nch ? h->chunks[c1].row0 : n;
             CUDA_TRY(cudaMemcpyAsync(b_host + r0 * s, bd + r0 * s, (size_t)(r1 - r0) * s * 8, cudaMemcpyDeviceToHost,
-                                     h->copy_stream));
+                                     hc.copy_stream));
         }
-        CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
+        CUDA_TRY(cudaStreamSynchronize(hc.copy_stream));
         CUDA_TRY(cudaStreamSynchronize(st));
         return HODLR_OK;
     } else if (working == HODLR_FMT_FP64) {
-        CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(copy_x_in(xd));
         if (!(h->sv_ok && s == 1) || ((uintptr_t)b_map & 15)) b_map = nullptr;  // multi-pass writers / unaligned: stage in HBM
         r = run_local<double>(h, xd, s, b_map ? b_map : bd, s, s, ws, st);
         if (r != HODLR_OK) return r;
     } else {
         // (x is still staged by the copy engine: one kernel reading 2 MB of mapped
         // host memory measured slower than the copy, cfg5 eps=1e-2 e2e 180 -> 247 us)
-        CUDA_TRY(cudaMemcpyAsync(xd, x_host, n * s * 8, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(copy_x_in(xd));
         CUDA_TRY(launch_round_in<float>(xd, (float*)xw, n, s, s, s, st));
         r = run_local<float>(h, (const float*)xw, s, (float*)bw, s, s, ws, st);
         if (r != HODLR_OK) return r;
