@@ -61,6 +61,24 @@ def summarize(path):
     print(f"  items per CTA: A {cnt[:, 0].mean():.2f} (max {cnt[:, 0].max():.0f})  BC {cnt[:, 1].mean():.2f} "
           f"(max {cnt[:, 1].max():.0f})  R {cnt[:, 2].sum():.0f} total")
     print(f"  kernel span {(T[:, 10].max() - t0) / 1000:.2f} us")
+    # who ends last?  per-CTA rows sorted by exit time (first / last 8) and correlations
+    us = lambda i: np.where(T[:, i] > 0, (T[:, i] - t0) / 1000.0, np.nan)
+    ex = us(10)
+    cols = [("A", cnt[:, 0]), ("BC", cnt[:, 1]), ("R", cnt[:, 2]), ("firstBC", us(3)), ("coefReady", us(6)),
+            ("qExhaust", us(7)), ("firstU", us(14)), ("lastU", us(8)), ("consDone", us(9)), ("exit", ex)]
+    order = np.argsort(ex)
+    print("  per-CTA (sorted by exit):  cta " + " ".join(f"{n:>9s}" for n, _ in cols))
+    for i in list(order[:8]) + [-1] + list(order[-8:]):
+        if i < 0:
+            print("    ...")
+            continue
+        print(f"    {i:4d} " + " ".join(f"{v[i]:9.2f}" for _, v in cols))
+    for n, v in cols[:-1]:
+        ok = ~np.isnan(v)
+        if ok.sum() > 2 and np.std(v[ok]) > 0:
+            print(f"  corr(exit, {n}) = {np.corrcoef(ex[ok], v[ok])[0, 1]:+.2f}")
+    sm_lo, sm_hi = ex[: grid // 2], ex[grid // 2:]
+    print(f"  exit by CTA index half: first {np.nanmean(sm_lo):.2f}  second {np.nanmean(sm_hi):.2f}")
 
 
 def main():
