@@ -507,8 +507,11 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
                 sub.push_back(nd);
                 sub.back().level -= L;
             }
+        // geometry 1 (4 CTAs per SM) for binary32-working matrices; HODLR_B200_SV_GEO=0/1 overrides
+        int geo = h->leaf_fmt == HODLR_FMT_FP32 ? 1 : 0;
+        if (const char* g = getenv("HODLR_B200_SV_GEO")) geo = atoi(g) == 1 ? 1 : 0;
         SvInput si{&sub, &h->chunks, &h->leaves, &h->chunk_nodes, depth - L, (const uint8_t*)h->arena.p,
-                   h->arena_bytes};
+                   h->arena_bytes, geo};
         hodlr_status st = sv_prepare(si, h->sv, &h->sv_ok);
         if (st != HODLR_OK) return cleanup(st);
         if (h->sv_ok && P > 1) {
@@ -518,7 +521,7 @@ hodlr_status build(const hodlr_desc* d, int device, hodlr_shard shard, hodlr_han
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
             if (const char* r = getenv("HODLR_B200_SHARD_RESERVE_SMS")) reserve = atoi(r);
             reserve = std::max(0, std::min(reserve, sms - 1));
-            sv_set_grid(h->sv, 2 * (sms - reserve));
+            sv_set_grid(h->sv, h->sv.ctas_per_sm * (sms - reserve));
         }
     }
     *out = h;

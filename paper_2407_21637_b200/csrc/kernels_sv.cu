@@ -47,6 +47,17 @@
 #include "common.cuh"
 #include "sv.h"
 
+// This file is compiled twice (Makefile): HODLR_SV_GEO = 0 with the default geometry and
+// HODLR_SV_GEO = 1 with HODLR_CTAS / HODLR_CONSUMERS / HODLR_KNS / HODLR_KSTAGE of the
+// binary32-working geometry (SvInput::geo).  The geometry-specific entry points carry a
+// _g0 / _g1 suffix; the geometry-0 object also holds the dispatchers declared in sv.h.
+#ifndef HODLR_SV_GEO
+#define HODLR_SV_GEO 0
+#endif
+#define SVG_CAT(a, b) a##b
+#define SVG_X(n, g) SVG_CAT(n, g)
+#define SVG(n) SVG_X(n##_g, HODLR_SV_GEO)
+
 namespace hodlr {
 
 namespace {
@@ -1064,8 +1075,10 @@ int64_t round_up16(int64_t v) { return (v + 15) / 16 * 16; }
 }  // namespace
 
 // ============================================================== host side
-hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
+hodlr_status SVG(sv_prepare)(const SvInput& in, SvPlan& sv, bool* ok) {
     sv = SvPlan{};
+    sv.geo = HODLR_SV_GEO;
+    sv.ctas_per_sm = kCtasPerSm;
     *ok = false;
     const auto& nodes = *in.nodes;
     const auto& leaves = *in.leaves;
@@ -1407,22 +1420,20 @@ hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
     return HODLR_OK;
 }
 
-void sv_set_grid(SvPlan& sv, int grid) {
+void SVG(sv_set_grid)(SvPlan& sv, int grid) {
     sv.grid = std::max(1, std::min(sv.grid, grid));
     SvParams& P = *reinterpret_cast<SvParams*>(sv.params);
     P.pos_r = std::min(P.pos_r, sv.grid * (kFifo - 2));
 }
 
-void sv_release(SvPlan& sv) {
+void SVG(sv_release)(SvPlan& sv) {
     if (sv.dev) cudaFree(sv.dev);
     delete reinterpret_cast<SvParams*>(sv.params);
     sv = SvPlan{};
 }
-size_t sv_extra_ws(const SvPlan& sv, int64_t) { return sv.extra_ws; }
-int sv_launches(const SvPlan& sv) { return sv.launches; }
 
 template <typename W>
-cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* partial, W* tbuf_unused,
+cudaError_t SVG(sv_matvec)(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* partial, W* tbuf_unused,
                       void* extra, cudaStream_t st) {
     (void)p;
     (void)tbuf_unused;
@@ -1504,9 +1515,42 @@ cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* 
     return err;
 }
 
+template cudaError_t SVG(sv_matvec)<double>(const PlanView&, const SvPlan&, const double*, double*, double*, double*,
+                                       void*, cudaStream_t);
+template cudaError_t SVG(sv_matvec)<float>(const PlanView&, const SvPlan&, const float*, float*, float*, float*, void*,
+                                      cudaStream_t);
+
+#if HODLR_SV_GEO == 0
+// ------------------------------------------------------------ dispatch on SvPlan::geo
+hodlr_status sv_prepare_g1(const SvInput& in, SvPlan& sv, bool* ok);
+void sv_set_grid_g1(SvPlan& sv, int grid);
+void sv_release_g1(SvPlan& sv);
+template <typename W>
+cudaError_t sv_matvec_g1(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* partial, W* tbuf, void* extra,
+                         cudaStream_t st);
+
+hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok) {
+    if (in.geo == 1) {
+        hodlr_status st = sv_prepare_g1(in, sv, ok);
+        if (st != HODLR_OK || *ok) return st;
+        sv_release_g1(sv);  // the shape does not fit that geometry: the default one may
+    }
+    return sv_prepare_g0(in, sv, ok);
+}
+void sv_set_grid(SvPlan& sv, int grid) { sv.geo == 1 ? sv_set_grid_g1(sv, grid) : sv_set_grid_g0(sv, grid); }
+void sv_release(SvPlan& sv) { sv.geo == 1 ? sv_release_g1(sv) : sv_release_g0(sv); }
+size_t sv_extra_ws(const SvPlan& sv, int64_t) { return sv.extra_ws; }
+int sv_launches(const SvPlan& sv) { return sv.launches; }
+template <typename W>
+cudaError_t sv_matvec(const PlanView& p, const SvPlan& sv, const W* x, W* b, W* partial, W* tbuf, void* extra,
+                      cudaStream_t st) {
+    return sv.geo == 1 ? sv_matvec_g1<W>(p, sv, x, b, partial, tbuf, extra, st)
+                       : sv_matvec_g0<W>(p, sv, x, b, partial, tbuf, extra, st);
+}
 template cudaError_t sv_matvec<double>(const PlanView&, const SvPlan&, const double*, double*, double*, double*,
                                        void*, cudaStream_t);
 template cudaError_t sv_matvec<float>(const PlanView&, const SvPlan&, const float*, float*, float*, float*, void*,
                                       cudaStream_t);
+#endif
 
 }  // namespace hodlr

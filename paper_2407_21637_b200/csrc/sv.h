@@ -25,6 +25,8 @@ struct SvPlan {
     int64_t part_count = 0;     // fast-path partial buffer (elements)
     size_t extra_ws = 0;        // bytes of workspace for sync state + coefficients
     int leaf_fmt = 4;
+    int geo = 0;                // kernel geometry of this plan (SvInput::geo)
+    int ctas_per_sm = 2;        // pipelines per SM of that geometry
 };
 
 struct SvInput {
@@ -35,6 +37,12 @@ struct SvInput {
     int nlev;
     const uint8_t* d_arena;     // generic (level-batched) arena, already quantised
     size_t arena_bytes;
+    // Kernel geometry (kernels_sv.cu is compiled twice): 0 = 2 CTAs per SM x 8 consumer
+    // warps, ring of 3 x 32.5 KB (binary64 working: cfg2 and the fp64 half of cfg5);
+    // 1 = 4 CTAs per SM x 4 consumer warps, ring of 2 x 20.3 KB (binary32 working: twice
+    // the elements per byte, so more pieces are consumed concurrently; cfg5 eps = 1e-2:
+    // 76.1 -> 68.4 us, and 45.7 vs 39.7 us on cfg2, which is why it is not the default).
+    int geo = 0;
 };
 
 hodlr_status sv_prepare(const SvInput& in, SvPlan& sv, bool* ok);

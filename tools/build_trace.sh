@@ -9,4 +9,4 @@ nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler
      ${TRACE_FLAGS:--DHODLR_TC_TRACE} -c kernels_tc.cu -o /tmp/kernels_tc_trace.o
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/variants/libhodlr_tctrace.so \
      build/capi.o build/kernels_generic.o build/kernels_seq.o build/kernels_sv.o build/kernels_shard.o \
-     build/kernels_mrhs.o /tmp/kernels_tc_trace.o -cudart static
+     build/kernels_mrhs.o build/kernels_sv_g1.o /tmp/kernels_tc_trace.o -cudart static

@@ -12,6 +12,6 @@ for spec in "$@"; do
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr \
        $defs -c kernels_sv.cu -o build/kv_$tag.o
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/variants/libhodlr_b200_$tag.so \
-       build/capi.o build/kernels_generic.o build/kernels_seq.o build/kernels_shard.o build/kernels_mrhs.o build/kernels_tc.o build/kv_$tag.o -cudart static
+       build/capi.o build/kernels_generic.o build/kernels_seq.o build/kernels_shard.o build/kernels_mrhs.o build/kernels_tc.o build/kernels_sv_g1.o build/kv_$tag.o -cudart static
   echo built $tag
 done
