@@ -350,6 +350,11 @@ def time_e2e(op, X, K, stream):
     for _ in range(3):
         op.matvec_host_ptr(xh.data_ptr(), bh.data_ptr(), s, stream=stream.cuda_stream)
     torch.cuda.synchronize()
+    # short calls: enough of them for ~30 ms of timed region (a dozen 100-us calls is noise)
+    t0 = time.perf_counter()
+    op.matvec_host_ptr(xh.data_ptr(), bh.data_ptr(), s, stream=stream.cuda_stream)
+    est_ms = max((time.perf_counter() - t0) * 1e3, 1e-3)
+    K = int(min(400, max(K, 30.0 / est_ms)))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(K):
@@ -435,8 +440,12 @@ def measure_config(cfg, args, dev, clocks=None, cpu=True):
     ms, ms_hot = time_device(op, xd, bd, K, args.warmup, flush, stream, clocks)
     ms_e2e, b_e2e = time_e2e(op, X, max(10, min(K, 200) // 4), stream)
     parity["e2e_matches"] = bool(np.linalg.norm(b_e2e - b_gpu) <= parity["tol_vs_oracle"] * np.linalg.norm(b_gpu))
-    ms_e2e2, same2 = time_e2e_two_callers(op, X, int(min(500, max(5, 40.0 / ms_e2e))), b_e2e)  # ~80 ms of calls
-    parity["e2e_two_callers_bitwise_equal"] = bool(same2)
+    try:  # a secondary figure: never fails the headline line
+        ms_e2e2, same2 = time_e2e_two_callers(op, X, int(min(500, max(5, 40.0 / ms_e2e))), b_e2e)  # ~80 ms of calls
+        parity["e2e_two_callers_bitwise_equal"] = bool(same2)
+    except Exception as e:
+        print(f"[bench] two-caller e2e skipped: {e!r}", file=sys.stderr)
+        ms_e2e2 = None
     del flush
 
     B = alg_bytes(H, s, wb)
@@ -535,7 +544,8 @@ def run_single(args):
         "e2e": {"value": 1000.0 / r["ms_e2e"], "unit": "matvec/s", "h2d_bytes_per_step": int(H.n * s * 8),
                 "d2h_bytes_per_step": int(H.n * s * 8), "ms_per_step": r["ms_e2e"],
                 "path": "hodlr_matvec_host (pinned binary64 X in, B out), one caller, calls back to back",
-                "two_callers": {"value": 1000.0 / r["ms_e2e2"], "unit": "matvec/s", "ms_per_step": r["ms_e2e2"],
+                "two_callers": {"value": 1000.0 / r["ms_e2e2"] if r["ms_e2e2"] else None, "unit": "matvec/s",
+                                "ms_per_step": r["ms_e2e2"],
                                 "note": "same entry point from two host threads on two streams (two staging "
                                         "contexts per handle): one call's D2H overlaps the other's H2D; "
                                         "every call copies its X in and its B out"}},
@@ -563,7 +573,7 @@ def run_single(args):
             "workload": r2["desc"], "value": 1000.0 / r2["ms"], "unit": "matvec/s", "ms_per_step": r2["ms"],
             "kernel_path": r2["path"], "roofline": r2["roofline"], "parity": r2["parity"],
             "e2e": {"value": 1000.0 / r2["ms_e2e"], "unit": "matvec/s", "ms_per_step": r2["ms_e2e"],
-                    "two_callers": {"value": 1000.0 / r2["ms_e2e2"], "unit": "matvec/s",
+                    "two_callers": {"value": 1000.0 / r2["ms_e2e2"] if r2["ms_e2e2"] else None, "unit": "matvec/s",
                                     "ms_per_step": r2["ms_e2e2"]}},
             "hot_cache_ms": r2["ms_hot"], "gpu_launches": args.steps * r2["launches"], "clocks": c2.summary()}}
         line["gpu_launches"] += args.steps * r2["launches"]

@@ -155,6 +155,28 @@ def test_wide_levels_split_into_column_groups(cuda):
     assert rel(b, matvec_oracle(H, x)) <= 1e-5
 
 
+@pytest.mark.parametrize("geo", [0, 1])
+@pytest.mark.parametrize("working,fmts", FMT_SETS)
+def test_fused_both_kernel_geometries(cuda, monkeypatch, working, fmts, geo):
+    """The fused kernel is built in two geometries (sv.h SvInput::geo: 2 CTAs per SM x 8
+    consumer warps, or 4 x 4 for binary32-working matrices); HODLR_B200_SV_GEO forces one at
+    create time.  Either geometry matches the oracle for either working precision, and
+    repeated calls are bit-identical (fixed summation order inside a geometry)."""
+    torch = cuda
+    monkeypatch.setenv("HODLR_B200_SV_GEO", str(geo))
+    H = random_hodlr(4096, 4, (fmts + fmts)[:4], [24, 17, 9, 3], working, seed=17 + geo)
+    op = make_op(H)
+    assert op.launches_per_matvec == 1, "fused path not selected"
+    x = np.random.default_rng(3).standard_normal(H.n)
+    dt = torch.float64 if working == "fp64" else torch.float32
+    xd = torch.from_numpy(x).cuda().to(dt)
+    b1 = op.matvec(xd).clone()
+    b2 = op.matvec(xd).clone()
+    assert torch.equal(b1, b2)
+    tol = 1e-12 if working == "fp64" else 1e-5
+    assert rel(b1.double().cpu().numpy(), matvec_oracle(H, x)) <= tol
+
+
 @pytest.mark.parametrize("depth", [1, 2, 5])
 def test_fused_depths(cuda, depth):
     torch = cuda
