@@ -813,6 +813,7 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
     struct CtxLease {
         hodlr_handle* h;
         hodlr_handle::HostCtx* c = nullptr;
+        bool contended = false;  // another host-buffer call is in flight on this handle
         explicit CtxLease(hodlr_handle* hh) : h(hh) {
             std::unique_lock<std::mutex> lk(h->mu);
             h->hcv.wait(lk, [&] {
@@ -826,6 +827,8 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
                     break;
                 }
             c->busy = true;
+            for (auto& x : h->hctx)
+                if (x.busy && &x != c) contended = true;
         }
         ~CtxLease() {
             {
@@ -866,8 +869,13 @@ hodlr_status hodlr_matvec_host(hodlr_handle* h, int32_t working, const double* x
         return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
     };
     // x in: ordered after the previous call's host-to-device copy (see hodlr_handle::last_h2d)
+    // (a lone caller needs no ordering and records no event)
     auto copy_x_in = [&](double* dst) -> cudaError_t {
         std::lock_guard<std::mutex> lk(h->h2d_mu);
+        if (!lease.contended) {
+            h->last_h2d = nullptr;
+            return cudaMemcpyAsync(dst, x_host, n * s * 8, cudaMemcpyHostToDevice, st);
+        }
         cudaError_t e = cudaSuccess;
         if (!hc.h2d_ev) e = cudaEventCreateWithFlags(&hc.h2d_ev, cudaEventDisableTiming);
         if (e == cudaSuccess && h->last_h2d && h->last_h2d != hc.h2d_ev) e = cudaStreamWaitEvent(st, h->last_h2d, 0);
