@@ -1206,6 +1206,10 @@ hodlr_status SVG(sv_prepare)(const SvInput& in, SvPlan& sv, bool* ok) {
     // partials for the reduction; cfg2 42.5 -> 41.5 us, profiles/round1_sv_sweep_cfg2.txt)
     P.a_group = nleaves >= 2 * kCtasPerSm * sms_now ? P.napieces
                 : (P.nag == 1 && P.napieces > 2 && P.napieces % 2 == 0) ? 2 : 1;
+    // 4-CTA geometry (small stages, so more pieces per leaf): whole leaves already at one leaf
+    // per CTA once a leaf has >= 4 pieces (cfg5 eps=1e-4: 74.6 -> 72.7 us; with 2 pieces per
+    // leaf, eps=1e-2, single pieces stay 1% ahead)
+    if (kCtasPerSm >= 4 && nleaves >= kCtasPerSm * sms_now && P.napieces >= 4) P.a_group = P.napieces;
     if (getenv("HODLR_B200_A_GROUP")) {
         // 1: single pieces; k (one format group, k | napieces): k consecutive row
         // pieces per item, npc = napieces / k partials per leaf; else whole leaves
