@@ -208,6 +208,8 @@ class HodlrOperator:
         dt = torch.float32 if code == 3 else torch.float64
         if not (isinstance(x, torch.Tensor) and x.is_cuda):
             raise TypeError("HodlrOperator.matvec expects a CUDA tensor; use matvec_host for host arrays")
+        if x.device.index != self.device:
+            raise ValueError(f"tensor on cuda:{x.device.index}, operator on cuda:{self.device}")
         vec = x.dim() == 1
         X = x.reshape(-1, 1) if vec else x
         if X.dim() != 2 or X.shape[0] != self.n_local:
